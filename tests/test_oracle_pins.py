@@ -1,0 +1,541 @@
+"""Pins for the FP64 oracle: each check ties the oracle to something other than itself --
+closed forms, library routines (scipy, mpmath), brute force, finite differences, invariants
+and planted truth -- so that a dropped term, a wrong sign/index or a transposed operand fails.
+(SURVEY.md 8(c) table C-P.)  CPU only."""
+import math
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+import scipy.special as sps
+from scipy.spatial.transform import Rotation
+
+import gen
+import oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+rng = np.random.default_rng(20260318)
+
+
+def rand_euler():
+    return np.array([rng.uniform(0, 2 * np.pi), rng.uniform(0, np.pi), rng.uniform(0, 2 * np.pi)])
+
+
+# ------------------------------------------------------------------ rotations (Eq. 3)
+def test_euler_golden():
+    for line in open(os.path.join(GOLD, "rotations.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        a, r = line.split("|")
+        e = np.array([float(x) for x in a.split()]) * np.pi
+        R = np.array([float(x) for x in r.split()]).reshape(3, 3)
+        assert np.abs(O.euler_to_matrix(e) - R).max() < 1e-12
+
+
+def test_euler_vs_scipy_and_roundtrip():
+    for _ in range(50):
+        e = rand_euler()
+        R = O.euler_to_matrix(e)
+        Rs = Rotation.from_euler("ZYZ", e).as_matrix()  # intrinsic z-y-z = r_z(a) r_y(b) r_z(g)
+        assert np.abs(R - Rs).max() < 1e-12
+        assert np.abs(R @ R.T - np.eye(3)).max() < 1e-12 and abs(np.linalg.det(R) - 1) < 1e-12
+        e2 = O.matrix_to_euler(R)
+        assert np.abs(O.euler_to_matrix(e2) - R).max() < 1e-9
+    # gimbal convention (reading C7): r_z(0.7) -> (0.7, 0, 0)
+    e = O.matrix_to_euler(O.euler_to_matrix([0.7, 0, 0]))
+    assert np.allclose(e, [0.7, 0, 0], atol=1e-12)
+
+
+def test_canon_preserves_rotation():
+    for _ in range(50):
+        e = rng.uniform(-10, 10, 3)
+        c = O.canon(e)
+        assert 0 <= c[0] < 2 * np.pi and 0 <= c[1] <= np.pi and 0 <= c[2] < 2 * np.pi
+        assert np.abs(O.euler_to_matrix(c) - O.euler_to_matrix(e)).max() < 1e-12
+
+
+# ------------------------------------------------------------------ quadrature / Legendre
+def test_gauss_legendre_vs_scipy():
+    for n in (1, 2, 17, 65, 129):
+        x, w = O.gauss_legendre(n)
+        xs, ws = sps.roots_legendre(n)
+        assert np.abs(x - xs).max() < 1e-13 and np.abs(w - ws).max() < 1e-13
+
+
+def test_legendre_norm_vs_scipy_sph_harm():
+    L = 40
+    for x in (-0.93, -0.2, 0.0, 0.51, 0.999):
+        P = O.legendre_norm(L, x)
+        th = np.arccos(x)
+        for l in range(L + 1):
+            for m in range(l + 1):
+                ref = sps.sph_harm_y(l, m, th, 0.0).real  # Y_lm(theta, 0) = P_lm(cos theta), CS phase
+                assert abs(P[l * (l + 1) // 2 + m] - ref) < 1e-12 * max(1.0, abs(ref))
+
+
+# ------------------------------------------------------------------ Wigner d / D (App. A.3)
+def _d_explicit(l, m, n, b):
+    """Wigner's explicit finite sum, 40 digits."""
+    mp.mp.dps = 40
+    b = mp.mpf(b)
+    c, s = mp.cos(b / 2), mp.sin(b / 2)
+    f = mp.factorial
+    tot = mp.mpf(0)
+    for k in range(0, 2 * l + 1):
+        if l + n - k < 0 or m - n + k < 0 or l - m - k < 0:
+            continue
+        tot += ((-1) ** (m - n + k) * mp.sqrt(f(l + m) * f(l - m) * f(l + n) * f(l - n))
+                / (f(l + n - k) * f(k) * f(m - n + k) * f(l - m - k)) * c ** (2 * l + n - m - 2 * k) * s ** (m - n + 2 * k))
+    return float(tot)
+
+
+@pytest.mark.parametrize("l", [0, 1, 2, 7, 12, 20])
+def test_wigner_d_vs_explicit_sum(l):
+    for b in (0.0, 0.31, 1.7, np.pi - 1e-3, np.pi):
+        d = O.wigner_d(l, b)
+        for m in range(-l, l + 1):
+            for n in range(-l, l + 1):
+                assert abs(d[m + l, n + l] - _d_explicit(l, m, n, b)) < 1e-13
+
+
+def test_wigner_d1_golden():
+    for line in open(os.path.join(GOLD, "wigner_d1.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        m, n, expr = line.split(None, 2)
+        for b in (0.2, 1.3, 2.9):
+            ref = eval(expr, {"cos": math.cos, "sin": math.sin, "sqrt": math.sqrt, "b": b})
+            assert abs(O.wigner_d(1, b)[int(m) + 1, int(n) + 1] - ref) < 1e-14
+
+
+def test_wigner_d00_is_legendre():
+    for l in (3, 17, 40, 64):
+        for b in (0.1, 1.0, 2.5):
+            assert abs(O.wigner_d(l, b)[l, l] - sps.eval_legendre(l, np.cos(b))) < 1e-12
+
+
+@pytest.mark.parametrize("l", [1, 8, 32, 64])
+def test_wigner_unitarity(l):
+    for _ in range(3):
+        D = O.wigner_D(l, rand_euler())
+        assert np.abs(D @ D.conj().T - np.eye(2 * l + 1)).max() < 1e-10
+
+
+def test_wigner_homomorphism_and_identity():
+    for _ in range(5):
+        e1, e2 = rand_euler(), rand_euler()
+        e12 = O.matrix_to_euler(O.euler_to_matrix(e1) @ O.euler_to_matrix(e2))
+        for l in (1, 2, 5, 16):
+            assert np.abs(O.wigner_D(l, e12) - O.wigner_D(l, e1) @ O.wigner_D(l, e2)).max() < 1e-9
+    for l in (0, 3, 9):
+        assert np.abs(O.wigner_D(l, [0, 0, 0]) - np.eye(2 * l + 1)).max() < 1e-14
+
+
+def test_wigner_character():
+    """sum_m D^l_mm(g) = sin((2l+1) w/2) / sin(w/2), w the rotation angle."""
+    for _ in range(5):
+        e = rand_euler()
+        R = O.euler_to_matrix(e)
+        w = np.arccos(np.clip((np.trace(R) - 1) / 2, -1, 1))
+        for l in (1, 4, 11):
+            chi = np.trace(O.wigner_D(l, e)).real
+            assert abs(chi - np.sin((2 * l + 1) * w / 2) / np.sin(w / 2)) < 1e-10
+
+
+def test_wigner_symmetries():
+    for l in (3, 10):
+        b = 1.234
+        d = O.wigner_d(l, b)
+        dpi = O.wigner_d(l, np.pi - b)
+        for m in range(-l, l + 1):
+            for n in range(-l, l + 1):
+                s = (-1) ** ((m - n) & 1)
+                assert abs(d[-m + l, -n + l] - s * d[m + l, n + l]) < 1e-13
+                assert abs(d[n + l, m + l] - s * d[m + l, n + l]) < 1e-13
+                assert abs(dpi[m + l, n + l] - (-1) ** ((l + m) & 1) * d[m + l, -n + l]) < 1e-12
+
+
+def test_wigner_orthogonality_monte_carlo():
+    """Haar average of D^l_mn conj(D^l'_m'n') = delta/(2l+1) (reading C8: P:1285's 1/(8 pi^2) is garbled)."""
+    q = rng.normal(size=(20000, 4))
+    Rs = Rotation.from_quat(q).as_matrix()
+    acc = np.zeros((3, 3), complex)
+    cross = 0.0
+    for R in Rs:
+        e = O.matrix_to_euler(R)
+        D1 = O.wigner_D(1, e)
+        acc += np.abs(D1) ** 2
+        cross += (D1[0, 1] * np.conj(D1[1, 1]))
+    acc /= len(Rs)
+    assert np.abs(acc - 1.0 / 3.0).max() < 0.02
+    assert abs(cross / len(Rs)) < 0.02
+
+
+def test_ladder_derivatives_fd():
+    h = 1e-5
+    for l in (1, 6, 16):
+        b = rng.uniform(0.3, 2.8)
+        d, d1, d2 = O.wigner_d(l, b, derivs=True)
+        fd1 = (O.wigner_d(l, b + h) - O.wigner_d(l, b - h)) / (2 * h)
+        assert np.abs(d1 - fd1).max() < 1e-6 * max(1, np.abs(d1).max())
+        h2 = 1e-4
+        fd2 = (O.wigner_d(l, b + h2) - 2 * d + O.wigner_d(l, b - h2)) / h2**2
+        assert np.abs(d2 - fd2).max() < 1e-4 * max(1, np.abs(d2).max())
+
+
+# ------------------------------------------------------------------ stage 1 SH analysis
+def _poly(deg, scale):
+    t = []
+    for a in range(deg + 1):
+        for b in range(deg + 1 - a):
+            for c in range(deg + 1 - a - b):
+                t.append((rng.normal() * scale ** (a + b + c), a, b, c))
+    return t
+
+
+def test_sh_closed_forms():
+    N, L = 32, 6
+    r = np.arange(N // 2) + 0.5
+    F = O.sh_analysis_poly([(1, 0, 0, 0)], N, L)
+    assert np.abs(F[0] - np.sqrt(4 * np.pi)).max() < 1e-12 and np.abs(F[1:]).max() < 1e-12
+    F = O.sh_analysis_poly([(1, 0, 0, 1)], N, L)  # u = z
+    assert np.abs(F[1] - r * np.sqrt(4 * np.pi / 3)).max() < 1e-11
+    F = O.sh_analysis_poly([(1, 1, 0, 0)], N, L)  # u = x: f_{1,1} = -r sqrt(2pi/3)
+    assert np.abs(F[2] + r * np.sqrt(2 * np.pi / 3)).max() < 1e-11
+    F = O.sh_analysis_poly([(1, 0, 1, 0)], N, L)  # u = y: f_{1,1} = i r sqrt(2pi/3)... (y = r sin th sin ph)
+    assert np.abs(F[2] - 1j * r * np.sqrt(2 * np.pi / 3)).max() < 1e-11
+
+
+def test_sh_volume_path_exact_for_multilinear():
+    """Trilinear interpolation is exact for multilinear u, so the voxel path equals the analytic one."""
+    N, L = 16, 4
+    c = (N - 1) / 2
+    z, y, x = np.meshgrid(np.arange(N) - c, np.arange(N) - c, np.arange(N) - c, indexing="ij")
+    terms = [(0.3, 0, 0, 0), (1.1, 1, 0, 0), (-0.7, 0, 1, 0), (0.5, 0, 0, 1), (0.05, 1, 1, 0), (-0.02, 0, 1, 1),
+             (0.01, 1, 0, 1), (0.003, 1, 1, 1)]
+    vol = sum(cf * x**a * y**b * z**cc for cf, a, b, cc in terms).astype(np.float64)
+    Fa = O.sh_analysis_poly(terms, N, L)
+    Fv = O.sh_analysis(vol.astype(np.float32), L)
+    Fa32 = O.sh_analysis_poly(terms, N, L)
+    assert np.abs(Fv - Fa).max() < 1e-5 * np.abs(Fa).max()
+    assert np.abs(Fa32 - Fa).max() == 0
+
+
+def test_sh_equivariance():
+    """analysis(g o u)_{lm} = sum_n D^l_mn(g) analysis(u)_{ln} for band-limited u (reading C1)."""
+    N, L = 16, 4
+    R = N // 2
+    pf = _poly(L, 1.0 / R)
+    for _ in range(3):
+        e = rand_euler()
+        Fu = O.sh_analysis_poly(pf, N, L)
+        Fg = O.sh_analysis_poly(pf, N, L, R=O.euler_to_matrix(e))
+        for l in range(L + 1):
+            full = np.array([Fu[l * (l + 1) // 2 + m] if m >= 0 else (-1) ** (m & 1) * np.conj(Fu[l * (l + 1) // 2 - m])
+                             for m in range(-l, l + 1)])
+            pred = O.wigner_D(l, e) @ full
+            got = Fg[l * (l + 1) // 2:(l * (l + 1) // 2 + l + 1)]
+            assert np.abs(pred[l:] - got).max() < 1e-12 * np.abs(Fu).max()
+
+
+def test_sh_parseval_on_shell():
+    """sum_j W_j (2pi/n) sum_k u^2 = sum_{l,m} |f_lm|^2 for band-limited u (quadrature exact)."""
+    N, L = 16, 3
+    pf = _poly(L, 1.0 / 8)
+    F = O.sh_analysis_poly(pf, N, L, qover=2)
+    # energy from coefficients with m<0 mirrored
+    ecoef = np.zeros(N // 2)
+    for l in range(L + 1):
+        for m in range(l + 1):
+            ecoef += (1 if m == 0 else 2) * np.abs(F[l * (l + 1) // 2 + m]) ** 2
+    # direct quadrature of u^2 (degree 2L <= 2 Lq + 1)
+    Lq = 2 * L
+    x, w = O.gauss_legendre(Lq + 1)
+    nph = 2 * Lq + 2
+    ph = 2 * np.pi * np.arange(nph) / nph
+    for i in range(N // 2):
+        r = i + 0.5
+        st = np.sqrt(1 - x**2)
+        X = r * st[:, None] * np.cos(ph)[None]
+        Y = r * st[:, None] * np.sin(ph)[None]
+        Z = r * x[:, None] * np.ones_like(ph)[None]
+        u = sum(cf * X**a * Y**b * Z**c for cf, a, b, c in pf)
+        quad = (w[:, None] * u**2).sum() * 2 * np.pi / nph
+        assert abs(quad - ecoef[i]) < 1e-10 * quad
+
+
+# ------------------------------------------------------------------ stage 2 M
+def test_corr_invariants():
+    N, L = 16, 6
+    vol = gen.particles(N, 1, 0.5, seed=3).vols[0]
+    F = O.sh_analysis(vol, L)
+    Mf = O.corr_full(F, F, L)
+    H = O.sh_analysis(gen.particles(N, 1, 0.5, seed=4).vols[0], L)
+    Mfh = O.corr_full(F, H, L)
+    for l in range(L + 1):
+        w = 2 * l + 1
+        A = Mf[O.full_offset(l):O.full_offset(l) + w * w].reshape(w, w)
+        assert np.abs(A - A.conj().T).max() < 1e-10 * np.abs(A).max()
+        assert np.linalg.eigvalsh(A).min() > -1e-9 * np.abs(A).max()
+        B = Mfh[O.full_offset(l):O.full_offset(l) + w * w].reshape(w, w)
+        for m in range(-l, l + 1):
+            for n in range(-l, l + 1):
+                assert abs(B[-m + l, -n + l] - (-1) ** ((m + n) & 1) * np.conj(B[m + l, n + l])) < 1e-12 * np.abs(B).max()
+        s = np.linalg.svd(B, compute_uv=False)
+        assert (s > 1e-10 * s[0]).sum() <= min(N // 2, w)
+    # half-plane round trip
+    Mh = O.full_to_half(Mfh, L)
+    assert np.abs(O.half_to_full(Mh, L) - Mfh).max() < 1e-12 * np.abs(Mfh).max()
+    # single shell => rank one (P:1331 rank bound with |K_l| = 1)
+    F1 = F.copy()
+    F1[:, 1:] = 0
+    M1 = O.corr_full(F1, H, L)
+    for l in range(1, L + 1):
+        w = 2 * l + 1
+        s = np.linalg.svd(M1[O.full_offset(l):O.full_offset(l) + w * w].reshape(w, w), compute_uv=False)
+        assert (s > 1e-10 * s[0]).sum() <= 1
+
+
+# ------------------------------------------------------------------ C_L (Eq. 4 with reading C1)
+def test_corr_brute_force_conj_placement():
+    """C_L(g) = sum_i w_i sum_jk W_jk f(c + r w_jk) h(c + r g^-1 w_jk), exact for band-limited f, h."""
+    N, L = 16, 3
+    R = N // 2
+    pf, ph = _poly(L, 1.0 / R), _poly(L, 1.0 / R)
+    F, H = O.sh_analysis_poly(pf, N, L), O.sh_analysis_poly(ph, N, L)
+    Mf = O.corr_full(F, H, L)
+    Lq = 2 * L
+    x, w = O.gauss_legendre(Lq + 1)
+    nph = 2 * Lq + 2
+    phi = 2 * np.pi * np.arange(nph) / nph
+    st = np.sqrt(1 - x**2)
+    om = np.stack([st[:, None] * np.cos(phi)[None], st[:, None] * np.sin(phi)[None], x[:, None] + 0 * phi[None]], -1)
+
+    def pe(t, P):
+        return sum(cf * P[..., 0]**a * P[..., 1]**b * P[..., 2]**c for cf, a, b, c in t)
+
+    for _ in range(3):
+        e = rand_euler()
+        G = O.euler_to_matrix(e)
+        tot = 0.0
+        for i in range(R):
+            r = i + 0.5
+            P = r * om
+            tot += r * r * (w[:, None] * pe(pf, P) * pe(ph, P @ G)).sum() * 2 * np.pi / nph  # (G^T P) = P @ G
+        C = O.eval_corr(Mf, L, e)[0]
+        assert abs(C - tot) < 1e-12 * abs(tot)
+        # the literal sigma*D form of Eq. (4) evaluates the mirrored rotation (reading C1)
+        Cm = O.eval_corr(np.conj(Mf), L, [-e[0], e[1], -e[2]])[0]
+        assert abs(Cm - tot) < 1e-10 * abs(tot)
+
+
+def test_corr_special_cases():
+    N, L = 16, 5
+    F = O.sh_analysis(gen.particles(N, 1, 1.0, seed=5).vols[0], L)
+    Mf = O.corr_full(F, F, L)
+    tr = sum(np.trace(Mf[O.full_offset(l):O.full_offset(l) + (2 * l + 1) ** 2].reshape(2 * l + 1, -1)).real
+             for l in range(L + 1))
+    assert abs(O.eval_corr(Mf, L, [0, 0, 0])[0] - tr) < 1e-12 * abs(tr)
+    # M^1 = I only -> C = 1 + 2 cos(w)... here l=1 only: C = chi_1(w) = 1 + 2 cos w
+    Mi = np.zeros(O.full_size(1), complex)
+    Mi[O.full_offset(1):] = np.eye(3).reshape(-1)
+    for _ in range(5):
+        e = rand_euler()
+        w = np.arccos(np.clip((np.trace(O.euler_to_matrix(e)) - 1) / 2, -1, 1))
+        assert abs(O.eval_corr(Mi, 1, e)[0] - (1 + 2 * np.cos(w))) < 1e-12
+    # only l = 0 -> constant
+    M0 = np.zeros(O.full_size(2), complex)
+    M0[0] = 2.5
+    for _ in range(3):
+        C, g, h = O.eval_corr(M0, 2, rand_euler())
+        assert abs(C - 2.5) < 1e-14 and np.abs(g).max() < 1e-14 and np.abs(h).max() < 1e-14
+
+
+def test_eval_derivatives_fd():
+    N, L = 16, 8
+    b = gen.particles(N, 2, 1.0, seed=6)
+    F, H = O.sh_analysis(b.vols[0], L), O.sh_analysis(b.vols[1], L)
+    Mf = O.corr_full(F, H, L)
+    h1, h2 = 1e-5, 1e-4
+    for _ in range(4):
+        e = rand_euler()
+        e[1] = rng.uniform(0.3, 2.8)
+        C, g, H6 = O.eval_corr(Mf, L, e)
+        fdg = np.zeros(3)
+        fdH = np.zeros((3, 3))
+        for k in range(3):
+            ep, em = e.copy(), e.copy()
+            ep[k] += h1
+            em[k] -= h1
+            fdg[k] = (O.eval_corr(Mf, L, ep)[0] - O.eval_corr(Mf, L, em)[0]) / (2 * h1)
+            for j in range(3):
+                def f(da, db):
+                    x = e.copy()
+                    x[k] += da
+                    x[j] += db
+                    return O.eval_corr(Mf, L, x)[0]
+                fdH[k, j] = (f(h2, h2) - f(h2, -h2) - f(-h2, h2) + f(-h2, -h2)) / (4 * h2 * h2)
+        scale = np.abs(g).max()
+        assert np.abs(g - fdg).max() < 1e-6 * scale
+        Hm = np.array([[H6[0], H6[3], H6[4]], [H6[3], H6[1], H6[5]], [H6[4], H6[5], H6[2]]])
+        assert np.abs(Hm - fdH).max() < 1e-4 * np.abs(Hm).max()
+
+
+# ------------------------------------------------------------------ stage 3 grid + maxima
+def test_grid_nodes_equal_direct_and_flat_l0():
+    N, L0, K = 16, 4, 2
+    b = gen.particles(N, 2, 1.0, seed=7)
+    Mf = O.corr_full(O.sh_analysis(b.vols[0], L0), O.sh_analysis(b.vols[1], L0), L0)
+    g = O.grid_eval(Mf, L0, K)
+    nb, na, ng = g.shape
+    assert (nb, na, ng) == (10, 20, 20)
+    for _ in range(20):
+        idx = int(rng.integers(0, g.size))
+        e = O.grid_node_euler(idx, L0, K)
+        assert abs(g.reshape(-1)[idx] - O.eval_corr(Mf, L0, e)[0]) < 1e-12 * np.abs(g).max()
+    M0 = np.zeros(O.full_size(L0), complex)
+    M0[0] = 1.7
+    g0 = O.grid_eval(M0, L0, K)
+    assert np.abs(g0 - 1.7).max() < 1e-14
+    idx, sc, n = O.find_maxima(g0, 4)
+    assert n == 1 and idx[0] == 0 and idx[1] == -1 and np.isneginf(sc[1])  # ties -> lowest index (C10, C11)
+
+
+def test_maxima_bruteforce_and_two_lobes():
+    nb, na, ng = 6, 8, 8
+    for _ in range(5):
+        g = rng.integers(0, 5, size=(nb, na, ng)).astype(float)  # many exact ties
+        idx, sc, n = O.find_maxima(g, 200)
+        # brute force by the definition: lexicographic (value desc, index asc) local maximum
+        flat = g.reshape(-1)
+        found = []
+        for j in range(nb):
+            for a in range(na):
+                for c in range(ng):
+                    p = (j * na + a) * ng + c
+                    ok = True
+                    for dj in (-1, 0, 1):
+                        if not 0 <= j + dj < nb:
+                            continue
+                        for da in (-1, 0, 1):
+                            for dc in (-1, 0, 1):
+                                q = ((j + dj) * na + (a + da) % na) * ng + (c + dc) % ng
+                                if q != p and not (flat[p] > flat[q] or (flat[p] == flat[q] and p < q)):
+                                    ok = False
+                    if ok:
+                        found.append((-flat[p], p))
+        found.sort()
+        assert n == len(found)
+        assert list(idx[:n]) == [p for _, p in found]
+    # two separated lobes in order
+    j, a, c = np.meshgrid(np.arange(nb), np.arange(na), np.arange(ng), indexing="ij")
+    g = 2.0 * np.exp(-((j - 1) ** 2 + (a - 2) ** 2 + (c - 2) ** 2)) + np.exp(-((j - 4) ** 2 + (a - 6) ** 2 + (c - 5) ** 2))
+    idx, sc, n = O.find_maxima(g, 3)
+    assert n == 2 and idx[0] == (1 * na + 2) * ng + 2 and idx[1] == (4 * na + 6) * ng + 5
+
+
+# ------------------------------------------------------------------ stage 4 Newton
+def test_newton_delta_rules():
+    g = np.array([0.3, -1.2, 0.7])
+    # negative definite: plain Newton
+    A = rng.normal(size=(3, 3))
+    Hn = -(A @ A.T + 0.5 * np.eye(3))
+    h6 = [Hn[0, 0], Hn[1, 1], Hn[2, 2], Hn[0, 1], Hn[0, 2], Hn[1, 2]]
+    assert np.abs(O.newton_delta(g, h6) - np.linalg.solve(Hn, -g)).max() < 1e-12
+    # indefinite: eigen shift -> ascent direction (g . delta > 0)
+    Hi = np.diag([2.0, -1.0, 0.5])
+    d = O.newton_delta(g, [2.0, -1.0, 0.5, 0, 0, 0])
+    lmax = 2.0
+    fro = np.sqrt((Hi**2).sum())
+    assert np.abs(d - np.linalg.solve(Hi - (lmax + 1e-6 * fro) * np.eye(3), -g)).max() < 1e-9
+    assert g @ d > 0
+    assert np.abs(O.newton_delta([0, 0, 0], h6)).max() == 0.0
+
+
+def _analytic_pair(L, N, e_true, deg=None):
+    R = N // 2
+    ph = _poly(deg or L, 1.0 / R)
+    H = O.sh_analysis_poly(ph, N, L)
+    F = O.sh_analysis_poly(ph, N, L, R=O.euler_to_matrix(e_true))  # f = g* o h exactly
+    return F, H
+
+
+def test_newton_quadratic_convergence_and_exact_recovery():
+    """Noise-free analytic band-limited fixture: C_L is maximised exactly at g* (Re tr(A U) <= tr A),
+    Newton converges quadratically from a few-degree start."""
+    N, L = 16, 6
+    e_true = np.array([1.1, 1.3, 4.2])
+    F, H = _analytic_pair(L, N, e_true)
+    Mf = O.corr_full(F, H, L)
+    th = e_true + np.radians([2.0, -1.5, 2.5])
+    errs = []
+    for _ in range(5):
+        C, g, h = O.eval_corr(Mf, L, th)
+        th = O.canon(th + O.newton_delta(g, h))
+        errs.append(O.geodesic_deg(th, e_true))
+    assert errs[3] < 1e-9
+    assert errs[1] < errs[0] ** 1.5 or errs[1] < 1e-9  # superlinear
+    C, g, h = O.eval_corr(Mf, L, e_true)
+    assert np.abs(g).max() < 1e-9 * abs(C)  # critical point at g*
+    assert np.abs(O.newton_delta(g, h)).max() < 1e-9
+
+
+def test_algorithm1_exact_recovery_analytic():
+    """Whole Algorithm 1 (grid -> maxima -> marching Newton) on an exactly band-limited fixture."""
+    N, L = 16, 6
+    for _ in range(3):
+        e_true = O.matrix_to_euler(Rotation.random(random_state=int(rng.integers(1 << 30))).as_matrix())
+        F, H = _analytic_pair(L, N, e_true)
+        Mf = O.corr_full(F, H, L)
+        L0, K = 3, 2
+        g = O.grid_eval(Mf, L0, K)
+        idx, sc, n = O.find_maxima(g, 4)
+        eu = np.array([O.grid_node_euler(i, L0, K) if i >= 0 else np.zeros(3) for i in idx])
+        eu2, sc2, best = O.refine(Mf, [3, 4, 6, 6, 6], 1, eu, idx)
+        assert O.geodesic_deg(eu2[best], e_true) < 1e-6
+        assert sc2[best] == max(sc2)
+
+
+def test_whole_path_noise_free_voxels_c1_shape():
+    """c1 shape (32^3, L0=4 -> 8, N_C=4), planted Haar rotations, noise-free voxels, T=1."""
+    b = gen.particles(32, 3, float("inf"), seed=11)
+    P = dict(L=8, qover=2, L0=4, K=2, ncand=4, bands=[4, 6, 8], iters=1, T=1, W=0)
+    poses = O.align_batch(b.vols, b.ref, P)
+    for p in range(3):
+        err = O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p])
+        assert err < 0.1, err
+
+
+# ------------------------------------------------------------------ stage 5 translation
+def test_translation_integer_shifts_exact():
+    N = 16
+    ref = gen.render(gen.reference_blobs(), N)[0]
+    for t in [(0, 0, 0), (1, -2, 1), (3, 0, -2), (-1, 2, 3)]:
+        vol = np.roll(ref, shift=(t[2], t[1], t[0]), axis=(0, 1, 2))  # f(x) = h(x - t)
+        sh, pk = O.translation(vol, ref, [0, 0, 0], 3)
+        assert np.abs(sh - np.array(t)).max() < 1e-9
+
+
+def test_rotate_volume_identity_and_quarter_turn():
+    N = 16
+    ref = gen.render(gen.reference_blobs(), N)[0]
+    assert np.abs(O.rotate_volume(ref, [0, 0, 0]) - ref).max() < 1e-6
+    # r_z(pi/2): rho(x) = h(R^T x): rho[z, y, x] = h[z, x', y'] with x' = y - c + c, y' = -(x - c) + c
+    rho = O.rotate_volume(ref, [np.pi / 2, 0, 0])
+    exp = np.zeros_like(ref)
+    for y in range(N):
+        for x in range(N):
+            exp[:, y, x] = ref[:, N - 1 - x, y]
+    assert np.abs(rho - exp).max() < 1e-5
+
+
+@pytest.mark.slow
+def test_alternation_exact_recovery_c1():
+    """c1 exact-recovery fixture: planted g*, integer t* = (1,-2,1), 32^3, L0=4->8, T=8."""
+    b = gen.particles(32, 1, float("inf"), seed=12, shift_mode=gen.SHIFT_FIXED, fixed_shift=(1.0, -2.0, 1.0))
+    P = dict(L=8, qover=2, L0=4, K=2, ncand=4, bands=[4, 6, 8], iters=1, T=8, W=4)
+    pose = O.align_batch(b.vols, b.ref, P)[0]
+    err = O.geodesic_deg_matrix(O.euler_to_matrix(pose[:3]), b.truth_R[0])
+    assert err < 0.05, err
+    assert np.abs(pose[3:6] - b.truth_t[0]).max() < 0.01
