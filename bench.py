@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""bench.py -- particles aligned/s (box 64^3, L0=8 -> L=32, device-timed) on 1..8 B200.
+
+A "step" is one pass of the whole hot path over one batch of synthetic particles: reference
+coefficients (rank 0, broadcast over NCCL when N>1), then per particle stage 1 (shell SH analysis),
+stage 2 (Wigner coefficient tensor), stage 3 (coarse SO(3) search), stage 4 (frequency-marching
+Newton, final C_{L_J}, argmax), pose gather (all_gather over NCCL when N>1).  Weak scaling: every
+rank aligns its own --particles (default 1,000 = BASELINE configs[1], "c2").
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl matcha|reference] [--config c2|c5]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement" for the roofline arithmetic.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particles aligned/s (box 64³, L0=8→L=32, device-timed)"
+CONFIGS = {
+    # BASELINE.json configs[1] (c2) -- the metric's workload; c4 = the same shape at STA scale
+    "c2": dict(N=64, L=32, bands=[8, 12, 16, 24, 32], ncand=10, K=2, snr=0.1, particles=1000, iters=1),
+    "c4": dict(N=64, L=32, bands=[8, 12, 16, 24, 32], ncand=10, K=2, snr=0.1, particles=12500, iters=1),
+    # configs[4] (c5), high-bandwidth Newton stress
+    "c5": dict(N=128, L=64, bands=[12, 16, 24, 32, 48, 64], ncand=16, K=2, snr=0.1, particles=1000, iters=1),
+    # configs[0] (c1) rotation part, small
+    "c1": dict(N=32, L=8, bands=[4, 6, 8], ncand=4, K=2, snr=float("inf"), particles=64, iters=1),
+}
+SEED = 1
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def mh(L):
+    return (L + 1) * (L + 2) * (4 * L + 3) // 6
+
+
+def ncoef(L):
+    return (L + 1) * (L + 2) // 2
+
+
+def stage_work(c):
+    """Algorithmic (flops, bytes) per particle for each kernel."""
+    N, L, K, nc = c["N"], c["L"], c["K"], c["ncand"]
+    R, Lq = N // 2, 2 * L
+    nth, nph = Lq + 1, 2 * Lq + 2
+    Jh, Kh = (nth + 1) // 2, (nph // 2 - 1) // 2
+    samples = R * nth * nph
+    sh_fl = 20 * samples + R * nth * (L + 1) * (4 * Kh + 2) + R * Jh * ncoef(L) * 8
+    sh_by = 4 * N ** 3 + 8 * ncoef(L) * R
+    corr_fl = 8 * R * mh(L)
+    corr_by = 8 * ncoef(L) * R + 8 * mh(L)
+    L0 = c["bands"][0]
+    nb, na = K * (L0 + 1), 2 * K * (L0 + 1)
+    srch_fl = nb * (mh(L0) * 12 + (L0 + 1) * na * (2 * L0 + 1) * 8 + na * na * L0 * 4 + na * na * 26)
+    srch_by = 8 * mh(L0)
+    nw_fl = sum(c["iters"] * mh(Lj) * nc * 28 for Lj in c["bands"]) + mh(c["bands"][-1]) * nc * 8
+    nw_by = sum(c["iters"] * 8 * mh(Lj) for Lj in c["bands"]) + 8 * mh(c["bands"][-1])
+    return {"sh_analysis": (sh_fl, sh_by), "corr_coeffs": (corr_fl, corr_by), "so3_search": (srch_fl, srch_by),
+            "newton_refine": (nw_fl, nw_by), "gather_poses": (0, 48)}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.rows = []
+        self.t0 = self.t1 = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200", "-i", str(index)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, start):
+        if start:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        rows = [r for t, r in self.rows if self.t0 is not None and self.t0 - 0.2 <= t <= (self.t1 or t) + 0.2]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        rows = [r for r in rows if len(r) >= 8]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_batch(c, rank, world, P):
+    import gen
+    return gen.particles(c["N"], P, c["snr"], seed=SEED, first=rank * P)
+
+
+def oracle_params(c):
+    return dict(L=c["L"], qover=2, L0=c["bands"][0], K=c["K"], ncand=c["ncand"], bands=c["bands"],
+                iters=c["iters"], T=1, W=0)
+
+
+def time_oracle(vols, ref, c, n, nthreads):
+    import oracle as O
+    t = time.perf_counter()
+    O.align_batch(vols[:n], ref, oracle_params(c), nthreads=nthreads)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(batch, c, budget_s=20.0):
+    """The FP64 oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
+    cores = os.cpu_count() or 1
+    t1 = time_oracle(batch.vols, batch.ref, c, 1, 1)
+    n = int(max(1, min(len(batch.vols), budget_s * cores / max(t1, 1e-3))))
+    n = max(min(n, len(batch.vols)), min(cores, len(batch.vols)))
+    t = time_oracle(batch.vols, batch.ref, c, n, cores)
+    return {"value": n / t, "unit": "particles/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} of the {len(batch.vols)} {c['N']}^3 particles of this workload (same seed), "
+                      f"std::thread pool of {cores}, FP64 C++ oracle (oracle/oracle.cpp)"}
+
+
+def run_reference(args, c, rank, world):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores, rank 0 only."""
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    batch = make_batch(c, 0, 1, min(c["particles"], 4096))
+    t1 = time_oracle(batch.vols, batch.ref, c, 1, 1)
+    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    S = int(max(1, min(len(batch.vols), per_step_budget * cores / max(t1, 1e-3))))
+    for _ in range(args.warmup):
+        time_oracle(batch.vols, batch.ref, c, S, cores)
+    t = 0.0
+    for _ in range(args.steps):
+        t += time_oracle(batch.vols, batch.ref, c, S, cores)
+    value = S * args.steps / t
+    sample = (f"{S} particles per step of the {c['N']}^3 workload (same seed), std::thread pool of {cores}, "
+              "FP64 C++ oracle")
+    out = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"{args.config}: {c['N']}^3, L0={c['bands'][0]}->L={c['L']}, "
+                                  f"bands {c['bands']}, N_C={c['ncand']}, K={c['K']}, SNR {c['snr']}",
+                      "particles_per_step": S},
+           "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cores, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="matcha", choices=["matcha", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--particles", type=int, default=None, help="particles per rank (weak scaling)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_SHORT"), "W >= 3"
+    c = dict(CONFIGS[args.config])
+    if args.particles:
+        c["particles"] = args.particles
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, c, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2603_15285_b200 as mt
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = c["particles"]
+    batch = make_batch(c, rank, world, P)
+    vols_host = torch.from_numpy(batch.vols).pin_memory()
+    ref_host = torch.from_numpy(batch.ref).pin_memory()
+    vols = vols_host.to(dev)
+    ref = ref_host.to(dev)
+    h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=P)
+    params = mt.Params(bands=c["bands"], n_cand=c["ncand"], oversample=c["K"], newton_iters=c["iters"])
+    H = torch.empty((ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
+    poses = torch.empty((P, 8), dtype=torch.float32, device=dev)
+    gathered = torch.empty((P * world, 8), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def step():
+        if rank == 0:
+            h.sh_analysis(ref[None], out=H[None])          # reference coefficients (stage a3)
+        if world > 1:
+            dist.broadcast(H, src=0)                        # NCCL over NVLink: 140 KiB at c2
+        h.align_batch(vols, None, params, ref_coeffs=H, out=poses)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, poses)    # 32 B per particle
+
+    for _ in range(args.warmup):
+        step()
+    h.status()
+    torch.cuda.synchronize()
+
+    clk = ClockSampler(local)
+    time.sleep(0.3)
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = h.launches
+    h.profile_begin()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.mark(True)
+    e0.record(s)
+    for _ in range(args.steps):
+        step()
+    e1.record(s)
+    torch.cuda.synchronize()
+    clk.mark(False)
+    if world > 1:
+        dist.barrier()
+    stages = h.profile_end()
+    n_launch = h.launches - n_launch0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clocks = clk.stop()
+    h.status()
+
+    value = P * world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API on host buffers (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty((P, 8), dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            h.align_batch_host(vols_host, ref_host, params, out=out_host)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ksteps = max(3, min(args.steps, 10))
+        for _ in range(ksteps):
+            h.align_batch_host(vols_host, ref_host, params, out=out_host)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": P * world * ksteps / dt, "unit": "particles/s",
+               "h2d_bytes_per_step": int(vols_host.numel() * 4 + ref_host.numel() * 4),
+               "d2h_bytes_per_step": int(out_host.numel() * 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (live CUDA-event timing of each stage launch)
+    pk, src = peaks()
+    sm_max = (clocks or {}).get("sm_max_mhz") or pk.get("sm_max_mhz", 1965.0)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12  # FP32 FFMA pipe, TFLOP/s
+    hbm_peak = pk["hbm_gbs"]
+    work = stage_work(c)
+    tot_ms = sum(v[0] for v in stages.values())
+    dom = max(stages, key=lambda k: stages[k][0])
+    dms, dn = stages[dom]
+    # units the dominant stage processed in the timed region (sh_analysis also analyses the reference)
+    units = args.steps * (P + (1 if dom == "sh_analysis" else 0))
+    fl, by = work[dom]
+    t_stage = dms / 1e3
+    t_alu, t_hbm = fl / (alu_peak * 1e12), by / (hbm_peak * 1e9)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        tr = json.load(open(tp)).get(args.config, {}).get(dom)
+        traffic = tr
+    if t_alu >= t_hbm:
+        achieved = fl * units / t_stage / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                "frac": achieved / alu_peak, "traffic": traffic}
+    else:
+        achieved = by * units / t_stage / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic}
+    roof.update({"kernel": dom, "share_of_step": dms / tot_ms if tot_ms else None,
+                 "peak_source": (f"{nsm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (guide unit counts)"
+                                 if roof["bound"] == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({src})"),
+                 "launches": dn, "avg_launch_ms": dms / dn,
+                 "work_per_particle": {"flop": fl, "bytes": by},
+                 "hbm_gbs_achieved": by * units / t_stage / 1e9,
+                 "alu_tflops_achieved": fl * units / t_stage / 1e12,
+                 "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()}})
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(batch, c)
+
+    out = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"{args.config}: {P} particles/rank of {c['N']}^3, SNR {c['snr']}, "
+                                  f"L0={c['bands'][0]}->L={c['L']} bands {c['bands']}, N_C={c['ncand']}, "
+                                  f"K={c['K']}, 1 Newton step/band, rotation only",
+                      "particles_per_rank": P, "parallelism": f"dp{world}",
+                      "l2": f"inputs larger than L2 ({P * c['N'] ** 3 * 4 / 2**30:.2f} GiB per rank resident)"},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch, "clocks": clocks}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

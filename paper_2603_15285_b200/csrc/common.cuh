@@ -1,0 +1,109 @@
+// common.cuh -- shared device/host helpers of libmatcha (product path; no oracle code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/matcha.h"
+
+namespace matcha {
+
+// ------------------------------------------------------------------ real / complex types
+template <typename T> struct Cplx;
+template <> struct Cplx<float> { using type = float2; };
+template <> struct Cplx<double> { using type = double2; };
+template <typename T> using cplx_t = typename Cplx<T>::type;
+
+template <typename T> __host__ __device__ __forceinline__ cplx_t<T> mk(T x, T y) {
+  cplx_t<T> r;
+  r.x = x;
+  r.y = y;
+  return r;
+}
+
+// ------------------------------------------------------------------ index layouts
+__host__ __device__ __forceinline__ int ncoef(int L) { return (L + 1) * (L + 2) / 2; }
+__host__ __device__ __forceinline__ int lm_index(int l, int m) { return l * (l + 1) / 2 + m; }
+// half-plane M: (l, m in [0,l], n in [-l,l]) at half_offset(l) + m(2l+1) + (n+l)
+__host__ __device__ __forceinline__ int64_t half_offset(int l) { return (int64_t)l * (l + 1) * (4 * l - 1) / 6; }
+__host__ __device__ __forceinline__ int64_t half_size(int L) { return half_offset(L + 1); }
+// number of (m >= 0, n) pairs with max(m,|n|) <= L
+__host__ __device__ __forceinline__ int pair_count(int L) { return (L + 1) * (2 * L + 1); }
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+constexpr int kMaxL = 128;
+constexpr int kMaxCand = 32;
+
+// device error flags
+enum : int { FLAG_NONFINITE = 1, FLAG_OVERFLOW = 2 };
+
+// Stage-4 pair descriptor: (m, n) with m >= 0, grouped by shell l0 = max(m,|n|) (long l-runs first).
+// lnc = 1/2 ln C(2 l0, |m+n|) (seed normalisation), in double on the host.
+struct PairDesc {
+  int16_t m, n;
+};
+
+// ------------------------------------------------------------------ kernel argument packs
+template <typename T> struct ShTables {
+  const cplx_t<T>* node;  // [n_theta] (cos th_j, sin th_j), x_j ascending
+  const cplx_t<T>* tw;    // [n_phi] (cos phi_k, sin phi_k)
+  const T* pw;            // [Jh][ncoef] W_j Pbar_lm(x_j), j < Jh = (n_theta+1)/2 (x_j ascending)
+  int N, R, L, nth, nph, Jh;
+};
+
+template <typename T> struct NewtonArgs {
+  const cplx_t<T>* M;
+  int64_t strideM;  // Mh(L_M)
+  int L_M;
+  int64_t B;
+  int Q;                 // candidates (rotations) per particle
+  T* euler;              // [B][Q][3] in/out
+  const int32_t* idx;    // [B][Q] or null: <0 = inactive
+  // eval mode outputs
+  T* value;
+  T* grad;
+  T* hess;
+  int L_eval;
+  // refine mode
+  int nbands;
+  int bands[16];
+  int iters;
+  double tol_grad, tol_step, tol_obj;
+  T* score;
+  int32_t* best;
+  const PairDesc* pairs;
+  const T* pair_lnc;
+  int* flags;
+};
+
+template <typename T> struct SearchArgs {
+  const cplx_t<T>* M;
+  int64_t strideM;
+  int64_t B;
+  int L0, K, ncand;
+  T* euler;     // [B][ncand][3]
+  T* score;     // [B][ncand]
+  int32_t* idx; // [B][ncand]
+  const PairDesc* pairs;
+  const T* pair_lnc;
+  int* flags;
+};
+
+// ------------------------------------------------------------------ launchers (explicitly instantiated)
+template <typename T>
+cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, int shift_stride, const ShTables<T>& tab,
+                               cplx_t<T>* F, cudaStream_t s);
+template <typename T>
+cudaError_t launch_corr_coeffs(const cplx_t<T>* F, const cplx_t<T>* H, int64_t B, int L, int Lmax, int R,
+                               cplx_t<T>* M, cudaStream_t s);
+template <typename T> cudaError_t launch_so3_search(const SearchArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_eval_corr(const NewtonArgs<T>& a, bool derivs, cudaStream_t s);
+template <typename T> cudaError_t launch_newton_refine(const NewtonArgs<T>& a, cudaStream_t s);
+template <typename T>
+cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
+                                T* poses, cudaStream_t s);
+size_t search_smem_bytes(int L0, int K, bool fp64);
+
+}  // namespace matcha

@@ -1,0 +1,511 @@
+// k_newton.cu -- stage 4: evaluation of C_L, grad, Hess and the frequency-marching Newton refinement.
+//
+// PAPER.md: Eq. 4 with reading C1, C_L(g) = sum_l sum_{m,n} conj(M^l_mn) D^l_mn(g);
+// closed-form derivatives; Newton in the Euler chart;
+// Algorithm 1 lines 3-8.  Half-plane form:
+//   per (m >= 0, n) and rotation:  T0 = sum_l conj(M^l_mn) d^l,  T1 = sum_l conj(M^l_mn) d'^l,
+//   U = sum_l l(l+1) conj(M^l_mn) d^l,  T2 = -cot(b) T1 + q_mn T0 - U  (Wigner ODE for d''),
+//   q_mn = (m^2 + n^2 - 2mn cos b)/sin^2 b;  z_k = T_k e^{-i(ma+ng)}, w = 1 (m=0) or 2:
+//   C = sum w Re z0, dC/da = sum w m Im z0, dC/db = sum w Re z1, dC/dg = sum w n Im z0,
+//   H_aa = -sum w m^2 Re z0, H_gg = -sum w n^2 Re z0, H_ag = -sum w mn Re z0,
+//   H_ab = sum w m Im z1, H_bg = sum w n Im z1, H_bb = sum w Re z2.
+//
+// B200 mapping: one CTA per particle; every (m,n) pair's l-run is walked by one thread which keeps
+// CG candidates' recurrence state in registers, so each M^l_mn load (8 B) and each recurrence
+// coefficient (one rsqrt) is shared by CG candidates.  Pairs are grouped by l0 (long runs first) and
+// dealt to threads in a boustrophedon order for balance.  Block reductions are warp-shuffle butterflies
+// plus a fixed-order shared-memory pass (deterministic: no atomics).  The 3x3 Newton solve runs in FP64.
+#include <float.h>
+
+#include "common.cuh"
+#include "wigner.cuh"
+
+namespace matcha {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+template <typename T> struct CandShared {
+  T cb, sb, cot, invs2;
+  BetaLogs<T> bl;
+};
+
+struct SmemLayout {
+  // offsets in bytes
+  size_t theta, cand, ea, eg, red, sums, prevc, invl, invll, flags, total;
+};
+
+template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, int L) {
+  SmemLayout s;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 15) & ~size_t(15);
+    return r;
+  };
+  s.theta = take(sizeof(double) * 3 * Q);
+  s.cand = take(sizeof(CandShared<T>) * Q);
+  s.ea = take(sizeof(cplx_t<T>) * Q * (L + 1));
+  s.eg = take(sizeof(cplx_t<T>) * Q * (2 * L + 1));
+  s.red = take(sizeof(T) * kWarps * 10 * 8);
+  s.sums = take(sizeof(double) * 10 * Q);
+  s.prevc = take(sizeof(double) * Q);
+  s.invl = take(sizeof(T) * (kMaxL + 2));
+  s.invll = take(sizeof(T) * (kMaxL + 2));
+  s.flags = take(sizeof(int) * (2 * Q + 4));
+  s.total = o;
+  return s;
+}
+
+__device__ __forceinline__ double wrap2pi(double x) {
+  double y = fmod(x, 2.0 * kPi);
+  if (y < 0) y += 2.0 * kPi;
+  if (y >= 2.0 * kPi) y -= 2.0 * kPi;
+  return y;
+}
+
+// chart canonicalisation (reading C15)
+__device__ __forceinline__ void canon(double* e) {
+  double b = wrap2pi(e[1]);
+  double a = e[0], g = e[2];
+  if (b > kPi) {
+    b = 2.0 * kPi - b;
+    a += kPi;
+    g += kPi;
+  }
+  e[0] = wrap2pi(a);
+  e[1] = b;
+  e[2] = wrap2pi(g);
+}
+
+// largest eigenvalue of a symmetric 3x3 (aa,bb,gg,ab,ag,bg), closed-form trigonometric roots
+__device__ double sym3_lambda_max(const double* h) {
+  const double a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5];
+  const double p1 = d * d + e * e + f * f;
+  const double q = (a + b + c) / 3.0;
+  if (p1 == 0.0) return fmax(a, fmax(b, c));
+  const double p2 = (a - q) * (a - q) + (b - q) * (b - q) + (c - q) * (c - q) + 2.0 * p1;
+  const double p = sqrt(p2 / 6.0);
+  const double ba = (a - q) / p, bb = (b - q) / p, bc = (c - q) / p, bd = d / p, be = e / p, bf = f / p;
+  double r = 0.5 * (ba * (bb * bc - bf * bf) - bd * (bd * bc - bf * be) + be * (bd * bf - bb * be));
+  r = fmin(1.0, fmax(-1.0, r));
+  const double phi = acos(r) / 3.0;
+  return q + 2.0 * p * cos(phi);
+}
+
+// Newton step with the eigen-shift safeguard (reading C13): H_reg = H if lambda_max < 0,
+// else H - (lambda_max + 1e-6 ||H||_F) I; delta = -H_reg^{-1} g  (0 if H_reg is singular)
+__device__ void newton_delta(const double* g, const double* h, double* dl) {
+  const double lmax = sym3_lambda_max(h);
+  const double fro = sqrt(h[0] * h[0] + h[1] * h[1] + h[2] * h[2] + 2.0 * (h[3] * h[3] + h[4] * h[4] + h[5] * h[5]));
+  const double sh = (lmax < 0.0) ? 0.0 : (lmax + 1e-6 * fro);
+  const double a = h[0] - sh, b = h[1] - sh, c = h[2] - sh, d = h[3], e = h[4], f = h[5];
+  // symmetric [[a d e][d b f][e f c]] ; adjugate
+  const double c00 = b * c - f * f, c01 = e * f - d * c, c02 = d * f - b * e;
+  const double c11 = a * c - e * e, c12 = d * e - a * f, c22 = a * b - d * d;
+  const double det = a * c00 + d * c01 + e * c02;
+  if (det == 0.0 || !isfinite(det)) {
+    dl[0] = dl[1] = dl[2] = 0.0;
+    return;
+  }
+  const double inv = 1.0 / det;
+  dl[0] = -(c00 * g[0] + c01 * g[1] + c02 * g[2]) * inv;
+  dl[1] = -(c01 * g[0] + c11 * g[1] + c12 * g[2]) * inv;
+  dl[2] = -(c02 * g[0] + c12 * g[1] + c22 * g[2]) * inv;
+}
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Prepare per-rotation shared data for candidates [0, Q): trig of beta and phase tables.
+template <typename T>
+__device__ void prepare_candidates(const double* theta, int Q, int L, CandShared<T>* cs, cplx_t<T>* ea,
+                                   cplx_t<T>* eg) {
+  for (int c = threadIdx.x; c < Q; c += blockDim.x) {
+    const double b = theta[3 * c + 1];
+    double sb = sin(b), cb = cos(b);
+    double sbc = fmax(fabs(sb), 1e-6);  // reading C16: clamp in cot b and 1/sin^2 b
+    CandShared<T> s;
+    s.cb = (T)cb;
+    s.sb = (T)sb;
+    s.cot = (T)(cb / sbc);
+    s.invs2 = (T)(1.0 / (sbc * sbc));
+    s.bl = beta_logs<T>(b);
+    cs[c] = s;
+  }
+  // e^{-i m a} (m = 0..L), e^{-i n g} (n = -L..L), phases reduced in FP64
+  const int na = L + 1, ng = 2 * L + 1;
+  for (int t = threadIdx.x; t < Q * (na + ng); t += blockDim.x) {
+    const int c = t / (na + ng), r = t % (na + ng);
+    double ph;
+    if (r < na) ph = -(double)r * theta[3 * c + 0];
+    else ph = -(double)(r - na - L) * theta[3 * c + 2];
+    ph = fmod(ph, 2.0 * kPi);
+    double s, co;
+    sincos(ph, &s, &co);
+    if (r < na) ea[c * na + r] = mk<T>((T)co, (T)s);
+    else eg[c * ng + (r - na)] = mk<T>((T)co, (T)s);
+  }
+}
+
+// Evaluate C_L (and, if DERIV, grad and Hess) at rotations [0,Q) -> sums[c][10] (FP64 in smem).
+template <typename T, int CG, bool DERIV>
+__device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const PairDesc* __restrict__ pairs,
+                           const T* __restrict__ pair_lnc, const CandShared<T>* cs, const cplx_t<T>* ea,
+                           const cplx_t<T>* eg, const T* inv_l, const T* inv_ll, T* red, double* sums) {
+  constexpr int NV = DERIV ? 10 : 1;
+  const int npairs = pair_count(L);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int na = L + 1, ng = 2 * L + 1;
+  for (int c0 = 0; c0 < Q; c0 += CG) {
+    T acc[NV][CG];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int k = 0; k < CG; ++k) acc[v][k] = T(0);
+    // candidate indices of this group (clamped: duplicates of the last are computed, then ignored)
+    int cid[CG];
+#pragma unroll
+    for (int k = 0; k < CG; ++k) cid[k] = min(c0 + k, Q - 1);
+
+    for (int r = 0;; ++r) {
+      const int base = r * kThreads;
+      if (base >= npairs) break;
+      const int pi = base + ((r & 1) ? (kThreads - 1 - tid) : tid);
+      if (pi >= npairs) continue;
+      const PairDesc pd = pairs[pi];
+      const int m = pd.m, n = pd.n;
+      const int l0 = max(m, abs(n));
+      const T lnC = pair_lnc[pi];
+      const int mn = m * n, m2 = m * m, n2 = n * n;
+      // recurrence state
+      T d[CG], dprev[CG], dp[CG], dpprev[CG];
+      T t0r[CG], t0i[CG], t1r[CG], t1i[CG], ur[CG], ui[CG];
+#pragma unroll
+      for (int k = 0; k < CG; ++k) {
+        T dd, ddp = T(0);
+        wigner_seed<T, DERIV>(m, n, lnC, cs[cid[k]].bl, dd, ddp);
+        d[k] = dd;
+        dp[k] = ddp;
+        dprev[k] = T(0);
+        dpprev[k] = T(0);
+        t0r[k] = t0i[k] = t1r[k] = t1i[k] = ur[k] = ui[k] = T(0);
+      }
+      T cbk[CG], sbk[CG];
+#pragma unroll
+      for (int k = 0; k < CG; ++k) {
+        cbk[k] = cs[cid[k]].cb;
+        sbk[k] = cs[cid[k]].sb;
+      }
+      int64_t off = half_offset(l0) + (int64_t)m * (2 * l0 + 1) + (n + l0);
+      T sq = T(0);
+      for (int l = l0;; ++l) {
+        const cplx_t<T> Ml = __ldg(&M[off]);
+        const T mr = Ml.x, mi = Ml.y;  // conj(M) = (mr, -mi)
+#pragma unroll
+        for (int k = 0; k < CG; ++k) {
+          t0r[k] = fma(mr, d[k], t0r[k]);
+          t0i[k] = fma(-mi, d[k], t0i[k]);
+        }
+        if (DERIV) {
+          const T ll = (T)(l * (l + 1));
+          const T umr = ll * mr, umi = ll * mi;
+#pragma unroll
+          for (int k = 0; k < CG; ++k) {
+            t1r[k] = fma(mr, dp[k], t1r[k]);
+            t1i[k] = fma(-mi, dp[k], t1i[k]);
+            ur[k] = fma(umr, d[k], ur[k]);
+            ui[k] = fma(-umi, d[k], ui[k]);
+          }
+        }
+        if (l == L) break;
+        T A, Bc, Cc;
+        rec_coef<T>(l, mn, m2, n2, inv_l, inv_ll, A, Bc, Cc, sq);
+#pragma unroll
+        for (int k = 0; k < CG; ++k) {
+          const T x = A * d[k];
+          const T dn = fma(x, cbk[k], -fma(Bc, d[k], Cc * dprev[k]));
+          if (DERIV) {
+            const T y = fma(cbk[k], dp[k], -sbk[k] * d[k]);
+            const T dpn = fma(A, y, -fma(Bc, dp[k], Cc * dpprev[k]));
+            dpprev[k] = dp[k];
+            dp[k] = dpn;
+          }
+          dprev[k] = d[k];
+          d[k] = dn;
+        }
+        off += (int64_t)(l + 1) * (2 * l + 1) + 2 * m + 1;
+      }
+      // assembly with the phase e^{-i(m a + n g)}
+      const T w = (m == 0) ? T(1) : T(2);
+      const T fm = (T)m, fn = (T)n;
+#pragma unroll
+      for (int k = 0; k < CG; ++k) {
+        const cplx_t<T> pa = ea[cid[k] * na + m], pg = eg[cid[k] * ng + (n + L)];
+        const T er = pa.x * pg.x - pa.y * pg.y, ei = pa.x * pg.y + pa.y * pg.x;
+        const T z0r = t0r[k] * er - t0i[k] * ei, z0i = t0r[k] * ei + t0i[k] * er;
+        acc[0][k] = fma(w, z0r, acc[0][k]);
+        if (DERIV) {
+          const CandShared<T>& c = cs[cid[k]];
+          const T z1r = t1r[k] * er - t1i[k] * ei, z1i = t1r[k] * ei + t1i[k] * er;
+          const T qmn = ((T)(m2 + n2) - T(2) * (T)mn * c.cb) * c.invs2;
+          const T t2r = -c.cot * t1r[k] + qmn * t0r[k] - ur[k];
+          const T t2i = -c.cot * t1i[k] + qmn * t0i[k] - ui[k];
+          const T z2r = t2r * er - t2i * ei;
+          const T wz0 = w * z0r;
+          acc[1][k] = fma(w * fm, z0i, acc[1][k]);
+          acc[2][k] = fma(w, z1r, acc[2][k]);
+          acc[3][k] = fma(w * fn, z0i, acc[3][k]);
+          acc[4][k] = fma(-fm * fm, wz0, acc[4][k]);
+          acc[5][k] = fma(w, z2r, acc[5][k]);
+          acc[6][k] = fma(-fn * fn, wz0, acc[6][k]);
+          acc[7][k] = fma(w * fm, z1i, acc[7][k]);
+          acc[8][k] = fma(-fm * fn, wz0, acc[8][k]);
+          acc[9][k] = fma(w * fn, z1i, acc[9][k]);
+        }
+      }
+    }
+    // deterministic block reduction: warp butterflies, then fixed-order sum over warps
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int k = 0; k < CG; ++k) {
+        const T s = warp_sum(acc[v][k]);
+        if (lane == 0) red[warp * (NV * CG) + v * CG + k] = s;
+      }
+    __syncthreads();
+    if (tid < NV * CG) {
+      const int v = tid / CG, k = tid % CG;
+      double s = 0.0;
+      for (int wi = 0; wi < kWarps; ++wi) s += (double)red[wi * (NV * CG) + v * CG + k];
+      if (c0 + k < Q) sums[(c0 + k) * 10 + v] = s;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__device__ void load_inv_tables(T* inv_l, T* inv_ll) {
+  for (int l = threadIdx.x; l <= kMaxL + 1; l += blockDim.x) {
+    inv_l[l] = l ? (T)(1.0 / l) : T(0);
+    inv_ll[l] = l ? (T)(1.0 / ((double)l * (l + 1))) : T(0);
+  }
+}
+
+// ------------------------------------------------------------------ matcha_eval_corr kernel
+template <typename T, int CG>
+__global__ void __launch_bounds__(kThreads) k_eval_corr(NewtonArgs<T> a, bool derivs) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L = a.L_eval, Q = a.Q;
+  const SmemLayout lay = smem_layout<T>(Q, L);
+  double* theta = (double*)(smem + lay.theta);
+  CandShared<T>* cs = (CandShared<T>*)(smem + lay.cand);
+  cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
+  cplx_t<T>* eg = (cplx_t<T>*)(smem + lay.eg);
+  T* red = (T*)(smem + lay.red);
+  double* sums = (double*)(smem + lay.sums);
+  T* inv_l = (T*)(smem + lay.invl);
+  T* inv_ll = (T*)(smem + lay.invll);
+  const int64_t p = blockIdx.x;
+  const cplx_t<T>* M = a.M + p * a.strideM;
+  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) theta[t] = (double)a.euler[p * Q * 3 + t];
+  load_inv_tables(inv_l, inv_ll);
+  __syncthreads();
+  prepare_candidates<T>(theta, Q, L, cs, ea, eg);
+  __syncthreads();
+  if (derivs) eval_block<T, CG, true>(M, L, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+  else eval_block<T, CG, false>(M, L, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+  for (int c = threadIdx.x; c < Q; c += blockDim.x) {
+    const double* s = sums + c * 10;
+    a.value[p * Q + c] = (T)s[0];
+    if (!isfinite(s[0])) atomicOr(a.flags, FLAG_NONFINITE);
+    if (derivs) {
+      if (a.grad)
+        for (int k = 0; k < 3; ++k) a.grad[(p * Q + c) * 3 + k] = (T)s[1 + k];
+      if (a.hess)
+        for (int k = 0; k < 6; ++k) a.hess[(p * Q + c) * 6 + k] = (T)s[4 + k];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ matcha_newton_refine kernel
+template <typename T, int CG>
+__global__ void __launch_bounds__(kThreads) k_newton_refine(NewtonArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Q = a.Q;
+  const int Lmax_b = a.bands[a.nbands - 1];
+  const SmemLayout lay = smem_layout<T>(Q, Lmax_b);
+  double* theta = (double*)(smem + lay.theta);
+  CandShared<T>* cs = (CandShared<T>*)(smem + lay.cand);
+  cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
+  cplx_t<T>* eg = (cplx_t<T>*)(smem + lay.eg);
+  T* red = (T*)(smem + lay.red);
+  double* sums = (double*)(smem + lay.sums);
+  T* inv_l = (T*)(smem + lay.invl);
+  T* inv_ll = (T*)(smem + lay.invll);
+  double* prevc = (double*)(smem + lay.prevc);
+  int* act = (int*)(smem + lay.flags);   // [Q] active (not padding)
+  int* run = act + Q;                    // [Q] still iterating in this band
+  int* any = run + Q;                    // [1]
+  const int64_t p = blockIdx.x;
+  const cplx_t<T>* M = a.M + p * a.strideM;
+  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) theta[t] = (double)a.euler[p * Q * 3 + t];
+  for (int c = threadIdx.x; c < Q; c += blockDim.x) act[c] = a.idx ? (a.idx[p * Q + c] >= 0) : 1;
+  load_inv_tables(inv_l, inv_ll);
+  __syncthreads();
+  for (int j = 0; j < a.nbands; ++j) {
+    const int L = a.bands[j];
+    for (int c = threadIdx.x; c < Q; c += blockDim.x) run[c] = act[c];
+    for (int s = 0; s < a.iters; ++s) {
+      if (threadIdx.x == 0) {
+        int x = 0;
+        for (int c = 0; c < Q; ++c) x |= run[c];
+        *any = x;
+      }
+      __syncthreads();
+      if (!*any) break;
+      prepare_candidates<T>(theta, Q, L, cs, ea, eg);
+      __syncthreads();
+      eval_block<T, CG, true>(M, L, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+      for (int c = threadIdx.x; c < Q; c += blockDim.x) {
+        if (!run[c]) continue;
+        const double* sm = sums + c * 10;
+        bool fin = true;
+        for (int k = 0; k < 10; ++k) fin = fin && isfinite(sm[k]);
+        if (!fin) {
+          atomicOr(a.flags, FLAG_NONFINITE);
+          run[c] = 0;
+          continue;
+        }
+        const double C = sm[0];
+        const double gn = sqrt(sm[1] * sm[1] + sm[2] * sm[2] + sm[3] * sm[3]);
+        if (a.tol_grad > 0 && gn < a.tol_grad * fabs(C)) { run[c] = 0; continue; }
+        if (s > 0 && a.tol_obj > 0 && fabs(C - prevc[c]) < a.tol_obj * fabs(C)) { run[c] = 0; continue; }
+        prevc[c] = C;
+        double dl[3];
+        newton_delta(sm + 1, sm + 4, dl);
+        double* th = theta + 3 * c;
+        th[0] += dl[0];
+        th[1] += dl[1];
+        th[2] += dl[2];
+        canon(th);
+        const double dn = sqrt(dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]);
+        if (a.tol_step > 0 && dn < a.tol_step) run[c] = 0;
+      }
+      __syncthreads();
+    }
+  }
+  // final C_{L_J} of every candidate and the argmax
+  prepare_candidates<T>(theta, Q, Lmax_b, cs, ea, eg);
+  __syncthreads();
+  eval_block<T, CG, false>(M, Lmax_b, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) a.euler[p * Q * 3 + t] = (T)theta[t];
+  for (int c = threadIdx.x; c < Q; c += blockDim.x) {
+    const double v = act[c] ? sums[c * 10] : -INFINITY;
+    a.score[p * Q + c] = (T)v;
+    if (act[c] && !isfinite(v)) atomicOr(a.flags, FLAG_NONFINITE);
+  }
+  if (threadIdx.x == 0) {
+    int b = -1;
+    double bv = -INFINITY;
+    for (int c = 0; c < Q; ++c)
+      if (act[c] && (b < 0 || sums[c * 10] > bv)) {
+        b = c;
+        bv = sums[c * 10];
+      }
+    a.best[p] = b;
+  }
+}
+
+template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a, bool derivs, cudaStream_t s) {
+  const SmemLayout lay = smem_layout<T>(a.Q, a.L_eval);
+  cudaError_t e = cudaFuncSetAttribute(k_eval_corr<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
+  if (e != cudaSuccess) return e;
+  k_eval_corr<T, CG><<<(unsigned)a.B, kThreads, lay.total, s>>>(a, derivs);
+  return cudaGetLastError();
+}
+
+template <typename T, int CG> cudaError_t launch_newton_cg(const NewtonArgs<T>& a, cudaStream_t s) {
+  const SmemLayout lay = smem_layout<T>(a.Q, a.bands[a.nbands - 1]);
+  cudaError_t e =
+      cudaFuncSetAttribute(k_newton_refine<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
+  if (e != cudaSuccess) return e;
+  k_newton_refine<T, CG><<<(unsigned)a.B, kThreads, lay.total, s>>>(a);
+  return cudaGetLastError();
+}
+
+// candidate-group size: registers hold 10*CG recurrence values and 10*CG accumulators per thread
+template <typename T> int pick_cg(int Q) {
+  if (sizeof(T) == 8) return Q >= 2 ? 2 : 1;
+  if (Q <= 2) return Q;
+  if (Q <= 4) return 4;
+  if (Q % 5 == 0 || Q == 9) return 5;
+  return 4;
+}
+
+}  // namespace
+
+template <typename T> cudaError_t launch_eval_corr(const NewtonArgs<T>& a, bool derivs, cudaStream_t s) {
+  if (a.B == 0 || a.Q == 0) return cudaSuccess;
+  switch (pick_cg<T>(a.Q)) {
+    case 1: return launch_eval_cg<T, 1>(a, derivs, s);
+    case 2: return launch_eval_cg<T, 2>(a, derivs, s);
+    case 4: return launch_eval_cg<T, 4>(a, derivs, s);
+    default: return launch_eval_cg<T, 5>(a, derivs, s);
+  }
+}
+
+template <typename T> cudaError_t launch_newton_refine(const NewtonArgs<T>& a, cudaStream_t s) {
+  if (a.B == 0 || a.Q == 0) return cudaSuccess;
+  switch (pick_cg<T>(a.Q)) {
+    case 1: return launch_newton_cg<T, 1>(a, s);
+    case 2: return launch_newton_cg<T, 2>(a, s);
+    case 4: return launch_newton_cg<T, 4>(a, s);
+    default: return launch_newton_cg<T, 5>(a, s);
+  }
+}
+
+template cudaError_t launch_eval_corr<float>(const NewtonArgs<float>&, bool, cudaStream_t);
+template cudaError_t launch_eval_corr<double>(const NewtonArgs<double>&, bool, cudaStream_t);
+template cudaError_t launch_newton_refine<float>(const NewtonArgs<float>&, cudaStream_t);
+template cudaError_t launch_newton_refine<double>(const NewtonArgs<double>&, cudaStream_t);
+
+// poses[b] = {alpha, beta, gamma, (shift untouched), score, best}
+template <typename T>
+__global__ void k_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
+                               T* poses) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int k = best[b];
+  T* o = poses + b * 8;
+  if (k >= 0) {
+    o[0] = euler[(b * Q + k) * 3 + 0];
+    o[1] = euler[(b * Q + k) * 3 + 1];
+    o[2] = euler[(b * Q + k) * 3 + 2];
+    o[6] = score[b * Q + k];
+  } else {
+    o[0] = o[1] = o[2] = T(0);
+    o[6] = -INFINITY;
+  }
+  if (zero_shift) o[3] = o[4] = o[5] = T(0);
+  o[7] = (T)k;
+}
+
+template <typename T>
+cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
+                                T* poses, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  k_gather_poses<T><<<(unsigned)((B + 127) / 128), 128, 0, s>>>(euler, score, best, B, Q, zero_shift, poses);
+  return cudaGetLastError();
+}
+template cudaError_t launch_gather_poses<float>(const float*, const float*, const int32_t*, int64_t, int, bool,
+                                                float*, cudaStream_t);
+template cudaError_t launch_gather_poses<double>(const double*, const double*, const int32_t*, int64_t, int, bool,
+                                                 double*, cudaStream_t);
+
+}  // namespace matcha

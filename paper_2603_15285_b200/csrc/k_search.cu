@@ -1,0 +1,280 @@
+// k_search.cu -- stage 3: coarse exhaustive SO(3) search of C_{L0} and top-N_C local maxima.
+//
+// north_star stage (3); PAPER.md P:147-151 (SOFFT grid of O((K L0)^3) points, N_C strongest local maxima),
+// Algorithm 1 lines 1-2; readings C9 (grid), C10-C11 (local maxima, ties, padding).
+// Per beta slice j:
+//   X_{j,mn} = sum_{l=max(m,|n|)}^{L0} conj(M^l_mn) d^l_mn(beta_j)       (Wigner-d contraction)
+//   C(alpha_a, beta_j, gamma_c) = Re Y_{0,c} + 2 Re sum_{m>=1} Y_{m,c} e^{-i m alpha_a},
+//   Y_{m,c} = sum_n X_{j,mn} e^{-i n gamma_c}                             (separable 2-D DFT, Hermitian X)
+//
+// B200 mapping: one CTA per particle.  M(l <= L0) is staged in shared memory (4 KiB at L0 = 8); d is
+// produced on the fly by the l-recurrence (no table traffic); the grid is never materialised: a rolling
+// 3-slice window in shared memory feeds the 26-neighbour test of slice j-1 while slice j is computed, so
+// L0 = 12 (70k nodes, 275 KiB) needs no cluster.  Maxima go to a shared list; the N_C winners are chosen
+// by an order-independent block arg-max on (score desc, index asc) -- deterministic.
+#include "common.cuh"
+#include "wigner.cuh"
+
+namespace matcha {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kCap = 2048;
+
+struct SearchLayout {
+  size_t Ms, X, Y, sl, tw, cs, cs_idx, invl, invll, misc, red_s, red_i, total;
+};
+
+template <typename T> __host__ __device__ inline SearchLayout search_layout(int L0, int K) {
+  const int nb = K * (L0 + 1), na = 2 * K * (L0 + 1);
+  (void)nb;
+  SearchLayout s;
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t r = o;
+    o += (b + 15) & ~size_t(15);
+    return r;
+  };
+  s.Ms = take(sizeof(cplx_t<T>) * half_size(L0));
+  s.X = take(sizeof(cplx_t<T>) * (L0 + 1) * (2 * L0 + 1));
+  s.Y = take(sizeof(cplx_t<T>) * (L0 + 1) * na);
+  s.sl = take(sizeof(T) * 3 * na * na);
+  s.tw = take(sizeof(cplx_t<T>) * na);
+  s.cs = take(sizeof(T) * kCap);
+  s.cs_idx = take(sizeof(int) * kCap);
+  s.invl = take(sizeof(T) * (kMaxL + 2));
+  s.invll = take(sizeof(T) * (kMaxL + 2));
+  s.misc = take(sizeof(T) * 8 + sizeof(int) * 8);
+  s.red_s = take(sizeof(T) * kWarps);
+  s.red_i = take(sizeof(int) * kWarps);
+  s.total = o;
+  return s;
+}
+
+// key order: (score desc, index asc); returns true if (s1,i1) ranks before (s2,i2)
+template <typename T> __device__ __forceinline__ bool before(T s1, int i1, T s2, int i2) {
+  return s1 > s2 || (s1 == s2 && i1 < i2);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L0 = a.L0, K = a.K;
+  const int nb = K * (L0 + 1), na = 2 * K * (L0 + 1), ng = na;
+  const SearchLayout lay = search_layout<T>(L0, K);
+  cplx_t<T>* Ms = (cplx_t<T>*)(smem + lay.Ms);
+  cplx_t<T>* X = (cplx_t<T>*)(smem + lay.X);
+  cplx_t<T>* Y = (cplx_t<T>*)(smem + lay.Y);
+  T* sl = (T*)(smem + lay.sl);
+  cplx_t<T>* tw = (cplx_t<T>*)(smem + lay.tw);
+  T* cs = (T*)(smem + lay.cs);
+  int* ci = (int*)(smem + lay.cs_idx);
+  T* inv_l = (T*)(smem + lay.invl);
+  T* inv_ll = (T*)(smem + lay.invll);
+  T* bsh = (T*)(smem + lay.misc);                 // [0]=cos b, [1]=lnc, [2]=lns
+  int* cnt = (int*)(smem + lay.misc + sizeof(T) * 8);
+  T* red_s = (T*)(smem + lay.red_s);
+  int* red_i = (int*)(smem + lay.red_i);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t p = blockIdx.x;
+
+  const cplx_t<T>* Mp = a.M + p * a.strideM;
+  for (int t = tid; t < half_size(L0); t += kThreads) Ms[t] = Mp[t];
+  for (int t = tid; t < na; t += kThreads) {
+    double s, c;
+    sincospi(2.0 * t / na, &s, &c);
+    tw[t] = mk<T>((T)c, (T)(-s));  // e^{-2 pi i t/na}
+  }
+  for (int l = tid; l <= kMaxL + 1; l += kThreads) {
+    inv_l[l] = l ? (T)(1.0 / l) : T(0);
+    inv_ll[l] = l ? (T)(1.0 / ((double)l * (l + 1))) : T(0);
+  }
+  if (tid == 0) *cnt = 0;
+  __syncthreads();
+
+  const int npairs = pair_count(L0);
+  const int w0 = 2 * L0 + 1;
+  auto test_slice = [&](int jj) {
+    const T* cur = sl + (jj % 3) * na * ng;
+    for (int t = tid; t < na * ng; t += kThreads) {
+      const int aa = t / ng, c = t - aa * ng;
+      const T vp = cur[t];
+      const int ip = (jj * na + aa) * ng + c;
+      bool ok = true;
+      for (int dj = -1; dj <= 1 && ok; ++dj) {
+        const int j2 = jj + dj;
+        if (j2 < 0 || j2 >= nb) continue;
+        const T* s2 = sl + (j2 % 3) * na * ng;
+        for (int da = -1; da <= 1 && ok; ++da) {
+          const int a2 = (aa + da + na) % na;
+          for (int dc = -1; dc <= 1; ++dc) {
+            if (!dj && !da && !dc) continue;
+            const int c2 = (c + dc + ng) % ng;
+            const int iq = (j2 * na + a2) * ng + c2;
+            if (iq == ip) continue;
+            const T vq = s2[a2 * ng + c2];
+            if (!before(vp, ip, vq, iq)) {
+              ok = false;
+              break;
+            }
+          }
+        }
+      }
+      if (ok) {
+        const int slot = atomicAdd(cnt, 1);
+        if (slot < kCap) {
+          cs[slot] = vp;
+          ci[slot] = ip;
+        } else {
+          atomicOr(a.flags, FLAG_OVERFLOW);
+        }
+      }
+    }
+  };
+
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      const double beta = (j + 0.5) * kPi / nb;
+      const BetaLogs<T> bl = beta_logs<T>(beta);
+      bsh[0] = (T)cos(beta);
+      bsh[1] = bl.lnc;
+      bsh[2] = bl.lns;
+    }
+    __syncthreads();
+    const T cb = bsh[0];
+    BetaLogs<T> bl;
+    bl.lnc = bsh[1];
+    bl.lns = bsh[2];
+    // X_{j,mn}
+    for (int pi = tid; pi < npairs; pi += kThreads) {
+      const PairDesc pd = a.pairs[pi];
+      const int m = pd.m, n = pd.n, l0 = max(m, abs(n));
+      T d, dd, dprev = T(0), sq = T(0);
+      wigner_seed<T, false>(m, n, a.pair_lnc[pi], bl, d, dd);
+      T xr = T(0), xi = T(0);
+      int off = (int)half_offset(l0) + m * (2 * l0 + 1) + (n + l0);
+      for (int l = l0;; ++l) {
+        const cplx_t<T> Ml = Ms[off];
+        xr = fma(Ml.x, d, xr);
+        xi = fma(-Ml.y, d, xi);
+        if (l == L0) break;
+        T A, Bc, Cc;
+        rec_coef<T>(l, m * n, m * m, n * n, inv_l, inv_ll, A, Bc, Cc, sq);
+        const T dn = fma(A * d, cb, -fma(Bc, d, Cc * dprev));
+        dprev = d;
+        d = dn;
+        off += (l + 1) * (2 * l + 1) + 2 * m + 1;
+      }
+      X[m * w0 + (n + L0)] = mk<T>(xr, xi);
+    }
+    __syncthreads();
+    // Y_{m,c} = sum_n X_mn e^{-i n gamma_c}
+    for (int t = tid; t < (L0 + 1) * ng; t += kThreads) {
+      const int m = t / ng, c = t - m * ng;
+      T yr = T(0), yi = T(0);
+      for (int n = -L0; n <= L0; ++n) {
+        const cplx_t<T> x = X[m * w0 + (n + L0)];
+        int k = (n * c) % ng;
+        if (k < 0) k += ng;
+        const cplx_t<T> e = tw[k];
+        yr = fma(x.x, e.x, fma(-x.y, e.y, yr));
+        yi = fma(x.x, e.y, fma(x.y, e.x, yi));
+      }
+      Y[m * ng + c] = mk<T>(yr, yi);
+    }
+    __syncthreads();
+    // C(alpha_a, beta_j, gamma_c)
+    T* cur = sl + (j % 3) * na * ng;
+    for (int t = tid; t < na * ng; t += kThreads) {
+      const int aa = t / ng, c = t - aa * ng;
+      T s = Y[c].x;
+      T s2 = T(0);
+      int k = 0;
+      for (int m = 1; m <= L0; ++m) {
+        k += aa;
+        if (k >= na) k -= na;
+        const cplx_t<T> y = Y[m * ng + c], e = tw[k];
+        s2 = fma(y.x, e.x, fma(-y.y, e.y, s2));
+      }
+      cur[t] = fma(T(2), s2, s);
+    }
+    __syncthreads();
+    if (j >= 1) test_slice(j - 1);
+    __syncthreads();
+  }
+  test_slice(nb - 1);
+  __syncthreads();
+
+  // top-N_C selection by (score desc, index asc)
+  const int total = min(*cnt, kCap);
+  for (int k = 0; k < a.ncand; ++k) {
+    T bs = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int t = tid; t < total; t += kThreads)
+      if (ci[t] >= 0 && before(cs[t], ci[t], bs, bi)) {
+        bs = cs[t];
+        bi = ci[t];
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (before(s2, i2, bs, bi)) {
+        bs = s2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      red_s[warp] = bs;
+      red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      T s = red_s[0];
+      int i = red_i[0];
+      for (int w = 1; w < kWarps; ++w)
+        if (before(red_s[w], red_i[w], s, i)) {
+          s = red_s[w];
+          i = red_i[w];
+        }
+      const int64_t o = p * a.ncand + k;
+      if (i != 0x7fffffff) {
+        const int c = i % ng, aa = (i / ng) % na, jj = i / (ng * na);
+        a.euler[o * 3 + 0] = (T)(2.0 * kPi * aa / na);
+        a.euler[o * 3 + 1] = (T)((jj + 0.5) * kPi / nb);
+        a.euler[o * 3 + 2] = (T)(2.0 * kPi * c / ng);
+        a.score[o] = s;
+        a.idx[o] = i;
+        for (int t = 0; t < total; ++t)
+          if (ci[t] == i) ci[t] = -1;  // taken
+      } else {
+        a.euler[o * 3 + 0] = a.euler[o * 3 + 1] = a.euler[o * 3 + 2] = T(0);
+        a.score[o] = -INFINITY;
+        a.idx[o] = -1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+template <typename T> cudaError_t launch_so3_search(const SearchArgs<T>& a, cudaStream_t s) {
+  if (a.B == 0) return cudaSuccess;
+  const size_t bytes = search_layout<T>(a.L0, a.K).total;
+  cudaError_t e = cudaFuncSetAttribute(k_so3_search<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  k_so3_search<T><<<(unsigned)a.B, kThreads, bytes, s>>>(a);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_so3_search<float>(const SearchArgs<float>&, cudaStream_t);
+template cudaError_t launch_so3_search<double>(const SearchArgs<double>&, cudaStream_t);
+
+size_t search_smem_bytes(int L0, int K, bool fp64) {
+  return fp64 ? search_layout<double>(L0, K).total : search_layout<float>(L0, K).total;
+}
+
+}  // namespace matcha

@@ -1,0 +1,623 @@
+// matcha.cu -- host side of libmatcha: handle, FP64 table construction, C-ABI entry points and the
+// align orchestration (App. C alternation around Algorithm 1, chunked over particles, one stream).
+//
+// Tables are computed here in double precision (own Gauss-Legendre Newton solve and normalised
+// associated-Legendre recurrence; no code is shared with oracle/) and cast to the handle precision.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace matcha;
+
+struct matcha_ctx {
+  matcha_config_t cfg;
+  int device = 0;
+  bool fp64 = false;
+  size_t rsz = 4;  // sizeof(real)
+  int R = 0, L = 0, Lq = 0, nth = 0, nph = 0, Jh = 0, ncf = 0;
+  void* d_node = nullptr;
+  void* d_tw = nullptr;
+  void* d_pw = nullptr;
+  PairDesc* d_pairs = nullptr;
+  void* d_pair_lnc = nullptr;
+  int* d_flags = nullptr;
+  // align workspace (sized by max_batch)
+  void* ws_F = nullptr;
+  void* ws_M = nullptr;
+  void* ws_H = nullptr;
+  void* ws_euler = nullptr;
+  void* ws_score = nullptr;
+  int32_t* ws_idx = nullptr;
+  int32_t* ws_best = nullptr;
+  // host-buffer path
+  float* ws_vols[2] = {nullptr, nullptr};
+  void* ws_poses = nullptr;
+  float* ws_ref = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_used[2] = {nullptr, nullptr};
+  int64_t launches = 0;
+  std::string err;
+  // per-stage event tracing
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_stage;  // stage of event pair k (events 2k, 2k+1)
+  size_t ev_next = 0;
+};
+
+namespace {
+
+matcha_status_t fail(matcha_handle_t h, matcha_status_t s, const std::string& msg) {
+  if (h) h->err = msg;
+  return s;
+}
+
+matcha_status_t cuda_fail(matcha_handle_t h, cudaError_t e, const char* where) {
+  return fail(h, MATCHA_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MATCHA_CUDA(h, expr)                          \
+  do {                                                \
+    cudaError_t _e = (expr);                          \
+    if (_e != cudaSuccess) return cuda_fail(h, _e, #expr); \
+  } while (0)
+
+// ---------------------------------------------------------------- FP64 tables (host)
+// Gauss-Legendre nodes on [-1,1], ascending, by Newton iteration on P_n from Tricomi's initial guess.
+void gl_nodes(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int k = 1; k <= n; ++k) {
+    const double th = kPi * (4.0 * k - 1.0) / (4.0 * n + 2.0);
+    double z = (1.0 - (n - 1.0) / (8.0 * n * n * n)) * std::cos(th);
+    double dp = 1.0;
+    for (int it = 0; it < 60; ++it) {
+      double pm = 1.0, p = z;  // P_0, P_1
+      for (int j = 1; j < n; ++j) {
+        const double pn = ((2.0 * j + 1.0) * z * p - j * pm) / (j + 1.0);
+        pm = p;
+        p = pn;
+      }
+      if (n == 1) { p = z; pm = 1.0; }
+      dp = n * (pm - z * p) / (1.0 - z * z);
+      const double dz = p / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-15 * std::max(1.0, std::fabs(z))) {
+        // refresh derivative at the converged point
+        double qm = 1.0, q = z;
+        for (int j = 1; j < n; ++j) {
+          const double qn = ((2.0 * j + 1.0) * z * q - j * qm) / (j + 1.0);
+          qm = q;
+          q = qn;
+        }
+        if (n == 1) { q = z; qm = 1.0; }
+        dp = n * (qm - z * q) / (1.0 - z * z);
+        break;
+      }
+    }
+    x[n - k] = z;  // k = 1 is the largest root
+    w[n - k] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+// normalised associated Legendre Pbar_lm(x) (Condon-Shortley phase), all 0 <= m <= l <= L
+void plm_table(int L, double x, std::vector<double>& out) {
+  out.assign(ncoef(L), 0.0);
+  const double s = std::sqrt(std::max(0.0, (1.0 - x) * (1.0 + x)));
+  double diag = 0.5 / std::sqrt(kPi);  // Pbar_00 = 1/sqrt(4 pi)
+  for (int m = 0; m <= L; ++m) {
+    if (m) diag *= -s * std::sqrt((2.0 * m + 1.0) / (2.0 * m));
+    double p2 = diag;
+    out[lm_index(m, m)] = p2;
+    if (m == L) break;
+    double p1 = x * std::sqrt(2.0 * m + 3.0) * diag;
+    out[lm_index(m + 1, m)] = p1;
+    for (int l = m + 2; l <= L; ++l) {
+      const double l2 = (double)l * l, m2 = (double)m * m;
+      const double a = std::sqrt((4.0 * l2 - 1.0) / (l2 - m2));
+      const double b = std::sqrt(((l - 1.0) * (l - 1.0) - m2) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
+      const double p = a * (x * p1 - b * p2);
+      out[lm_index(l, m)] = p;
+      p2 = p1;
+      p1 = p;
+    }
+  }
+}
+
+template <typename T> void upload(void** dst, const std::vector<double>& src, cudaError_t& e) {
+  std::vector<T> v(src.begin(), src.end());
+  if (e == cudaSuccess) e = cudaMalloc(dst, sizeof(T) * std::max<size_t>(1, v.size()));
+  if (e == cudaSuccess) e = cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+}
+
+template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
+  ShTables<T> t;
+  t.node = (const cplx_t<T>*)h->d_node;
+  t.tw = (const cplx_t<T>*)h->d_tw;
+  t.pw = (const T*)h->d_pw;
+  t.N = h->cfg.N;
+  t.R = h->R;
+  t.L = h->L;
+  t.nth = h->nth;
+  t.nph = h->nph;
+  t.Jh = h->Jh;
+  return t;
+}
+
+bool valid_params(const matcha_params_t* p, int LM, std::string& why) {
+  if (!p) { why = "params is NULL"; return false; }
+  if (p->n_bands < 1 || p->n_bands > 16) { why = "n_bands must be in [1,16]"; return false; }
+  for (int j = 0; j < p->n_bands; ++j) {
+    if (p->bands[j] < 1 || p->bands[j] > LM) { why = "band outside [1, L_M]"; return false; }
+    if (j && p->bands[j] <= p->bands[j - 1]) { why = "bands must be strictly increasing"; return false; }
+  }
+  if (p->newton_iters < 0 || p->newton_iters > 64) { why = "newton_iters must be in [0,64]"; return false; }
+  if (p->n_cand < 1 || p->n_cand > kMaxCand) { why = "n_cand must be in [1,32]"; return false; }
+  if (p->oversample < 1 || p->oversample > 8) { why = "oversample must be in [1,8]"; return false; }
+  if (p->n_alternations < 1 || p->n_alternations > 64) { why = "n_alternations must be in [1,64]"; return false; }
+  return true;
+}
+
+template <typename T> NewtonArgs<T> newton_args(matcha_handle_t h) {
+  NewtonArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.pairs = h->d_pairs;
+  a.pair_lnc = (const T*)h->d_pair_lnc;
+  a.flags = h->d_flags;
+  return a;
+}
+
+// RAII event pair around one stage launch (no-op unless profiling)
+struct ProfScope {
+  matcha_handle_t h;
+  cudaStream_t s;
+  size_t k = (size_t)-1;
+  ProfScope(matcha_handle_t h_, int stage, cudaStream_t s_) : h(h_), s(s_) {
+    if (!h->prof) return;
+    k = h->ev_next++;
+    while (h->ev_pool.size() < 2 * (k + 1)) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      h->ev_pool.push_back(e);
+    }
+    if (h->ev_stage.size() < k + 1) h->ev_stage.resize(k + 1);
+    h->ev_stage[k] = stage;
+    cudaEventRecord(h->ev_pool[2 * k], s);
+  }
+  ~ProfScope() {
+    if (k != (size_t)-1) cudaEventRecord(h->ev_pool[2 * k + 1], s);
+  }
+};
+
+}  // namespace
+
+template <typename T>
+static cudaError_t do_search(matcha_handle_t h, const void* M, int32_t L_M, int64_t B, int32_t L0, int32_t K,
+                             int32_t nc, void* euler, void* score, int32_t* idx, cudaStream_t s) {
+  SearchArgs<T> a;
+  a.M = (const cplx_t<T>*)M;
+  a.strideM = half_size(L_M);
+  a.B = B;
+  a.L0 = L0;
+  a.K = K;
+  a.ncand = nc;
+  a.euler = (T*)euler;
+  a.score = (T*)score;
+  a.idx = idx;
+  a.pairs = h->d_pairs;
+  a.pair_lnc = (const T*)h->d_pair_lnc;
+  a.flags = h->d_flags;
+  return launch_so3_search<T>(a, s);
+}
+
+template <typename T>
+static cudaError_t do_eval(matcha_handle_t h, const void* M, int32_t L_M, int64_t B, int32_t Q, int32_t L,
+                           const void* euler, void* value, void* grad, void* hess, cudaStream_t s) {
+  NewtonArgs<T> a = newton_args<T>(h);
+  a.M = (const cplx_t<T>*)M;
+  a.strideM = half_size(L_M);
+  a.L_M = L_M;
+  a.B = B;
+  a.Q = Q;
+  a.euler = (T*)euler;  // read only in eval mode
+  a.value = (T*)value;
+  a.grad = (T*)grad;
+  a.hess = (T*)hess;
+  a.L_eval = L;
+  return launch_eval_corr<T>(a, grad != nullptr || hess != nullptr, s);
+}
+
+template <typename T>
+static cudaError_t do_refine(matcha_handle_t h, const void* M, int32_t L_M, int64_t B, int32_t nc,
+                             const matcha_params_t* p, void* euler, const int32_t* idx, void* score, int32_t* best,
+                             cudaStream_t s) {
+  NewtonArgs<T> a = newton_args<T>(h);
+  a.M = (const cplx_t<T>*)M;
+  a.strideM = half_size(L_M);
+  a.L_M = L_M;
+  a.B = B;
+  a.Q = nc;
+  a.euler = (T*)euler;
+  a.idx = idx;
+  a.nbands = p->n_bands;
+  for (int j = 0; j < p->n_bands; ++j) a.bands[j] = p->bands[j];
+  a.iters = p->newton_iters;
+  a.tol_grad = p->tol_grad;
+  a.tol_step = p->tol_step;
+  a.tol_obj = p->tol_obj;
+  a.score = (T*)score;
+  a.best = best;
+  return launch_newton_refine<T>(a, s);
+}
+
+// App. C alternation around Algorithm 1 for particles [0, B) of `vols`, chunked by max_batch.
+static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_t B, const float* ref,
+                                    const void* ref_coeffs, const matcha_params_t* p, void* poses, cudaStream_t s) {
+  const int N = h->cfg.N;
+  const int64_t n3 = (int64_t)N * N * N;
+  const int LJ = p->bands[p->n_bands - 1], L0 = p->bands[0];
+  const void* H = ref_coeffs;
+  matcha_status_t st;
+  if (!H) {
+    st = matcha_sh_analysis(h, ref, 1, nullptr, h->ws_H, s);
+    if (st != MATCHA_OK) return st;
+    H = h->ws_H;
+  }
+  const int T = p->n_alternations;
+  const bool translate = p->shift_window > 0;
+  for (int64_t c0 = 0; c0 < B; c0 += h->cfg.max_batch) {
+    const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
+    char* pc = (char*)poses + c0 * 8 * h->rsz;
+    for (int tau = 0; tau < T; ++tau) {
+      const void* sh = (tau > 0 && translate) ? (const void*)(pc + 3 * h->rsz) : nullptr;
+      cudaError_t e;
+      {
+      ProfScope ps(h, 0, s);
+      if (h->fp64)
+        e = launch_sh_analysis<double>(vols + c0 * n3, nb, (const double*)sh, 8, sh_tables<double>(h),
+                                       (double2*)h->ws_F, s);
+      else
+        e = launch_sh_analysis<float>(vols + c0 * n3, nb, (const float*)sh, 8, sh_tables<float>(h), (float2*)h->ws_F,
+                                      s);
+      }
+      if (e != cudaSuccess) return cuda_fail(h, e, "align: sh_analysis");
+      h->launches++;
+      if ((st = matcha_corr_coeffs(h, h->ws_F, H, nb, LJ, h->ws_M, s)) != MATCHA_OK) return st;
+      if ((st = matcha_so3_search(h, h->ws_M, LJ, nb, L0, p->oversample, p->n_cand, h->ws_euler, h->ws_score,
+                                  h->ws_idx, s)) != MATCHA_OK)
+        return st;
+      if ((st = matcha_newton_refine(h, h->ws_M, LJ, nb, p->n_cand, p, h->ws_euler, h->ws_idx, h->ws_score,
+                                     h->ws_best, s)) != MATCHA_OK)
+        return st;
+      {
+      ProfScope ps(h, 4, s);
+      e = h->fp64 ? launch_gather_poses<double>((const double*)h->ws_euler, (const double*)h->ws_score, h->ws_best,
+                                                nb, p->n_cand, !translate, (double*)pc, s)
+                  : launch_gather_poses<float>((const float*)h->ws_euler, (const float*)h->ws_score, h->ws_best, nb,
+                                               p->n_cand, !translate, (float*)pc, s);
+      }
+      if (e != cudaSuccess) return cuda_fail(h, e, "align: gather_poses");
+      h->launches++;
+      if (translate) {
+        return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align: translation update not implemented yet");
+      }
+    }
+  }
+  return MATCHA_OK;
+}
+
+extern "C" {
+
+MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_handle_t* out) {
+  if (!cfg || !out) return MATCHA_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (cfg->N < 8 || cfg->N > 512 || (cfg->N & 1)) return MATCHA_ERR_INVALID_ARG;
+  if (cfg->L_max < 1 || cfg->L_max > kMaxL) return MATCHA_ERR_DEGREE;
+  if (cfg->quad_oversample < 1 || cfg->quad_oversample > 8) return MATCHA_ERR_INVALID_ARG;
+  if (cfg->max_batch < 1) return MATCHA_ERR_INVALID_ARG;
+  if (cfg->precision != MATCHA_FP32 && cfg->precision != MATCHA_FP64) return MATCHA_ERR_INVALID_ARG;
+  matcha_handle_t h = new matcha_ctx();
+  h->cfg = *cfg;
+  cudaGetDevice(&h->device);
+  h->fp64 = cfg->precision == MATCHA_FP64;
+  h->rsz = h->fp64 ? 8 : 4;
+  h->R = cfg->N / 2;
+  h->L = cfg->L_max;
+  h->Lq = cfg->quad_oversample * cfg->L_max;
+  h->nth = h->Lq + 1;
+  h->nph = 2 * h->Lq + 2;
+  h->Jh = (h->nth + 1) / 2;
+  h->ncf = ncoef(h->L);
+
+  // quadrature tables (readings C4): nodes ascending, phi_k = 2 pi k / n_phi
+  std::vector<double> x, w;
+  gl_nodes(h->nth, x, w);
+  std::vector<double> node(2 * h->nth), tw(2 * h->nph);
+  for (int j = 0; j < h->nth; ++j) {
+    node[2 * j] = x[j];
+    node[2 * j + 1] = std::sqrt(std::max(0.0, (1.0 - x[j]) * (1.0 + x[j])));
+  }
+  for (int k = 0; k < h->nph; ++k) {
+    tw[2 * k] = std::cos(2.0 * kPi * k / h->nph);
+    tw[2 * k + 1] = std::sin(2.0 * kPi * k / h->nph);
+  }
+  std::vector<double> pw((size_t)h->Jh * h->ncf), P;
+  for (int j = 0; j < h->Jh; ++j) {
+    plm_table(h->L, x[j], P);
+    for (int i = 0; i < h->ncf; ++i) pw[(size_t)j * h->ncf + i] = w[j] * P[i];
+  }
+  // stage-3/4 pair table, grouped by shell l0 = max(m,|n|): long l-runs first
+  std::vector<PairDesc> pairs;
+  std::vector<double> plnc;
+  for (int k = 0; k <= h->L; ++k) {
+    auto add = [&](int m, int n) {
+      pairs.push_back(PairDesc{(int16_t)m, (int16_t)n});
+      const int p = std::abs(m + n);
+      plnc.push_back(0.5 * (std::lgamma(2.0 * k + 1.0) - std::lgamma(p + 1.0) - std::lgamma(2.0 * k - p + 1.0)));
+    };
+    if (k == 0) { add(0, 0); continue; }
+    for (int n = -k; n <= k; ++n) add(k, n);
+    for (int m = 0; m < k; ++m) { add(m, -k); add(m, k); }
+  }
+  cudaError_t e = cudaSuccess;
+  if (h->fp64) {
+    upload<double>(&h->d_node, node, e);
+    upload<double>(&h->d_tw, tw, e);
+    upload<double>(&h->d_pw, pw, e);
+    upload<double>(&h->d_pair_lnc, plnc, e);
+  } else {
+    upload<float>(&h->d_node, node, e);
+    upload<float>(&h->d_tw, tw, e);
+    upload<float>(&h->d_pw, pw, e);
+    upload<float>(&h->d_pair_lnc, plnc, e);
+  }
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pairs, sizeof(PairDesc) * pairs.size());
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_pairs, pairs.data(), sizeof(PairDesc) * pairs.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_flags, sizeof(int) * 4);
+  if (e == cudaSuccess) e = cudaMemset(h->d_flags, 0, sizeof(int) * 4);
+  // align workspace
+  const size_t cb = 2 * h->rsz, mb = cfg->max_batch;
+  if (e == cudaSuccess) e = cudaMalloc(&h->ws_F, cb * mb * h->ncf * h->R);
+  if (e == cudaSuccess) e = cudaMalloc(&h->ws_M, cb * mb * half_size(h->L));
+  if (e == cudaSuccess) e = cudaMalloc(&h->ws_H, cb * h->ncf * h->R);
+  if (e == cudaSuccess) e = cudaMalloc(&h->ws_euler, h->rsz * mb * kMaxCand * 3);
+  if (e == cudaSuccess) e = cudaMalloc(&h->ws_score, h->rsz * mb * kMaxCand);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->ws_idx, sizeof(int32_t) * mb * kMaxCand);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->ws_best, sizeof(int32_t) * mb);
+  if (e != cudaSuccess) {
+    matcha_destroy(h);
+    return e == cudaErrorMemoryAllocation ? MATCHA_ERR_ALLOC : MATCHA_ERR_CUDA;
+  }
+  *out = h;
+  return MATCHA_OK;
+}
+
+MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H,
+                  h->ws_euler, h->ws_score, h->ws_idx, h->ws_best, h->ws_vols[0], h->ws_vols[1], h->ws_poses,
+                  h->ws_ref};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
+    if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
+  }
+  delete h;
+  return MATCHA_OK;
+}
+
+MATCHA_API int64_t matcha_coeff_count(matcha_handle_t h) { return h ? (int64_t)h->ncf * h->R : -1; }
+MATCHA_API int64_t matcha_corr_count(int32_t L) { return L < 0 ? 0 : half_size(L); }
+MATCHA_API int64_t matcha_launch_count(matcha_handle_t h) { return h ? h->launches : -1; }
+MATCHA_API const char* matcha_last_error_string(matcha_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+
+MATCHA_API matcha_status_t matcha_profile_begin(matcha_handle_t h) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  h->prof = true;
+  h->ev_next = 0;
+  return MATCHA_OK;
+}
+
+MATCHA_API matcha_status_t matcha_profile_end(matcha_handle_t h, double* stage_ms, int64_t* stage_launches) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  double ms[MATCHA_NUM_STAGES] = {0};
+  int64_t cnt[MATCHA_NUM_STAGES] = {0};
+  if (h->ev_next) MATCHA_CUDA(h, cudaEventSynchronize(h->ev_pool[2 * (h->ev_next - 1) + 1]));
+  for (size_t k = 0; k < h->ev_next; ++k) {
+    float t = 0.f;
+    MATCHA_CUDA(h, cudaEventElapsedTime(&t, h->ev_pool[2 * k], h->ev_pool[2 * k + 1]));
+    ms[h->ev_stage[k]] += t;
+    cnt[h->ev_stage[k]] += 1;
+  }
+  h->prof = false;
+  h->ev_next = 0;
+  for (int i = 0; i < MATCHA_NUM_STAGES; ++i) {
+    if (stage_ms) stage_ms[i] = ms[i];
+    if (stage_launches) stage_launches[i] = cnt[i];
+  }
+  return MATCHA_OK;
+}
+
+MATCHA_API matcha_status_t matcha_get_status(matcha_handle_t h, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  MATCHA_CUDA(h, cudaStreamSynchronize(s));
+  int f = 0;
+  MATCHA_CUDA(h, cudaMemcpy(&f, h->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+  MATCHA_CUDA(h, cudaMemset(h->d_flags, 0, sizeof(int)));
+  if (f & FLAG_NONFINITE) return fail(h, MATCHA_ERR_NONFINITE, "non-finite value produced on device");
+  if (f & FLAG_OVERFLOW) return fail(h, MATCHA_ERR_OVERFLOW, "coarse-grid local-maximum list overflowed");
+  return MATCHA_OK;
+}
+
+MATCHA_API matcha_status_t matcha_sh_analysis(matcha_handle_t h, const float* vols, int64_t B, const void* shifts,
+                                              void* coeffs, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!vols || !coeffs))) return fail(h, MATCHA_ERR_INVALID_ARG, "sh_analysis: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  ProfScope ps(h, 0, s);
+  if (h->fp64)
+    e = launch_sh_analysis<double>(vols, B, (const double*)shifts, 3, sh_tables<double>(h), (double2*)coeffs, s);
+  else
+    e = launch_sh_analysis<float>(vols, B, (const float*)shifts, 3, sh_tables<float>(h), (float2*)coeffs, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "sh_analysis launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
+MATCHA_API matcha_status_t matcha_corr_coeffs(matcha_handle_t h, const void* f, const void* href, int64_t B,
+                                              int32_t L, void* M, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!f || !href || !M))) return fail(h, MATCHA_ERR_INVALID_ARG, "corr_coeffs: bad arguments");
+  if (L < 0 || L > h->L) return fail(h, MATCHA_ERR_DEGREE, "corr_coeffs: L > L_max");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  ProfScope ps(h, 1, s);
+  if (h->fp64)
+    e = launch_corr_coeffs<double>((const double2*)f, (const double2*)href, B, L, h->L, h->R, (double2*)M, s);
+  else
+    e = launch_corr_coeffs<float>((const float2*)f, (const float2*)href, B, L, h->L, h->R, (float2*)M, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "corr_coeffs launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
+
+MATCHA_API matcha_status_t matcha_so3_search(matcha_handle_t h, const void* M, int32_t L_M, int64_t B, int32_t L0,
+                                             int32_t oversample, int32_t n_cand, void* euler, void* score,
+                                             int32_t* grid_idx, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!M || !euler || !score || !grid_idx)))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "so3_search: bad arguments");
+  if (L_M < 0 || L_M > h->L) return fail(h, MATCHA_ERR_DEGREE, "so3_search: L_M > L_max");
+  if (L0 < 1 || L0 > L_M) return fail(h, MATCHA_ERR_CUTOFF, "so3_search: L0 outside [1, L_M]");
+  if (oversample < 1 || oversample > 8 || n_cand < 1 || n_cand > kMaxCand)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "so3_search: oversample in [1,8], n_cand in [1,32]");
+  if (search_smem_bytes(L0, oversample, h->fp64) > 220 * 1024)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "so3_search: grid too large for one CTA (reduce L0*K)");
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope ps(h, 2, s);
+  cudaError_t e = h->fp64 ? do_search<double>(h, M, L_M, B, L0, oversample, n_cand, euler, score, grid_idx, s)
+                          : do_search<float>(h, M, L_M, B, L0, oversample, n_cand, euler, score, grid_idx, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "so3_search launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
+
+MATCHA_API matcha_status_t matcha_eval_corr(matcha_handle_t h, const void* M, int32_t L_M, int64_t B, int32_t Q,
+                                            int32_t L, const void* euler, void* value, void* grad, void* hess,
+                                            void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || Q < 1 || Q > 1024 || (B > 0 && (!M || !euler || !value)))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "eval_corr: bad arguments");
+  if (L_M < 0 || L_M > h->L) return fail(h, MATCHA_ERR_DEGREE, "eval_corr: L_M > L_max");
+  if (L < 0 || L > L_M) return fail(h, MATCHA_ERR_CUTOFF, "eval_corr: L > L_M");
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope ps(h, 3, s);
+  cudaError_t e = h->fp64 ? do_eval<double>(h, M, L_M, B, Q, L, euler, value, grad, hess, s)
+                          : do_eval<float>(h, M, L_M, B, Q, L, euler, value, grad, hess, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "eval_corr launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
+
+MATCHA_API matcha_status_t matcha_newton_refine(matcha_handle_t h, const void* M, int32_t L_M, int64_t B,
+                                                int32_t n_cand, const matcha_params_t* params, void* euler,
+                                                const int32_t* grid_idx, void* score, int32_t* best, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || n_cand < 1 || n_cand > kMaxCand || (B > 0 && (!M || !euler || !score || !best)))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "newton_refine: bad arguments");
+  if (L_M < 0 || L_M > h->L) return fail(h, MATCHA_ERR_DEGREE, "newton_refine: L_M > L_max");
+  std::string why;
+  if (!valid_params(params, L_M, why)) return fail(h, MATCHA_ERR_CUTOFF, "newton_refine: " + why);
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope ps(h, 3, s);
+  cudaError_t e = h->fp64 ? do_refine<double>(h, M, L_M, B, n_cand, params, euler, grid_idx, score, best, s)
+                          : do_refine<float>(h, M, L_M, B, n_cand, params, euler, grid_idx, score, best, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "newton_refine launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
+MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const float* vols, int64_t B,
+                                                     const float* ref, const void* euler, int32_t window,
+                                                     void* shifts, void* peak, void* stream) {
+  (void)vols; (void)B; (void)ref; (void)euler; (void)window; (void)shifts; (void)peak; (void)stream;
+  return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "translation_update: not implemented yet");
+}
+
+
+MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vols, int64_t B, const float* ref,
+                                              const void* ref_coeffs, const matcha_params_t* params, void* poses,
+                                              void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!vols || !poses))) return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: bad arguments");
+  std::string why;
+  if (!valid_params(params, h->L, why)) return fail(h, MATCHA_ERR_CUTOFF, "align_batch: " + why);
+  if (!ref_coeffs && !ref) return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: need ref or ref_coeffs");
+  if (params->shift_window > 0 && (!ref || params->shift_window > h->cfg.N / 4))
+    return fail(h, MATCHA_ERR_WINDOW, "align_batch: shift window needs ref and W <= N/4");
+  if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: coarse grid too large for one CTA");
+  return align_device(h, vols, B, ref, ref_coeffs, params, poses, (cudaStream_t)stream);
+}
+
+MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const float* vols_host, int64_t B,
+                                                   const float* ref_host, const matcha_params_t* params,
+                                                   void* poses_host, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!vols_host || !poses_host)) || !ref_host)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch_host: bad arguments");
+  std::string why;
+  if (!valid_params(params, h->L, why)) return fail(h, MATCHA_ERR_CUTOFF, "align_batch_host: " + why);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int N = h->cfg.N;
+  const int64_t n3 = (int64_t)N * N * N, mb = h->cfg.max_batch;
+  // lazily allocate the double-buffered staging area and the copy stream
+  if (!h->copy_stream) {
+    MATCHA_CUDA(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      MATCHA_CUDA(h, cudaMalloc((void**)&h->ws_vols[i], sizeof(float) * mb * n3));
+      MATCHA_CUDA(h, cudaEventCreateWithFlags(&h->ev_copied[i], cudaEventDisableTiming));
+      MATCHA_CUDA(h, cudaEventCreateWithFlags(&h->ev_used[i], cudaEventDisableTiming));
+    }
+    MATCHA_CUDA(h, cudaMalloc(&h->ws_poses, 8 * h->rsz * mb));
+    MATCHA_CUDA(h, cudaMalloc((void**)&h->ws_ref, sizeof(float) * n3));
+  }
+  MATCHA_CUDA(h, cudaMemcpyAsync(h->ws_ref, ref_host, sizeof(float) * n3, cudaMemcpyHostToDevice, s));
+  // reference coefficients once
+  matcha_status_t st = matcha_sh_analysis(h, h->ws_ref, 1, nullptr, h->ws_H, s);
+  if (st != MATCHA_OK) return st;
+  const int64_t nchunks = (B + mb - 1) / mb;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int buf = (int)(c & 1);
+    const int64_t c0 = c * mb, nb = std::min<int64_t>(mb, B - c0);
+    // copy stream waits until compute has finished with this buffer, then uploads chunk c
+    MATCHA_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_used[buf], 0));
+    MATCHA_CUDA(h, cudaMemcpyAsync(h->ws_vols[buf], vols_host + c0 * n3, sizeof(float) * nb * n3,
+                                   cudaMemcpyHostToDevice, h->copy_stream));
+    MATCHA_CUDA(h, cudaEventRecord(h->ev_copied[buf], h->copy_stream));
+    MATCHA_CUDA(h, cudaStreamWaitEvent(s, h->ev_copied[buf], 0));
+    st = align_device(h, h->ws_vols[buf], nb, h->ws_ref, h->ws_H, params, h->ws_poses, s);
+    if (st != MATCHA_OK) return st;
+    MATCHA_CUDA(h, cudaMemcpyAsync((char*)poses_host + c0 * 8 * h->rsz, h->ws_poses, 8 * h->rsz * nb,
+                                   cudaMemcpyDeviceToHost, s));
+    MATCHA_CUDA(h, cudaEventRecord(h->ev_used[buf], s));
+  }
+  MATCHA_CUDA(h, cudaStreamSynchronize(s));
+  return MATCHA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path through the C ABI vs the FP64 oracle, element by element on the same seeded
+inputs (tolerances: SURVEY.md 8(c) / tests/parity_util.py).  Run on a B200 with `pytest -m gpu`."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle as O
+from parity_util import (TOL_ROT_DEG, c_tol, g_tol, h_tol, rot_err_deg, topk_index_must_match)
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2603_15285_b200 as mt  # noqa: E402  (raises if libmatcha.so is missing: no CPU fallback)
+
+DEV = torch.device("cuda", 0)
+rng = np.random.default_rng(7)
+
+
+def cuda(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(DEV)
+
+
+def to_np(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module", params=["fp32", "fp64"])
+def prec(request):
+    return request.param
+
+
+def handle(N, L, prec="fp32", max_batch=64):
+    return mt.Handle(N=N, L_max=L, quad_oversample=2, max_batch=max_batch, precision=prec)
+
+
+# ------------------------------------------------------------------ stage 1
+@pytest.mark.parametrize("N,L,B", [(32, 8, 5), (64, 32, 3), (16, 5, 7)])
+def test_sh_analysis_parity(N, L, B, prec):
+    b = gen.particles(N, B, 0.1, seed=21, shift_mode=gen.SHIFT_UNIFORM, shift_max=2.0)
+    h = handle(N, L, prec)
+    vols = cuda(b.vols)
+    shifts = rng.uniform(-3, 3, size=(B, 3))
+    shifts[0] = [N / 2, -N / 2 + 1, 0.5]  # samples leave the box: zero extension (reading C5)
+    for sh in (None, shifts):
+        F = to_np(h.sh_analysis(vols, None if sh is None else cuda(sh, h.real)))
+        Fo = O.sh_analysis_batch(b.vols, L, 2, sh)
+        for p in range(B):
+            scale = np.abs(Fo[p]).max()
+            tol = (1e-11 if prec == "fp64" else 2e-5) * scale
+            assert np.abs(F[p] - Fo[p]).max() <= tol, (p, np.abs(F[p] - Fo[p]).max() / scale)
+
+
+def test_sh_analysis_empty_batch():
+    h = handle(16, 4)
+    out = h.sh_analysis(torch.empty((0, 16, 16, 16), device=DEV))
+    assert out.shape[0] == 0
+
+
+# ------------------------------------------------------------------ stage 2
+@pytest.mark.parametrize("N,L,Lc", [(64, 32, 32), (64, 32, 16), (32, 8, 8)])
+def test_corr_coeffs_parity(N, L, Lc, prec):
+    b = gen.particles(N, 3, 0.1, seed=22)
+    Fo = O.sh_analysis_batch(b.vols, L)
+    Ho = O.sh_analysis(b.ref, L)
+    h = handle(N, L, prec)
+    M = to_np(h.corr_coeffs(cuda(Fo, h.cplx), cuda(Ho, h.cplx), Lc))
+    for p in range(3):
+        Mo = O.full_to_half(O.corr_full(Fo[p], Ho, Lc), Lc)
+        scale = np.abs(Mo).max()
+        assert np.abs(M[p] - Mo).max() <= (1e-12 if prec == "fp64" else 2e-6) * scale
+
+
+# ------------------------------------------------------------------ C_L, grad, Hess (the evaluation kernel)
+@pytest.mark.parametrize("N,L,Leval", [(64, 32, 32), (64, 32, 24), (64, 32, 8), (32, 8, 8), (128, 64, 64)])
+def test_eval_corr_parity(N, L, Leval, prec):
+    b = gen.particles(N, 2, 0.1, seed=23)
+    Fo = O.sh_analysis_batch(b.vols, L)
+    Ho = O.sh_analysis(b.ref, L)
+    Q = 12
+    eul = np.stack([rng.uniform(0, 2 * np.pi, (2, Q)), rng.uniform(0, np.pi, (2, Q)),
+                    rng.uniform(0, 2 * np.pi, (2, Q))], -1)
+    eul[:, 0, 1] = 0.02          # near the poles (reading C16 clamp never triggers here)
+    eul[:, 1, 1] = np.pi - 0.03
+    eul[:, 2, 1] = np.pi / 2
+    h = handle(N, L, prec)
+    Mh = np.stack([O.full_to_half(O.corr_full(Fo[p], Ho, L), L) for p in range(2)])
+    val, grad, hess = h.eval_corr(cuda(Mh, h.cplx), L, Leval, cuda(eul, h.real))
+    val, grad, hess = to_np(val), to_np(grad), to_np(hess)
+    eul_used = to_np(cuda(eul, h.real)).astype(np.float64)  # the rotations the GPU actually saw
+    fp64 = prec == "fp64"
+    for p in range(2):
+        Mf = O.corr_full(Fo[p], Ho, Leval)
+        E = O.energy(Fo[p], Ho, Leval)
+        for q in range(Q):
+            C, g, H = O.eval_corr(Mf, Leval, eul_used[p, q])
+            assert abs(val[p, q] - C) <= c_tol(C, E, fp64), (p, q, val[p, q], C)
+            assert np.abs(grad[p, q] - g).max() <= g_tol(g, E, Leval, fp64), (p, q)
+            assert np.abs(hess[p, q] - H).max() <= h_tol(H, E, Leval, fp64), (p, q, hess[p, q], H)
+
+
+# ------------------------------------------------------------------ stage 3
+@pytest.mark.parametrize("N,L,L0,K,nc", [(64, 32, 8, 2, 10), (32, 8, 4, 2, 4), (128, 64, 12, 2, 16),
+                                         (32, 8, 8, 1, 32)])
+def test_so3_search_parity(N, L, L0, K, nc, prec):
+    B = 3
+    b = gen.particles(N, B, 0.1, seed=24)
+    Fo = O.sh_analysis_batch(b.vols, L)
+    Ho = O.sh_analysis(b.ref, L)
+    h = handle(N, L, prec)
+    Mh = np.stack([O.full_to_half(O.corr_full(Fo[p], Ho, L), L) for p in range(B)])
+    eul, sc, idx = h.so3_search(cuda(Mh, h.cplx), L, L0, K, nc)
+    eul, sc, idx = to_np(eul), to_np(sc), to_np(idx)
+    compared = 0
+    for p in range(B):
+        Mf = O.corr_full(Fo[p], Ho, L0)
+        grid = O.grid_eval(Mf, L0, K)
+        all_idx, all_sc, n = O.find_maxima(grid, 100000)
+        all_idx, all_sc = all_idx[:n], all_sc[:n]
+        E0 = O.energy(Fo[p], Ho, L0)
+        for k in range(nc):
+            if k >= n:
+                assert idx[p, k] == -1 and np.isneginf(sc[p, k])
+                continue
+            if topk_index_must_match(all_sc, all_idx, k, grid, E0):
+                compared += 1
+                assert idx[p, k] == all_idx[k], (p, k)
+                assert abs(sc[p, k] - all_sc[k]) <= c_tol(all_sc[k], E0, prec == "fp64")
+                assert np.allclose(eul[p, k], O.grid_node_euler(all_idx[k], L0, K), atol=1e-6)
+    assert compared >= B * min(nc, 3)
+
+
+# ------------------------------------------------------------------ stage 4
+@pytest.mark.parametrize("N,L,bands,nc,iters", [(64, 32, [8, 12, 16, 24, 32], 10, 1), (32, 8, [4, 6, 8], 4, 2),
+                                                (64, 32, [16, 32], 5, 3)])
+def test_newton_refine_parity(N, L, bands, nc, iters, prec):
+    B = 4
+    b = gen.particles(N, B, 0.1, seed=25)
+    Fo = O.sh_analysis_batch(b.vols, L)
+    Ho = O.sh_analysis(b.ref, L)
+    L0, K = bands[0], 2
+    h = handle(N, L, prec)
+    eul0 = np.zeros((B, nc, 3))
+    idx0 = np.zeros((B, nc), np.int64)
+    Mh = []
+    for p in range(B):
+        Mf = O.corr_full(Fo[p], Ho, L)
+        Mh.append(O.full_to_half(Mf, L))
+        idx, sc, n = O.find_maxima(O.grid_eval(O.corr_full(Fo[p], Ho, L0), L0, K), nc)
+        idx0[p] = idx
+        eul0[p] = [O.grid_node_euler(i, L0, K) if i >= 0 else np.zeros(3) for i in idx]
+    params = mt.Params(bands=bands, newton_iters=iters, n_cand=nc, oversample=K)
+    eg, sg, bg = h.newton_refine(cuda(np.stack(Mh), h.cplx), L, cuda(eul0, h.real), params,
+                                 cuda(idx0.astype(np.int32)))
+    eg, sg, bg = to_np(eg), to_np(sg), to_np(bg)
+    nbad = ntot = 0
+    for p in range(B):
+        Mf = O.corr_full(Fo[p], Ho, L)
+        eo, so, bo = O.refine(Mf, bands, iters, eul0[p], idx0[p])
+        E = O.energy(Fo[p], Ho, bands[-1])
+        for c in range(nc):
+            if idx0[p, c] < 0:
+                assert np.isneginf(sg[p, c])
+                continue
+            ntot += 1
+            if rot_err_deg(eg[p, c], eo[c]) > TOL_ROT_DEG:
+                nbad += 1
+            assert abs(sg[p, c] - so[c]) <= c_tol(so[c], E, prec == "fp64") or rot_err_deg(eg[p, c], eo[c]) > 1e-3
+        # selected candidate: same rotation, or a tie within the C tolerance (reading C23)
+        if bg[p] != bo:
+            assert abs(so[bg[p]] - so[bo]) <= c_tol(so[bo], E)
+    assert nbad <= 0.001 * ntot + (1 if ntot > 500 else 0), (nbad, ntot)
+
+
+# ------------------------------------------------------------------ whole path
+def _align_compare(N, L, bands, nc, snr, B, sample, prec="fp32", max_batch=64, seed=31, L0=None):
+    b = gen.particles(N, B, snr, seed=seed)
+    h = handle(N, L, prec, max_batch=max_batch)
+    params = mt.Params(bands=bands, n_cand=nc, oversample=2)
+    poses = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    h.status()
+    P = dict(L=L, qover=2, L0=bands[0], K=2, ncand=nc, bands=bands, iters=1, T=1, W=0)
+    sel = np.arange(B) if sample is None else np.unique(np.linspace(0, B - 1, sample).astype(int))
+    po = O.align_batch(b.vols[sel], b.ref, P)
+    Ho = O.sh_analysis(b.ref, L)
+    bad = []
+    for i, p in enumerate(sel):
+        err = rot_err_deg(poses[p, :3], po[i, :3])
+        if err > TOL_ROT_DEG:
+            # several results can be correct (C23): accept a different candidate whose oracle score ties
+            Fo = O.sh_analysis(b.vols[p], L)
+            Mf = O.corr_full(Fo, Ho, L)
+            C_g = O.eval_corr(Mf, L, poses[p, :3])[0]
+            E = O.energy(Fo, Ho, L)
+            if abs(C_g - po[i, 6]) > c_tol(po[i, 6], E):
+                bad.append((p, err))
+    return bad, len(sel), poses, b
+
+
+def test_align_c1_noise_free_exact():
+    """c1 rotation part (32^3, L0=4 -> 8, N_C=4, noise-free): GPU == oracle, both near the planted truth."""
+    bad, n, poses, b = _align_compare(32, 8, [4, 6, 8], 4, float("inf"), 8, None)
+    assert not bad
+    for p in range(8):
+        assert O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) < 0.1
+
+
+def test_align_parity_1000_particles_c1_shape_noisy():
+    """>= 1,000 compared particles (SURVEY 8(c) pass rate >= 99.9%) at the c1 shape with SNR 0.1."""
+    bad, n, _, _ = _align_compare(32, 8, [4, 6, 8], 4, 0.1, 1000, None, max_batch=256, seed=32)
+    assert len(bad) <= 1, bad
+
+
+def test_align_parity_c2_full_size_sampled():
+    """c2 at full size (1,000 x 64^3, L0=8 -> 32, N_C=10) in the bench's launch configuration; the oracle
+    recomputes a sample of particles one by one."""
+    bad, n, poses, b = _align_compare(64, 32, [8, 12, 16, 24, 32], 10, 0.1, 1000, 24, max_batch=1000, seed=33)
+    assert not bad, bad
+    errs = [O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) for p in range(0, 1000, 50)]
+    assert np.median(errs) < 1.0  # sanity vs planted truth (median ~0.3 deg at SNR 0.1)
+
+
+def test_align_ragged_chunks_and_fp64():
+    bad, n, _, _ = _align_compare(32, 8, [4, 6, 8], 4, 0.1, 37, None, prec="fp64", max_batch=16, seed=34)
+    assert not bad
+
+
+def test_align_bitwise_deterministic():
+    b = gen.particles(32, 20, 0.1, seed=35)
+    h = handle(32, 8)
+    params = mt.Params(bands=[4, 6, 8], n_cand=4)
+    p1 = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    p2 = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    assert np.array_equal(p1, p2)
+    # shard invariance: particles 7..19 alone give the same bits (multi-GPU invariant)
+    p3 = to_np(h.align_batch(cuda(b.vols[7:]), cuda(b.ref), params))
+    assert np.array_equal(p1[7:], p3)
+
+
+def test_align_host_path_matches_device_path():
+    b = gen.particles(32, 40, 0.1, seed=36)
+    h = handle(32, 8, max_batch=16)
+    params = mt.Params(bands=[4, 6, 8], n_cand=4)
+    pd = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    ph = h.align_batch_host(torch.from_numpy(b.vols).pin_memory(), torch.from_numpy(b.ref).pin_memory(), params)
+    assert np.array_equal(pd, ph.numpy())
+
+
+def test_invalid_arguments_rejected():
+    h = handle(32, 8)
+    M = torch.zeros((1, mt.corr_count(8)), dtype=torch.complex64, device=DEV)
+    with pytest.raises(mt.MatchaError):
+        h.so3_search(M, 8, 9)  # L0 > L_M
+    with pytest.raises(mt.MatchaError):
+        h.newton_refine(M, 8, torch.zeros((1, 4, 3), device=DEV), mt.Params(bands=[6, 4]))
+    with pytest.raises(mt.MatchaError):
+        mt.Handle(N=33, L_max=8)
