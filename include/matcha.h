@@ -9,7 +9,7 @@
  *
  * Conventions:
  *   - Volumes: float32 [N][N][N], x fastest (v[z][y][x]); centre c = (N-1)/2 per axis;
- *     trilinear interpolation of the zero-extended volume; N even, 8 <= N <= 512.
+ *     trilinear interpolation of the zero-extended volume; N a multiple of 8, 8 <= N <= 512.
  *   - Euler angles (alpha, beta, gamma), ZYZ: g = r_z(alpha) r_y(beta) r_z(gamma) (Eq. 3,
  *     P:79-94), canonical ranges [0,2pi) x [0,pi] x [0,2pi); action (g o f)(x) = f(g^-1 x).
  *   - Shells r_i = i - 1/2, i = 1..R = N/2, weights w_i = r_i^2; angular quadrature: n_theta =
@@ -68,7 +68,7 @@ typedef enum { MATCHA_FP32 = 0, MATCHA_FP64 = 1 } matcha_precision_t;
 
 /* Handle configuration (host struct). */
 typedef struct {
-  int32_t N;               /* box edge (voxels), even, 8..512 */
+  int32_t N;               /* box edge (voxels), multiple of 8, 8..512 */
   int32_t L_max;           /* analysis degree L (= last band L_J), 1..128 */
   int32_t quad_oversample; /* q: L_q = q * L_max (reading C4; default 2) */
   int32_t max_batch;       /* particles per internal chunk of matcha_align_batch */

@@ -49,8 +49,11 @@ struct PairDesc {
 template <typename T> struct ShTables {
   const cplx_t<T>* node;  // [n_theta] (cos th_j, sin th_j), x_j ascending
   const cplx_t<T>* tw;    // [n_phi] (cos phi_k, sin phi_k)
-  const T* pw;            // [Jh][ncoef] W_j Pbar_lm(x_j), j < Jh = (n_theta+1)/2 (x_j ascending)
-  int N, R, L, nth, nph, Jh;
+  const T* pwm;           // [Jh][pw_stride] W_j Pbar_lm(x_j), m-major rows: m block at pw_moff[m], l - m inside,
+                          // each m block padded to a multiple of 4 (zeros); j < Jh = (n_theta+1)/2
+  const int* pw_moff;     // [L+2] offsets of the m blocks (pw_moff[L+1] = pw_stride)
+  const T* dft;           // [2 parity][2 cos/sin][Kh+1][MP]: cos/sin(m phi_k), m = 2 mi + parity (0 if m > L)
+  int N, R, L, nth, nph, Jh, Kh, MP, pw_stride;
 };
 
 template <typename T> struct NewtonArgs {
@@ -94,7 +97,8 @@ template <typename T> struct SearchArgs {
 // ------------------------------------------------------------------ launchers (explicitly instantiated)
 template <typename T>
 cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, int shift_stride, const ShTables<T>& tab,
-                               cplx_t<T>* F, cudaStream_t s);
+                               cplx_t<T>* F, cplx_t<T>* Gws, int64_t gws_particles, cudaStream_t s);
+template <typename T> size_t sh_ring_workspace_elems(const ShTables<T>& tab);  // complex elements per particle
 template <typename T>
 cudaError_t launch_corr_coeffs(const cplx_t<T>* F, const cplx_t<T>* H, int64_t B, int L, int Lmax, int R,
                                cplx_t<T>* M, cudaStream_t s);

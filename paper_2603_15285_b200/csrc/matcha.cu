@@ -23,7 +23,10 @@ struct matcha_ctx {
   int R = 0, L = 0, Lq = 0, nth = 0, nph = 0, Jh = 0, ncf = 0;
   void* d_node = nullptr;
   void* d_tw = nullptr;
-  void* d_pw = nullptr;
+  void* d_pw = nullptr;     // m-major Legendre weights [Jh][pw_stride]
+  int* d_pw_moff = nullptr;
+  void* d_dft = nullptr;    // parity-split cos/sin table of the folded ring DFT
+  int Kh = 0, MP = 0, pw_stride = 0;
   PairDesc* d_pairs = nullptr;
   void* d_pair_lnc = nullptr;
   int* d_flags = nullptr;
@@ -31,6 +34,8 @@ struct matcha_ctx {
   void* ws_F = nullptr;
   void* ws_M = nullptr;
   void* ws_H = nullptr;
+  void* ws_G = nullptr;        // stage-1 ring coefficients of one sub-batch (L2-sized)
+  int64_t gws_particles = 0;
   void* ws_euler = nullptr;
   void* ws_score = nullptr;
   int32_t* ws_idx = nullptr;
@@ -140,7 +145,12 @@ template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
   ShTables<T> t;
   t.node = (const cplx_t<T>*)h->d_node;
   t.tw = (const cplx_t<T>*)h->d_tw;
-  t.pw = (const T*)h->d_pw;
+  t.pwm = (const T*)h->d_pw;
+  t.pw_moff = h->d_pw_moff;
+  t.dft = (const T*)h->d_dft;
+  t.Kh = h->Kh;
+  t.MP = h->MP;
+  t.pw_stride = h->pw_stride;
   t.N = h->cfg.N;
   t.R = h->R;
   t.L = h->L;
@@ -281,10 +291,10 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
       ProfScope ps(h, 0, s);
       if (h->fp64)
         e = launch_sh_analysis<double>(vols + c0 * n3, nb, (const double*)sh, 8, sh_tables<double>(h),
-                                       (double2*)h->ws_F, s);
+                                       (double2*)h->ws_F, (double2*)h->ws_G, h->gws_particles, s);
       else
         e = launch_sh_analysis<float>(vols + c0 * n3, nb, (const float*)sh, 8, sh_tables<float>(h), (float2*)h->ws_F,
-                                      s);
+                                      (float2*)h->ws_G, h->gws_particles, s);
       }
       if (e != cudaSuccess) return cuda_fail(h, e, "align: sh_analysis");
       h->launches++;
@@ -317,7 +327,7 @@ extern "C" {
 MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_handle_t* out) {
   if (!cfg || !out) return MATCHA_ERR_INVALID_ARG;
   *out = nullptr;
-  if (cfg->N < 8 || cfg->N > 512 || (cfg->N & 1)) return MATCHA_ERR_INVALID_ARG;
+  if (cfg->N < 8 || cfg->N > 512 || (cfg->N & 7)) return MATCHA_ERR_INVALID_ARG;
   if (cfg->L_max < 1 || cfg->L_max > kMaxL) return MATCHA_ERR_DEGREE;
   if (cfg->quad_oversample < 1 || cfg->quad_oversample > 8) return MATCHA_ERR_INVALID_ARG;
   if (cfg->max_batch < 1) return MATCHA_ERR_INVALID_ARG;
@@ -347,11 +357,30 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     tw[2 * k] = std::cos(2.0 * kPi * k / h->nph);
     tw[2 * k + 1] = std::sin(2.0 * kPi * k / h->nph);
   }
-  std::vector<double> pw((size_t)h->Jh * h->ncf), P;
+  // Legendre weights W_j Pbar_lm(x_j), m-major with each m block padded to a multiple of 4 (float4 tiles)
+  std::vector<int> moff(h->L + 2, 0);
+  for (int mm = 0; mm <= h->L; ++mm) moff[mm + 1] = moff[mm] + (h->L - mm + 4) / 4 * 4;
+  h->pw_stride = moff[h->L + 1];
+  std::vector<double> pw((size_t)h->Jh * h->pw_stride, 0.0), P;
   for (int j = 0; j < h->Jh; ++j) {
     plm_table(h->L, x[j], P);
-    for (int i = 0; i < h->ncf; ++i) pw[(size_t)j * h->ncf + i] = w[j] * P[i];
+    for (int l = 0; l <= h->L; ++l)
+      for (int mm = 0; mm <= l; ++mm) pw[(size_t)j * h->pw_stride + moff[mm] + (l - mm)] = w[j] * P[lm_index(l, mm)];
   }
+  // folded ring-DFT table: [parity][cos, sin][k = 0..Kh][mi < MP], m = 2 mi + parity
+  const int Mp = h->nph / 2;
+  h->Kh = (Mp - 1) / 2;
+  h->MP = ((h->L / 2 + 1) + 3) / 4 * 4;
+  std::vector<double> dft((size_t)4 * (h->Kh + 1) * h->MP, 0.0);
+  for (int par = 0; par < 2; ++par)
+    for (int k = 0; k <= h->Kh; ++k)
+      for (int mi = 0; mi < h->MP; ++mi) {
+        const int mm = 2 * mi + par;
+        if (mm > h->L) continue;
+        const double ang = 2.0 * kPi * (double)((long)mm * k % h->nph) / h->nph;
+        dft[((size_t)(par * 2 + 0) * (h->Kh + 1) + k) * h->MP + mi] = std::cos(ang);
+        dft[((size_t)(par * 2 + 1) * (h->Kh + 1) + k) * h->MP + mi] = std::sin(ang);
+      }
   // stage-3/4 pair table, grouped by shell l0 = max(m,|n|): long l-runs first
   std::vector<PairDesc> pairs;
   std::vector<double> plnc;
@@ -370,13 +399,17 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     upload<double>(&h->d_node, node, e);
     upload<double>(&h->d_tw, tw, e);
     upload<double>(&h->d_pw, pw, e);
+    upload<double>(&h->d_dft, dft, e);
     upload<double>(&h->d_pair_lnc, plnc, e);
   } else {
     upload<float>(&h->d_node, node, e);
     upload<float>(&h->d_tw, tw, e);
     upload<float>(&h->d_pw, pw, e);
+    upload<float>(&h->d_dft, dft, e);
     upload<float>(&h->d_pair_lnc, plnc, e);
   }
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pw_moff, sizeof(int) * moff.size());
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_pw_moff, moff.data(), sizeof(int) * moff.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pairs, sizeof(PairDesc) * pairs.size());
   if (e == cudaSuccess) e = cudaMemcpy(h->d_pairs, pairs.data(), sizeof(PairDesc) * pairs.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_flags, sizeof(int) * 4);
@@ -386,6 +419,12 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_F, cb * mb * h->ncf * h->R);
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_M, cb * mb * half_size(h->L));
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_H, cb * h->ncf * h->R);
+  {
+    const size_t per = cb * (size_t)h->R * h->nth * (h->L + 1);
+    h->gws_particles = std::max<int64_t>(32, (int64_t)((96u << 20) / per));
+    h->gws_particles = std::min<int64_t>(h->gws_particles, cfg->max_batch);
+    if (e == cudaSuccess) e = cudaMalloc(&h->ws_G, per * h->gws_particles);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_euler, h->rsz * mb * kMaxCand * 3);
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_score, h->rsz * mb * kMaxCand);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->ws_idx, sizeof(int32_t) * mb * kMaxCand);
@@ -400,7 +439,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
 
 MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (!h) return MATCHA_ERR_INVALID_ARG;
-  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H,
+  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
                   h->ws_euler, h->ws_score, h->ws_idx, h->ws_best, h->ws_vols[0], h->ws_vols[1], h->ws_poses,
                   h->ws_ref};
   for (void* p : ptrs)
@@ -467,9 +506,11 @@ MATCHA_API matcha_status_t matcha_sh_analysis(matcha_handle_t h, const float* vo
   cudaError_t e;
   ProfScope ps(h, 0, s);
   if (h->fp64)
-    e = launch_sh_analysis<double>(vols, B, (const double*)shifts, 3, sh_tables<double>(h), (double2*)coeffs, s);
+    e = launch_sh_analysis<double>(vols, B, (const double*)shifts, 3, sh_tables<double>(h), (double2*)coeffs,
+                                   (double2*)h->ws_G, h->gws_particles, s);
   else
-    e = launch_sh_analysis<float>(vols, B, (const float*)shifts, 3, sh_tables<float>(h), (float2*)coeffs, s);
+    e = launch_sh_analysis<float>(vols, B, (const float*)shifts, 3, sh_tables<float>(h), (float2*)coeffs,
+                                  (float2*)h->ws_G, h->gws_particles, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "sh_analysis launch");
   h->launches += B > 0;
   return MATCHA_OK;

@@ -136,6 +136,17 @@ def test_so3_search_parity(N, L, L0, K, nc, prec):
 
 
 # ------------------------------------------------------------------ stage 4
+def _oracle_stable(Mf, bands, iters, eul0, idx0, e_ref, seed):
+    """Candidates whose oracle trajectory is insensitive to an FP32-sized perturbation (1e-6 relative on M,
+    start angles rounded to float32).  Weak candidates on a noisy landscape take huge, chaotic Newton steps
+    (SURVEY 8(c) "parity unpinned: noisy-landscape Newton paths"): there several results are correct, so
+    only their validity is checked."""
+    r = np.random.default_rng(seed)
+    Mp = Mf * (1 + 1e-6 * r.normal(size=Mf.shape))
+    ep, _, _ = O.refine(Mp, bands, iters, eul0.astype(np.float32).astype(np.float64), idx0)
+    return np.array([rot_err_deg(ep[c], e_ref[c]) < 0.01 for c in range(len(e_ref))])
+
+
 @pytest.mark.parametrize("N,L,bands,nc,iters", [(64, 32, [8, 12, 16, 24, 32], 10, 1), (32, 8, [4, 6, 8], 4, 2),
                                                 (64, 32, [16, 32], 5, 3)])
 def test_newton_refine_parity(N, L, bands, nc, iters, prec):
@@ -162,19 +173,29 @@ def test_newton_refine_parity(N, L, bands, nc, iters, prec):
     for p in range(B):
         Mf = O.corr_full(Fo[p], Ho, L)
         eo, so, bo = O.refine(Mf, bands, iters, eul0[p], idx0[p])
+        stable = _oracle_stable(Mf, bands, iters, eul0[p], idx0[p], eo, seed=p)
         E = O.energy(Fo[p], Ho, bands[-1])
         for c in range(nc):
             if idx0[p, c] < 0:
                 assert np.isneginf(sg[p, c])
                 continue
+            # every candidate: valid chart point with a finite score
+            assert np.isfinite(sg[p, c]) and 0 <= eg[p, c, 1] <= np.pi + 1e-6
+            assert 0 <= eg[p, c, 0] < 2 * np.pi + 1e-6 and 0 <= eg[p, c, 2] < 2 * np.pi + 1e-6
+            if not stable[c]:
+                continue
             ntot += 1
-            if rot_err_deg(eg[p, c], eo[c]) > TOL_ROT_DEG:
+            err = rot_err_deg(eg[p, c], eo[c])
+            if err > TOL_ROT_DEG:
                 nbad += 1
-            assert abs(sg[p, c] - so[c]) <= c_tol(so[c], E, prec == "fp64") or rot_err_deg(eg[p, c], eo[c]) > 1e-3
-        # selected candidate: same rotation, or a tie within the C tolerance (reading C23)
+            else:
+                assert abs(sg[p, c] - so[c]) <= c_tol(so[c], E, prec == "fp64")
+        # the selected pose: same candidate, or a tie within the C tolerance (reading C23)
+        assert stable[bo]
         if bg[p] != bo:
             assert abs(so[bg[p]] - so[bo]) <= c_tol(so[bo], E)
-    assert nbad <= 0.001 * ntot + (1 if ntot > 500 else 0), (nbad, ntot)
+        assert rot_err_deg(eg[p, bg[p]], eo[bo]) <= TOL_ROT_DEG or abs(so[bg[p]] - so[bo]) <= c_tol(so[bo], E)
+    assert ntot >= B and nbad <= 0.001 * ntot, (nbad, ntot)
 
 
 # ------------------------------------------------------------------ whole path
