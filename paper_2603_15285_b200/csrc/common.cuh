@@ -52,7 +52,7 @@ template <typename T> struct ShTables {
   const T* pwm;           // [Jh][pw_stride] W_j Pbar_lm(x_j), m-major rows: m block at pw_moff[m], l - m inside,
                           // each m block padded to a multiple of 4 (zeros); j < Jh = (n_theta+1)/2
   const int* pw_moff;     // [L+2] offsets of the m blocks (pw_moff[L+1] = pw_stride)
-  const T* dft;           // [2 parity][2 cos/sin][Kh+1][MP]: cos/sin(m phi_k), m = 2 mi + parity (0 if m > L)
+  const cplx_t<T>* dft;   // [Kh+1][L+1]: (cos, sin)(m phi_k) for the folded ring DFT
   int N, R, L, nth, nph, Jh, Kh, MP, pw_stride;
 };
 

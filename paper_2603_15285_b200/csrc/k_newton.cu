@@ -116,6 +116,23 @@ __device__ void newton_delta(const double* g, const double* h, double* dl) {
   dl[2] = -(c02 * g[0] + c12 * g[1] + c22 * g[2]) * inv;
 }
 
+// Warp reduce-scatter of N (multiple of 32) per-lane values: 5 halving levels with N/2 + N/4 + ... shuffles
+// (instead of 5N); afterwards lane l holds the warp totals of indices l*(N/32) + i, i < N/32.
+template <typename T, int N, int O>
+__device__ __forceinline__ void rs_levels(T* v, int lane) {
+  if constexpr (O >= 1) {
+    constexpr int H = N / 2;
+    const bool upper = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      const T send = upper ? v[i] : v[i + H];
+      const T keep = upper ? v[i + H] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    rs_levels<T, H, O / 2>(v, lane);
+  }
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -270,14 +287,29 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
         }
       }
     }
-    // deterministic block reduction: warp butterflies, then fixed-order sum over warps
+    // deterministic block reduction: warp reduce-scatter (or butterflies for few values), then a
+    // fixed-order sum over warps
+    constexpr int NVAL = NV * CG;
+    if constexpr (NVAL >= 16) {
+      constexpr int NP = (NVAL + 31) / 32 * 32;
+      T v[NP];
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+      for (int i = 0; i < NP; ++i) v[i] = (i < NVAL) ? acc[i / CG][i % CG] : T(0);
+      rs_levels<T, NP, 16>(v, lane);
 #pragma unroll
-      for (int k = 0; k < CG; ++k) {
-        const T s = warp_sum(acc[v][k]);
-        if (lane == 0) red[warp * (NV * CG) + v * CG + k] = s;
+      for (int i = 0; i < NP / 32; ++i) {
+        const int idx = lane * (NP / 32) + i;
+        if (idx < NVAL) red[warp * (NV * CG) + idx] = v[i];
       }
+    } else {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int k = 0; k < CG; ++k) {
+          const T s = warp_sum(acc[v][k]);
+          if (lane == 0) red[warp * (NV * CG) + v * CG + k] = s;
+        }
+    }
     __syncthreads();
     if (tid < NV * CG) {
       const int v = tid / CG, k = tid % CG;
@@ -299,7 +331,7 @@ __device__ void load_inv_tables(T* inv_l, T* inv_ll) {
 
 // ------------------------------------------------------------------ matcha_eval_corr kernel
 template <typename T, int CG>
-__global__ void __launch_bounds__(kThreads) k_eval_corr(NewtonArgs<T> a, bool derivs) {
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) k_eval_corr(NewtonArgs<T> a, bool derivs) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int L = a.L_eval, Q = a.Q;
   const SmemLayout lay = smem_layout<T>(Q, L);
@@ -335,7 +367,7 @@ __global__ void __launch_bounds__(kThreads) k_eval_corr(NewtonArgs<T> a, bool de
 
 // ------------------------------------------------------------------ matcha_newton_refine kernel
 template <typename T, int CG>
-__global__ void __launch_bounds__(kThreads) k_newton_refine(NewtonArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) k_newton_refine(NewtonArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
   const int Lmax_b = a.bands[a.nbands - 1];

@@ -24,7 +24,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 2048;
 
 struct SearchLayout {
-  size_t Ms, X, Y, sl, tw, cs, cs_idx, invl, invll, misc, red_s, red_i, total;
+  size_t Ms, X, Y, sl, tmv, tmi, mxv, mxi, tw, cs, cs_idx, invl, invll, misc, red_s, red_i, total;
 };
 
 template <typename T> __host__ __device__ inline SearchLayout search_layout(int L0, int K) {
@@ -40,7 +40,11 @@ template <typename T> __host__ __device__ inline SearchLayout search_layout(int 
   s.Ms = take(sizeof(cplx_t<T>) * half_size(L0));
   s.X = take(sizeof(cplx_t<T>) * (L0 + 1) * (2 * L0 + 1));
   s.Y = take(sizeof(cplx_t<T>) * (L0 + 1) * na);
-  s.sl = take(sizeof(T) * 3 * na * na);
+  s.sl = take(sizeof(T) * na * na);             // raw C values of the current beta slice
+  s.tmv = take(sizeof(T) * na * na);            // gamma-pass of the 3x3 (alpha,gamma) max filter
+  s.tmi = take(sizeof(int) * na * na);
+  s.mxv = take(sizeof(T) * 3 * na * na);        // rolling 3-slice window of the in-slice 3x3 maxima
+  s.mxi = take(sizeof(int) * 3 * na * na);
   s.tw = take(sizeof(cplx_t<T>) * na);
   s.cs = take(sizeof(T) * kCap);
   s.cs_idx = take(sizeof(int) * kCap);
@@ -68,6 +72,10 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
   cplx_t<T>* X = (cplx_t<T>*)(smem + lay.X);
   cplx_t<T>* Y = (cplx_t<T>*)(smem + lay.Y);
   T* sl = (T*)(smem + lay.sl);
+  T* tmv = (T*)(smem + lay.tmv);
+  int* tmi = (int*)(smem + lay.tmi);
+  T* mxv = (T*)(smem + lay.mxv);
+  int* mxi = (int*)(smem + lay.mxi);
   cplx_t<T>* tw = (cplx_t<T>*)(smem + lay.tw);
   T* cs = (T*)(smem + lay.cs);
   int* ci = (int*)(smem + lay.cs_idx);
@@ -96,41 +104,80 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
 
   const int npairs = pair_count(L0);
   const int w0 = 2 * L0 + 1;
+  // Local maxima by a separable max filter on the unique keys (score desc, index asc): node p is a strict local
+  // maximum over its 26 neighbours iff it is the best key of its closed 3x3x3 neighbourhood.
   auto test_slice = [&](int jj) {
-    const T* cur = sl + (jj % 3) * na * ng;
     for (int t = tid; t < na * ng; t += kThreads) {
-      const int aa = t / ng, c = t - aa * ng;
-      const T vp = cur[t];
-      const int ip = (jj * na + aa) * ng + c;
-      bool ok = true;
-      for (int dj = -1; dj <= 1 && ok; ++dj) {
-        const int j2 = jj + dj;
-        if (j2 < 0 || j2 >= nb) continue;
-        const T* s2 = sl + (j2 % 3) * na * ng;
-        for (int da = -1; da <= 1 && ok; ++da) {
-          const int a2 = (aa + da + na) % na;
-          for (int dc = -1; dc <= 1; ++dc) {
-            if (!dj && !da && !dc) continue;
-            const int c2 = (c + dc + ng) % ng;
-            const int iq = (j2 * na + a2) * ng + c2;
-            if (iq == ip) continue;
-            const T vq = s2[a2 * ng + c2];
-            if (!before(vp, ip, vq, iq)) {
-              ok = false;
-              break;
-            }
-          }
+      const int ip = jj * na * ng + t;
+      T bv = mxv[(jj % 3) * na * ng + t];
+      int bi = mxi[(jj % 3) * na * ng + t];
+      if (jj > 0) {
+        const T v = mxv[((jj - 1) % 3) * na * ng + t];
+        const int i = mxi[((jj - 1) % 3) * na * ng + t];
+        if (before(v, i, bv, bi)) {
+          bv = v;
+          bi = i;
         }
       }
-      if (ok) {
+      if (jj + 1 < nb) {
+        const T v = mxv[((jj + 1) % 3) * na * ng + t];
+        const int i = mxi[((jj + 1) % 3) * na * ng + t];
+        if (before(v, i, bv, bi)) {
+          bv = v;
+          bi = i;
+        }
+      }
+      if (bi == ip) {
         const int slot = atomicAdd(cnt, 1);
         if (slot < kCap) {
-          cs[slot] = vp;
+          cs[slot] = bv;
           ci[slot] = ip;
         } else {
           atomicOr(a.flags, FLAG_OVERFLOW);
         }
       }
+    }
+  };
+  // in-slice 3x3 (alpha, gamma periodic) max of the keys of slice j -> window slot j % 3
+  auto filter_slice = [&](int j) {
+    for (int t = tid; t < na * ng; t += kThreads) {
+      const int aa = t / ng, c = t - aa * ng;
+      const int cm = c == 0 ? ng - 1 : c - 1, cp = c == ng - 1 ? 0 : c + 1;
+      const int base = j * na * ng + aa * ng;
+      T bv = sl[t];
+      int bi = base + c;
+      const T v1 = sl[aa * ng + cm], v2 = sl[aa * ng + cp];
+      if (before(v1, base + cm, bv, bi)) {
+        bv = v1;
+        bi = base + cm;
+      }
+      if (before(v2, base + cp, bv, bi)) {
+        bv = v2;
+        bi = base + cp;
+      }
+      tmv[t] = bv;
+      tmi[t] = bi;
+    }
+    __syncthreads();
+    T* ov = mxv + (j % 3) * na * ng;
+    int* oi = mxi + (j % 3) * na * ng;
+    for (int t = tid; t < na * ng; t += kThreads) {
+      const int aa = t / ng, c = t - aa * ng;
+      const int am = aa == 0 ? na - 1 : aa - 1, ap = aa == na - 1 ? 0 : aa + 1;
+      T bv = tmv[t];
+      int bi = tmi[t];
+      const T v1 = tmv[am * ng + c], v2 = tmv[ap * ng + c];
+      const int i1 = tmi[am * ng + c], i2 = tmi[ap * ng + c];
+      if (before(v1, i1, bv, bi)) {
+        bv = v1;
+        bi = i1;
+      }
+      if (before(v2, i2, bv, bi)) {
+        bv = v2;
+        bi = i2;
+      }
+      ov[t] = bv;
+      oi[t] = bi;
     }
   };
 
@@ -186,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
     }
     __syncthreads();
     // C(alpha_a, beta_j, gamma_c)
-    T* cur = sl + (j % 3) * na * ng;
+    T* cur = sl;
     for (int t = tid; t < na * ng; t += kThreads) {
       const int aa = t / ng, c = t - aa * ng;
       T s = Y[c].x;
@@ -201,8 +248,9 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
       cur[t] = fma(T(2), s2, s);
     }
     __syncthreads();
-    if (j >= 1) test_slice(j - 1);
+    filter_slice(j);
     __syncthreads();
+    if (j >= 1) test_slice(j - 1);
   }
   test_slice(nb - 1);
   __syncthreads();

@@ -33,16 +33,20 @@ constexpr int kWarps = kThreads / 32;
 
 constexpr int kRingThreads = 512;
 constexpr int kRingWarps = kRingThreads / 32;
+constexpr int kG = 8;  // rings per warp group (register tile of the DFT)
 
 struct RingLayout {
-  size_t tw, node, dft, pl, list, wsum, fold, mid, total;
+  size_t tw, node, dft, pl, list, wsum, wbuf, total;
 };
 
 // staged plane rows are padded to N + 4 floats (16-byte aligned rows for cp.async; bank = (4y + x) mod 32)
 __host__ __device__ inline int plane_pitch(int N) { return N + 4; }
 
+// per-warp fold buffer: [4 comps][Kh+1][kG] + mid [2][kG]
+__host__ __device__ inline int wbuf_elems(int Kh) { return 4 * (Kh + 1) * kG + 2 * kG; }
+
 template <typename T>
-__host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph, int R, int RB, int Kh, int MP,
+__host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph, int R, int Kh, int MP,
                                                    bool dft_smem = true) {
   RingLayout s;
   size_t o = 0;
@@ -53,19 +57,19 @@ __host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph
   };
   s.tw = take(sizeof(cplx_t<T>) * nph);
   s.node = take(sizeof(cplx_t<T>) * nth);
-  s.dft = take(dft_smem ? sizeof(T) * 4 * (size_t)(Kh + 1) * MP : 0);
+  s.dft = take(dft_smem ? sizeof(cplx_t<T>) * (size_t)(Kh + 1) * MP : 0);
   s.pl = take(sizeof(float) * (size_t)(S + 1) * N * plane_pitch(N));
   s.list = take(sizeof(int) * (size_t)R * nth);
   s.wsum = take(sizeof(int) * (kRingWarps + 2));
-  s.fold = take(sizeof(T) * 4 * (size_t)(Kh + 1) * RB);
-  s.mid = take(sizeof(T) * 2 * RB);
+  s.wbuf = take(sizeof(T) * (size_t)kRingWarps * wbuf_elems(Kh));
   s.total = o;
   return s;
 }
 
 // trilinear interpolation from the staged planes; pz0 = plane of floor(z) relative to the slab
-template <typename T>
-__device__ __forceinline__ T tri_smem(const float* __restrict__ pl, int N, int S, T px, T py, int pz0, T fz) {
+template <typename T, int NT>
+__device__ __forceinline__ T tri_smem(const float* __restrict__ pl, int Nr, int S, T px, T py, int pz0, T fz) {
+  const int N = NT ? NT : Nr;
   const int W = plane_pitch(N), P = N * W;
   const T fx0 = floor(px), fy0 = floor(py);
   const int x0 = (int)fx0, y0 = (int)fy0;
@@ -109,13 +113,6 @@ template <> struct V4<float> {
 template <> struct V4<double> {
   using t = double4;
 };
-template <typename T> struct V2;
-template <> struct V2<float> {
-  using t = float2;
-};
-template <> struct V2<double> {
-  using t = double2;
-};
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
@@ -123,25 +120,113 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool va
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n));
 }
 
+template <typename T> __device__ __forceinline__ T warp_allsum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Ring DFT outputs of one warp group: lanes own m (rounds of 32); an isolated leftover m (<= 2 of them)
+// is reduced across lanes instead of idling 30 lanes.
 template <typename T>
-__global__ void __launch_bounds__(kRingThreads) k_sh_rings(const float* __restrict__ vols,
-                                                           const T* __restrict__ shifts, int shift_stride,
-                                                           ShTables<T> tab, int S, int nslab, int RB,
-                                                           bool dft_smem, cplx_t<T>* __restrict__ G) {
+__device__ __forceinline__ void group_dft(const T* __restrict__ wb, int nr, int Kh, int L, bool mid,
+                                          const cplx_t<T>* __restrict__ dft, int MP, T dscale,
+                                          cplx_t<T>* const* __restrict__ gout, int lane) {
+  const int K1 = Kh + 1;
+  const T* midv = wb + 4 * K1 * kG;
+  int full = (L + 1) / 32, rem = (L + 1) - 32 * full;
+  if (rem > 2) {
+    ++full;
+    rem = 0;
+  }
+  for (int c = 0; c < full; ++c) {
+    const int m = 32 * c + lane;
+    const bool act = m <= L;
+    const int mm = act ? m : L;
+    const int par = mm & 1;
+    const T* P = wb + (2 * par) * K1 * kG;
+    const T* Q = wb + (2 * par + 1) * K1 * kG;
+    T re[kG], im[kG];
+#pragma unroll
+    for (int r = 0; r < kG; ++r) re[r] = im[r] = T(0);
+#pragma unroll 2
+    for (int k = 0; k < K1; ++k) {
+      const cplx_t<T> w = dft[k * MP + mm];
+      const typename V4<T>::t p0 = *reinterpret_cast<const typename V4<T>::t*>(P + k * kG);
+      const typename V4<T>::t p1 = *reinterpret_cast<const typename V4<T>::t*>(P + k * kG + 4);
+      const typename V4<T>::t q0 = *reinterpret_cast<const typename V4<T>::t*>(Q + k * kG);
+      const typename V4<T>::t q1 = *reinterpret_cast<const typename V4<T>::t*>(Q + k * kG + 4);
+      const T pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+      const T qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int r = 0; r < kG; ++r) {
+        re[r] = fma(pv[r], w.x, re[r]);
+        im[r] = fma(-qv[r], w.y, im[r]);
+      }
+    }
+    if (act)
+#pragma unroll
+      for (int r = 0; r < kG; ++r) {
+        if (r >= nr) break;
+        T vr = re[r], vi = im[r];
+        if (mid) {
+          const T am = midv[par * kG + r];
+          switch (m & 3) {  // e^{-i m pi/2}
+            case 0: vr += am; break;
+            case 1: vi -= am; break;
+            case 2: vr -= am; break;
+            default: vi += am; break;
+          }
+        }
+        gout[r][m] = mk<T>(vr * dscale, vi * dscale);
+      }
+  }
+  // leftover m (at most 2): lane r < nr owns ring r and runs the k loop itself
+  for (int e = 0; e < rem; ++e) {
+    const int m = 32 * full + e, par = m & 1;
+    if (lane < nr) {
+      const T* P = wb + (2 * par) * K1 * kG + lane;
+      const T* Q = wb + (2 * par + 1) * K1 * kG + lane;
+      T vr = T(0), vi = T(0);
+      for (int k = 0; k < K1; ++k) {
+        const cplx_t<T> w = dft[k * MP + m];
+        vr = fma(P[k * kG], w.x, vr);
+        vi = fma(-Q[k * kG], w.y, vi);
+      }
+      if (mid) {
+        const T am = midv[par * kG + lane];
+        switch (m & 3) {
+          case 0: vr += am; break;
+          case 1: vi -= am; break;
+          case 2: vr -= am; break;
+          default: vi += am; break;
+        }
+      }
+      gout[lane][m] = mk<T>(vr * dscale, vi * dscale);
+    }
+  }
+}
+
+template <typename T, int NT, bool DFT_SMEM>
+__global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __restrict__ vols,
+                                                              const T* __restrict__ shifts, int shift_stride,
+                                                              ShTables<T> tab, int S, int nslab,
+                                                              cplx_t<T>* __restrict__ G) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int N = tab.N, R = tab.R, L = tab.L, nth = tab.nth, nph = tab.nph, Kh = tab.Kh, MP = tab.MP;
-  const int Mp = nph / 2;
+  constexpr bool dft_smem = DFT_SMEM;
+  const int N = NT ? NT : tab.N;
+  const int R = tab.R, L = tab.L, nth = tab.nth, nph = tab.nph, Kh = tab.Kh, MP = tab.MP;
+  const int Mp = nph / 2, K1 = Kh + 1;
   const bool mid = (Mp % 2) == 0;
-  const RingLayout lay = ring_layout<T>(N, S, nth, nph, R, RB, Kh, MP, dft_smem);
+  const RingLayout lay = ring_layout<T>(N, S, nth, nph, R, Kh, MP, dft_smem);
   cplx_t<T>* tw = (cplx_t<T>*)(smem + lay.tw);
   cplx_t<T>* node = (cplx_t<T>*)(smem + lay.node);
-  const T* dft = dft_smem ? (const T*)(smem + lay.dft) : tab.dft;  // [p][cs][k][MP]
+  const cplx_t<T>* dft = dft_smem ? (const cplx_t<T>*)(smem + lay.dft) : tab.dft;
   float* pl = (float*)(smem + lay.pl);
   int* list = (int*)(smem + lay.list);  // packed (i << 16) | j
   int* wsum = (int*)(smem + lay.wsum);
-  T* fold = (T*)(smem + lay.fold);  // [4: Pe, Qe, Po, Qo][k][RB]
-  T* midv = (T*)(smem + lay.mid);   // [2][RB]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* wb = (T*)(smem + lay.wbuf) + (size_t)warp * wbuf_elems(Kh);
 
   const int64_t p = blockIdx.x / nslab;
   const int slab = blockIdx.x % nslab, zs = slab * S;
@@ -182,7 +267,7 @@ __global__ void __launch_bounds__(kRingThreads) k_sh_rings(const float* __restri
   for (int t = tid; t < nph; t += kRingThreads) tw[t] = tab.tw[t];
   for (int t = tid; t < nth; t += kRingThreads) node[t] = tab.node[t];
   if (dft_smem)
-    for (int t = tid; t < 4 * (Kh + 1) * MP; t += kRingThreads) ((T*)(smem + lay.dft))[t] = tab.dft[t];
+    for (int t = tid; t < K1 * MP; t += kRingThreads) ((cplx_t<T>*)(smem + lay.dft))[t] = tab.dft[t];
   // 2. ordered list of the rings whose floor(z) belongs to this slab: one thread per node j counts its
   //    shells (z = c_z + r_i x_j is monotone in i), then an ordered scan over j (deterministic)
   int count = 0;
@@ -199,7 +284,6 @@ __global__ void __launch_bounds__(kRingThreads) k_sh_rings(const float* __restri
           cnt += (zb >= lo && zb < hi);
         }
       }
-      // block exclusive scan of cnt
       int v = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -225,114 +309,68 @@ __global__ void __launch_bounds__(kRingThreads) k_sh_rings(const float* __restri
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
+  // 3. warp-local work: a balanced contiguous range of rings per warp, in groups of kG
   const T dscale = T(2.0 * kPi) / (T)nph;
-  const int nm0 = L / 2 + 1, nm1 = (L + 1) / 2;  // number of even / odd m in [0, L]
-  const int mt0 = (nm0 + 3) / 4, mt1 = (nm1 + 3) / 4;
-  // 3. batches of RB rings: gather + fold (one warp per ring, lanes over k), then the tiled real GEMMs
-  for (int b0 = 0; b0 < count; b0 += RB) {
-    const int nb = min(RB, count - b0);
-    // items (ring rr, k in [0, Kh]) flattened over the CTA; (rr, k) advanced incrementally
+  const int r_begin = (int)(((long long)count * warp) / kRingWarps);
+  const int r_end = (int)(((long long)count * (warp + 1)) / kRingWarps);
+  for (int g0 = r_begin; g0 < r_end; g0 += kG) {
+    const int nr = min(kG, r_end - g0);
+    // fold items (ring r, k): r = item / K1, k = item % K1, advanced incrementally by 32
     {
-      const int K1 = Kh + 1;
-      const int drr = kRingThreads / K1, dk = kRingThreads - drr * K1;
-      int rr = tid / K1, k = tid - rr * K1;
-      for (; rr < nb;) {
-        const int ring = list[b0 + rr];
+      int r = 0, k = lane;
+      while (k >= K1) {
+        k -= K1;
+        ++r;
+      }
+      for (; r < nr;) {
+        const int ring = list[g0 + r];
         const int i = ring >> 16, j = ring & 0xffff;
-        const T r = (T)i + T(0.5);
+        const T rad = (T)i + T(0.5);
         const cplx_t<T> nd = node[j];
-        const T rs = r * nd.y;
-        const T z = fma(r, nd.x, cz);
+        const T rs = rad * nd.y;
+        const T z = fma(rad, nd.x, cz);
         const T fz0 = floor(z);
         const int pz0 = (int)fz0 - zs;
         const T fz = z - fz0;
         auto samp = [&](int kk) {
           const cplx_t<T> ph = tw[kk];
-          return tri_smem<T>(pl, N, S, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0, fz);
+          return tri_smem<T, NT>(pl, N, S, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0, fz);
         };
         const bool k0 = (k == 0);
-        const int k2 = Mp - k;
         const T s1 = samp(k), s2 = samp(k + Mp);
-        const T s3 = k0 ? T(0) : samp(k2), s4 = k0 ? T(0) : samp(k2 + Mp);
+        T s3 = T(0), s4 = T(0);
+        if (!k0) {
+          s3 = samp(Mp - k);
+          s4 = samp(2 * Mp - k);
+        }
         const T ap = s1 + s2, am = s1 - s2, bp = s3 + s4, bm = s3 - s4;
-        fold[(0 * K1 + k) * RB + rr] = ap + bp;               // even m, cos
-        fold[(1 * K1 + k) * RB + rr] = k0 ? T(0) : ap - bp;   // even m, sin
-        fold[(2 * K1 + k) * RB + rr] = am - bm;               // odd m, cos
-        fold[(3 * K1 + k) * RB + rr] = k0 ? T(0) : am + bm;   // odd m, sin
+        wb[(0 * K1 + k) * kG + r] = ap + bp;  // even m, cos
+        wb[(1 * K1 + k) * kG + r] = ap - bp;  // even m, sin (0 at k = 0)
+        wb[(2 * K1 + k) * kG + r] = am - bm;  // odd m, cos
+        wb[(3 * K1 + k) * kG + r] = am + bm;  // odd m, sin (0 at k = 0)
         if (k0 && mid) {
           const int km = Mp / 2;
           const T a = samp(km), bb = samp(km + Mp);
-          midv[rr] = a + bb;
-          midv[RB + rr] = a - bb;
+          wb[4 * K1 * kG + r] = a + bb;
+          wb[4 * K1 * kG + kG + r] = a - bb;
         }
-        rr += drr;
-        k += dk;
-        if (k >= K1) {
+        k += 32;
+        while (k >= K1) {
           k -= K1;
-          ++rr;
+          ++r;
         }
       }
     }
-    __syncthreads();
-    // tiles: (parity, m-tile of 4, ring-pair)
-    const int rt = RB / 2;
-    const int ntile = (mt0 + mt1) * rt;
-    for (int t = tid; t < ntile; t += kRingThreads) {
-      const int mtl = t / rt, rp = t - mtl * rt;
-      const int par = mtl >= mt0 ? 1 : 0;
-      const int mt = par ? mtl - mt0 : mtl;
-      if (2 * rp >= nb) continue;
-      const T* P = fold + (2 * par) * (Kh + 1) * RB + 2 * rp;
-      const T* Q = fold + (2 * par + 1) * (Kh + 1) * RB + 2 * rp;
-      const T* C = dft + ((par * 2 + 0) * (Kh + 1)) * MP + 4 * mt;
-      const T* Sn = dft + ((par * 2 + 1) * (Kh + 1)) * MP + 4 * mt;
-      T re[2][4], im[2][4];
+    __syncwarp();
+    cplx_t<T>* gout[kG];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) re[a][b] = im[a][b] = T(0);
-#pragma unroll 4
-      for (int k = 0; k <= Kh; ++k) {
-        const typename V2<T>::t pv = *reinterpret_cast<const typename V2<T>::t*>(P + k * RB);
-        const typename V2<T>::t qv = *reinterpret_cast<const typename V2<T>::t*>(Q + k * RB);
-        const typename V4<T>::t cv = *reinterpret_cast<const typename V4<T>::t*>(C + k * MP);
-        const typename V4<T>::t sv = *reinterpret_cast<const typename V4<T>::t*>(Sn + k * MP);
-        const T pr[2] = {pv.x, pv.y}, qr[2] = {qv.x, qv.y};
-        const T cr[4] = {cv.x, cv.y, cv.z, cv.w}, sr[4] = {sv.x, sv.y, sv.z, sv.w};
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            re[a][b] = fma(pr[a], cr[b], re[a][b]);
-            im[a][b] = fma(-qr[a], sr[b], im[a][b]);
-          }
-      }
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int rr = 2 * rp + a;
-        if (rr >= nb) continue;
-        const int ring = list[b0 + rr];
-        const int i = ring >> 16, j = ring & 0xffff;
-        cplx_t<T>* Gr = G + (((int64_t)p * R + i) * nth + j) * (L + 1);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int m = 2 * (4 * mt + b) + par;
-          if (m > L) continue;
-          T vr = re[a][b], vi = im[a][b];
-          if (mid) {
-            const T am = midv[par * RB + rr];
-            switch (m & 3) {  // e^{-i m pi/2}
-              case 0: vr += am; break;
-              case 1: vi -= am; break;
-              case 2: vr -= am; break;
-              default: vi += am; break;
-            }
-          }
-          Gr[m] = mk<T>(vr * dscale, vi * dscale);
-        }
-      }
+    for (int r = 0; r < kG; ++r) {
+      const int ring = list[g0 + min(r, nr - 1)];
+      const int i = ring >> 16, j = ring & 0xffff;
+      gout[r] = G + (((int64_t)p * R + i) * nth + j) * (L + 1);
     }
-    __syncthreads();
+    group_dft<T>(wb, nr, Kh, L, mid, dft, MP, dscale, gout, lane);
+    __syncwarp();
   }
 }
 
@@ -441,37 +479,33 @@ __global__ void __launch_bounds__(512) k_sh_legendre(const cplx_t<T>* __restrict
 }
 
 template <typename T> struct ShPlan {
-  int RB, S, nslab;
+  int S, nslab;
   bool dft_smem;
   size_t rbytes;
 };
 
 template <typename T> ShPlan<T> sh_plan(const ShTables<T>& tab) {
-  // one CTA (512 threads) per SM: the deepest slab (<= 8 planes) and the largest ring batch that fit;
-  // the DFT table moves to global memory (L1) only if shared memory cannot hold it
+  // one CTA (512 threads) per SM: the deepest slab (<= 8 planes) that fits; the DFT table moves to global
+  // memory (read through L1) only if shared memory cannot hold it
   ShPlan<T> pl;
-  const size_t budget = 220 * 1024;
+  const size_t budget = 224 * 1024;
   for (int pass = 0; pass < 2; ++pass) {
     const bool ds = (pass == 0);
     for (int S = 8; S >= 1; --S) {
-      int RB = 64;
-      auto tot = [&](int rb) { return ring_layout<T>(tab.N, S, tab.nth, tab.nph, tab.R, rb, tab.Kh, tab.MP, ds).total; };
-      while (RB > 8 && tot(RB) > budget) RB -= 8;
-      if (tot(RB) <= budget && (RB >= 32 || S == 1)) {
+      const size_t tot = ring_layout<T>(tab.N, S, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, ds).total;
+      if (tot <= budget) {
         pl.S = S;
-        pl.RB = RB;
         pl.dft_smem = ds;
         pl.nslab = (tab.N + S - 1) / S;
-        pl.rbytes = tot(RB);
+        pl.rbytes = tot;
         return pl;
       }
     }
   }
   pl.S = 1;
-  pl.RB = 8;
   pl.dft_smem = false;
   pl.nslab = tab.N;
-  pl.rbytes = ring_layout<T>(tab.N, 1, tab.nth, tab.nph, tab.R, 8, tab.Kh, tab.MP, false).total;
+  pl.rbytes = ring_layout<T>(tab.N, 1, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false).total;
   return pl;
 }
 
@@ -481,28 +515,50 @@ template <typename T> size_t sh_ring_workspace_elems(const ShTables<T>& tab) {
   return (size_t)tab.R * tab.nth * (tab.L + 1);
 }
 
+template <typename T, int NT, bool DS>
+static cudaError_t launch_rings_nt(const float* vols, int64_t nb, const T* shifts, int shift_stride,
+                                   const ShTables<T>& tab, const ShPlan<T>& plan, cplx_t<T>* Gws, cudaStream_t st) {
+  cudaError_t e =
+      cudaFuncSetAttribute(k_sh_rings<T, NT, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.rbytes);
+  if (e != cudaSuccess) return e;
+  k_sh_rings<T, NT, DS><<<(unsigned)(nb * plan.nslab), kRingThreads, plan.rbytes, st>>>(vols, shifts, shift_stride, tab,
+                                                                                       plan.S, plan.nslab, Gws);
+  return cudaGetLastError();
+}
+
+template <typename T, bool DS>
+static cudaError_t launch_rings(const float* vols, int64_t nb, const T* shifts, int shift_stride,
+                                const ShTables<T>& tab, const ShPlan<T>& plan, cplx_t<T>* Gws, cudaStream_t st) {
+  switch (tab.N) {  // compile-time box edges: immediate shared-memory offsets in the trilinear gathers
+    case 16: return launch_rings_nt<T, 16, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
+    case 32: return launch_rings_nt<T, 32, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
+    case 64: return launch_rings_nt<T, 64, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
+    case 96: return launch_rings_nt<T, 96, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
+    case 128: return launch_rings_nt<T, 128, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
+    default: return launch_rings_nt<T, 0, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
+  }
+}
+
 template <typename T>
 cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, int shift_stride, const ShTables<T>& tab,
                                cplx_t<T>* F, cplx_t<T>* Gws, int64_t gws_particles, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   const int N = tab.N, ncf = ncoef(tab.L);
   const ShPlan<T> plan = sh_plan<T>(tab);
-  cudaError_t e = cudaFuncSetAttribute(k_sh_rings<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.rbytes);
-  if (e != cudaSuccess) return e;
   const int JP = 8;
   const size_t lbytes = leg_layout<T>(4, JP, tab.L).total;
   const int lthreads = std::min(512, (leg_tiles(tab.L) + 31) / 32 * 32);
-  e = cudaFuncSetAttribute(k_sh_legendre<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes);
+  cudaError_t e = cudaFuncSetAttribute(k_sh_legendre<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes);
   if (e != cudaSuccess) return e;
   for (int64_t c0 = 0; c0 < B; c0 += gws_particles) {
     const int64_t nb = std::min<int64_t>(gws_particles, B - c0);
-    k_sh_rings<T><<<(unsigned)(nb * plan.nslab), kRingThreads, plan.rbytes, st>>>(
-        vols + c0 * (int64_t)N * N * N, shifts ? shifts + c0 * shift_stride : nullptr, shift_stride, tab, plan.S,
-        plan.nslab, plan.RB, plan.dft_smem, Gws);
-    e = cudaGetLastError();
+    const float* v = vols + c0 * (int64_t)N * N * N;
+    const T* sh = shifts ? shifts + c0 * shift_stride : nullptr;
+    e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
+                      : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
     if (e != cudaSuccess) return e;
     k_sh_legendre<T><<<(unsigned)(nb * (tab.R / 4)), lthreads, lbytes, st>>>(Gws, tab, JP,
-                                                                                 F + c0 * (int64_t)ncf * tab.R);
+                                                                              F + c0 * (int64_t)ncf * tab.R);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

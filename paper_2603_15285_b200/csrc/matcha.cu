@@ -147,7 +147,7 @@ template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
   t.tw = (const cplx_t<T>*)h->d_tw;
   t.pwm = (const T*)h->d_pw;
   t.pw_moff = h->d_pw_moff;
-  t.dft = (const T*)h->d_dft;
+  t.dft = (const cplx_t<T>*)h->d_dft;
   t.Kh = h->Kh;
   t.MP = h->MP;
   t.pw_stride = h->pw_stride;
@@ -367,20 +367,17 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     for (int l = 0; l <= h->L; ++l)
       for (int mm = 0; mm <= l; ++mm) pw[(size_t)j * h->pw_stride + moff[mm] + (l - mm)] = w[j] * P[lm_index(l, mm)];
   }
-  // folded ring-DFT table: [parity][cos, sin][k = 0..Kh][mi < MP], m = 2 mi + parity
+  // folded ring-DFT table: [k = 0..Kh][m = 0..L] (cos, sin)(m phi_k)
   const int Mp = h->nph / 2;
   h->Kh = (Mp - 1) / 2;
-  h->MP = ((h->L / 2 + 1) + 3) / 4 * 4;
-  std::vector<double> dft((size_t)4 * (h->Kh + 1) * h->MP, 0.0);
-  for (int par = 0; par < 2; ++par)
-    for (int k = 0; k <= h->Kh; ++k)
-      for (int mi = 0; mi < h->MP; ++mi) {
-        const int mm = 2 * mi + par;
-        if (mm > h->L) continue;
-        const double ang = 2.0 * kPi * (double)((long)mm * k % h->nph) / h->nph;
-        dft[((size_t)(par * 2 + 0) * (h->Kh + 1) + k) * h->MP + mi] = std::cos(ang);
-        dft[((size_t)(par * 2 + 1) * (h->Kh + 1) + k) * h->MP + mi] = std::sin(ang);
-      }
+  h->MP = h->L + 1;
+  std::vector<double> dft((size_t)2 * (h->Kh + 1) * h->MP, 0.0);
+  for (int k = 0; k <= h->Kh; ++k)
+    for (int mm = 0; mm <= h->L; ++mm) {
+      const double ang = 2.0 * kPi * (double)((long)mm * k % h->nph) / h->nph;
+      dft[2 * ((size_t)k * h->MP + mm)] = std::cos(ang);
+      dft[2 * ((size_t)k * h->MP + mm) + 1] = std::sin(ang);
+    }
   // stage-3/4 pair table, grouped by shell l0 = max(m,|n|): long l-runs first
   std::vector<PairDesc> pairs;
   std::vector<double> plnc;

@@ -26,13 +26,16 @@ template <> __device__ __forceinline__ double exp_t<double>(double x) { return e
 
 // Per-rotation quantities used by the seeds: ln cos(b/2), ln sin(b/2) (clamped away from -inf).
 template <typename T> struct BetaLogs {
-  T lnc, lns;
+  T lnc, lns;  // ln cos(b/2), ln sin(b/2)
+  T cs, sc;    // cos(b/2)/sin(b/2), sin(b/2)/cos(b/2) (clamped), for the seed derivative
 };
 template <typename T> __device__ __forceinline__ BetaLogs<T> beta_logs(double beta) {
   double c = cos(0.5 * beta), s = sin(0.5 * beta);
   BetaLogs<T> r;
   r.lnc = (T)log(fmax(c, 1e-300));
   r.lns = (T)log(fmax(s, 1e-300));
+  r.cs = (T)(c / fmax(s, 1e-30));
+  r.sc = (T)(s / fmax(c, 1e-30));
   return r;
 }
 
@@ -45,11 +48,8 @@ __device__ __forceinline__ void wigner_seed(int m, int n, T lnC, const BetaLogs<
   const T eq = q ? (T)q * bl.lns : T(0);
   d = sgn * exp_t<T>(lnC + ep + eq);
   if (DERIV) {
-    // d/db [c^p s^q] = 1/2 (q c^{p+1} s^{q-1} - p c^{p-1} s^{q+1}),  c = cos(b/2), s = sin(b/2)
-    T t1 = T(0), t2 = T(0);
-    if (q) t1 = (T)q * exp_t<T>(lnC + (T)(p + 1) * bl.lnc + (q > 1 ? (T)(q - 1) * bl.lns : T(0)));
-    if (p) t2 = (T)p * exp_t<T>(lnC + (p > 1 ? (T)(p - 1) * bl.lnc : T(0)) + (T)(q + 1) * bl.lns);
-    dp = sgn * T(0.5) * (t1 - t2);
+    // d/db [c^p s^q] = 1/2 c^p s^q (q c/s - p s/c),  c = cos(b/2), s = sin(b/2)
+    dp = T(0.5) * d * ((T)q * bl.cs - (T)p * bl.sc);
   }
 }
 
