@@ -109,5 +109,12 @@ template <typename T>
 cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
                                 T* poses, cudaStream_t s);
 size_t search_smem_bytes(int L0, int K, bool fp64);
+template <typename T>
+cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estride, int64_t nb, T* rho, cudaStream_t s);
+template <typename T> cudaError_t launch_to_real(const float* in, T* out, int64_t n, cudaStream_t s);
+template <typename T> cudaError_t launch_cross_spectrum(const cplx_t<T>* F, cplx_t<T>* X, int64_t n, cudaStream_t s);
+template <typename T>
+cudaError_t launch_window_peak(const T* corr, int N, int W, int64_t nb, T* shifts, int sstride, T* peak,
+                               cudaStream_t s);
 
 }  // namespace matcha

@@ -4,6 +4,7 @@
 // Tables are computed here in double precision (own Gauss-Legendre Newton solve and normalised
 // associated-Legendre recurrence; no code is shared with oracle/) and cast to the handle precision.
 #include <cuda_runtime.h>
+#include <cufft.h>
 
 #include <algorithm>
 #include <cmath>
@@ -49,6 +50,14 @@ struct matcha_ctx {
   cudaEvent_t ev_used[2] = {nullptr, nullptr};
   int64_t launches = 0;
   std::string err;
+  // stage 5 (translation): batched cuFFT plans and workspaces, allocated on first use
+  cufftHandle plan_r2c = 0, plan_c2r = 0;
+  int64_t plan_batch = 0;
+  void* ws_Fhat = nullptr;   // complex [mb][N][N][N/2+1]  F^ of the chunk's particles
+  void* ws_Xhat = nullptr;   // complex [mb][N][N][N/2+1]  rho^, then the cross spectrum
+  void* ws_rho = nullptr;    // real [mb][N^3]             rotated references, then c(t)
+  void* ws_peak = nullptr;   // real [mb]
+  void* ws_euler1 = nullptr; // real [mb][3]
   // per-stage event tracing
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -266,6 +275,84 @@ static cudaError_t do_refine(matcha_handle_t h, const void* M, int32_t L_M, int6
   return launch_newton_refine<T>(a, s);
 }
 
+// ---------------------------------------------------------------- stage 5 helpers
+static matcha_status_t trans_prepare(matcha_handle_t h, int64_t nb) {
+  const int N = h->cfg.N;
+  const int64_t nr = (int64_t)N * N * N, nc = (int64_t)N * N * (N / 2 + 1), mb = h->cfg.max_batch;
+  if (!h->ws_Fhat) {
+    cudaError_t e = cudaMalloc(&h->ws_Fhat, 2 * h->rsz * nc * mb);
+    if (e == cudaSuccess) e = cudaMalloc(&h->ws_Xhat, 2 * h->rsz * nc * mb);
+    if (e == cudaSuccess) e = cudaMalloc(&h->ws_rho, h->rsz * nr * mb);
+    if (e == cudaSuccess) e = cudaMalloc(&h->ws_peak, h->rsz * mb);
+    if (e == cudaSuccess) e = cudaMalloc(&h->ws_euler1, 3 * h->rsz * mb);
+    if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation workspace allocation failed");
+  }
+  if (h->plan_batch != nb) {
+    if (h->plan_r2c) cufftDestroy(h->plan_r2c);
+    if (h->plan_c2r) cufftDestroy(h->plan_c2r);
+    h->plan_r2c = h->plan_c2r = 0;
+    int n[3] = {N, N, N};
+    if (cufftPlanMany(&h->plan_r2c, 3, n, nullptr, 1, 0, nullptr, 1, 0, h->fp64 ? CUFFT_D2Z : CUFFT_R2C, (int)nb) !=
+            CUFFT_SUCCESS ||
+        cufftPlanMany(&h->plan_c2r, 3, n, nullptr, 1, 0, nullptr, 1, 0, h->fp64 ? CUFFT_Z2D : CUFFT_C2R, (int)nb) !=
+            CUFFT_SUCCESS)
+      return fail(h, MATCHA_ERR_CUDA, "cuFFT plan creation failed");
+    h->plan_batch = nb;
+  }
+  return MATCHA_OK;
+}
+
+static bool fft_r2c(matcha_handle_t h, void* in, void* out, cudaStream_t s) {
+  cufftSetStream(h->plan_r2c, s);
+  return (h->fp64 ? cufftExecD2Z(h->plan_r2c, (cufftDoubleReal*)in, (cufftDoubleComplex*)out)
+                  : cufftExecR2C(h->plan_r2c, (cufftReal*)in, (cufftComplex*)out)) == CUFFT_SUCCESS;
+}
+static bool fft_c2r(matcha_handle_t h, void* in, void* out, cudaStream_t s) {
+  cufftSetStream(h->plan_c2r, s);
+  return (h->fp64 ? cufftExecZ2D(h->plan_c2r, (cufftDoubleComplex*)in, (cufftDoubleReal*)out)
+                  : cufftExecC2R(h->plan_c2r, (cufftComplex*)in, (cufftReal*)out)) == CUFFT_SUCCESS;
+}
+
+// F^ of nb particle volumes into ws_Fhat (once per chunk; the particles do not change across alternations)
+static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t nb, cudaStream_t s) {
+  const int N = h->cfg.N;
+  const int64_t nr = (int64_t)N * N * N;
+  matcha_status_t st = trans_prepare(h, nb);
+  if (st != MATCHA_OK) return st;
+  void* in = (void*)vols;
+  if (h->fp64) {
+    cudaError_t e = launch_to_real<double>(vols, (double*)h->ws_rho, nb * nr, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: to_real");
+    h->launches++;
+    in = h->ws_rho;
+  }
+  if (!fft_r2c(h, in, h->ws_Fhat, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT R2C of the particles failed");
+  return MATCHA_OK;
+}
+
+// t = windowed argmax of c(t) = IFFT(F^ conj(rho^)) for the rotations `euler` (stride estride)
+static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* ref, const void* euler, int estride,
+                                    int W, void* shifts, int sstride, void* peak, cudaStream_t s) {
+  const int N = h->cfg.N;
+  const int64_t nc = (int64_t)N * N * (N / 2 + 1);
+  cudaError_t e;
+  ProfScope ps(h, 5, s);
+  e = h->fp64 ? launch_rotate_ref<double>(ref, N, (const double*)euler, estride, nb, (double*)h->ws_rho, s)
+              : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
+  if (!fft_r2c(h, h->ws_rho, h->ws_Xhat, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT R2C of rho failed");
+  e = h->fp64 ? launch_cross_spectrum<double>((const double2*)h->ws_Fhat, (double2*)h->ws_Xhat, nb * nc, s)
+              : launch_cross_spectrum<float>((const float2*)h->ws_Fhat, (float2*)h->ws_Xhat, nb * nc, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "translation: cross_spectrum");
+  if (!fft_c2r(h, h->ws_Xhat, h->ws_rho, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT C2R failed");
+  e = h->fp64 ? launch_window_peak<double>((const double*)h->ws_rho, N, W, nb, (double*)shifts, sstride,
+                                           (double*)peak, s)
+              : launch_window_peak<float>((const float*)h->ws_rho, N, W, nb, (float*)shifts, sstride, (float*)peak, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "translation: window_peak");
+  h->launches += 3;
+  return MATCHA_OK;
+}
+
 // App. C alternation around Algorithm 1 for particles [0, B) of `vols`, chunked by max_batch.
 static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_t B, const float* ref,
                                     const void* ref_coeffs, const matcha_params_t* p, void* poses, cudaStream_t s) {
@@ -315,7 +402,13 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
       if (e != cudaSuccess) return cuda_fail(h, e, "align: gather_poses");
       h->launches++;
       if (translate) {
-        return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align: translation update not implemented yet");
+        if (tau == 0) {
+          st = trans_fhat(h, vols + c0 * n3, nb, s);
+          if (st != MATCHA_OK) return st;
+        }
+        // t^tau from the rotation just estimated (poses[b][0..2]) -> poses[b][3..5]
+        st = trans_update(h, nb, ref, pc, 8, p->shift_window, pc + 3 * h->rsz, 8, h->ws_peak, s);
+        if (st != MATCHA_OK) return st;
       }
     }
   }
@@ -442,6 +535,10 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->plan_r2c) cufftDestroy(h->plan_r2c);
+  if (h->plan_c2r) cufftDestroy(h->plan_c2r);
+  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1})
+    if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
@@ -592,8 +689,21 @@ MATCHA_API matcha_status_t matcha_newton_refine(matcha_handle_t h, const void* M
 MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const float* vols, int64_t B,
                                                      const float* ref, const void* euler, int32_t window,
                                                      void* shifts, void* peak, void* stream) {
-  (void)vols; (void)B; (void)ref; (void)euler; (void)window; (void)shifts; (void)peak; (void)stream;
-  return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "translation_update: not implemented yet");
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!vols || !ref || !euler || !shifts)))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "translation_update: bad arguments");
+  if (window < 0 || window > h->cfg.N / 4) return fail(h, MATCHA_ERR_WINDOW, "translation_update: W > N/4");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n3 = (int64_t)h->cfg.N * h->cfg.N * h->cfg.N;
+  for (int64_t c0 = 0; c0 < B; c0 += h->cfg.max_batch) {
+    const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
+    matcha_status_t st = trans_fhat(h, vols + c0 * n3, nb, s);
+    if (st != MATCHA_OK) return st;
+    st = trans_update(h, nb, ref, (const char*)euler + c0 * 3 * h->rsz, 3, window, (char*)shifts + c0 * 3 * h->rsz, 3,
+                      peak ? (char*)peak + c0 * h->rsz : h->ws_peak, s);
+    if (st != MATCHA_OK) return st;
+  }
+  return MATCHA_OK;
 }
 
 

@@ -281,3 +281,64 @@ def test_invalid_arguments_rejected():
         h.newton_refine(M, 8, torch.zeros((1, 4, 3), device=DEV), mt.Params(bands=[6, 4]))
     with pytest.raises(mt.MatchaError):
         mt.Handle(N=33, L_max=8)
+
+
+# ------------------------------------------------------------------ stage 5: translation (App. C)
+@pytest.mark.parametrize("N,W,shift_mode", [(32, 4, gen.SHIFT_FIXED), (32, 3, gen.SHIFT_UNIFORM), (64, 8, gen.SHIFT_UNIFORM)])
+def test_translation_update_parity(N, W, shift_mode, prec):
+    B = 4
+    b = gen.particles(N, B, 1.0, seed=41, shift_mode=shift_mode, shift_max=W - 1.0, fixed_shift=(1.0, -2.0, 1.0))
+    eul = np.array([O.matrix_to_euler(R) for R in b.truth_R])
+    eul[1] += 0.01  # a slightly wrong rotation: the peak is still well defined
+    h = handle(N, 8, prec)
+    sh, pk = h.translation_update(cuda(b.vols), cuda(b.ref), cuda(eul, h.real), W)
+    sh, pk = to_np(sh), to_np(pk)
+    eul_used = to_np(cuda(eul, h.real)).astype(np.float64)
+    for p in range(B):
+        so, po = O.translation(b.vols[p], b.ref, eul_used[p], W)
+        assert np.abs(sh[p] - so).max() < (1e-6 if prec == "fp64" else 2e-3), (p, sh[p], so)
+        assert abs(pk[p] - po) <= (1e-9 if prec == "fp64" else 1e-4) * abs(po)
+        assert np.abs(sh[p] - b.truth_t[p]).max() < 0.6  # near the planted shift
+
+
+def test_translation_integer_shifts_exact_gpu():
+    N = 32
+    ref = gen.render(gen.reference_blobs(), N)[0]
+    shifts = [(0, 0, 0), (3, -2, 1), (-4, 4, -1), (1, 1, -3)]
+    vols = np.stack([np.roll(ref, shift=(t[2], t[1], t[0]), axis=(0, 1, 2)) for t in shifts])
+    h = handle(N, 8, "fp64")
+    sh, _ = h.translation_update(cuda(vols), cuda(ref), cuda(np.zeros((4, 3)), h.real), 4)
+    assert np.abs(to_np(sh) - np.array(shifts, float)).max() < 1e-9
+
+
+def test_alternation_c1_exact_recovery():
+    """configs[0]: one noise-free 32^3 volume, known rotation + integer shift (1,-2,1), L0=4 -> 8, N_C=4, T=8."""
+    b = gen.particles(32, 2, float("inf"), seed=12, shift_mode=gen.SHIFT_FIXED, fixed_shift=(1.0, -2.0, 1.0))
+    h = handle(32, 8)
+    params = mt.Params(bands=[4, 6, 8], n_cand=4, oversample=2, n_alternations=8, shift_window=4)
+    poses = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    h.status()
+    po = O.align_batch(b.vols, b.ref, dict(L=8, qover=2, L0=4, K=2, ncand=4, bands=[4, 6, 8], iters=1, T=8, W=4))
+    for p in range(2):
+        assert rot_err_deg(poses[p, :3], po[p, :3]) < TOL_ROT_DEG
+        assert np.abs(poses[p, 3:6] - po[p, 3:6]).max() < 0.1
+        assert O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) < 0.05
+        assert np.abs(poses[p, 3:6] - b.truth_t[p]).max() < 0.01
+
+
+def test_alternation_c3_shape_sampled():
+    """configs[2] shape: 96^3, SNR 0.05, L0=8 -> 48, shifts U[-4,4]^3, T=3, W=6 (App. C); oracle on a sample."""
+    B = 48
+    b = gen.particles(96, B, 0.05, seed=43, shift_mode=gen.SHIFT_UNIFORM, shift_max=4.0)
+    bands = [8, 12, 16, 24, 32, 48]
+    h = handle(96, 48, max_batch=B)
+    params = mt.Params(bands=bands, n_cand=10, oversample=2, n_alternations=3, shift_window=6)
+    poses = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    h.status()
+    sel = [0, 17, 33]
+    po = O.align_batch(b.vols[sel], b.ref, dict(L=48, qover=2, L0=8, K=2, ncand=10, bands=bands, iters=1, T=3, W=6))
+    for i, p in enumerate(sel):
+        assert rot_err_deg(poses[p, :3], po[i, :3]) < TOL_ROT_DEG, (p, rot_err_deg(poses[p, :3], po[i, :3]))
+        assert np.abs(poses[p, 3:6] - po[i, 3:6]).max() < 0.1
+    errs = [O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) for p in range(B)]
+    assert np.median(errs) < 2.0
