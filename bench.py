@@ -226,18 +226,14 @@ def main():
     ref = ref_host.to(dev)
     h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=P)
     params = mt.Params(bands=c["bands"], n_cand=c["ncand"], oversample=c["K"], newton_iters=c["iters"])
+    from paper_2603_15285_b200 import dist as D
     H = torch.empty((ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
-    poses = torch.empty((P, 8), dtype=torch.float32, device=dev)
-    gathered = torch.empty((P * world, 8), dtype=torch.float32, device=dev) if world > 1 else None
+    counts = [P] * world
 
     def step():
-        if rank == 0:
-            h.sh_analysis(ref[None], out=H[None])          # reference coefficients (stage a3)
-        if world > 1:
-            dist.broadcast(H, src=0)                        # NCCL over NVLink: 140 KiB at c2
-        h.align_batch(vols, None, params, ref_coeffs=H, out=poses)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, poses)    # 32 B per particle
+        # rank 0: reference coefficients (stage a3) -> NCCL broadcast (140 KiB at c2) -> every rank aligns its
+        # shard -> NCCL all_gather of the poses (32 B per particle)
+        D.align_step(h, vols, ref, params, H, rank, counts=counts)
 
     for _ in range(args.warmup):
         step()
@@ -264,11 +260,7 @@ def main():
         dist.barrier()
     stages = h.profile_end()
     n_launch = h.launches - n_launch0
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = D.max_over_ranks(e0.elapsed_time(e1), device=dev)
     clocks = clk.stop()
     h.status()
 
@@ -287,11 +279,7 @@ def main():
         ksteps = max(3, min(args.steps, 10))
         for _ in range(ksteps):
             h.align_batch_host(vols_host, ref_host, params, out=out_host)
-        dt = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([dt], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = D.max_over_ranks(time.perf_counter() - t0, device=dev)
         e2e = {"value": P * world * ksteps / dt, "unit": "particles/s",
                "h2d_bytes_per_step": int(vols_host.numel() * 4 + ref_host.numel() * 4),
                "d2h_bytes_per_step": int(out_host.numel() * 4)}

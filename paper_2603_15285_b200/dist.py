@@ -1,0 +1,68 @@
+"""Data-parallel driver over particles: one process per GPU, torch.distributed for plumbing.
+
+The path shards naturally -- particles are independent -- so there is no exchange inside it.  The only two
+collectives (NCCL over NVLink on B200; any backend works, the CPU tests use gloo):
+  1. broadcast of the reference coefficients H (complex [ncoef][R], 140 KiB at 64^3/L=32) from rank 0;
+  2. all_gather of the poses (8 reals = 32 B per particle in FP32).
+Rank r of G owns the contiguous particle range [floor(r P/G), floor((r+1) P/G)).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard(P: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous particle range of `rank` (SURVEY 8(e) partitioning)."""
+    return (P * rank) // world, (P * (rank + 1)) // world
+
+
+def broadcast_ref_coeffs(H: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """Reference coefficients computed on `src` are broadcast in place (complex tensors are sent as real views)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast(torch.view_as_real(H) if H.is_complex() else H, src=src, group=group)
+    return H
+
+
+def gather_poses(poses: torch.Tensor, counts: Optional[list[int]] = None, group=None) -> torch.Tensor:
+    """All-gather per-rank pose blocks [n_r, 8] into [sum n_r, 8] in rank order (ragged shards padded)."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return poses
+    world = dist.get_world_size(group)
+    if counts is None:
+        n = torch.tensor([poses.shape[0]], device=poses.device, dtype=torch.int64)
+        alln = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(alln, n, group=group)
+        counts = [int(x.item()) for x in alln]
+    mx = max(counts)
+    buf = torch.zeros((mx, poses.shape[1]), dtype=poses.dtype, device=poses.device)
+    buf[: poses.shape[0]] = poses
+    out = torch.empty((mx * world, poses.shape[1]), dtype=poses.dtype, device=poses.device)
+    if poses.is_cuda:
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        parts = list(out.chunk(world))
+        dist.all_gather(parts, buf, group=group)
+    return torch.cat([out[r * mx: r * mx + counts[r]] for r in range(world)])
+
+
+def max_over_ranks(x: float, device=None, group=None) -> float:
+    """Elapsed time of a multi-GPU run = max over ranks (device-timed by each rank)."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def align_step(handle, vols_local: torch.Tensor, ref: torch.Tensor, params, H: torch.Tensor,
+               rank: int, group=None, counts: Optional[list[int]] = None) -> torch.Tensor:
+    """One data-parallel step: rank 0 analyses the reference, H is broadcast, every rank aligns its shard with
+    the shared H, the poses are gathered.  `handle` is a paper_2603_15285_b200.Handle (or a test double)."""
+    if rank == 0:
+        handle.sh_analysis(ref[None], out=H[None])
+    broadcast_ref_coeffs(H, src=0, group=group)
+    poses = handle.align_batch(vols_local, None, params, ref_coeffs=H)
+    return gather_poses(poses, counts=counts, group=group)

@@ -1,0 +1,86 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the data-parallel host logic of bench.py / dist.py:
+sharding covers every particle exactly once, the reference coefficients are broadcast from rank 0, poses are
+gathered in global particle order (ragged shards too), and the elapsed time is the max over ranks."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_15285_b200 import dist as D
+
+
+def test_shard_covers_all_particles_once():
+    for P in (0, 1, 7, 1000, 100001):
+        for world in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(world):
+                a, b = D.shard(P, world, r)
+                assert 0 <= a <= b <= P
+                seen.extend(range(a, b))
+            assert seen == list(range(P))
+            sizes = [D.shard(P, world, r)[1] - D.shard(P, world, r)[0] for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+
+
+class FakeHandle:
+    """CPU test double with the Handle call signatures: encodes inputs into the outputs."""
+
+    def sh_analysis(self, vols, out):
+        out.copy_(torch.full_like(out, complex(float(vols.sum()), 1.0)))
+        return out
+
+    def align_batch(self, vols, ref, params, ref_coeffs=None):
+        n = vols.shape[0]
+        poses = torch.zeros((n, 8), dtype=torch.float32)
+        poses[:, 0] = vols.reshape(n, -1)[:, 0]          # global particle id planted in voxel 0
+        poses[:, 6] = float(torch.view_as_real(ref_coeffs).sum())
+        return poses
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, P, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = D.shard(P, world, rank)
+        vols = torch.zeros((b - a, 4, 4, 4))
+        vols.reshape(b - a, -1)[:, 0] = torch.arange(a, b, dtype=torch.float32)
+        ref = torch.full((4, 4, 4), 0.5)
+        H = torch.zeros((3, 2), dtype=torch.complex64)  # rank 1 starts with zeros: must receive rank 0's
+        poses = D.align_step(FakeHandle(), vols, ref, None, H, rank)
+        t = D.max_over_ranks(float(rank + 1))
+        q.put((rank, poses[:, 0].tolist(), poses[:, 6].tolist(), H.clone(), t))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P", [10, 7])
+def test_align_step_world2_gloo(P):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, P, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    expect_H = torch.full((3, 2), complex(0.5 * 64, 1.0), dtype=torch.complex64)
+    for rank, ids, checks, H, t in res:
+        assert ids == [float(i) for i in range(P)]                  # gathered in global order
+        assert torch.equal(H, expect_H)                            # broadcast from rank 0
+        assert all(abs(c - float(torch.view_as_real(expect_H).sum())) < 1e-3 for c in checks)
+        assert t == 2.0                                             # max over ranks
