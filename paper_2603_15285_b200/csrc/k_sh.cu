@@ -39,8 +39,9 @@ struct RingLayout {
   size_t tw, node, dft, pl, list, wsum, wbuf, total;
 };
 
-// staged plane rows are padded to N + 4 floats (16-byte aligned rows for cp.async; bank = (4y + x) mod 32)
-__host__ __device__ inline int plane_pitch(int N) { return N + 4; }
+// staged plane rows are padded to N + 8 floats (16-byte aligned rows; bank = (8y + x) mod 32 at N = 64, the
+// lowest bank-conflict degree of the quarter-arc gathers among the 16-byte-aligned pitches)
+__host__ __device__ inline int plane_pitch(int N) { return N + 8; }
 
 // per-warp fold buffer: [4 comps][Kh+1][kG] + mid [2][kG]
 __host__ __device__ inline int wbuf_elems(int Kh) { return 4 * (Kh + 1) * kG + 2 * kG; }
@@ -106,6 +107,55 @@ __device__ __forceinline__ T tri_smem(const float* __restrict__ pl, int Nr, int 
   return fma(fz, c1 - c0, c0);
 }
 
+// four trilinear samples in one plane pair with a single bounds test, so the 32 shared-memory loads are
+// issued back to back (ILP) on the common in-box path
+template <typename T, int NT>
+__device__ __forceinline__ void tri4(const float* __restrict__ pl, int Nr, int S, const T* px, const T* py, int pz0,
+                                     T fz, T* out) {
+  const int N = NT ? NT : Nr;
+  const int W = plane_pitch(N), P = N * W;
+  int x0[4], y0[4];
+  T fx[4], fy[4];
+  bool ok = (unsigned)pz0 < (unsigned)S;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const T fx0 = floor(px[i]), fy0 = floor(py[i]);
+    x0[i] = (int)fx0;
+    y0[i] = (int)fy0;
+    fx[i] = px[i] - fx0;
+    fy[i] = py[i] - fy0;
+    ok = ok && (unsigned)x0[i] < (unsigned)(N - 1) && (unsigned)y0[i] < (unsigned)(N - 1);
+  }
+  if (ok) {
+    float c[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float* b = pl + pz0 * P + y0[i] * W + x0[i];
+      c[i][0] = b[0];
+      c[i][1] = b[1];
+      c[i][2] = b[W];
+      c[i][3] = b[W + 1];
+      c[i][4] = b[P];
+      c[i][5] = b[P + 1];
+      c[i][6] = b[P + W];
+      c[i][7] = b[P + W + 1];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const T c00 = fma(fx[i], (T)c[i][1] - (T)c[i][0], (T)c[i][0]);
+      const T c01 = fma(fx[i], (T)c[i][3] - (T)c[i][2], (T)c[i][2]);
+      const T c10 = fma(fx[i], (T)c[i][5] - (T)c[i][4], (T)c[i][4]);
+      const T c11 = fma(fx[i], (T)c[i][7] - (T)c[i][6], (T)c[i][6]);
+      const T c0 = fma(fy[i], c01 - c00, c00);
+      const T c1 = fma(fy[i], c11 - c10, c10);
+      out[i] = fma(fz, c1 - c0, c0);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = tri_smem<T, NT>(pl, N, S, px[i], py[i], pz0, fz);
+  }
+}
+
 template <typename T> struct V4;
 template <> struct V4<float> {
   using t = float4;
@@ -149,19 +199,28 @@ __device__ __forceinline__ void group_dft(const T* __restrict__ wb, int nr, int 
     T re[kG], im[kG];
 #pragma unroll
     for (int r = 0; r < kG; ++r) re[r] = im[r] = T(0);
-#pragma unroll 2
-    for (int k = 0; k < K1; ++k) {
-      const cplx_t<T> w = dft[k * MP + mm];
-      const typename V4<T>::t p0 = *reinterpret_cast<const typename V4<T>::t*>(P + k * kG);
-      const typename V4<T>::t p1 = *reinterpret_cast<const typename V4<T>::t*>(P + k * kG + 4);
-      const typename V4<T>::t q0 = *reinterpret_cast<const typename V4<T>::t*>(Q + k * kG);
-      const typename V4<T>::t q1 = *reinterpret_cast<const typename V4<T>::t*>(Q + k * kG + 4);
-      const T pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-      const T qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    // twiddles (cos, sin)(m phi_k): reseeded from the table every 8 k, advanced by one complex rotation in
+    // between (keeps shared-memory wavefronts for the fold operands; <= 8 ulp drift)
+    const cplx_t<T> w1 = dft[1 * MP + mm];
+    for (int k0 = 0; k0 < K1; k0 += 8) {
+      cplx_t<T> w = dft[k0 * MP + mm];
 #pragma unroll
-      for (int r = 0; r < kG; ++r) {
-        re[r] = fma(pv[r], w.x, re[r]);
-        im[r] = fma(-qv[r], w.y, im[r]);
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = k0 + kk;
+        if (k >= K1) break;
+        const typename V4<T>::t p0 = *reinterpret_cast<const typename V4<T>::t*>(P + k * kG);
+        const typename V4<T>::t p1 = *reinterpret_cast<const typename V4<T>::t*>(P + k * kG + 4);
+        const typename V4<T>::t q0 = *reinterpret_cast<const typename V4<T>::t*>(Q + k * kG);
+        const typename V4<T>::t q1 = *reinterpret_cast<const typename V4<T>::t*>(Q + k * kG + 4);
+        const T pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+        const T qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int r = 0; r < kG; ++r) {
+          re[r] = fma(pv[r], w.x, re[r]);
+          im[r] = fma(-qv[r], w.y, im[r]);
+        }
+        const T wx = w.x * w1.x - w.y * w1.y, wy = w.y * w1.x + w.x * w1.y;
+        w = mk<T>(wx, wy);
       }
     }
     if (act)
@@ -181,20 +240,27 @@ __device__ __forceinline__ void group_dft(const T* __restrict__ wb, int nr, int 
         gout[r][m] = mk<T>(vr * dscale, vi * dscale);
       }
   }
-  // leftover m (at most 2): lane r < nr owns ring r and runs the k loop itself
+  // leftover m (at most 2): lanes = (ring r = lane % kG, k-quarter = lane / kG); each lane sums a quarter of the
+  // k range, then two butterfly steps combine the quarters (fixed order)
   for (int e = 0; e < rem; ++e) {
     const int m = 32 * full + e, par = m & 1;
+    const int r = lane % kG, qk = lane / kG;
+    const T* P = wb + (2 * par) * K1 * kG + r;
+    const T* Q = wb + (2 * par + 1) * K1 * kG + r;
+    T vr = T(0), vi = T(0);
+    for (int k = qk; k < K1; k += 32 / kG) {
+      const cplx_t<T> w = dft[k * MP + m];
+      vr = fma(P[k * kG], w.x, vr);
+      vi = fma(-Q[k * kG], w.y, vi);
+    }
+#pragma unroll
+    for (int o = kG; o < 32; o <<= 1) {
+      vr += __shfl_xor_sync(0xffffffffu, vr, o);
+      vi += __shfl_xor_sync(0xffffffffu, vi, o);
+    }
     if (lane < nr) {
-      const T* P = wb + (2 * par) * K1 * kG + lane;
-      const T* Q = wb + (2 * par + 1) * K1 * kG + lane;
-      T vr = T(0), vi = T(0);
-      for (int k = 0; k < K1; ++k) {
-        const cplx_t<T> w = dft[k * MP + m];
-        vr = fma(P[k * kG], w.x, vr);
-        vi = fma(-Q[k * kG], w.y, vi);
-      }
       if (mid) {
-        const T am = midv[par * kG + lane];
+        const T am = midv[par * kG + r];
         switch (m & 3) {
           case 0: vr += am; break;
           case 1: vi -= am; break;
@@ -315,50 +381,104 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
   const int r_end = (int)(((long long)count * (warp + 1)) / kRingWarps);
   for (int g0 = r_begin; g0 < r_end; g0 += kG) {
     const int nr = min(kG, r_end - g0);
-    // fold items (ring r, k): r = item / K1, k = item % K1, advanced incrementally by 32
+    // folds: lanes walk consecutive k along ONE ring (gathers at neighbouring points: few bank conflicts); a lane
+    // keeps its 4 fold values of all kG rings in registers and writes each k-row with two 16-byte stores
+    // (conflict-free).  k beyond the last full round of 32 is done with (ring, k) items spread over lanes.
     {
-      int r = 0, k = lane;
-      while (k >= K1) {
-        k -= K1;
-        ++r;
+      const int nfull = K1 / 32;
+      for (int kb = 0; kb < nfull * 32; kb += 32) {
+        const int k = kb + lane;
+        T vals[4][kG];
+#pragma unroll
+        for (int r = 0; r < kG; ++r) {
+          vals[0][r] = vals[1][r] = vals[2][r] = vals[3][r] = T(0);
+          if (r < nr) {
+            const int ring = list[g0 + r];
+            const int i = ring >> 16, j = ring & 0xffff;
+            const T rad = (T)i + T(0.5);
+            const cplx_t<T> nd = node[j];
+            const T rs = rad * nd.y;
+            const T z = fma(rad, nd.x, cz);
+            const T fz0 = floor(z);
+            const int pz0 = (int)fz0 - zs;
+            const T fz = z - fz0;
+            const bool k0 = (k == 0);
+            const int kk[4] = {k, k + Mp, k0 ? Mp : Mp - k, k0 ? 0 : 2 * Mp - k};
+            T px[4], py[4], sv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const cplx_t<T> ph = tw[kk[q]];
+              px[q] = fma(rs, ph.x, cx);
+              py[q] = fma(rs, ph.y, cy);
+            }
+            tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
+            const T s3 = k0 ? T(0) : sv[2], s4 = k0 ? T(0) : sv[3];
+            const T ap = sv[0] + sv[1], am = sv[0] - sv[1], bp = s3 + s4, bm = s3 - s4;
+            vals[0][r] = ap + bp;  // even m, cos
+            vals[1][r] = ap - bp;  // even m, sin (0 at k = 0)
+            vals[2][r] = am - bm;  // odd m, cos
+            vals[3][r] = am + bm;  // odd m, sin (0 at k = 0)
+            if (k0 && mid) {
+              const int km = Mp / 2;
+              const cplx_t<T> pa = tw[km], pb = tw[km + Mp];
+              const T a = tri_smem<T, NT>(pl, N, S, fma(rs, pa.x, cx), fma(rs, pa.y, cy), pz0, fz);
+              const T bb = tri_smem<T, NT>(pl, N, S, fma(rs, pb.x, cx), fma(rs, pb.y, cy), pz0, fz);
+              wb[4 * K1 * kG + r] = a + bb;
+              wb[4 * K1 * kG + kG + r] = a - bb;
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          typename V4<T>::t* dst = reinterpret_cast<typename V4<T>::t*>(wb + (c * K1 + k) * kG);
+          dst[0] = typename V4<T>::t{vals[c][0], vals[c][1], vals[c][2], vals[c][3]};
+          dst[1] = typename V4<T>::t{vals[c][4], vals[c][5], vals[c][6], vals[c][7]};
+        }
       }
-      for (; r < nr;) {
-        const int ring = list[g0 + r];
-        const int i = ring >> 16, j = ring & 0xffff;
-        const T rad = (T)i + T(0.5);
-        const cplx_t<T> nd = node[j];
-        const T rs = rad * nd.y;
-        const T z = fma(rad, nd.x, cz);
-        const T fz0 = floor(z);
-        const int pz0 = (int)fz0 - zs;
-        const T fz = z - fz0;
-        auto samp = [&](int kk) {
-          const cplx_t<T> ph = tw[kk];
-          return tri_smem<T, NT>(pl, N, S, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0, fz);
-        };
-        const bool k0 = (k == 0);
-        const T s1 = samp(k), s2 = samp(k + Mp);
-        T s3 = T(0), s4 = T(0);
-        if (!k0) {
-          s3 = samp(Mp - k);
-          s4 = samp(2 * Mp - k);
+      // leftover k in [32 nfull, K1): items (ring r, k) spread over the lanes, r fastest
+      const int kl0 = nfull * 32, nk = K1 - kl0;
+      for (int it = lane; it < nk * kG; it += 32) {
+        const int r = it % kG, k = kl0 + it / kG;
+        T v0 = T(0), v1 = T(0), v2 = T(0), v3 = T(0);
+        if (r < nr) {
+          const int ring = list[g0 + r];
+          const int i = ring >> 16, j = ring & 0xffff;
+          const T rad = (T)i + T(0.5);
+          const cplx_t<T> nd = node[j];
+          const T rs = rad * nd.y;
+          const T z = fma(rad, nd.x, cz);
+          const T fz0 = floor(z);
+          const int pz0 = (int)fz0 - zs;
+          const T fz = z - fz0;
+          const bool k0 = (k == 0);
+          const int kk[4] = {k, k + Mp, k0 ? Mp : Mp - k, k0 ? 0 : 2 * Mp - k};
+          T px[4], py[4], sv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const cplx_t<T> ph = tw[kk[q]];
+            px[q] = fma(rs, ph.x, cx);
+            py[q] = fma(rs, ph.y, cy);
+          }
+          tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
+          const T s3 = k0 ? T(0) : sv[2], s4 = k0 ? T(0) : sv[3];
+          const T ap = sv[0] + sv[1], am = sv[0] - sv[1], bp = s3 + s4, bm = s3 - s4;
+          v0 = ap + bp;
+          v1 = ap - bp;
+          v2 = am - bm;
+          v3 = am + bm;
+          if (k0 && mid) {
+            const int km = Mp / 2;
+            const cplx_t<T> pa = tw[km], pb = tw[km + Mp];
+            const T a = tri_smem<T, NT>(pl, N, S, fma(rs, pa.x, cx), fma(rs, pa.y, cy), pz0, fz);
+            const T bb = tri_smem<T, NT>(pl, N, S, fma(rs, pb.x, cx), fma(rs, pb.y, cy), pz0, fz);
+            wb[4 * K1 * kG + r] = a + bb;
+            wb[4 * K1 * kG + kG + r] = a - bb;
+          }
         }
-        const T ap = s1 + s2, am = s1 - s2, bp = s3 + s4, bm = s3 - s4;
-        wb[(0 * K1 + k) * kG + r] = ap + bp;  // even m, cos
-        wb[(1 * K1 + k) * kG + r] = ap - bp;  // even m, sin (0 at k = 0)
-        wb[(2 * K1 + k) * kG + r] = am - bm;  // odd m, cos
-        wb[(3 * K1 + k) * kG + r] = am + bm;  // odd m, sin (0 at k = 0)
-        if (k0 && mid) {
-          const int km = Mp / 2;
-          const T a = samp(km), bb = samp(km + Mp);
-          wb[4 * K1 * kG + r] = a + bb;
-          wb[4 * K1 * kG + kG + r] = a - bb;
-        }
-        k += 32;
-        while (k >= K1) {
-          k -= K1;
-          ++r;
-        }
+        wb[(0 * K1 + k) * kG + r] = v0;
+        wb[(1 * K1 + k) * kG + r] = v1;
+        wb[(2 * K1 + k) * kG + r] = v2;
+        wb[(3 * K1 + k) * kG + r] = v3;
       }
     }
     __syncwarp();

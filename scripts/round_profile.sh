@@ -1,0 +1,16 @@
+# Full evidence run (under gpurun): GPU tests, the default bench line, the ncu launch list of the same bench
+# command, one ncu --set full capture of the dominant kernels, clocks.  Outputs in gpurun_out/<tag>_*.
+TAG=${1:-r1}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv,noheader > gpurun_out/${TAG}_gpu.txt
+nproc > gpurun_out/${TAG}_nproc.txt; grep -m1 "model name" /proc/cpuinfo >> gpurun_out/${TAG}_nproc.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke_exit=$?
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo pytest_exit=$?
+tail -3 gpurun_out/${TAG}_pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench_exit=$?
+tail -c 1500 gpurun_out/${TAG}_bench.json
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+$CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu1.log 2>&1; echo launches_exit=$?
+$CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k "regex:k_sh_rings|k_sh_legendre|k_newton_refine|k_so3_search|k_corr_coeffs" -s 5 -c 5 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu2.log 2>&1; echo full_exit=$?
