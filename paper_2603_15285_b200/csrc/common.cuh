@@ -109,6 +109,10 @@ template <typename T>
 cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
                                 T* poses, cudaStream_t s);
 size_t search_smem_bytes(int L0, int K, bool fp64);
+size_t corr_tc_smem_bytes(int L, int R);
+bool corr_tc_supported(int L, int R);
+cudaError_t launch_corr_coeffs_tc(const float2* F, const float2* H, int64_t B, int L, int Lmax, int R, float2* M,
+                                  int num_sms, cudaStream_t s);
 template <typename T>
 cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estride, int64_t nb, T* rho, cudaStream_t s);
 template <typename T> cudaError_t launch_to_real(const float* in, T* out, int64_t n, cudaStream_t s);

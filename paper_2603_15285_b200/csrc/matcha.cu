@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,7 +20,9 @@ using namespace matcha;
 struct matcha_ctx {
   matcha_config_t cfg;
   int device = 0;
+  int num_sms = 148;
   bool fp64 = false;
+  bool use_tc = true;  // tcgen05 path for stage 2 (FP32 handles)
   size_t rsz = 4;  // sizeof(real)
   int R = 0, L = 0, Lq = 0, nth = 0, nph = 0, Jh = 0, ncf = 0;
   void* d_node = nullptr;
@@ -428,6 +431,8 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   matcha_handle_t h = new matcha_ctx();
   h->cfg = *cfg;
   cudaGetDevice(&h->device);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (const char* v = getenv("MATCHA_CORR_SIMT")) h->use_tc = !(v[0] == '1');
   h->fp64 = cfg->precision == MATCHA_FP64;
   h->rsz = h->fp64 ? 8 : 4;
   h->R = cfg->N / 2;
@@ -620,6 +625,8 @@ MATCHA_API matcha_status_t matcha_corr_coeffs(matcha_handle_t h, const void* f, 
   ProfScope ps(h, 1, s);
   if (h->fp64)
     e = launch_corr_coeffs<double>((const double2*)f, (const double2*)href, B, L, h->L, h->R, (double2*)M, s);
+  else if (h->use_tc && corr_tc_supported(L, h->R))
+    e = launch_corr_coeffs_tc((const float2*)f, (const float2*)href, B, L, h->L, h->R, (float2*)M, h->num_sms, s);
   else
     e = launch_corr_coeffs<float>((const float2*)f, (const float2*)href, B, L, h->L, h->R, (float2*)M, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "corr_coeffs launch");
