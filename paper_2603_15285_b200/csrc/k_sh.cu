@@ -381,51 +381,55 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
   const int r_end = (int)(((long long)count * (warp + 1)) / kRingWarps);
   for (int g0 = r_begin; g0 < r_end; g0 += kG) {
     const int nr = min(kG, r_end - g0);
-    // folds: lanes walk consecutive k along ONE ring (gathers at neighbouring points: few bank conflicts); a lane
-    // keeps its 4 fold values of all kG rings in registers and writes each k-row with two 16-byte stores
-    // (conflict-free).  k beyond the last full round of 32 is done with (ring, k) items spread over lanes.
+    // folds: lanes walk consecutive k in [1, Kh] along ONE ring (gathers at neighbouring points: few bank
+    // conflicts), 4 mirrored samples each; a lane keeps its 4 fold values of all kG rings in registers and writes
+    // each k-row with two 16-byte stores.  k beyond the full rounds of 32 uses (ring, k) items spread over the
+    // lanes; the k = 0 items (2 samples) are one sample per lane, combined by a shuffle.
     {
-      const int nfull = K1 / 32;
+      auto ring_geom = [&](int r, T& rs, T& fz, int& pz0) {
+        const int ring = list[g0 + r];
+        const int i = ring >> 16, j = ring & 0xffff;
+        const T rad = (T)i + T(0.5);
+        const cplx_t<T> nd = node[j];
+        rs = rad * nd.y;
+        const T z = fma(rad, nd.x, cz);
+        const T fz0 = floor(z);
+        pz0 = (int)fz0 - zs;
+        fz = z - fz0;
+      };
+      auto fold4 = [&](int k, T rs, T fz, int pz0, T* v) {
+        const int kk[4] = {k, k + Mp, Mp - k, 2 * Mp - k};
+        T px[4], py[4], sv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const cplx_t<T> ph = tw[kk[q]];
+          px[q] = fma(rs, ph.x, cx);
+          py[q] = fma(rs, ph.y, cy);
+        }
+        tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
+        const T ap = sv[0] + sv[1], am = sv[0] - sv[1], bp = sv[2] + sv[3], bm = sv[2] - sv[3];
+        v[0] = ap + bp;  // even m, cos
+        v[1] = ap - bp;  // even m, sin
+        v[2] = am - bm;  // odd m, cos
+        v[3] = am + bm;  // odd m, sin
+      };
+      const int nfull = Kh / 32;
       for (int kb = 0; kb < nfull * 32; kb += 32) {
-        const int k = kb + lane;
+        const int k = kb + lane + 1;
         T vals[4][kG];
 #pragma unroll
         for (int r = 0; r < kG; ++r) {
           vals[0][r] = vals[1][r] = vals[2][r] = vals[3][r] = T(0);
           if (r < nr) {
-            const int ring = list[g0 + r];
-            const int i = ring >> 16, j = ring & 0xffff;
-            const T rad = (T)i + T(0.5);
-            const cplx_t<T> nd = node[j];
-            const T rs = rad * nd.y;
-            const T z = fma(rad, nd.x, cz);
-            const T fz0 = floor(z);
-            const int pz0 = (int)fz0 - zs;
-            const T fz = z - fz0;
-            const bool k0 = (k == 0);
-            const int kk[4] = {k, k + Mp, k0 ? Mp : Mp - k, k0 ? 0 : 2 * Mp - k};
-            T px[4], py[4], sv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const cplx_t<T> ph = tw[kk[q]];
-              px[q] = fma(rs, ph.x, cx);
-              py[q] = fma(rs, ph.y, cy);
-            }
-            tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
-            const T s3 = k0 ? T(0) : sv[2], s4 = k0 ? T(0) : sv[3];
-            const T ap = sv[0] + sv[1], am = sv[0] - sv[1], bp = s3 + s4, bm = s3 - s4;
-            vals[0][r] = ap + bp;  // even m, cos
-            vals[1][r] = ap - bp;  // even m, sin (0 at k = 0)
-            vals[2][r] = am - bm;  // odd m, cos
-            vals[3][r] = am + bm;  // odd m, sin (0 at k = 0)
-            if (k0 && mid) {
-              const int km = Mp / 2;
-              const cplx_t<T> pa = tw[km], pb = tw[km + Mp];
-              const T a = tri_smem<T, NT>(pl, N, S, fma(rs, pa.x, cx), fma(rs, pa.y, cy), pz0, fz);
-              const T bb = tri_smem<T, NT>(pl, N, S, fma(rs, pb.x, cx), fma(rs, pb.y, cy), pz0, fz);
-              wb[4 * K1 * kG + r] = a + bb;
-              wb[4 * K1 * kG + kG + r] = a - bb;
-            }
+            T rs, fz;
+            int pz0;
+            ring_geom(r, rs, fz, pz0);
+            T v[4];
+            fold4(k, rs, fz, pz0, v);
+            vals[0][r] = v[0];
+            vals[1][r] = v[1];
+            vals[2][r] = v[2];
+            vals[3][r] = v[3];
           }
         }
 #pragma unroll
@@ -435,50 +439,47 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
           dst[1] = typename V4<T>::t{vals[c][4], vals[c][5], vals[c][6], vals[c][7]};
         }
       }
-      // leftover k in [32 nfull, K1): items (ring r, k) spread over the lanes, r fastest
-      const int kl0 = nfull * 32, nk = K1 - kl0;
+      // leftover k in [32 nfull + 1, Kh]: items (ring r, k), r fastest
+      const int kl0 = nfull * 32 + 1, nk = Kh - kl0 + 1;
       for (int it = lane; it < nk * kG; it += 32) {
         const int r = it % kG, k = kl0 + it / kG;
-        T v0 = T(0), v1 = T(0), v2 = T(0), v3 = T(0);
+        T v[4] = {T(0), T(0), T(0), T(0)};
         if (r < nr) {
-          const int ring = list[g0 + r];
-          const int i = ring >> 16, j = ring & 0xffff;
-          const T rad = (T)i + T(0.5);
-          const cplx_t<T> nd = node[j];
-          const T rs = rad * nd.y;
-          const T z = fma(rad, nd.x, cz);
-          const T fz0 = floor(z);
-          const int pz0 = (int)fz0 - zs;
-          const T fz = z - fz0;
-          const bool k0 = (k == 0);
-          const int kk[4] = {k, k + Mp, k0 ? Mp : Mp - k, k0 ? 0 : 2 * Mp - k};
-          T px[4], py[4], sv[4];
+          T rs, fz;
+          int pz0;
+          ring_geom(r, rs, fz, pz0);
+          fold4(k, rs, fz, pz0, v);
+        }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const cplx_t<T> ph = tw[kk[q]];
-            px[q] = fma(rs, ph.x, cx);
-            py[q] = fma(rs, ph.y, cy);
-          }
-          tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
-          const T s3 = k0 ? T(0) : sv[2], s4 = k0 ? T(0) : sv[3];
-          const T ap = sv[0] + sv[1], am = sv[0] - sv[1], bp = s3 + s4, bm = s3 - s4;
-          v0 = ap + bp;
-          v1 = ap - bp;
-          v2 = am - bm;
-          v3 = am + bm;
-          if (k0 && mid) {
-            const int km = Mp / 2;
-            const cplx_t<T> pa = tw[km], pb = tw[km + Mp];
-            const T a = tri_smem<T, NT>(pl, N, S, fma(rs, pa.x, cx), fma(rs, pa.y, cy), pz0, fz);
-            const T bb = tri_smem<T, NT>(pl, N, S, fma(rs, pb.x, cx), fma(rs, pb.y, cy), pz0, fz);
-            wb[4 * K1 * kG + r] = a + bb;
-            wb[4 * K1 * kG + kG + r] = a - bb;
+        for (int c = 0; c < 4; ++c) wb[(c * K1 + k) * kG + r] = v[c];
+      }
+      // k = 0: samples phi = 0 and phi = pi (+ pi/2, 3pi/2 when the middle index exists), one per lane
+      {
+        const int r = lane >> 1, q = lane & 1;
+        T s0 = T(0), sm = T(0);
+        if (r < nr) {
+          T rs, fz;
+          int pz0;
+          ring_geom(r, rs, fz, pz0);
+          const cplx_t<T> ph = tw[q ? Mp : 0];
+          s0 = tri_smem<T, NT>(pl, N, S, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0, fz);
+          if (mid) {
+            const cplx_t<T> pm = tw[Mp / 2 + (q ? Mp : 0)];
+            sm = tri_smem<T, NT>(pl, N, S, fma(rs, pm.x, cx), fma(rs, pm.y, cy), pz0, fz);
           }
         }
-        wb[(0 * K1 + k) * kG + r] = v0;
-        wb[(1 * K1 + k) * kG + r] = v1;
-        wb[(2 * K1 + k) * kG + r] = v2;
-        wb[(3 * K1 + k) * kG + r] = v3;
+        const T s1 = __shfl_xor_sync(0xffffffffu, s0, 1);
+        const T sm1 = __shfl_xor_sync(0xffffffffu, sm, 1);
+        if (q == 0 && r < kG) {
+          wb[(0 * K1) * kG + r] = r < nr ? s0 + s1 : T(0);
+          wb[(1 * K1) * kG + r] = T(0);
+          wb[(2 * K1) * kG + r] = r < nr ? s0 - s1 : T(0);
+          wb[(3 * K1) * kG + r] = T(0);
+          if (mid) {
+            wb[4 * K1 * kG + r] = sm + sm1;
+            wb[4 * K1 * kG + kG + r] = sm - sm1;
+          }
+        }
       }
     }
     __syncwarp();
