@@ -1,6 +1,6 @@
 """Summarise an ncu report's source page (cuda,sass view): stall reasons and the hottest CUDA source lines.
 
-usage: python scripts/ncu_hot.py report.ncu-rep kernel-regex [top]
+usage: python scripts/ncu_hot.py report.ncu-rep kernel-regex [top] [column]
 """
 import collections
 import csv
@@ -10,6 +10,7 @@ import sys
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+col = sys.argv[4] if len(sys.argv) > 4 else "Warp Stall Sampling (All Samples)"  # e.g. "Instructions Executed"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kre}", "--print-source",
                       "cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -35,7 +36,7 @@ for r in rows:
     key = (fname, int(r[0]))
     src[key] = r[1].strip()[:100]
     try:
-        per_line[key] += float(r[hdr["Warp Stall Sampling (All Samples)"]] or 0)
+        per_line[key] += float(r[hdr[col]] or 0)
     except (ValueError, KeyError):
         pass
     for h, i in hdr.items():
