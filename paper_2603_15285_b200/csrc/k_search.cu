@@ -24,12 +24,11 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 2048;
 
 struct SearchLayout {
-  size_t Ms, X, Y, sl, tmv, tmi, mxv, mxi, tw, cs, cs_idx, invl, invll, misc, red_s, red_i, total;
+  size_t Ms, X, Y, sl, tmv, tmi, mxv, mxi, tw, cs, cs_idx, invl, invll, misc, beta, red_s, red_i, total;
 };
 
 template <typename T> __host__ __device__ inline SearchLayout search_layout(int L0, int K) {
   const int nb = K * (L0 + 1), na = 2 * K * (L0 + 1);
-  (void)nb;
   SearchLayout s;
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -51,6 +50,7 @@ template <typename T> __host__ __device__ inline SearchLayout search_layout(int 
   s.invl = take(sizeof(T) * (kMaxL + 2));
   s.invll = take(sizeof(T) * (kMaxL + 2));
   s.misc = take(sizeof(T) * 8 + sizeof(int) * 8);
+  s.beta = take(sizeof(T) * 3 * nb);           // per slice: cos beta_j, ln cos(beta_j/2), ln sin(beta_j/2)
   s.red_s = take(sizeof(T) * kWarps);
   s.red_i = take(sizeof(int) * kWarps);
   s.total = o;
@@ -61,6 +61,9 @@ template <typename T> __host__ __device__ inline SearchLayout search_layout(int 
 template <typename T> __device__ __forceinline__ bool before(T s1, int i1, T s2, int i2) {
   return s1 > s2 || (s1 == s2 && i1 < i2);
 }
+
+// t / d for 0 <= t < 2^32 / d^2 (d <= 128 here): multiply-high by ceil(2^32 / d), no integer division
+__device__ __forceinline__ int fdiv(int t, uint32_t magic) { return (int)__umulhi((uint32_t)t, magic); }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
@@ -81,8 +84,9 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
   int* ci = (int*)(smem + lay.cs_idx);
   T* inv_l = (T*)(smem + lay.invl);
   T* inv_ll = (T*)(smem + lay.invll);
-  T* bsh = (T*)(smem + lay.misc);                 // [0]=cos b, [1]=lnc, [2]=lns
   int* cnt = (int*)(smem + lay.misc + sizeof(T) * 8);
+  T* bsl = (T*)(smem + lay.beta);  // [3][nb]
+  const uint32_t mg = (uint32_t)((0x100000000ull + ng - 1) / ng);  // fdiv magic for ng
   T* red_s = (T*)(smem + lay.red_s);
   int* red_i = (int*)(smem + lay.red_i);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -98,6 +102,13 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
   for (int l = tid; l <= kMaxL + 1; l += kThreads) {
     inv_l[l] = l ? (T)(1.0 / l) : T(0);
     inv_ll[l] = l ? (T)(1.0 / ((double)l * (l + 1))) : T(0);
+  }
+  for (int j = tid; j < nb; j += kThreads) {
+    const double beta = (j + 0.5) * kPi / nb;
+    const BetaLogs<T> bl = beta_logs<T>(beta);
+    bsl[j] = (T)cos(beta);
+    bsl[nb + j] = bl.lnc;
+    bsl[2 * nb + j] = bl.lns;
   }
   if (tid == 0) *cnt = 0;
   __syncthreads();
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
   // in-slice 3x3 (alpha, gamma periodic) max of the keys of slice j -> window slot j % 3
   auto filter_slice = [&](int j) {
     for (int t = tid; t < na * ng; t += kThreads) {
-      const int aa = t / ng, c = t - aa * ng;
+      const int aa = fdiv(t, mg), c = t - aa * ng;
       const int cm = c == 0 ? ng - 1 : c - 1, cp = c == ng - 1 ? 0 : c + 1;
       const int base = j * na * ng + aa * ng;
       T bv = sl[t];
@@ -162,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
     T* ov = mxv + (j % 3) * na * ng;
     int* oi = mxi + (j % 3) * na * ng;
     for (int t = tid; t < na * ng; t += kThreads) {
-      const int aa = t / ng, c = t - aa * ng;
+      const int aa = fdiv(t, mg), c = t - aa * ng;
       const int am = aa == 0 ? na - 1 : aa - 1, ap = aa == na - 1 ? 0 : aa + 1;
       T bv = tmv[t];
       int bi = tmi[t];
@@ -182,18 +193,10 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
   };
 
   for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      const double beta = (j + 0.5) * kPi / nb;
-      const BetaLogs<T> bl = beta_logs<T>(beta);
-      bsh[0] = (T)cos(beta);
-      bsh[1] = bl.lnc;
-      bsh[2] = bl.lns;
-    }
-    __syncthreads();
-    const T cb = bsh[0];
+    const T cb = bsl[j];
     BetaLogs<T> bl;
-    bl.lnc = bsh[1];
-    bl.lns = bsh[2];
+    bl.lnc = bsl[nb + j];
+    bl.lns = bsl[2 * nb + j];
     // X_{j,mn}
     for (int pi = tid; pi < npairs; pi += kThreads) {
       const PairDesc pd = a.pairs[pi];
@@ -219,13 +222,14 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
     __syncthreads();
     // Y_{m,c} = sum_n X_mn e^{-i n gamma_c}
     for (int t = tid; t < (L0 + 1) * ng; t += kThreads) {
-      const int m = t / ng, c = t - m * ng;
+      const int m = fdiv(t, mg), c = t - m * ng;
       T yr = T(0), yi = T(0);
+      int k = (ng - (L0 * c) % ng) % ng;  // (n c) mod ng at n = -L0, then + c per step
       for (int n = -L0; n <= L0; ++n) {
         const cplx_t<T> x = X[m * w0 + (n + L0)];
-        int k = (n * c) % ng;
-        if (k < 0) k += ng;
         const cplx_t<T> e = tw[k];
+        k += c;
+        if (k >= ng) k -= ng;
         yr = fma(x.x, e.x, fma(-x.y, e.y, yr));
         yi = fma(x.x, e.y, fma(x.y, e.x, yi));
       }
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
     // C(alpha_a, beta_j, gamma_c)
     T* cur = sl;
     for (int t = tid; t < na * ng; t += kThreads) {
-      const int aa = t / ng, c = t - aa * ng;
+      const int aa = fdiv(t, mg), c = t - aa * ng;
       T s = Y[c].x;
       T s2 = T(0);
       int k = 0;
