@@ -22,11 +22,16 @@ oracle: oracle/liboracle.so
 oracle/liboracle.so: oracle/oracle.cpp
 	$(CXX) -O2 -std=c++17 -fPIC -shared -o $@ $< -lpthread
 
+CU_OBJS   := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CU_SRCS))
+
 cuda: $(PKG)/libmatcha.so
-$(PKG)/libmatcha.so: $(CU_SRCS) $(CU_HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) -lcufft 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+build/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
+$(PKG)/libmatcha.so: $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcufft
 
 clean:
-	rm -f gen/*.so oracle/*.so $(PKG)/*.so $(PKG)/ptxas.log
+	rm -rf gen/*.so oracle/*.so $(PKG)/*.so build
 
 .PHONY: all gen oracle cuda clean

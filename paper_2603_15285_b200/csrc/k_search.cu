@@ -7,11 +7,14 @@
 //   C(alpha_a, beta_j, gamma_c) = Re Y_{0,c} + 2 Re sum_{m>=1} Y_{m,c} e^{-i m alpha_a},
 //   Y_{m,c} = sum_n X_{j,mn} e^{-i n gamma_c}                             (separable 2-D DFT, Hermitian X)
 //
-// B200 mapping: one CTA per particle.  M(l <= L0) is staged in shared memory (4 KiB at L0 = 8); d is
+// B200 mapping: one CTA per particle.  When the grid fits in shared memory (L0 <= 9 at K = 2) k_so3_grid keeps it
+// resident and runs each phase over the whole grid (few barriers); otherwise k_so3_search (below) streams it:  M(l <= L0) is staged in shared memory (4 KiB at L0 = 8); d is
 // produced on the fly by the l-recurrence (no table traffic); the grid is never materialised: a rolling
 // 3-slice window in shared memory feeds the 26-neighbour test of slice j-1 while slice j is computed, so
 // L0 = 12 (70k nodes, 275 KiB) needs no cluster.  Maxima go to a shared list; the N_C winners are chosen
 // by an order-independent block arg-max on (score desc, index asc) -- deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "wigner.cuh"
 
@@ -311,10 +314,318 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
   }
 }
 
+// ------------------------------------------------------------------ full-grid variant (grid resident in smem)
+// Used when the whole (beta, alpha, gamma) grid of C_{L0} fits in shared memory (L0 <= 9 at K = 2): every phase is
+// data-parallel over the whole grid, so the CTA passes ~6 barriers instead of ~5 per beta slice.
+//   phase 1  X[j][m][n] for all slices: one item = (pair, kJG slices) sharing the recurrence coefficients
+//   phase 2  Y[j][m][c] = sum_n X e^{-i n gamma_c}          (per chunk of jc slices)
+//   phase 3  C[j][a][c] = Re Y[j][0][c] + 2 Re sum_m Y e^{-i m alpha_a}   (4 alphas per item, Y loads shared)
+//   phase 4  strict 26-neighbour maxima by direct comparison of keys (score desc, index asc), early exit
+//   phase 5  top-N_C by one warp: N_C rounds of a warp arg-max over the candidate list (deterministic)
+constexpr int kGThreads = 512;
+constexpr int kJG = 4;
+
+struct GridLayout {
+  size_t Ms, ea, eg, beta, invl, invll, X, Y, C, cs, ci, misc, total;
+};
+
+template <typename T> __host__ __device__ inline GridLayout grid_layout(int L0, int K, int jc) {
+  const int nb = K * (L0 + 1), na = 2 * K * (L0 + 1), nm = L0 + 1, w0 = 2 * L0 + 1;
+  GridLayout s;
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    size_t r = o;
+    o += (b + 15) & ~size_t(15);
+    return r;
+  };
+  s.Ms = take(sizeof(cplx_t<T>) * half_size(L0));
+  s.ea = take(sizeof(cplx_t<T>) * nm * na);  // e^{-i m alpha_a}
+  s.eg = take(sizeof(cplx_t<T>) * w0 * na);  // e^{-i n gamma_c}, n = -L0..L0
+  s.beta = take(sizeof(T) * 3 * nb);
+  s.invl = take(sizeof(T) * (L0 + 2));
+  s.invll = take(sizeof(T) * (L0 + 2));
+  s.X = take(sizeof(cplx_t<T>) * (size_t)nb * nm * w0);
+  s.Y = take(sizeof(cplx_t<T>) * (size_t)jc * nm * na);
+  s.C = take(sizeof(T) * (size_t)nb * (na + 2) * (na + 2));  // one-node periodic halo in alpha and gamma
+  s.cs = take(sizeof(T) * kCap);
+  s.ci = take(sizeof(int) * kCap);
+  s.misc = take(sizeof(int) * 4);
+  s.total = o;
+  return s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L0 = a.L0, K = a.K;
+  const int nb = K * (L0 + 1), na = 2 * K * (L0 + 1), ng = na, nm = L0 + 1, w0 = 2 * L0 + 1;
+  const GridLayout lay = grid_layout<T>(L0, K, jc);
+  cplx_t<T>* Ms = (cplx_t<T>*)(smem + lay.Ms);
+  cplx_t<T>* Ea = (cplx_t<T>*)(smem + lay.ea);
+  cplx_t<T>* Eg = (cplx_t<T>*)(smem + lay.eg);
+  T* bsl = (T*)(smem + lay.beta);  // [3][nb]: cos beta_j, ln cos(beta_j/2), ln sin(beta_j/2)
+  T* inv_l = (T*)(smem + lay.invl);
+  T* inv_ll = (T*)(smem + lay.invll);
+  cplx_t<T>* X = (cplx_t<T>*)(smem + lay.X);
+  cplx_t<T>* Y = (cplx_t<T>*)(smem + lay.Y);
+  T* C = (T*)(smem + lay.C);
+  T* cs = (T*)(smem + lay.cs);
+  int* ci = (int*)(smem + lay.ci);
+  int* cnt = (int*)(smem + lay.misc);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t p = blockIdx.x;
+
+  const cplx_t<T>* Mp = a.M + p * a.strideM;
+  for (int t = tid; t < half_size(L0); t += kGThreads) Ms[t] = Mp[t];
+  // phase tables e^{-2 pi i k/na} at k = (m a) mod na and (n c) mod ng (exact integer reduction)
+  for (int t = tid; t < (nm + w0) * na; t += kGThreads) {
+    const int r = t / na, c = t - r * na;
+    const int f = r < nm ? r : r - nm - L0;  // m, or n
+    const int k = ((f * c) % na + na) % na;
+    double sn, cn;
+    sincospi(2.0 * k / na, &sn, &cn);
+    const cplx_t<T> e = mk<T>((T)cn, (T)(-sn));
+    if (r < nm) Ea[t] = e;
+    else Eg[t - nm * na] = e;
+  }
+  for (int l = tid; l <= L0 + 1; l += kGThreads) {
+    inv_l[l] = l ? (T)(1.0 / l) : T(0);
+    inv_ll[l] = l ? (T)(1.0 / ((double)l * (l + 1))) : T(0);
+  }
+  for (int j = tid; j < nb; j += kGThreads) {
+    const double beta = (j + 0.5) * kPi / nb;
+    const BetaLogs<T> bl = beta_logs<T>(beta);
+    bsl[j] = (T)cos(beta);
+    bsl[nb + j] = bl.lnc;
+    bsl[2 * nb + j] = bl.lns;
+  }
+  if (tid == 0) *cnt = 0;
+  __syncthreads();
+
+  // phase 1: X_{j,mn} = sum_l conj(M^l_mn) d^l_mn(beta_j)
+  const int npairs = pair_count(L0), njg = (nb + kJG - 1) / kJG;
+  for (int it = tid; it < npairs * njg; it += kGThreads) {
+    const int pi = it % npairs, jg = it / npairs;
+    const PairDesc pd = a.pairs[pi];
+    const int m = pd.m, n = pd.n, l0 = max(m, abs(n));
+    const T lnC = a.pair_lnc[pi];
+    T d[kJG], dprev[kJG], xr[kJG], xi[kJG], cb[kJG];
+#pragma unroll
+    for (int q = 0; q < kJG; ++q) {
+      const int j = min(jg * kJG + q, nb - 1);
+      BetaLogs<T> bl;
+      bl.lnc = bsl[nb + j];
+      bl.lns = bsl[2 * nb + j];
+      T dd;
+      wigner_seed<T, false>(m, n, lnC, bl, d[q], dd);
+      cb[q] = bsl[j];
+      dprev[q] = xr[q] = xi[q] = T(0);
+    }
+    int off = (int)half_offset(l0) + m * (2 * l0 + 1) + (n + l0);
+    T sq = T(0);
+    for (int l = l0;; ++l) {
+      const cplx_t<T> Ml = Ms[off];
+#pragma unroll
+      for (int q = 0; q < kJG; ++q) {
+        xr[q] = fma(Ml.x, d[q], xr[q]);
+        xi[q] = fma(-Ml.y, d[q], xi[q]);
+      }
+      if (l == L0) break;
+      T A, Bc, Cc;
+      rec_coef<T>(l, m * n, m * m, n * n, inv_l, inv_ll, A, Bc, Cc, sq);
+#pragma unroll
+      for (int q = 0; q < kJG; ++q) {
+        const T dn = fma(A * d[q], cb[q], -fma(Bc, d[q], Cc * dprev[q]));
+        dprev[q] = d[q];
+        d[q] = dn;
+      }
+      off += (l + 1) * (2 * l + 1) + 2 * m + 1;
+    }
+#pragma unroll
+    for (int q = 0; q < kJG; ++q) {
+      const int j = jg * kJG + q;
+      if (j < nb) X[((size_t)j * nm + m) * w0 + (n + L0)] = mk<T>(xr[q], xi[q]);
+    }
+  }
+  __syncthreads();
+
+  const int PA = na + 2, PG = ng + 2, PP = PA * PG;  // padded grid: [nb][PA][PG]
+  const int naq = (PA + 3) / 4;
+  const uint32_t mgn = (uint32_t)((0x100000000ull + ng - 1) / ng), mgq = (uint32_t)((0x100000000ull + naq - 1) / naq);
+  const uint32_t mgp = (uint32_t)((0x100000000ull + PG - 1) / PG);
+  for (int j0 = 0; j0 < nb; j0 += jc) {
+    const int nj = min(jc, nb - j0);
+    // phase 2: Y_{m,c} = sum_n X_mn e^{-i n gamma_c}
+    for (int t = tid; t < nj * nm * ng; t += kGThreads) {
+      const int r = fdiv(t, mgn), c = t - r * ng;  // r = jj * nm + m
+      const cplx_t<T>* x = X + ((size_t)j0 * nm + r) * w0;
+      T yr = T(0), yi = T(0);
+      for (int n = 0; n < w0; ++n) {
+        const cplx_t<T> xv = x[n];
+        const cplx_t<T> e = Eg[n * ng + c];
+        yr = fma(xv.x, e.x, fma(-xv.y, e.y, yr));
+        yi = fma(xv.x, e.y, fma(xv.y, e.x, yi));
+      }
+      Y[t] = mk<T>(yr, yi);
+    }
+    __syncthreads();
+    // phase 3: C(alpha_a, beta_j, gamma_c) on the halo-padded grid (padded index a_p = a + 1, c_p = c + 1, wrapped),
+    // four alphas per item sharing the Y loads
+    for (int t = tid; t < nj * naq * PG; t += kGThreads) {
+      const int r = fdiv(t, mgp), cp = t - r * PG, jj = fdiv(r, mgq), aq = r - jj * naq;
+      const int c = cp == 0 ? ng - 1 : (cp > ng ? 0 : cp - 1);
+      const cplx_t<T>* y = Y + (size_t)jj * nm * ng + c;
+      int av[4];
+      T s2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ap = min(4 * aq + q, PA - 1);
+        av[q] = ap == 0 ? na - 1 : (ap > na ? 0 : ap - 1);
+        s2[q] = T(0);
+      }
+      const T s0 = y[0].x;
+      for (int m = 1; m <= L0; ++m) {
+        const cplx_t<T> yy = y[m * ng];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const cplx_t<T> e = Ea[m * na + av[q]];
+          s2[q] = fma(yy.x, e.x, fma(-yy.y, e.y, s2[q]));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * aq + q < PA) C[(size_t)(j0 + jj) * PP + (4 * aq + q) * PG + cp] = fma(T(2), s2[q], s0);
+    }
+    __syncthreads();
+  }
+
+  // phase 4: strict local maxima (26 neighbours; alpha, gamma periodic, beta clamped).  Every point first meets its
+  // 8 in-slice neighbours at constant offsets of the padded grid (branch-free; the exact key order is only needed on
+  // a value tie); the few survivors of a warp are then tested against their 18 neighbours in slices j +- 1 by 18
+  // lanes at once (one ballot per survivor).
+  const uint32_t mg_ng = (uint32_t)((0x100000000ull + ng - 1) / ng), mg_na = (uint32_t)((0x100000000ull + na - 1) / na);
+  const int ntot = nb * na * ng;
+  auto key_index = [&](int j, int ap, int cp) {  // logical node index of a padded position
+    const int a2 = ap == 0 ? na - 1 : (ap > na ? 0 : ap - 1);
+    const int c2 = cp == 0 ? ng - 1 : (cp > ng ? 0 : cp - 1);
+    return (j * na + a2) * ng + c2;
+  };
+  for (int base = 0; base < ntot; base += kGThreads) {
+    const int ip = base + tid;
+    const bool valid = ip < ntot;
+    const int ipc = valid ? ip : ntot - 1;
+    const int r = fdiv(ipc, mg_ng), c = ipc - r * ng, j = fdiv(r, mg_na), aa = r - j * na;
+    const T* cc = C + (size_t)j * PP + (aa + 1) * PG + (c + 1);
+    const T v = cc[0];
+    const T nv[8] = {cc[-PG - 1], cc[-PG], cc[-PG + 1], cc[-1], cc[1], cc[PG - 1], cc[PG], cc[PG + 1]};
+    bool gt = true, eq = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      gt = gt && (v > nv[q]);
+      eq = eq || (v == nv[q]);
+    }
+    bool surv = valid && gt;
+    if (valid && eq) {  // value tie: exact key order (score desc, index asc)
+      surv = true;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int qq = q < 4 ? q : q + 1;
+        const int iq = key_index(j, aa + 1 + qq / 3 - 1, c + 1 + qq % 3 - 1);
+        surv = surv && before(v, ipc, nv[q], iq);
+      }
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, surv);
+    while (bal) {
+      const int src = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const int ipx = __shfl_sync(0xffffffffu, ipc, src);
+      const T vx = __shfl_sync(0xffffffffu, v, src);
+      const int rx = fdiv(ipx, mg_ng), cx = ipx - rx * ng, jx = fdiv(rx, mg_na), ax = rx - jx * na;
+      bool ok = true;
+      if (lane < 18) {
+        const int jn = jx + (lane < 9 ? -1 : 1), q = lane < 9 ? lane : lane - 9;
+        if (jn >= 0 && jn < nb) {
+          const int ap = ax + q / 3, cp = cx + q % 3;  // padded: (ax + 1) + (q / 3 - 1)
+          ok = before(vx, ipx, C[(size_t)jn * PP + ap * PG + cp], key_index(jn, ap, cp));
+        }
+      }
+      if (__all_sync(0xffffffffu, ok) && lane == src) {
+        const int slot = atomicAdd(cnt, 1);
+        if (slot < kCap) {
+          cs[slot] = vx;
+          ci[slot] = ipx;
+        } else {
+          atomicOr(a.flags, FLAG_OVERFLOW);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // phase 5: top-N_C by (score desc, index asc), one warp
+  if (warp == 0) {
+    const int total = min(*cnt, kCap);
+    for (int k = 0; k < a.ncand; ++k) {
+      T bs = -INFINITY;
+      int bi = 0x7fffffff, bt = -1;
+      for (int t = lane; t < total; t += 32)
+        if (ci[t] >= 0 && before(cs[t], ci[t], bs, bi)) {
+          bs = cs[t];
+          bi = ci[t];
+          bt = t;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const T s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int t2 = __shfl_xor_sync(0xffffffffu, bt, o);
+        if (before(s2, i2, bs, bi)) {
+          bs = s2;
+          bi = i2;
+          bt = t2;
+        }
+      }
+      if (lane == 0) {
+        const int64_t o = p * a.ncand + k;
+        if (bi != 0x7fffffff) {
+          const int c = bi % ng, aa = (bi / ng) % na, jj = bi / (ng * na);
+          a.euler[o * 3 + 0] = (T)(2.0 * kPi * aa / na);
+          a.euler[o * 3 + 1] = (T)((jj + 0.5) * kPi / nb);
+          a.euler[o * 3 + 2] = (T)(2.0 * kPi * c / ng);
+          a.score[o] = bs;
+          a.idx[o] = bi;
+          ci[bt] = -1;  // taken
+        } else {
+          a.euler[o * 3 + 0] = a.euler[o * 3 + 1] = a.euler[o * 3 + 2] = T(0);
+          a.score[o] = -INFINITY;
+          a.idx[o] = -1;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// slices per Y chunk for the full-grid kernel (0 = the grid does not fit: use the rolling-window kernel)
+template <typename T> int grid_chunk(int L0, int K) {
+  const int nb = K * (L0 + 1);
+  for (int jc = nb; jc >= 1; --jc)
+    if (grid_layout<T>(L0, K, jc).total <= 225 * 1024) return jc;
+  return 0;
+}
+
 }  // namespace
 
 template <typename T> cudaError_t launch_so3_search(const SearchArgs<T>& a, cudaStream_t s) {
   if (a.B == 0) return cudaSuccess;
+  const int jc = getenv("MATCHA_SEARCH_WINDOW") ? 0 : grid_chunk<T>(a.L0, a.K);
+  if (jc > 0) {
+    const size_t bytes = grid_layout<T>(a.L0, a.K, jc).total;
+    cudaError_t e = cudaFuncSetAttribute(k_so3_grid<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    k_so3_grid<T><<<(unsigned)a.B, kGThreads, bytes, s>>>(a, jc);
+    return cudaGetLastError();
+  }
   const size_t bytes = search_layout<T>(a.L0, a.K).total;
   cudaError_t e = cudaFuncSetAttribute(k_so3_search<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
@@ -326,6 +637,8 @@ template cudaError_t launch_so3_search<float>(const SearchArgs<float>&, cudaStre
 template cudaError_t launch_so3_search<double>(const SearchArgs<double>&, cudaStream_t);
 
 size_t search_smem_bytes(int L0, int K, bool fp64) {
+  const int jc = fp64 ? grid_chunk<double>(L0, K) : grid_chunk<float>(L0, K);
+  if (jc > 0) return fp64 ? grid_layout<double>(L0, K, jc).total : grid_layout<float>(L0, K, jc).total;
   return fp64 ? search_layout<double>(L0, K).total : search_layout<float>(L0, K).total;
 }
 
