@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/matcha.h"
 
@@ -37,7 +38,7 @@ constexpr int kMaxL = 128;
 constexpr int kMaxCand = 32;
 
 // device error flags
-enum : int { FLAG_NONFINITE = 1, FLAG_OVERFLOW = 2 };
+enum : int { FLAG_NONFINITE = 1, FLAG_OVERFLOW = 2, FLAG_PLANES = 4 };
 
 // Stage-4 pair descriptor: (m, n) with m >= 0, grouped by shell l0 = max(m,|n|) (long l-runs first).
 // lnc = 1/2 ln C(2 l0, |m+n|) (seed normalisation), in double on the host.
@@ -54,6 +55,9 @@ template <typename T> struct ShTables {
   const int* pw_moff;     // [L+2] offsets of the m blocks (pw_moff[L+1] = pw_stride)
   const cplx_t<T>* dft;   // [Kh+1][L+1]: (cos, sin)(m phi_k) for the folded ring DFT
   int N, R, L, nth, nph, Jh, Kh, MP, pw_stride;
+  int tcP;                // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel), FP32 only
+  int num_sms;
+  int* flags;
 };
 
 template <typename T> struct NewtonArgs {
@@ -109,6 +113,10 @@ template <typename T>
 cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
                                 T* poses, cudaStream_t s);
 size_t search_smem_bytes(int L0, int K, bool fp64);
+int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode);
+cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shifts, int shift_stride,
+                               const ShTables<float>& tab, int P, float2* G, int* flags, int num_sms,
+                               cudaStream_t st);
 size_t corr_tc_smem_bytes(int L, int R);
 bool corr_tc_supported(int L, int R);
 cudaError_t launch_corr_coeffs_tc(const float2* F, const float2* H, int64_t B, int L, int Lmax, int R, float2* M,

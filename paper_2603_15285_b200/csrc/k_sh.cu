@@ -675,8 +675,16 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
     const int64_t nb = std::min<int64_t>(gws_particles, B - c0);
     const float* v = vols + c0 * (int64_t)N * N * N;
     const T* sh = shifts ? shifts + c0 * shift_stride : nullptr;
-    e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
-                      : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
+    if constexpr (sizeof(T) == 4) {
+      if (tab.tcP > 0)
+        e = launch_sh_rings_tc(v, nb, sh, shift_stride, tab, tab.tcP, Gws, tab.flags, tab.num_sms, st);
+      else
+        e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
+                          : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
+    } else {
+      e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
+                        : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
+    }
     if (e != cudaSuccess) return e;
     k_sh_legendre<T><<<(unsigned)(nb * (tab.R / 4)), lthreads, lbytes, st>>>(Gws, tab, JP,
                                                                               F + c0 * (int64_t)ncf * tab.R);

@@ -31,6 +31,7 @@ struct matcha_ctx {
   int* d_pw_moff = nullptr;
   void* d_dft = nullptr;    // parity-split cos/sin table of the folded ring DFT
   int Kh = 0, MP = 0, pw_stride = 0;
+  int tcP = 0;              // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel)
   PairDesc* d_pairs = nullptr;
   void* d_pair_lnc = nullptr;
   int* d_flags = nullptr;
@@ -169,6 +170,9 @@ template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
   t.nth = h->nth;
   t.nph = h->nph;
   t.Jh = h->Jh;
+  t.tcP = sizeof(T) == 4 ? h->tcP : 0;
+  t.num_sms = h->num_sms;
+  t.flags = h->d_flags;
   return t;
 }
 
@@ -514,9 +518,16 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_F, cb * mb * h->ncf * h->R);
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_M, cb * mb * half_size(h->L));
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_H, cb * h->ncf * h->R);
+  if (!h->fp64 && !(getenv("MATCHA_SH_SIMT") && getenv("MATCHA_SH_SIMT")[0] == '1')) {
+    std::vector<float> xn(h->nth);
+    for (int j = 0; j < h->nth; ++j) xn[j] = (float)x[j];
+    h->tcP = sh_tc_plane_slots(sh_tables<float>(h), xn);
+  }
   {
     const size_t per = cb * (size_t)h->R * h->nth * (h->L + 1);
     h->gws_particles = std::max<int64_t>(32, (int64_t)((96u << 20) / per));
+    // persistent tensor-core ring kernel: whole waves of one particle per SM
+    if (h->tcP > 0 && h->gws_particles >= h->num_sms) h->gws_particles = h->gws_particles / h->num_sms * h->num_sms;
     h->gws_particles = std::min<int64_t>(h->gws_particles, cfg->max_batch);
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_G, per * h->gws_particles);
   }
@@ -594,6 +605,7 @@ MATCHA_API matcha_status_t matcha_get_status(matcha_handle_t h, void* stream) {
   MATCHA_CUDA(h, cudaMemset(h->d_flags, 0, sizeof(int)));
   if (f & FLAG_NONFINITE) return fail(h, MATCHA_ERR_NONFINITE, "non-finite value produced on device");
   if (f & FLAG_OVERFLOW) return fail(h, MATCHA_ERR_OVERFLOW, "coarse-grid local-maximum list overflowed");
+  if (f & FLAG_PLANES) return fail(h, MATCHA_ERR_OVERFLOW, "stage-1 plane window overflowed (shift too large)");
   return MATCHA_OK;
 }
 
