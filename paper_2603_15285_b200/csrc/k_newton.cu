@@ -26,6 +26,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kMaxCG = 5;  // candidates per register group
 
 template <typename T> struct CandShared {
   T cb, sb, cot, invs2;
@@ -49,7 +50,7 @@ template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, i
   s.cand = take(sizeof(CandShared<T>) * Q);
   s.ea = take(sizeof(cplx_t<T>) * Q * (L + 1));
   s.eg = take(sizeof(cplx_t<T>) * Q * (2 * L + 1));
-  s.red = take(sizeof(T) * kWarps * 10 * 8);
+  s.red = take(sizeof(T) * 10 * kMaxCG * kThreads);  // per-thread partial sums [value][thread]
   s.sums = take(sizeof(double) * 10 * Q);
   s.prevc = take(sizeof(double) * Q);
   s.invl = take(sizeof(T) * (kMaxL + 2));
@@ -179,12 +180,11 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
   const int npairs = pair_count(L);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int na = L + 1, ng = 2 * L + 1;
+  constexpr int NVAL = NV * CG;
+  T* acc = red + tid;  // this thread's partial sums: value (v, k) at acc[(v * CG + k) * kThreads]
   for (int c0 = 0; c0 < Q; c0 += CG) {
-    T acc[NV][CG];
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int k = 0; k < CG; ++k) acc[v][k] = T(0);
+    for (int i = 0; i < NVAL; ++i) acc[i * kThreads] = T(0);
     // candidate indices of this group (clamped: duplicates of the last are computed, then ignored)
     int cid[CG];
 #pragma unroll
@@ -219,44 +219,72 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
         cbk[k] = cs[cid[k]].cb;
         sbk[k] = cs[cid[k]].sb;
       }
-      int64_t off = half_offset(l0) + (int64_t)m * (2 * l0 + 1) + (n + l0);
+      (void)sbk;
+      // M^l_mn for l = l0.. lives at half_offset(l) + m(2l+1) + n + l (consecutive l differ by (l+1)(2l+1)+2m+1).
+      // The l-loop is unrolled by two so that d^{l-1} is overwritten in place by d^{l+1} (no register rotation);
+      // M is loaded two degrees ahead of its use.
+      const cplx_t<T>* pM = M + ((int)half_offset(l0) + m * (2 * l0 + 1) + (n + l0));
+      int inc = (l0 + 1) * (2 * l0 + 1) + 2 * m + 1;  // pointer step l0 -> l0 + 1; grows by 4l + 5
+      auto next_ptr = [&](int l) {                   // advance pM from degree l to l + 1
+        pM += inc;
+        inc += 4 * l + 5;
+      };
+      const cplx_t<T> zero = mk<T>(T(0), T(0));
+      cplx_t<T> M0 = __ldg(pM), M1 = zero;
+      if (l0 < L) {
+        next_ptr(l0);
+        M1 = __ldg(pM);
+      }
       T sq = T(0);
-      for (int l = l0;; ++l) {
-        const cplx_t<T> Ml = __ldg(&M[off]);
+      auto accumulate = [&](int l, cplx_t<T> Ml, const T* dd, const T* ddp) {
         const T mr = Ml.x, mi = Ml.y;  // conj(M) = (mr, -mi)
 #pragma unroll
         for (int k = 0; k < CG; ++k) {
-          t0r[k] = fma(mr, d[k], t0r[k]);
-          t0i[k] = fma(-mi, d[k], t0i[k]);
+          t0r[k] = fma(mr, dd[k], t0r[k]);
+          t0i[k] = fma(-mi, dd[k], t0i[k]);
         }
         if (DERIV) {
           const T ll = (T)(l * (l + 1));
           const T umr = ll * mr, umi = ll * mi;
 #pragma unroll
           for (int k = 0; k < CG; ++k) {
-            t1r[k] = fma(mr, dp[k], t1r[k]);
-            t1i[k] = fma(-mi, dp[k], t1i[k]);
-            ur[k] = fma(umr, d[k], ur[k]);
-            ui[k] = fma(-umi, d[k], ui[k]);
+            t1r[k] = fma(mr, ddp[k], t1r[k]);
+            t1i[k] = fma(-mi, ddp[k], t1i[k]);
+            ur[k] = fma(umr, dd[k], ur[k]);
+            ui[k] = fma(-umi, dd[k], ui[k]);
           }
         }
-        if (l == L) break;
+      };
+      // (cur, old) = (d^l, d^{l-1}) -> old := d^{l+1}:  d^{l+1} = (A cos b - B) d^l - C d^{l-1},
+      //                                                 d'^{l+1} = (A cos b - B) d'^l - A sin b d^l - C d'^{l-1}
+      auto advance = [&](int l, const T* cur, T* old, const T* curp, T* oldp) {
         T A, Bc, Cc;
         rec_coef<T>(l, mn, m2, n2, inv_l, inv_ll, A, Bc, Cc, sq);
 #pragma unroll
         for (int k = 0; k < CG; ++k) {
-          const T x = A * d[k];
-          const T dn = fma(x, cbk[k], -fma(Bc, d[k], Cc * dprev[k]));
-          if (DERIV) {
-            const T y = fma(cbk[k], dp[k], -sbk[k] * d[k]);
-            const T dpn = fma(A, y, -fma(Bc, dp[k], Cc * dpprev[k]));
-            dpprev[k] = dp[k];
-            dp[k] = dpn;
-          }
-          dprev[k] = d[k];
-          d[k] = dn;
+          const T coef = fma(A, cbk[k], -Bc);
+          if (DERIV) oldp[k] = fma(coef, curp[k], fma(-A * sbk[k], cur[k], -Cc * oldp[k]));
+          old[k] = fma(coef, cur[k], -Cc * old[k]);
         }
-        off += (int64_t)(l + 1) * (2 * l + 1) + 2 * m + 1;
+      };
+      for (int l = l0;; l += 2) {
+        cplx_t<T> N0 = zero, N1 = zero;
+        if (l + 2 <= L) {
+          next_ptr(l + 1);
+          N0 = __ldg(pM);
+          if (l + 3 <= L) {
+            next_ptr(l + 2);
+            N1 = __ldg(pM);
+          }
+        }
+        accumulate(l, M0, d, dp);
+        if (l == L) break;
+        advance(l, d, dprev, dp, dpprev);  // dprev := d^{l+1}
+        accumulate(l + 1, M1, dprev, dpprev);
+        if (l + 1 == L) break;
+        advance(l + 1, dprev, d, dpprev, dp);  // d := d^{l+2}
+        M0 = N0;
+        M1 = N1;
       }
       // assembly with the phase e^{-i(m a + n g)}
       const T w = (m == 0) ? T(1) : T(2);
@@ -266,7 +294,7 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
         const cplx_t<T> pa = ea[cid[k] * na + m], pg = eg[cid[k] * ng + (n + L)];
         const T er = pa.x * pg.x - pa.y * pg.y, ei = pa.x * pg.y + pa.y * pg.x;
         const T z0r = t0r[k] * er - t0i[k] * ei, z0i = t0r[k] * ei + t0i[k] * er;
-        acc[0][k] = fma(w, z0r, acc[0][k]);
+        acc[(0 * CG + k) * kThreads] += w * z0r;
         if (DERIV) {
           const CandShared<T>& c = cs[cid[k]];
           const T z1r = t1r[k] * er - t1i[k] * ei, z1i = t1r[k] * ei + t1i[k] * er;
@@ -275,47 +303,29 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
           const T t2i = -c.cot * t1i[k] + qmn * t0i[k] - ui[k];
           const T z2r = t2r * er - t2i * ei;
           const T wz0 = w * z0r;
-          acc[1][k] = fma(w * fm, z0i, acc[1][k]);
-          acc[2][k] = fma(w, z1r, acc[2][k]);
-          acc[3][k] = fma(w * fn, z0i, acc[3][k]);
-          acc[4][k] = fma(-fm * fm, wz0, acc[4][k]);
-          acc[5][k] = fma(w, z2r, acc[5][k]);
-          acc[6][k] = fma(-fn * fn, wz0, acc[6][k]);
-          acc[7][k] = fma(w * fm, z1i, acc[7][k]);
-          acc[8][k] = fma(-fm * fn, wz0, acc[8][k]);
-          acc[9][k] = fma(w * fn, z1i, acc[9][k]);
+          acc[(1 * CG + k) * kThreads] += w * fm * z0i;
+          acc[(2 * CG + k) * kThreads] += w * z1r;
+          acc[(3 * CG + k) * kThreads] += w * fn * z0i;
+          acc[(4 * CG + k) * kThreads] += -fm * fm * wz0;
+          acc[(5 * CG + k) * kThreads] += w * z2r;
+          acc[(6 * CG + k) * kThreads] += -fn * fn * wz0;
+          acc[(7 * CG + k) * kThreads] += w * fm * z1i;
+          acc[(8 * CG + k) * kThreads] += -fm * fn * wz0;
+          acc[(9 * CG + k) * kThreads] += w * fn * z1i;
         }
       }
     }
-    // deterministic block reduction: warp reduce-scatter (or butterflies for few values), then a
-    // fixed-order sum over warps
-    constexpr int NVAL = NV * CG;
-    if constexpr (NVAL >= 16) {
-      constexpr int NP = (NVAL + 31) / 32 * 32;
-      T v[NP];
-#pragma unroll
-      for (int i = 0; i < NP; ++i) v[i] = (i < NVAL) ? acc[i / CG][i % CG] : T(0);
-      rs_levels<T, NP, 16>(v, lane);
-#pragma unroll
-      for (int i = 0; i < NP / 32; ++i) {
-        const int idx = lane * (NP / 32) + i;
-        if (idx < NVAL) red[warp * (NV * CG) + idx] = v[i];
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int k = 0; k < CG; ++k) {
-          const T s = warp_sum(acc[v][k]);
-          if (lane == 0) red[warp * (NV * CG) + v * CG + k] = s;
-        }
-    }
+    // deterministic block reduction: warp w sums values w, w + kWarps, ... over the 256 threads in a fixed order
+    // (FP64 lane partials, then a butterfly)
     __syncthreads();
-    if (tid < NV * CG) {
-      const int v = tid / CG, k = tid % CG;
-      double s = 0.0;
-      for (int wi = 0; wi < kWarps; ++wi) s += (double)red[wi * (NV * CG) + v * CG + k];
-      if (c0 + k < Q) sums[(c0 + k) * 10 + v] = s;
+    for (int i = warp; i < NVAL; i += kWarps) {
+      const T* row = red + i * kThreads;
+      double sacc = 0.0;
+#pragma unroll
+      for (int u = 0; u < kThreads / 32; ++u) sacc += (double)row[lane + 32 * u];
+      sacc = warp_sum(sacc);
+      const int v = i / CG, k = i % CG;
+      if (lane == 0 && c0 + k < Q) sums[(c0 + k) * 10 + v] = sacc;
     }
     __syncthreads();
   }

@@ -17,7 +17,12 @@
 namespace matcha {
 
 template <typename T> __device__ __forceinline__ T rsqrt_t(T x);
-template <> __device__ __forceinline__ float rsqrt_t<float>(float x) { return rsqrtf(x); }
+// x >= 1 here (Q_{l+1} is a positive integer): the approximate reciprocal square root without the denormal fix-up
+template <> __device__ __forceinline__ float rsqrt_t<float>(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 template <> __device__ __forceinline__ double rsqrt_t<double>(double x) { return rsqrt(x); }
 
 template <typename T> __device__ __forceinline__ T exp_t(T x);
