@@ -289,6 +289,7 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
       // assembly with the phase e^{-i(m a + n g)}
       const T w = (m == 0) ? T(1) : T(2);
       const T fm = (T)m, fn = (T)n;
+      const T wm = w * fm, wn = w * fn, wmm = -fm * fm, wnn = -fn * fn, wmn = -fm * fn;
 #pragma unroll
       for (int k = 0; k < CG; ++k) {
         const cplx_t<T> pa = ea[cid[k] * na + m], pg = eg[cid[k] * ng + (n + L)];
@@ -303,15 +304,15 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
           const T t2i = -c.cot * t1i[k] + qmn * t0i[k] - ui[k];
           const T z2r = t2r * er - t2i * ei;
           const T wz0 = w * z0r;
-          acc[(1 * CG + k) * kThreads] += w * fm * z0i;
+          acc[(1 * CG + k) * kThreads] += wm * z0i;
           acc[(2 * CG + k) * kThreads] += w * z1r;
-          acc[(3 * CG + k) * kThreads] += w * fn * z0i;
-          acc[(4 * CG + k) * kThreads] += -fm * fm * wz0;
+          acc[(3 * CG + k) * kThreads] += wn * z0i;
+          acc[(4 * CG + k) * kThreads] += wmm * wz0;
           acc[(5 * CG + k) * kThreads] += w * z2r;
-          acc[(6 * CG + k) * kThreads] += -fn * fn * wz0;
-          acc[(7 * CG + k) * kThreads] += w * fm * z1i;
-          acc[(8 * CG + k) * kThreads] += -fm * fn * wz0;
-          acc[(9 * CG + k) * kThreads] += w * fn * z1i;
+          acc[(6 * CG + k) * kThreads] += wnn * wz0;
+          acc[(7 * CG + k) * kThreads] += wm * z1i;
+          acc[(8 * CG + k) * kThreads] += wmn * wz0;
+          acc[(9 * CG + k) * kThreads] += wn * z1i;
         }
       }
     }
