@@ -21,6 +21,7 @@
 // Deterministic: fixed summation orders, ring lists built by an ordered block scan, no atomics.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -599,6 +600,99 @@ __global__ void __launch_bounds__(512) k_sh_legendre(const cplx_t<T>* __restrict
   }
 }
 
+// Legendre contraction, whole-shell-group variant: the CTA's SG shells of G (all nodes, all m) are copied to shared
+// memory in one cp.async pass and node-pair folded in place (G_j +- G_{n-1-j}); thread tiles (one m, 4 consecutive l)
+// x SG shells then stream the m-major weight rows W_j Pbar_lm(x_j) (float4, loaded two nodes ahead).
+template <typename T> __host__ __device__ inline size_t leg_full_bytes(int SG, int nth, int L) {
+  return sizeof(cplx_t<T>) * (size_t)SG * nth * (L + 1);
+}
+
+template <typename T, int SG>
+__global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __restrict__ G, ShTables<T> tab,
+                                                          cplx_t<T>* __restrict__ F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = tab.R, L = tab.L, nth = tab.nth, Jh = tab.Jh;
+  const int L1 = L + 1, ncf = ncoef(L);
+  cplx_t<T>* Gs = (cplx_t<T>*)smem;  // [SG][nth][L+1]
+  const int ngroups = R / SG;
+  const int64_t p = blockIdx.x / ngroups;
+  const int i0 = (blockIdx.x % ngroups) * SG;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  {
+    const cplx_t<T>* src = G + ((p * R + i0) * (int64_t)nth) * L1;
+    const int n = SG * nth * L1;
+    for (int e = tid; e < n; e += nthr) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Gs + e);
+      if (sizeof(T) == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + e));
+      else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + e));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+  {
+    const int half = nth / 2;  // node pairs (j, nth-1-j), j < half; an odd middle node stays as is
+    for (int e = tid; e < SG * half * L1; e += nthr) {
+      const int m = e % L1, r = e / L1, j = r % half, sh = r / half;
+      cplx_t<T>* a = Gs + ((size_t)sh * nth + j) * L1 + m;
+      cplx_t<T>* b = Gs + ((size_t)sh * nth + (nth - 1 - j)) * L1 + m;
+      const cplx_t<T> u = *a, v = *b;
+      *a = mk<T>(u.x + v.x, u.y + v.y);
+      *b = mk<T>(u.x - v.x, u.y - v.y);
+    }
+  }
+  __syncthreads();
+  const int ntiles = leg_tiles(L);
+  cplx_t<T>* Fp = F + p * (int64_t)ncf * R;
+  using V = typename V4<T>::t;
+  for (int tile = tid; tile < ntiles; tile += nthr) {
+    int m = 0, lb = tile;
+    for (; m <= L; ++m) {
+      const int nt = (L - m + 4) / 4;
+      if (lb < nt) break;
+      lb -= nt;
+    }
+    const int l0t = m + 4 * lb;
+    const int poff = __ldg(&tab.pw_moff[m]) + 4 * lb;
+    const bool odd0 = ((l0t + m) & 1) != 0;  // parity of l + m for a = 0 (alternates with a)
+    T ar[4][SG], ai[4][SG];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int s = 0; s < SG; ++s) ar[a][s] = ai[a][s] = T(0);
+    const T* wrow = tab.pwm + poff;
+    V wn0 = *reinterpret_cast<const V*>(wrow), wn1 = wn0;
+    if (Jh > 1) wn1 = *reinterpret_cast<const V*>(wrow + tab.pw_stride);
+    for (int q = 0; q < Jh; ++q) {
+      const V wv = wn0;
+      wn0 = wn1;
+      if (q + 2 < Jh) wn1 = *reinterpret_cast<const V*>(wrow + (size_t)(q + 2) * tab.pw_stride);
+      const T w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+      for (int s = 0; s < SG; ++s) {
+        const cplx_t<T> ge = Gs[((size_t)s * nth + q) * L1 + m];               // G+ (even l + m)
+        const cplx_t<T> go = Gs[((size_t)s * nth + (nth - 1 - q)) * L1 + m];  // G- (odd l + m)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const cplx_t<T> g = (odd0 ^ (a & 1)) ? go : ge;
+          ar[a][s] = fma(w[a], g.x, ar[a][s]);
+          ai[a][s] = fma(w[a], g.y, ai[a][s]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int l = l0t + a;
+      if (l > L) continue;
+      const int lm = l * (l + 1) / 2 + m;
+#pragma unroll
+      for (int s = 0; s < SG; ++s) Fp[(size_t)lm * R + i0 + s] = mk<T>(ar[a][s], ai[a][s]);
+    }
+  }
+}
+
 template <typename T> struct ShPlan {
   int S, nslab;
   bool dft_smem;
@@ -671,6 +765,16 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
   const int lthreads = std::min(512, (leg_tiles(tab.L) + 31) / 32 * 32);
   cudaError_t e = cudaFuncSetAttribute(k_sh_legendre<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lbytes);
   if (e != cudaSuccess) return e;
+  // whole-shell-group Legendre variant when SG shells of G fit in shared memory
+  int lsg = 0;
+  if (tab.R % 4 == 0 && leg_full_bytes<T>(4, tab.nth, tab.L) <= 110 * 1024) lsg = 4;
+  else if (tab.R % 2 == 0 && leg_full_bytes<T>(2, tab.nth, tab.L) <= 200 * 1024) lsg = 2;
+  if (getenv("MATCHA_LEG_OLD")) lsg = 0;
+  const size_t lfb = lsg ? leg_full_bytes<T>(lsg, tab.nth, tab.L) : 0;
+  if (lsg == 4) e = cudaFuncSetAttribute(k_sh_legendre_full<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
+  if (lsg == 2) e = cudaFuncSetAttribute(k_sh_legendre_full<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
+  if (e != cudaSuccess) return e;
+  const int lfthreads = std::min(256, (leg_tiles(tab.L) + 31) / 32 * 32);
   for (int64_t c0 = 0; c0 < B; c0 += gws_particles) {
     const int64_t nb = std::min<int64_t>(gws_particles, B - c0);
     const float* v = vols + c0 * (int64_t)N * N * N;
@@ -686,8 +790,13 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
                         : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
     }
     if (e != cudaSuccess) return e;
-    k_sh_legendre<T><<<(unsigned)(nb * (tab.R / 4)), lthreads, lbytes, st>>>(Gws, tab, JP,
-                                                                              F + c0 * (int64_t)ncf * tab.R);
+    if (lsg == 4)
+      k_sh_legendre_full<T, 4><<<(unsigned)(nb * (tab.R / 4)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
+    else if (lsg == 2)
+      k_sh_legendre_full<T, 2><<<(unsigned)(nb * (tab.R / 2)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
+    else
+      k_sh_legendre<T><<<(unsigned)(nb * (tab.R / 4)), lthreads, lbytes, st>>>(Gws, tab, JP,
+                                                                                F + c0 * (int64_t)ncf * tab.R);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
