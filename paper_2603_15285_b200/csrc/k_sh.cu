@@ -620,13 +620,18 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
   const int tid = threadIdx.x, nthr = blockDim.x;
   {
     const cplx_t<T>* src = G + ((p * R + i0) * (int64_t)nth) * L1;
-    const int n = SG * nth * L1;
-    for (int e = tid; e < n; e += nthr) {
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(Gs + e);
-      if (sizeof(T) == 4)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + e));
-      else
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + e));
+    const int nbytes = (int)sizeof(cplx_t<T>) * SG * nth * L1;
+    const bool al16 = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)nbytes) & 15) == 0;
+    if (al16) {
+      for (int e = tid; e < nbytes / 16; e += nthr) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared((unsigned char*)Gs + 16 * e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)src + 16 * e));
+      }
+    } else {
+      for (int e = tid; e < nbytes / 8; e += nthr) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared((unsigned char*)Gs + 8 * e);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"((const unsigned char*)src + 8 * e));
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 0;\n" ::);
@@ -634,8 +639,10 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
   __syncthreads();
   {
     const int half = nth / 2;  // node pairs (j, nth-1-j), j < half; an odd middle node stays as is
+    const uint32_t mgL = (uint32_t)((0x100000000ull + L1 - 1) / L1), mgH = (uint32_t)((0x100000000ull + half - 1) / half);
     for (int e = tid; e < SG * half * L1; e += nthr) {
-      const int m = e % L1, r = e / L1, j = r % half, sh = r / half;
+      const int r = (int)__umulhi((uint32_t)e, mgL), m = e - r * L1;
+      const int sh = (int)__umulhi((uint32_t)r, mgH), j = r - sh * half;
       cplx_t<T>* a = Gs + ((size_t)sh * nth + j) * L1 + m;
       cplx_t<T>* b = Gs + ((size_t)sh * nth + (nth - 1 - j)) * L1 + m;
       const cplx_t<T> u = *a, v = *b;
@@ -663,12 +670,15 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
 #pragma unroll
       for (int s = 0; s < SG; ++s) ar[a][s] = ai[a][s] = T(0);
     const T* wrow = tab.pwm + poff;
-    V wn0 = *reinterpret_cast<const V*>(wrow), wn1 = wn0;
-    if (Jh > 1) wn1 = *reinterpret_cast<const V*>(wrow + tab.pw_stride);
+    constexpr int PD = 4;  // weight rows in flight
+    V wq[PD];
+#pragma unroll
+    for (int u = 0; u < PD; ++u) wq[u] = *reinterpret_cast<const V*>(wrow + (size_t)min(u, Jh - 1) * tab.pw_stride);
     for (int q = 0; q < Jh; ++q) {
-      const V wv = wn0;
-      wn0 = wn1;
-      if (q + 2 < Jh) wn1 = *reinterpret_cast<const V*>(wrow + (size_t)(q + 2) * tab.pw_stride);
+      const V wv = wq[0];
+#pragma unroll
+      for (int u = 0; u + 1 < PD; ++u) wq[u] = wq[u + 1];
+      wq[PD - 1] = *reinterpret_cast<const V*>(wrow + (size_t)min(q + PD, Jh - 1) * tab.pw_stride);
       const T w[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
       for (int s = 0; s < SG; ++s) {
