@@ -308,7 +308,8 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         tr = json.load(open(tp)).get(args.config, {}).get(dom)
-        traffic = tr
+        if isinstance(tr, dict):
+            traffic = tr.get("bytes_per_particle")
     if t_alu >= t_hbm:
         achieved = fl * units / t_stage / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
@@ -322,6 +323,8 @@ def main():
                                  if roof["bound"] == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({src})"),
                  "launches": dn, "avg_launch_ms": dms / dn,
                  "work_per_particle": {"flop": fl, "bytes": by},
+                 "traffic_unit": "DRAM bytes per particle (ncu dram__bytes_read+write of the stage's kernels, "
+                                 "profiles/traffic.json); compare with work_per_particle.bytes",
                  "hbm_gbs_achieved": by * units / t_stage / 1e9,
                  "alu_tflops_achieved": fl * units / t_stage / 1e12,
                  "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()}})

@@ -1,5 +1,6 @@
 # Full evidence run (under gpurun): GPU tests, the default bench line, the ncu launch list of the same bench
-# command, one ncu --set full capture of the dominant kernels, clocks.  Outputs in gpurun_out/<tag>_*.
+# command, one ncu --set full capture per hot kernel (c2 sub-batch / full-batch launches), clocks.
+# Outputs in gpurun_out/<tag>_*; summarise here with: python scripts/summarize_profile.py <tag>
 TAG=${1:-r1}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv,noheader > gpurun_out/${TAG}_gpu.txt
@@ -12,5 +13,7 @@ tail -c 1500 gpurun_out/${TAG}_bench.json
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu1.log 2>&1; echo launches_exit=$?
-$CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:k_sh_rings|k_sh_legendre|k_newton_refine|k_so3_search|k_corr_coeffs" -s 5 -c 5 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_ncu2.log 2>&1; echo full_exit=$?
+# one --set full capture per kernel: skip the reference-analysis launch and warm-up launches
+for K in k_sh_rings_tc k_sh_legendre_full k_corr_tc k_so3_grid k_newton_refine; do
+  ncu --set full --clock-control none --import-source on -k "regex:$K" -s 3 -c 1 -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_$K.log 2>&1; echo full_$K=$?
+done

@@ -64,11 +64,15 @@ if os.path.exists(lc):
         out.append(f"| `{k}` | {n} | {t:.1f} | {100 * t / tot:.1f} % |")
     out.append("")
 
-rep = os.path.join(G, f"{tag}_full.ncu-rep")
+import glob
+reps = sorted(glob.glob(os.path.join(G, f"{tag}_full*.ncu-rep")))
 traffic = {}
-if os.path.exists(rep):
+header_done = False
+for rep in reps:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    if len(rows) < 3:
+        continue
     hdr = rows[0]
     want = ["gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
             "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
@@ -77,10 +81,12 @@ if os.path.exists(rep):
             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
-    out.append("## ncu --set full (one launch per kernel)\n")
-    out.append("| kernel | " + " | ".join(w.replace(".avg.pct_of_peak_sustained_active", " %").replace(".sum", "")
-                                         for w in want) + " |")
-    out.append("|" + "---|" * (len(want) + 1))
+    if not header_done:
+        header_done = True
+        out.append("## ncu --set full (one launch per kernel)\n")
+        out.append("| kernel | " + " | ".join(w.replace(".avg.pct_of_peak_sustained_active", " %").replace(".sum", "")
+                                             for w in want) + " |")
+        out.append("|" + "---|" * (len(want) + 1))
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("<unnamed>::", "")
         vals = []
@@ -93,13 +99,21 @@ if os.path.exists(rep):
             unit = rows[1][hdr.index("dram__bytes_read.sum")]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             key = "sh_analysis" if "k_sh" in name else "newton_refine" if "newton" in name else \
-                "so3_search" if "search" in name else "corr_coeffs" if "corr" in name else name
+                "so3_search" if ("search" in name or "so3" in name) else "corr_coeffs" if "corr" in name else name
+            # particles in the captured launch: the stage-1 kernels run on sub-batches of 148 (one per SM), the
+            # others on the whole 1,000-particle batch
+            per = 148 if "k_sh" in name else 1000
             traffic.setdefault(key, 0.0)
-            traffic[key] += (rd + wr) * scale
+            traffic[key] += (rd + wr) * scale / per
         except (ValueError, IndexError):
             pass
-    out.append("\n(dram units as printed by ncu; one launch = one sub-batch of particles)\n")
-    shutil.copy(rep, os.path.join(P, f"{tag}_full.ncu-rep"))
+    shutil.copy(rep, os.path.join(P, os.path.basename(rep)))
+if header_done:
+    out.append("\n(dram units as printed by ncu; stage-1 launches = sub-batches of 148 particles, the others = 1,000)\n")
+    out.append("DRAM traffic per particle (bytes, from the captures above): " +
+               ", ".join(f"{k} {v:.0f}" for k, v in traffic.items()) + "\n")
+    json.dump({"c2": {k: {"bytes_per_particle": v, "source": f"profiles/{tag}_full_*.ncu-rep dram__bytes_read+write"}
+                      for k, v in traffic.items()}}, open(os.path.join(P, "traffic.json"), "w"), indent=1)
 
 md = os.path.join(P, f"{tag}_summary.md")
 open(md, "w").write(f"# GPU evidence — {tag}\n\n" + "\n".join(out) + "\n")
