@@ -790,7 +790,9 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
     const float* v = vols + c0 * (int64_t)N * N * N;
     const T* sh = shifts ? shifts + c0 * shift_stride : nullptr;
     if constexpr (sizeof(T) == 4) {
-      if (tab.tcP > 0)
+      // the persistent tensor-core kernel gives one particle to one SM: small batches (e.g. the reference) go to
+      // the slab-parallel SIMT kernel instead, which spreads one particle over N/S CTAs
+      if (tab.tcP > 0 && nb * 4 >= tab.num_sms)
         e = launch_sh_rings_tc(v, nb, sh, shift_stride, tab, tab.tcP, Gws, tab.flags, tab.num_sms, st);
       else
         e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
