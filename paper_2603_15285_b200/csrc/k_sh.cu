@@ -607,7 +607,7 @@ template <typename T> __host__ __device__ inline size_t leg_full_bytes(int SG, i
   return sizeof(cplx_t<T>) * (size_t)SG * nth * (L + 1);
 }
 
-template <typename T, int SG>
+template <typename T, int SG, bool WS>
 __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __restrict__ G, ShTables<T> tab,
                                                           cplx_t<T>* __restrict__ F) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -631,6 +631,14 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
       for (int e = tid; e < nbytes / 8; e += nthr) {
         const unsigned sa = (unsigned)__cvta_generic_to_shared((unsigned char*)Gs + 8 * e);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"((const unsigned char*)src + 8 * e));
+      }
+    }
+    if (WS) {  // the whole m-major weight table W_j Pbar_lm(x_j), j < Jh (16-byte rows: pw_stride % 4 == 0)
+      const int wbytes = (int)sizeof(T) * Jh * tab.pw_stride;
+      unsigned char* wdst = smem + leg_full_bytes<T>(SG, nth, L);
+      for (int e = tid; e < wbytes / 16; e += nthr) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(wdst + 16 * e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)tab.pwm + 16 * e));
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -669,7 +677,7 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int s = 0; s < SG; ++s) ar[a][s] = ai[a][s] = T(0);
-    const T* wrow = tab.pwm + poff;
+    const T* wrow = (WS ? (const T*)(smem + leg_full_bytes<T>(SG, nth, L)) : tab.pwm) + poff;
     constexpr int PD = 4;  // weight rows in flight
     V wq[PD];
 #pragma unroll
@@ -701,6 +709,136 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
       for (int s = 0; s < SG; ++s) Fp[(size_t)lm * R + i0 + s] = mk<T>(ar[a][s], ai[a][s]);
     }
   }
+}
+
+// Persistent Legendre (FP32): one CTA per SM holds the whole weight table W_j Pbar_lm(x_j) in shared memory (loaded
+// once) and two independent 160-thread lanes, each walking its own (particle, 2-shell) items with the next item's G
+// prefetched by cp.async into a second buffer while the current one is folded and contracted.
+constexpr int kLegLaneThreads = 160;
+constexpr int kLegSG = 2;
+
+template <typename T>
+__global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
+    k_sh_legendre_pers(const cplx_t<T>* __restrict__ G, ShTables<T> tab, int64_t nitems, cplx_t<T>* __restrict__ F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int SG = kLegSG, LT = kLegLaneThreads;
+  const int R = tab.R, L = tab.L, nth = tab.nth, Jh = tab.Jh;
+  const int L1 = L + 1, ncf = ncoef(L);
+  const int tid = threadIdx.x, lane_id = tid / LT, ltid = tid % LT;
+  const size_t gbytes = sizeof(cplx_t<T>) * (size_t)SG * nth * L1;
+  const int wbytes = (int)sizeof(T) * Jh * tab.pw_stride;
+  const T* W = (const T*)smem;
+  cplx_t<T>* Gb[2];
+  Gb[0] = (cplx_t<T>*)(smem + (((size_t)wbytes + 15) & ~size_t(15)) + (size_t)(2 * lane_id) * gbytes);
+  Gb[1] = (cplx_t<T>*)((unsigned char*)Gb[0] + gbytes);
+  const int ngroups = R / SG;
+  // this CTA's contiguous item range; lane l takes items l, l + 2, ...
+  const int64_t i_begin = nitems * blockIdx.x / gridDim.x, i_end = nitems * (blockIdx.x + 1) / gridDim.x;
+  auto copy_item = [&](int64_t it, cplx_t<T>* dst) {
+    const int64_t p = it / ngroups;
+    const int i0 = (int)(it % ngroups) * SG;
+    const unsigned char* src = (const unsigned char*)(G + ((p * R + i0) * (int64_t)nth) * L1);
+    const bool al16 = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)gbytes) & 15) == 0;
+    if (al16) {
+      for (int e = ltid; e < (int)(gbytes / 16); e += LT) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared((unsigned char*)dst + 16 * e);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 16 * e));
+      }
+    } else {
+      for (int e = ltid; e < (int)(gbytes / 8); e += LT) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared((unsigned char*)dst + 8 * e);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + 8 * e));
+      }
+    }
+  };
+  for (int e = tid; e < wbytes / 16; e += 2 * LT) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem + 16 * e);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)tab.pwm + 16 * e));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  if (i_begin + lane_id < i_end) copy_item(i_begin + lane_id, Gb[0]);
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 1;\n" ::);  // this thread's part of the weight table
+  const int ntiles = leg_tiles(L);
+  __shared__ int tmap[kLegLaneThreads];            // thread tile -> (m, l-block)
+  for (int t = tid; t < ntiles; t += 2 * LT) {
+    int m = 0, lb = t;
+    for (; m <= L; ++m) {
+      const int nt = (L - m + 4) / 4;
+      if (lb < nt) break;
+      lb -= nt;
+    }
+    tmap[t] = (lb << 16) | m;
+  }
+  __syncthreads();                                // the whole weight table and the tile map
+  const int half = nth / 2;
+  const uint32_t mgL = (uint32_t)((0x100000000ull + L1 - 1) / L1), mgH = (uint32_t)((0x100000000ull + half - 1) / half);
+  auto lbar = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + lane_id), "r"(LT)); };
+  int k = 0;
+  for (int64_t it = i_begin + lane_id; it < i_end; it += 2, ++k) {
+    cplx_t<T>* Gs = Gb[k & 1];
+    if (it + 2 < i_end) copy_item(it + 2, Gb[(k + 1) & 1]);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    lbar();
+    // node-pair fold in place: (G_j, G_{n-1-j}) -> (G_j + G_{n-1-j}, G_j - G_{n-1-j})
+    for (int e = ltid; e < SG * half * L1; e += LT) {
+      const int r = (int)__umulhi((uint32_t)e, mgL), m = e - r * L1;
+      const int sh = (int)__umulhi((uint32_t)r, mgH), j = r - sh * half;
+      cplx_t<T>* a = Gs + ((size_t)sh * nth + j) * L1 + m;
+      cplx_t<T>* b = Gs + ((size_t)sh * nth + (nth - 1 - j)) * L1 + m;
+      const cplx_t<T> u = *a, v = *b;
+      *a = mk<T>(u.x + v.x, u.y + v.y);
+      *b = mk<T>(u.x - v.x, u.y - v.y);
+    }
+    lbar();
+    const int64_t p = it / ngroups;
+    const int i0 = (int)(it % ngroups) * SG;
+    cplx_t<T>* Fp = F + p * (int64_t)ncf * R;
+    for (int tile = ltid; tile < ntiles; tile += LT) {
+      const int m = tmap[tile] & 0xffff, lb = tmap[tile] >> 16;
+      const int l0t = m + 4 * lb;
+      const bool odd0 = ((l0t + m) & 1) != 0;
+      const T* wrow = W + __ldg(&tab.pw_moff[m]) + 4 * lb;
+      T ar[4][SG], ai[4][SG];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int s2 = 0; s2 < SG; ++s2) ar[a][s2] = ai[a][s2] = T(0);
+      using V = typename V4<T>::t;
+#pragma unroll 3
+      for (int q = 0; q < Jh; ++q) {
+        const V wv = *reinterpret_cast<const V*>(wrow + (size_t)q * tab.pw_stride);
+        const T w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int s2 = 0; s2 < SG; ++s2) {
+          const cplx_t<T> ge = Gs[((size_t)s2 * nth + q) * L1 + m];
+          const cplx_t<T> go = Gs[((size_t)s2 * nth + (nth - 1 - q)) * L1 + m];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const cplx_t<T> g = (odd0 ^ (a & 1)) ? go : ge;
+            ar[a][s2] = fma(w[a], g.x, ar[a][s2]);
+            ai[a][s2] = fma(w[a], g.y, ai[a][s2]);
+          }
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int l = l0t + a;
+        if (l > L) continue;
+        const int lm = l * (l + 1) / 2 + m;
+#pragma unroll
+        for (int s2 = 0; s2 < SG; ++s2) Fp[(size_t)lm * R + i0 + s2] = mk<T>(ar[a][s2], ai[a][s2]);
+      }
+    }
+    lbar();  // the buffer is refilled by the prefetch two items later
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+template <typename T> size_t leg_pers_bytes(const ShTables<T>& tab) {
+  const size_t w = (sizeof(T) * (size_t)tab.Jh * tab.pw_stride + 15) & ~size_t(15);
+  return w + 4 * sizeof(cplx_t<T>) * (size_t)kLegSG * tab.nth * (tab.L + 1);
 }
 
 template <typename T> struct ShPlan {
@@ -777,12 +915,25 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
   if (e != cudaSuccess) return e;
   // whole-shell-group Legendre variant when SG shells of G fit in shared memory
   int lsg = 0;
-  if (tab.R % 4 == 0 && leg_full_bytes<T>(4, tab.nth, tab.L) <= 110 * 1024) lsg = 4;
+  const size_t wtab = sizeof(T) * (size_t)tab.Jh * tab.pw_stride;
+  if (tab.R % 8 == 0 && leg_full_bytes<T>(8, tab.nth, tab.L) + wtab <= 220 * 1024) lsg = 8;
+  else if (tab.R % 4 == 0 && leg_full_bytes<T>(4, tab.nth, tab.L) <= 110 * 1024) lsg = 4;
   else if (tab.R % 2 == 0 && leg_full_bytes<T>(2, tab.nth, tab.L) <= 200 * 1024) lsg = 2;
   if (getenv("MATCHA_LEG_OLD")) lsg = 0;
-  const size_t lfb = lsg ? leg_full_bytes<T>(lsg, tab.nth, tab.L) : 0;
-  if (lsg == 4) e = cudaFuncSetAttribute(k_sh_legendre_full<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
-  if (lsg == 2) e = cudaFuncSetAttribute(k_sh_legendre_full<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
+  const bool lpers = sizeof(T) == 4 && tab.R % kLegSG == 0 && leg_tiles(tab.L) <= kLegLaneThreads &&
+                     leg_pers_bytes<T>(tab) <= 220 * 1024 && !getenv("MATCHA_LEG_NOPERS");
+  if (lpers) {
+    e = cudaFuncSetAttribute(k_sh_legendre_pers<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)leg_pers_bytes<T>(tab));
+    if (e != cudaSuccess) return e;
+  }
+  const size_t lfb = lsg ? leg_full_bytes<T>(lsg, tab.nth, tab.L) + (lsg == 8 ? wtab : 0) : 0;
+  if (lsg == 8)
+    e = cudaFuncSetAttribute(k_sh_legendre_full<T, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
+  if (lsg == 4)
+    e = cudaFuncSetAttribute(k_sh_legendre_full<T, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
+  if (lsg == 2)
+    e = cudaFuncSetAttribute(k_sh_legendre_full<T, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lfb);
   if (e != cudaSuccess) return e;
   const int lfthreads = std::min(256, (leg_tiles(tab.L) + 31) / 32 * 32);
   for (int64_t c0 = 0; c0 < B; c0 += gws_particles) {
@@ -802,10 +953,17 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
                         : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
     }
     if (e != cudaSuccess) return e;
-    if (lsg == 4)
-      k_sh_legendre_full<T, 4><<<(unsigned)(nb * (tab.R / 4)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
+    if (lpers) {
+      const int64_t items = nb * (tab.R / kLegSG);
+      const int grid = (int)std::min<int64_t>(tab.num_sms, (items + 1) / 2);
+      k_sh_legendre_pers<T><<<grid, 2 * kLegLaneThreads, leg_pers_bytes<T>(tab), st>>>(
+          Gws, tab, items, F + c0 * (int64_t)ncf * tab.R);
+    } else if (lsg == 8)
+      k_sh_legendre_full<T, 8, true><<<(unsigned)(nb * (tab.R / 8)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
+    else if (lsg == 4)
+      k_sh_legendre_full<T, 4, false><<<(unsigned)(nb * (tab.R / 4)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
     else if (lsg == 2)
-      k_sh_legendre_full<T, 2><<<(unsigned)(nb * (tab.R / 2)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
+      k_sh_legendre_full<T, 2, false><<<(unsigned)(nb * (tab.R / 2)), lfthreads, lfb, st>>>(Gws, tab, F + c0 * (int64_t)ncf * tab.R);
     else
       k_sh_legendre<T><<<(unsigned)(nb * (tab.R / 4)), lthreads, lbytes, st>>>(Gws, tab, JP,
                                                                                 F + c0 * (int64_t)ncf * tab.R);
