@@ -17,6 +17,8 @@
 // plus a fixed-order shared-memory pass (deterministic: no atomics).  The 3x3 Newton solve runs in FP64.
 #include <float.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "wigner.cuh"
 
@@ -26,7 +28,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCG = 5;  // candidates per register group
+constexpr int kMaxCG = 10;  // candidates per register group
 
 template <typename T> struct CandShared {
   T cb, sb, cot, invs2;
@@ -38,7 +40,7 @@ struct SmemLayout {
   size_t theta, cand, ea, eg, red, sums, prevc, invl, invll, flags, total;
 };
 
-template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, int L) {
+template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, int L, int cg) {
   SmemLayout s;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -50,7 +52,7 @@ template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, i
   s.cand = take(sizeof(CandShared<T>) * Q);
   s.ea = take(sizeof(cplx_t<T>) * Q * (L + 1));
   s.eg = take(sizeof(cplx_t<T>) * Q * (2 * L + 1));
-  s.red = take(sizeof(T) * 10 * kMaxCG * kThreads);  // per-thread partial sums [value][thread]
+  s.red = take(sizeof(T) * 10 * cg * kThreads);  // per-thread partial sums [value][thread]
   s.sums = take(sizeof(double) * 10 * Q);
   s.prevc = take(sizeof(double) * Q);
   s.invl = take(sizeof(T) * (kMaxL + 2));
@@ -342,10 +344,10 @@ __device__ void load_inv_tables(T* inv_l, T* inv_ll) {
 
 // ------------------------------------------------------------------ matcha_eval_corr kernel
 template <typename T, int CG>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) k_eval_corr(NewtonArgs<T> a, bool derivs) {
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1) k_eval_corr(NewtonArgs<T> a, bool derivs) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int L = a.L_eval, Q = a.Q;
-  const SmemLayout lay = smem_layout<T>(Q, L);
+  const SmemLayout lay = smem_layout<T>(Q, L, CG);
   double* theta = (double*)(smem + lay.theta);
   CandShared<T>* cs = (CandShared<T>*)(smem + lay.cand);
   cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
@@ -378,11 +380,11 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) k_eval_corr(
 
 // ------------------------------------------------------------------ matcha_newton_refine kernel
 template <typename T, int CG>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) k_newton_refine(NewtonArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1) k_newton_refine(NewtonArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int Q = a.Q;
   const int Lmax_b = a.bands[a.nbands - 1];
-  const SmemLayout lay = smem_layout<T>(Q, Lmax_b);
+  const SmemLayout lay = smem_layout<T>(Q, Lmax_b, CG);
   double* theta = (double*)(smem + lay.theta);
   CandShared<T>* cs = (CandShared<T>*)(smem + lay.cand);
   cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) k_newton_ref
 }
 
 template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a, bool derivs, cudaStream_t s) {
-  const SmemLayout lay = smem_layout<T>(a.Q, a.L_eval);
+  const SmemLayout lay = smem_layout<T>(a.Q, a.L_eval, CG);
   cudaError_t e = cudaFuncSetAttribute(k_eval_corr<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
   if (e != cudaSuccess) return e;
   k_eval_corr<T, CG><<<(unsigned)a.B, kThreads, lay.total, s>>>(a, derivs);
@@ -474,7 +476,7 @@ template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a,
 }
 
 template <typename T, int CG> cudaError_t launch_newton_cg(const NewtonArgs<T>& a, cudaStream_t s) {
-  const SmemLayout lay = smem_layout<T>(a.Q, a.bands[a.nbands - 1]);
+  const SmemLayout lay = smem_layout<T>(a.Q, a.bands[a.nbands - 1], CG);
   cudaError_t e =
       cudaFuncSetAttribute(k_newton_refine<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
   if (e != cudaSuccess) return e;
@@ -487,6 +489,7 @@ template <typename T> int pick_cg(int Q) {
   if (sizeof(T) == 8) return Q >= 2 ? 2 : 1;
   if (Q <= 2) return Q;
   if (Q <= 4) return 4;
+  if (Q == 10 && getenv("MATCHA_NEWTON_CG10")) return 10;
   if (Q % 5 == 0 || Q == 9) return 5;
   return 4;
 }
@@ -499,6 +502,7 @@ template <typename T> cudaError_t launch_eval_corr(const NewtonArgs<T>& a, bool 
     case 1: return launch_eval_cg<T, 1>(a, derivs, s);
     case 2: return launch_eval_cg<T, 2>(a, derivs, s);
     case 4: return launch_eval_cg<T, 4>(a, derivs, s);
+    case 10: return launch_eval_cg<T, 10>(a, derivs, s);
     default: return launch_eval_cg<T, 5>(a, derivs, s);
   }
 }
@@ -509,6 +513,7 @@ template <typename T> cudaError_t launch_newton_refine(const NewtonArgs<T>& a, c
     case 1: return launch_newton_cg<T, 1>(a, s);
     case 2: return launch_newton_cg<T, 2>(a, s);
     case 4: return launch_newton_cg<T, 4>(a, s);
+    case 10: return launch_newton_cg<T, 10>(a, s);
     default: return launch_newton_cg<T, 5>(a, s);
   }
 }
