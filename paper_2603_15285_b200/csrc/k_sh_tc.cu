@@ -23,6 +23,7 @@
 // Deterministic: fixed summation orders, no atomics on data.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -35,6 +36,7 @@ namespace matcha {
 namespace {
 
 constexpr int kThr = 512;
+__device__ unsigned long long g_sh_prof[8];  // MATCHA_SH_DBG & 8: cycles per phase, summed over sampler warps
 constexpr int kWarps = kThr / 32;
 constexpr int kNR = 64;   // rings per tile (UMMA_N)
 constexpr int kTM = 128;  // UMMA_M
@@ -388,6 +390,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       auto zfloor = [&](int i, int j) -> int { return (int)floorf(fmaf((float)i + 0.5f, node[j].x, cz)); };
       auto bucket = [&](int zb) { return min(max(zb, -2), N) + 2; };
 
+      long long tp0 = clock64();
       // ---- 1. counting sort of the rings by z bucket, then (j, i): deterministic (single writer per column j)
       for (int t = tid; t < nbk * nth; t += kThr) cnt[t] = 0;
       sbar();
@@ -426,6 +429,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           cnt[b] += 1;
         }
       sbar();
+      if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[0], (unsigned long long)(clock64() - tp0));
       // ---- 2. tiles: <= kNR consecutive rings whose planes fit the P-slot window (cut at z-bucket boundaries)
       if (tid == 0) {
         auto zlo_of = [&](int b) { return min(max(b - 2, -1), N - 1); };
@@ -475,12 +479,15 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       for (int t = 0; t <= ntiles; ++t) {
         const uint32_t gcur = gtile;  // global index of tile t (tiles handed to the MMA warp so far)
         const int buf = (int)(gcur & 1);
+        long long tq0 = clock64();
         if (t < ntiles) {
           const int lo = tlo[t], hi = thi[t];
           if (hi - lo + 1 > P && tid == 0) atomicOr(flags, FLAG_PLANES);
           if (zhave < hi) request(hi);
           asm volatile("cp.async.wait_group 0;\n" ::);
           sbar();  // planes of tile t resident; all samplers done with iteration t-1 (incl. drain of tile t-2)
+          long long tq1 = clock64();
+          if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[1], (unsigned long long)(tq1 - tq0));
           if (t + 1 < ntiles) {
             const int want = min(thi[t + 1], lo + P - 1);
             if (want > zhave) request(want);
@@ -558,14 +565,24 @@ __global__ void __launch_bounds__(kThr + 32, 1)
               ex = tri_xy<NT>(planes + b0, dz, N, fmaf(rs, phx.x, cx), fmaf(rs, phx.y, cy), fz);
             }
           }
-          // per-ring power-of-two scale (max |sample| -> [2^14, 2^15)), fp16 hi/lo split, 8-byte stores
+          long long tq2 = clock64();
+          if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[2], (unsigned long long)(tq2 - tq1));
+          // per-ring power-of-two scale (max |sample| -> [2^14, 2^15)), fp16 hi/lo split, 8-byte stores; the four
+          // rings' max reductions run interleaved
+          float mxv[RPW];
+#pragma unroll
+          for (int rr = 0; rr < RPW; ++rr) {
+            mxv[rr] = fmaxf(fmaxf(fabsf(sv[rr][0]), fabsf(sv[rr][1])), fmaxf(fabsf(sv[rr][2]), fabsf(sv[rr][3])));
+            if (xr == rr) mxv[rr] = fmaxf(mxv[rr], fabsf(ex));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) mxv[rr] = fmaxf(mxv[rr], __shfl_xor_sync(0xffffffffu, mxv[rr], o));
 #pragma unroll
           for (int rr = 0; rr < RPW; ++rr) {
             const int r = warp + rr * kWarps;
-            float mx = fmaxf(fmaxf(fabsf(sv[rr][0]), fabsf(sv[rr][1])), fmaxf(fabsf(sv[rr][2]), fabsf(sv[rr][3])));
-            if (xr == rr) mx = fmaxf(mx, fabsf(ex));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const float mx = mxv[rr];
             const int e = mx > 0.f ? (int)((__float_as_uint(mx) >> 23) & 0xff) - 127 : 0;
             const int es = min(max(14 - e, -100), 100);  // sc = 2^es, 1 / (1024 sc) = 2^-(es + 10)
             const float sc = __uint_as_float((uint32_t)(127 + es) << 23);
@@ -595,12 +612,14 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             }
             if (lane == 0) sl[kNR + r] = (int)((uint32_t)(127 - es - 10) << 23);
           }
+          if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[3], (unsigned long long)(clock64() - tq2));
           // S[buf] -> async proxy; hand the tile to the MMA warp
           cmd[buf] = 1;
           asm volatile("fence.proxy.async.shared::cta;\n" ::);
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&full[buf])) : "memory");
           gtile = gcur + 1;
         }
+        long long tq3 = clock64();
         // drain tile t - 1 (overlaps the MMAs of tile t): TMEM lane o = output row, 16 ring columns per warp
         if (t > 0 && !(dbg & 1)) {
           const int pb = (int)((gcur - 1) & 1), tp = t - 1;
@@ -629,6 +648,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
         }
         if (t > 0) dph ^= 1u << ((gcur - 1) & 1);
+        if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[4], (unsigned long long)(clock64() - tq3));
       }
       sbar();  // the next particle's sort overwrites the list, the slots and the planes
     }
@@ -686,6 +706,15 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
       if (e != cudaSuccess) return e;
       k_sh_rings_tc<0><<<grid, kThr + 32, bytes, st>>>(vols, nb, shifts, shift_stride, tab, P, G, flags, dbg);
       break;
+  }
+  if (dbg & 8) {
+    cudaStreamSynchronize(st);
+    unsigned long long h[8];
+    cudaMemcpyFromSymbol(h, g_sh_prof, sizeof(h));
+    fprintf(stderr, "sh_tc prof (warp-cycles, summed): sort %llu  plane-wait %llu  sample %llu  scale+store %llu  drain %llu\n",
+            h[0], h[1], h[2], h[3], h[4]);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_sh_prof, z, sizeof(z));
   }
   return cudaGetLastError();
 }
