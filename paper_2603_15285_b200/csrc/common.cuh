@@ -53,6 +53,9 @@ template <typename T> struct ShTables {
   const T* pwm;           // [Jh][pw_stride] W_j Pbar_lm(x_j), m-major rows: m block at pw_moff[m], l - m inside,
                           // each m block padded to a multiple of 4 (zeros); j < Jh = (n_theta+1)/2
   const int* pw_moff;     // [L+2] offsets of the m blocks (pw_moff[L+1] = pw_stride)
+  const T* pwp;           // [Jh][pwp_stride] the same weights, (m, parity of l - m) blocks of l = m + par + 2 i
+  const int* pwp_off;     // [L+1][2] offsets of those blocks (each padded to a multiple of 4)
+  int pwp_stride;
   const cplx_t<T>* dft;   // [Kh+1][L+1]: (cos, sin)(m phi_k) for the folded ring DFT
   int N, R, L, nth, nph, Jh, Kh, MP, pw_stride;
   int tcP;                // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel), FP32 only

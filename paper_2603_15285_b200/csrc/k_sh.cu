@@ -508,6 +508,13 @@ template <typename T> __host__ __device__ inline LegLayout leg_layout(int SG, in
   return s;
 }
 
+// thread tiles of the parity-split layout: per m, ceil(#even / 4) + ceil(#odd / 4)
+__host__ __device__ inline int leg_tiles_par(int L) {
+  int n = 0;
+  for (int m = 0; m <= L; ++m) n += ((L - m) / 2 + 1 + 3) / 4 + ((m + 1 <= L) ? ((L - m - 1) / 2 + 1 + 3) / 4 : 0);
+  return n;
+}
+
 __host__ __device__ inline int leg_tiles(int L) {
   int n = 0;
   for (int m = 0; m <= L; ++m) n += (L - m + 4) / 4;
@@ -714,7 +721,7 @@ __global__ void __launch_bounds__(256) k_sh_legendre_full(const cplx_t<T>* __res
 // Persistent Legendre (FP32): one CTA per SM holds the whole weight table W_j Pbar_lm(x_j) in shared memory (loaded
 // once) and two independent 160-thread lanes, each walking its own (particle, 2-shell) items with the next item's G
 // prefetched by cp.async into a second buffer while the current one is folded and contracted.
-constexpr int kLegLaneThreads = 160;
+constexpr int kLegLaneThreads = 192;
 constexpr int kLegSG = 2;
 
 template <typename T>
@@ -726,7 +733,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   const int L1 = L + 1, ncf = ncoef(L);
   const int tid = threadIdx.x, lane_id = tid / LT, ltid = tid % LT;
   const size_t gbytes = sizeof(cplx_t<T>) * (size_t)SG * nth * L1;
-  const int wbytes = (int)sizeof(T) * Jh * tab.pw_stride;
+  const int wbytes = (int)sizeof(T) * Jh * tab.pwp_stride;
   const T* W = (const T*)smem;
   cplx_t<T>* Gb[2];
   Gb[0] = (cplx_t<T>*)(smem + (((size_t)wbytes + 15) & ~size_t(15)) + (size_t)(2 * lane_id) * gbytes);
@@ -753,22 +760,25 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   };
   for (int e = tid; e < wbytes / 16; e += 2 * LT) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem + 16 * e);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)tab.pwm + 16 * e));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)tab.pwp + 16 * e));
   }
   asm volatile("cp.async.commit_group;\n" ::);
   if (i_begin + lane_id < i_end) copy_item(i_begin + lane_id, Gb[0]);
   asm volatile("cp.async.commit_group;\n" ::);
   asm volatile("cp.async.wait_group 1;\n" ::);  // this thread's part of the weight table
-  const int ntiles = leg_tiles(L);
-  __shared__ int tmap[kLegLaneThreads];            // thread tile -> (m, l-block)
+  const int ntiles = leg_tiles_par(L);
+  __shared__ int tmap[kLegLaneThreads];            // thread tile -> (m, parity, l-block)
   for (int t = tid; t < ntiles; t += 2 * LT) {
-    int m = 0, lb = t;
+    int m = 0, par = 0, lb = t;
     for (; m <= L; ++m) {
-      const int nt = (L - m + 4) / 4;
-      if (lb < nt) break;
-      lb -= nt;
+      const int ne = (L - m) / 2 + 1, no = (m + 1 <= L) ? (L - m - 1) / 2 + 1 : 0;
+      const int te = (ne + 3) / 4, to = (no + 3) / 4;
+      if (lb < te) { par = 0; break; }
+      lb -= te;
+      if (lb < to) { par = 1; break; }
+      lb -= to;
     }
-    tmap[t] = (lb << 16) | m;
+    tmap[t] = (lb << 17) | (par << 16) | m;
   }
   __syncthreads();                                // the whole weight table and the tile map
   const int half = nth / 2;
@@ -796,27 +806,27 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
     const int i0 = (int)(it % ngroups) * SG;
     cplx_t<T>* Fp = F + p * (int64_t)ncf * R;
     for (int tile = ltid; tile < ntiles; tile += LT) {
-      const int m = tmap[tile] & 0xffff, lb = tmap[tile] >> 16;
-      const int l0t = m + 4 * lb;
-      const bool odd0 = ((l0t + m) & 1) != 0;
-      const T* wrow = W + __ldg(&tab.pw_moff[m]) + 4 * lb;
+      const int m = tmap[tile] & 0xffff, par = (tmap[tile] >> 16) & 1, lb = tmap[tile] >> 17;
+      const int l0t = m + par + 8 * lb;  // degrees l0t, l0t + 2, l0t + 4, l0t + 6 (same parity of l - m)
+      const T* wrow = W + __ldg(&tab.pwp_off[2 * m + par]) + 4 * lb;
       T ar[4][SG], ai[4][SG];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int s2 = 0; s2 < SG; ++s2) ar[a][s2] = ai[a][s2] = T(0);
       using V = typename V4<T>::t;
+      // G+ (even l - m) sits at node q, G- (odd) at node n-1-q after the fold
+      const cplx_t<T>* g0 = Gs + (par ? (size_t)(nth - 1) * L1 : 0) + m;
+      const int gstep = par ? -L1 : L1;
 #pragma unroll 3
       for (int q = 0; q < Jh; ++q) {
-        const V wv = *reinterpret_cast<const V*>(wrow + (size_t)q * tab.pw_stride);
+        const V wv = *reinterpret_cast<const V*>(wrow + (size_t)q * tab.pwp_stride);
         const T w[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
         for (int s2 = 0; s2 < SG; ++s2) {
-          const cplx_t<T> ge = Gs[((size_t)s2 * nth + q) * L1 + m];
-          const cplx_t<T> go = Gs[((size_t)s2 * nth + (nth - 1 - q)) * L1 + m];
+          const cplx_t<T> g = g0[(size_t)s2 * nth * L1 + q * gstep];
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
-            const cplx_t<T> g = (odd0 ^ (a & 1)) ? go : ge;
             ar[a][s2] = fma(w[a], g.x, ar[a][s2]);
             ai[a][s2] = fma(w[a], g.y, ai[a][s2]);
           }
@@ -824,7 +834,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const int l = l0t + a;
+        const int l = l0t + 2 * a;
         if (l > L) continue;
         const int lm = l * (l + 1) / 2 + m;
 #pragma unroll
@@ -837,7 +847,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
 }
 
 template <typename T> size_t leg_pers_bytes(const ShTables<T>& tab) {
-  const size_t w = (sizeof(T) * (size_t)tab.Jh * tab.pw_stride + 15) & ~size_t(15);
+  const size_t w = (sizeof(T) * (size_t)tab.Jh * tab.pwp_stride + 15) & ~size_t(15);
   return w + 4 * sizeof(cplx_t<T>) * (size_t)kLegSG * tab.nth * (tab.L + 1);
 }
 
@@ -920,8 +930,8 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
   else if (tab.R % 4 == 0 && leg_full_bytes<T>(4, tab.nth, tab.L) <= 110 * 1024) lsg = 4;
   else if (tab.R % 2 == 0 && leg_full_bytes<T>(2, tab.nth, tab.L) <= 200 * 1024) lsg = 2;
   if (getenv("MATCHA_LEG_OLD")) lsg = 0;
-  const bool lpers = sizeof(T) == 4 && tab.R % kLegSG == 0 && leg_tiles(tab.L) <= kLegLaneThreads &&
-                     leg_pers_bytes<T>(tab) <= 220 * 1024 && !getenv("MATCHA_LEG_NOPERS");
+  const bool lpers = sizeof(T) == 4 && tab.R % kLegSG == 0 && leg_tiles_par(tab.L) <= kLegLaneThreads &&
+                     leg_pers_bytes<T>(tab) <= 226 * 1024 && !getenv("MATCHA_LEG_NOPERS");
   if (lpers) {
     e = cudaFuncSetAttribute(k_sh_legendre_pers<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)leg_pers_bytes<T>(tab));

@@ -29,6 +29,9 @@ struct matcha_ctx {
   void* d_tw = nullptr;
   void* d_pw = nullptr;     // m-major Legendre weights [Jh][pw_stride]
   int* d_pw_moff = nullptr;
+  void* d_pwp = nullptr;    // parity-split Legendre weights [Jh][pwp_stride]
+  int* d_pwp_off = nullptr; // [L+1][2] offsets of the (m, parity of l - m) blocks
+  int pwp_stride = 0;
   void* d_dft = nullptr;    // parity-split cos/sin table of the folded ring DFT
   int Kh = 0, MP = 0, pw_stride = 0;
   int tcP = 0;              // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel)
@@ -160,6 +163,9 @@ template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
   t.tw = (const cplx_t<T>*)h->d_tw;
   t.pwm = (const T*)h->d_pw;
   t.pw_moff = h->d_pw_moff;
+  t.pwp = (const T*)h->d_pwp;
+  t.pwp_off = h->d_pwp_off;
+  t.pwp_stride = h->pwp_stride;
   t.dft = (const cplx_t<T>*)h->d_dft;
   t.Kh = h->Kh;
   t.MP = h->MP;
@@ -469,6 +475,25 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     for (int l = 0; l <= h->L; ++l)
       for (int mm = 0; mm <= l; ++mm) pw[(size_t)j * h->pw_stride + moff[mm] + (l - mm)] = w[j] * P[lm_index(l, mm)];
   }
+  // the same weights with each m block split by the parity of l - m (l = m + p, m + p + 2, ...), each part padded
+  // to a multiple of 4: a thread tile of 4 same-parity degrees reads a single node-pair combination (G+ or G-)
+  std::vector<int> poff(2 * (h->L + 1), 0);
+  int pst = 0;
+  for (int mm = 0; mm <= h->L; ++mm)
+    for (int par = 0; par < 2; ++par) {
+      const int cnt = (mm + par <= h->L) ? (h->L - mm - par) / 2 + 1 : 0;
+      poff[2 * mm + par] = pst;
+      pst += (cnt + 3) / 4 * 4;
+    }
+  h->pwp_stride = std::max(pst, 4);
+  std::vector<double> pwp((size_t)h->Jh * h->pwp_stride, 0.0);
+  for (int j = 0; j < h->Jh; ++j)
+    for (int mm = 0; mm <= h->L; ++mm)
+      for (int l = mm; l <= h->L; ++l) {
+        const int par = (l - mm) & 1;
+        pwp[(size_t)j * h->pwp_stride + poff[2 * mm + par] + (l - mm - par) / 2] =
+            pw[(size_t)j * h->pw_stride + moff[mm] + (l - mm)];
+      }
   // folded ring-DFT table: [k = 0..Kh][m = 0..L] (cos, sin)(m phi_k)
   const int Mp = h->nph / 2;
   h->Kh = (Mp - 1) / 2;
@@ -498,15 +523,19 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     upload<double>(&h->d_node, node, e);
     upload<double>(&h->d_tw, tw, e);
     upload<double>(&h->d_pw, pw, e);
+    upload<double>(&h->d_pwp, pwp, e);
     upload<double>(&h->d_dft, dft, e);
     upload<double>(&h->d_pair_lnc, plnc, e);
   } else {
     upload<float>(&h->d_node, node, e);
     upload<float>(&h->d_tw, tw, e);
     upload<float>(&h->d_pw, pw, e);
+    upload<float>(&h->d_pwp, pwp, e);
     upload<float>(&h->d_dft, dft, e);
     upload<float>(&h->d_pair_lnc, plnc, e);
   }
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pwp_off, sizeof(int) * poff.size());
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_pwp_off, poff.data(), sizeof(int) * poff.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pw_moff, sizeof(int) * moff.size());
   if (e == cudaSuccess) e = cudaMemcpy(h->d_pw_moff, moff.data(), sizeof(int) * moff.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pairs, sizeof(PairDesc) * pairs.size());
@@ -545,7 +574,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
 
 MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (!h) return MATCHA_ERR_INVALID_ARG;
-  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
+  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
                   h->ws_euler, h->ws_score, h->ws_idx, h->ws_best, h->ws_vols[0], h->ws_vols[1], h->ws_poses,
                   h->ws_ref};
   for (void* p : ptrs)
