@@ -14,6 +14,6 @@ CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu1.log 2>&1; echo launches_exit=$?
 # one --set full capture per kernel: skip the reference-analysis launch and warm-up launches
-for K in k_sh_rings_tc k_sh_legendre_full k_corr_tc k_so3_grid k_newton_refine; do
+for K in k_sh_rings_tc k_sh_legendre_pers k_corr_tc k_so3_grid k_newton_refine; do
   ncu --set full --clock-control none --import-source on -k "regex:$K" -s 3 -c 1 -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_$K.log 2>&1; echo full_$K=$?
 done
