@@ -60,7 +60,8 @@ def _worker(rank, world, port, P, q):
         H = torch.zeros((3, 2), dtype=torch.complex64)  # rank 1 starts with zeros: must receive rank 0's
         poses = D.align_step(FakeHandle(), vols, ref, None, H, rank)
         t = D.max_over_ranks(float(rank + 1))
-        q.put((rank, poses[:, 0].tolist(), poses[:, 6].tolist(), H.clone(), t))
+        # plain Python values only: a tensor would travel as a shared-memory handle that dies with this process
+        q.put((rank, poses[:, 0].tolist(), poses[:, 6].tolist(), torch.view_as_real(H).tolist(), t))
     finally:
         dist.destroy_process_group()
 
@@ -81,6 +82,6 @@ def test_align_step_world2_gloo(P):
     expect_H = torch.full((3, 2), complex(0.5 * 64, 1.0), dtype=torch.complex64)
     for rank, ids, checks, H, t in res:
         assert ids == [float(i) for i in range(P)]                  # gathered in global order
-        assert torch.equal(H, expect_H)                            # broadcast from rank 0
+        assert torch.equal(torch.view_as_complex(torch.tensor(H)), expect_H)  # broadcast from rank 0
         assert all(abs(c - float(torch.view_as_real(expect_H).sum())) < 1e-3 for c in checks)
         assert t == 2.0                                             # max over ranks
