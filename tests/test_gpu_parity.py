@@ -56,6 +56,27 @@ def test_sh_analysis_parity(N, L, B, prec):
             assert np.abs(F[p] - Fo[p]).max() <= tol, (p, np.abs(F[p] - Fo[p]).max() / scale)
 
 
+@pytest.mark.parametrize("N,L,B", [(64, 32, 150), (32, 8, 160)])
+def test_sh_analysis_tensor_core_path_parity(N, L, B):
+    """Batches of at least a quarter of the SMs take the persistent tensor-core ring kernel (fp16 hi/lo split DFT,
+    z-sorted rings, plane ring buffer) -- compared with the oracle on sampled particles, unshifted and shifted
+    (including shifts that push samples out of the box and planes outside the volume), at the bench's launch
+    configuration (sub-batches of whole waves of particles)."""
+    b = gen.particles(N, B, 0.1, seed=26)
+    h = handle(N, L, "fp32", max_batch=B)
+    vols = cuda(b.vols)
+    shifts = rng.uniform(-3, 3, size=(B, 3))
+    shifts[1] = [N / 2, -N / 2 + 1, 0.5]
+    shifts[B - 1] = [0.25, -0.75, -N / 2 - 0.5]
+    sample = [0, 1, B // 2, B - 1]
+    for sh in (None, shifts):
+        F = to_np(h.sh_analysis(vols, None if sh is None else cuda(sh, h.real)))
+        for p in sample:
+            Fo = O.sh_analysis(b.vols[p], L, 2, None if sh is None else sh[p])
+            scale = np.abs(Fo).max()
+            assert np.abs(F[p] - Fo).max() <= 2e-5 * scale, (p, np.abs(F[p] - Fo).max() / scale)
+
+
 def test_sh_analysis_empty_batch():
     h = handle(16, 4)
     out = h.sh_analysis(torch.empty((0, 16, 16, 16), device=DEV))
