@@ -208,15 +208,23 @@ __device__ __forceinline__ void tri4_xy(const float* __restrict__ b0, int dz, in
       c[q][6] = b[dz + W];
       c[q][7] = b[dz + W + 1];
     }
+    // the seven lerps of two samples at a time on the packed FP32x2 pipe (FFMA2): lerp(a, b, f) = f b + (1 - f) a
+    // as fma(f, b, fma(-f, a, a))
+    const float2 fz2 = make_float2(fz, fz), nfz2 = make_float2(-fz, -fz);
+    auto lerp2 = [](float2 a, float2 b, float2 f, float2 nf) { return __ffma2_rn(f, b, __ffma2_rn(nf, a, a)); };
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float c00 = fmaf(fx[q], c[q][1] - c[q][0], c[q][0]);
-      const float c01 = fmaf(fx[q], c[q][3] - c[q][2], c[q][2]);
-      const float c10 = fmaf(fx[q], c[q][5] - c[q][4], c[q][4]);
-      const float c11 = fmaf(fx[q], c[q][7] - c[q][6], c[q][6]);
-      const float c0 = fmaf(fy[q], c01 - c00, c00);
-      const float c1 = fmaf(fy[q], c11 - c10, c10);
-      out[q] = fmaf(fz, c1 - c0, c0);
+    for (int pq = 0; pq < 4; pq += 2) {
+      float2 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = make_float2(c[pq][k], c[pq + 1][k]);
+      const float2 fx2 = make_float2(fx[pq], fx[pq + 1]), nfx2 = make_float2(-fx[pq], -fx[pq + 1]);
+      const float2 fy2 = make_float2(fy[pq], fy[pq + 1]), nfy2 = make_float2(-fy[pq], -fy[pq + 1]);
+      const float2 c00 = lerp2(v[0], v[1], fx2, nfx2), c01 = lerp2(v[2], v[3], fx2, nfx2);
+      const float2 c10 = lerp2(v[4], v[5], fx2, nfx2), c11 = lerp2(v[6], v[7], fx2, nfx2);
+      const float2 c0 = lerp2(c00, c01, fy2, nfy2), c1 = lerp2(c10, c11, fy2, nfy2);
+      const float2 o = lerp2(c0, c1, fz2, nfz2);
+      out[pq] = o.x;
+      out[pq + 1] = o.y;
     }
   } else {
 #pragma unroll
