@@ -399,11 +399,18 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       auto bucket = [&](int zb) { return min(max(zb, -2), N) + 2; };
 
       long long tp0 = clock64();
-      // ---- 1. counting sort of the rings by z bucket, then (j, i): deterministic (single writer per column j)
+      // ---- 1. counting sort of the rings by z bucket, then (j, i), one item per ring.  For fixed j the bucket is
+      //      monotone in i, so the rings of cell (bucket, j) are a contiguous i-range whose first i gives each ring
+      //      its rank: deterministic without ordered atomics.
+      int* cstart = cnt + nbk * nth;  // first i of each (bucket, j) cell (also aliases the planes)
       for (int t = tid; t < nbk * nth; t += kThr) cnt[t] = 0;
       sbar();
-      for (int j = tid; j < nth; j += kThr)
-        for (int i = 0; i < R; ++i) cnt[bucket(zfloor(i, j)) * nth + j] += 1;
+      for (int e = tid; e < nrings; e += kThr) {
+        const int j = e / R, i = e - j * R;
+        const int b = bucket(zfloor(i, j));
+        atomicAdd(&cnt[b * nth + j], 1);
+        if (i == 0 || bucket(zfloor(i - 1, j)) != b) cstart[b * nth + j] = i;
+      }
       sbar();
       {
         const int E = nbk * nth, per = (E + kThr - 1) / kThr;
@@ -430,14 +437,33 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       sbar();
       for (int b = tid; b < nbk; b += kThr) boff[b] = cnt[b * nth];
       if (tid == 0) boff[nbk] = nrings;
-      for (int j = tid; j < nth; j += kThr)
-        for (int i = 0; i < R; ++i) {
-          const int b = bucket(zfloor(i, j)) * nth + j;
-          list[cnt[b]] = (i << 16) | j;
-          cnt[b] += 1;
-        }
+      for (int e = tid; e < nrings; e += kThr) {
+        const int j = e / R, i = e - j * R;
+        const int c = bucket(zfloor(i, j)) * nth + j;
+        list[cnt[c] + (i - cstart[c])] = (i << 16) | j;
+      }
       sbar();
       if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[0], (unsigned long long)(clock64() - tp0));
+      // planes are requested in increasing z; plane z lives in slot zslot[z + 1] = z mod P (it replaces plane z - P,
+      // which the current tile no longer needs because every request stays below lo(t) + P).  The first window is
+      // requested before the tiles are built (it only depends on the lowest ring), so the load overlaps the build.
+      const int zfirst = min(max(bucket(zfloor(list[0] >> 16, list[0] & 0xffff)) - 2, -1), N - 1);
+      int zhave = zfirst - 1;
+      auto request = [&](int zto) {
+        const int n4 = N / 4;
+        for (int z = zhave + 1; z <= zto; ++z) {
+          float* dst = planes + zslot[z + 1] * PS;
+          const bool valid = z >= 0 && z < N;
+          const float* src = vol + (size_t)(valid ? z : 0) * N * N;
+          for (int t = tid; t < N * n4; t += kThr) {
+            const int y = t / n4, x4 = t - y * n4;
+            cp_async16(dst + y * PW + 4 * x4, src + y * N + 4 * x4, valid);
+          }
+        }
+        zhave = max(zhave, zto);
+        asm volatile("cp.async.commit_group;\n" ::);
+      };
+      request(min(zfirst + P - 1, N));
       // ---- 2. tiles: <= kNR consecutive rings whose planes fit the P-slot window (cut at z-bucket boundaries)
       if (tid == 0) {
         auto zlo_of = [&](int b) { return min(max(b - 2, -1), N - 1); };
@@ -465,24 +491,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       sbar();
       const int ntiles = *s_nt;
       float* const Gp = (float*)(G + p * (int64_t)R * nth * (L + 1));
-      // planes are requested in increasing z; plane z lives in slot zslot[z + 1] = z mod P (it replaces plane z - P,
-      // which the current tile no longer needs because every request stays below lo(t) + P)
-      int zhave = tlo[0] - 1;
-      auto request = [&](int zto) {
-        const int n4 = N / 4;
-        for (int z = zhave + 1; z <= zto; ++z) {
-          float* dst = planes + zslot[z + 1] * PS;
-          const bool valid = z >= 0 && z < N;
-          const float* src = vol + (size_t)(valid ? z : 0) * N * N;
-          for (int t = tid; t < N * n4; t += kThr) {
-            const int y = t / n4, x4 = t - y * n4;
-            cp_async16(dst + y * PW + 4 * x4, src + y * N + 4 * x4, valid);
-          }
-        }
-        zhave = max(zhave, zto);
-        asm volatile("cp.async.commit_group;\n" ::);
-      };
-      request(ntiles > 1 ? max(thi[0], min(thi[1], tlo[0] + P - 1)) : thi[0]);
+
 
       for (int t = 0; t <= ntiles; ++t) {
         const uint32_t gcur = gtile;  // global index of tile t (tiles handed to the MMA warp so far)
@@ -685,7 +694,7 @@ int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnod
   if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P).total > budget) return 0;
   while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1).total <= budget) ++P;
   // the counting-sort table aliases the planes
-  if ((size_t)(tab.N + 3) * tab.nth * sizeof(int) > (size_t)P * tab.N * plane_pitch_tc(tab.N) * sizeof(float)) return 0;
+  if ((size_t)2 * (tab.N + 3) * tab.nth * sizeof(int) > (size_t)P * tab.N * plane_pitch_tc(tab.N) * sizeof(float)) return 0;
   return P;
 }
 
