@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             const int want = min(thi[t + 1], lo + P - 1);
             if (want > zhave) request(want);
           }
+          if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[5], (unsigned long long)(clock64() - tq1));
           // sample tile t into S[buf] (fp16 hi/lo of the per-ring scaled samples): warp w takes ring slots
           // w, w + 16, ...; lanes walk k along the ring (4 mirrored phi indices per lane, one 8-byte store each)
           unsigned char* Shi = Bs + (size_t)(2 * buf) * Kc * LBO;
@@ -728,8 +729,8 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
     cudaStreamSynchronize(st);
     unsigned long long h[8];
     cudaMemcpyFromSymbol(h, g_sh_prof, sizeof(h));
-    fprintf(stderr, "sh_tc prof (warp-cycles, summed): sort %llu  plane-wait %llu  sample %llu  scale+store %llu  drain %llu\n",
-            h[0], h[1], h[2], h[3], h[4]);
+    fprintf(stderr, "sh_tc prof (warp-cycles, summed): sort %llu  plane-wait %llu  sample %llu (prefetch issue %llu)  "
+            "scale+store %llu  drain %llu\n", h[0], h[1], h[2], h[5], h[3], h[4]);
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_sh_prof, z, sizeof(z));
   }
