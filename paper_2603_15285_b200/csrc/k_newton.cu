@@ -379,12 +379,17 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
 }
 
 // ------------------------------------------------------------------ matcha_newton_refine kernel
+// One CTA per (particle, group of up to CG candidates) when a.qsplit > 1 (more, smaller CTAs: the last wave of
+// the grid is fuller); the candidates are independent, so the result equals the one-CTA-per-particle run.
 template <typename T, int CG>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1) k_newton_refine(NewtonArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int Q = a.Q;
+  const int QT = a.Q, G = a.qsplit;
+  const int64_t p = blockIdx.x / G;
+  const int q0 = (int)(blockIdx.x % G) * ((QT + G - 1) / G);
+  const int Q = min(QT - q0, (QT + G - 1) / G);  // candidates of this CTA: q0 .. q0 + Q - 1
   const int Lmax_b = a.bands[a.nbands - 1];
-  const SmemLayout lay = smem_layout<T>(Q, Lmax_b, CG);
+  const SmemLayout lay = smem_layout<T>((QT + G - 1) / G, Lmax_b, CG);
   double* theta = (double*)(smem + lay.theta);
   CandShared<T>* cs = (CandShared<T>*)(smem + lay.cand);
   cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
@@ -397,10 +402,10 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   int* act = (int*)(smem + lay.flags);   // [Q] active (not padding)
   int* run = act + Q;                    // [Q] still iterating in this band
   int* any = run + Q;                    // [1]
-  const int64_t p = blockIdx.x;
   const cplx_t<T>* M = a.M + p * a.strideM;
-  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) theta[t] = (double)a.euler[p * Q * 3 + t];
-  for (int c = threadIdx.x; c < Q; c += blockDim.x) act[c] = a.idx ? (a.idx[p * Q + c] >= 0) : 1;
+  const int64_t cb0 = p * QT + q0;       // global index of this CTA's first candidate
+  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) theta[t] = (double)a.euler[cb0 * 3 + t];
+  for (int c = threadIdx.x; c < Q; c += blockDim.x) act[c] = a.idx ? (a.idx[cb0 + c] >= 0) : 1;
   load_inv_tables(inv_l, inv_ll);
   __syncthreads();
   for (int j = 0; j < a.nbands; ++j) {
@@ -449,13 +454,14 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   prepare_candidates<T>(theta, Q, Lmax_b, cs, ea, eg);
   __syncthreads();
   eval_block<T, CG, false>(M, Lmax_b, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
-  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) a.euler[p * Q * 3 + t] = (T)theta[t];
+  for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) a.euler[cb0 * 3 + t] = (T)theta[t];
   for (int c = threadIdx.x; c < Q; c += blockDim.x) {
     const double v = act[c] ? sums[c * 10] : -INFINITY;
-    a.score[p * Q + c] = (T)v;
+    a.score[cb0 + c] = (T)v;
+    if (G > 1) a.cfinal[cb0 + c] = v;
     if (act[c] && !isfinite(v)) atomicOr(a.flags, FLAG_NONFINITE);
   }
-  if (threadIdx.x == 0) {
+  if (G == 1 && threadIdx.x == 0) {
     int b = -1;
     double bv = -INFINITY;
     for (int c = 0; c < Q; ++c)
@@ -467,6 +473,24 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   }
 }
 
+// argmax over the FP64 final scores when the candidates were split over CTAs (first maximum: reading C23)
+__global__ void k_best_of(const double* __restrict__ cfinal, const int32_t* __restrict__ idx, int64_t B, int Q,
+                          int32_t* __restrict__ best) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= B) return;
+  int b = -1;
+  double bv = -INFINITY;
+  for (int c = 0; c < Q; ++c) {
+    const bool act = idx ? idx[p * Q + c] >= 0 : true;
+    const double v = cfinal[p * Q + c];
+    if (act && (b < 0 || v > bv)) {
+      b = c;
+      bv = v;
+    }
+  }
+  best[p] = b;
+}
+
 template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a, bool derivs, cudaStream_t s) {
   const SmemLayout lay = smem_layout<T>(a.Q, a.L_eval, CG);
   cudaError_t e = cudaFuncSetAttribute(k_eval_corr<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
@@ -475,12 +499,19 @@ template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a,
   return cudaGetLastError();
 }
 
-template <typename T, int CG> cudaError_t launch_newton_cg(const NewtonArgs<T>& a, cudaStream_t s) {
-  const SmemLayout lay = smem_layout<T>(a.Q, a.bands[a.nbands - 1], CG);
+template <typename T, int CG> cudaError_t launch_newton_cg(NewtonArgs<T> a, cudaStream_t s) {
+  // optionally split the candidates over ceil(Q / CG) CTAs per particle (MATCHA_NEWTON_SPLIT; measured slower at c2:
+  // 0.93 vs 0.89 ms -- the duplicated per-CTA band setup outweighs the fuller last wave)
+  const int G = (a.cfinal && a.Q > CG && getenv("MATCHA_NEWTON_SPLIT")) ? (a.Q + CG - 1) / CG : 1;
+  a.qsplit = G;
+  const SmemLayout lay = smem_layout<T>((a.Q + G - 1) / G, a.bands[a.nbands - 1], CG);
   cudaError_t e =
       cudaFuncSetAttribute(k_newton_refine<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
   if (e != cudaSuccess) return e;
-  k_newton_refine<T, CG><<<(unsigned)a.B, kThreads, lay.total, s>>>(a);
+  k_newton_refine<T, CG><<<(unsigned)(a.B * G), kThreads, lay.total, s>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || G == 1) return e;
+  k_best_of<<<(unsigned)((a.B + 127) / 128), 128, 0, s>>>(a.cfinal, a.idx, a.B, a.Q, a.best);
   return cudaGetLastError();
 }
 
