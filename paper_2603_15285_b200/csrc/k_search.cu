@@ -354,10 +354,11 @@ template <typename T> __host__ __device__ inline GridLayout grid_layout(int L0, 
   return s;
 }
 
-template <typename T>
+// L0C, KC: compile-time L0 and oversampling (0 = runtime) -- with both fixed every grid index is a constant expression
+template <typename T, int L0C, int KC>
 __global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int L0 = a.L0, K = a.K;
+  const int L0 = L0C ? L0C : a.L0, K = KC ? KC : a.K;
   const int nb = K * (L0 + 1), na = 2 * K * (L0 + 1), ng = na, nm = L0 + 1, w0 = 2 * L0 + 1;
   const GridLayout lay = grid_layout<T>(L0, K, jc);
   cplx_t<T>* Ms = (cplx_t<T>*)(smem + lay.Ms);
@@ -385,8 +386,8 @@ __global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc)
     double sn, cn;
     sincospi(2.0 * k / na, &sn, &cn);
     const cplx_t<T> e = mk<T>((T)cn, (T)(-sn));
-    if (r < nm) Ea[t] = e;
-    else Eg[t - nm * na] = e;
+    if (r < nm) Ea[c * nm + r] = e;             // Ea[a][m] = e^{-i m alpha_a}
+    else Eg[c * w0 + (r - nm)] = e;             // Eg[c][n + L0] = e^{-i n gamma_c}
   }
   for (int l = tid; l <= L0 + 1; l += kGThreads) {
     inv_l[l] = l ? (T)(1.0 / l) : T(0);
@@ -459,10 +460,12 @@ __global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc)
     for (int t = tid; t < nj * nm * ng; t += kGThreads) {
       const int r = fdiv(t, mgn), c = t - r * ng;  // r = jj * nm + m
       const cplx_t<T>* x = X + ((size_t)j0 * nm + r) * w0;
+      const cplx_t<T>* eg = Eg + c * w0;
       T yr = T(0), yi = T(0);
+#pragma unroll
       for (int n = 0; n < w0; ++n) {
         const cplx_t<T> xv = x[n];
-        const cplx_t<T> e = Eg[n * ng + c];
+        const cplx_t<T> e = eg[n];
         yr = fma(xv.x, e.x, fma(-xv.y, e.y, yr));
         yi = fma(xv.x, e.y, fma(xv.y, e.x, yi));
       }
@@ -484,11 +487,15 @@ __global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc)
         s2[q] = T(0);
       }
       const T s0 = y[0].x;
+      const cplx_t<T>* eq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) eq[q] = Ea + av[q] * nm;
+#pragma unroll
       for (int m = 1; m <= L0; ++m) {
         const cplx_t<T> yy = y[m * ng];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const cplx_t<T> e = Ea[m * na + av[q]];
+          const cplx_t<T> e = eq[q][m];
           s2[q] = fma(yy.x, e.x, fma(-yy.y, e.y, s2[q]));
         }
       }
@@ -621,9 +628,11 @@ template <typename T> cudaError_t launch_so3_search(const SearchArgs<T>& a, cuda
   const int jc = getenv("MATCHA_SEARCH_WINDOW") ? 0 : grid_chunk<T>(a.L0, a.K);
   if (jc > 0) {
     const size_t bytes = grid_layout<T>(a.L0, a.K, jc).total;
-    cudaError_t e = cudaFuncSetAttribute(k_so3_grid<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    auto kern = (a.L0 == 8 && a.K == 2) ? k_so3_grid<T, 8, 2> : (a.L0 == 4 && a.K == 2) ? k_so3_grid<T, 4, 2>
+                                                                                           : k_so3_grid<T, 0, 0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    k_so3_grid<T><<<(unsigned)a.B, kGThreads, bytes, s>>>(a, jc);
+    kern<<<(unsigned)a.B, kGThreads, bytes, s>>>(a, jc);
     return cudaGetLastError();
   }
   const size_t bytes = search_layout<T>(a.L0, a.K).total;
