@@ -82,10 +82,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
 // split into tf32 hi/lo) into A buffer t & 1 and hand it to the MMA warp through an mbarrier; the MMA warp issues the
 // 3 x (2R/8) MMAs into accumulator t & 1 and commits; meanwhile the workers drain tile t - 1 from the other
 // accumulator straight to global memory.
+// RC: compile-time shell count (0 = runtime), so the staging index arithmetic reduces to shifts
+template <int RC>
 __global__ void __launch_bounds__(kTCThreads + 32, 1)
-    k_corr_tc(const float2* __restrict__ F, const float2* __restrict__ H, int64_t B, int L, int Lmax, int R,
+    k_corr_tc(const float2* __restrict__ F, const float2* __restrict__ H, int64_t B, int L, int Lmax, int Rr,
               int64_t ntiles, float2* __restrict__ M, int dbg) {
   extern __shared__ __align__(1024) unsigned char smem[];
+  const int R = RC ? RC : Rr;
   const int K = 2 * R;                       // real K (multiple of 8: R % 4 == 0)
   const int NMAX = tile_n(L);
   // layout: A_hi, A_lo [2 buffers][128 x K], B_hi, B_lo [NMAX x K] (fp32 words), row tables, mbarriers, tmem slot
@@ -361,11 +364,12 @@ cudaError_t launch_corr_coeffs_tc(const float2* F, const float2* H, int64_t B, i
   int64_t ntiles = 0;
   for (int l = 0; l <= L; ++l) ntiles += (B * (l + 1) + kTM - 1) / kTM;
   const size_t bytes = corr_tc_smem_bytes(L, R);
-  cudaError_t e = cudaFuncSetAttribute(k_corr_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  auto kern = R == 32 ? k_corr_tc<32> : R == 16 ? k_corr_tc<16> : k_corr_tc<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>(ntiles, num_sms);
   const char* dv = getenv("MATCHA_CORR_DBG");
-  k_corr_tc<<<grid, kTCThreads + 32, bytes, s>>>(F, H, B, L, Lmax, R, ntiles, M, dv ? atoi(dv) : 0);
+  kern<<<grid, kTCThreads + 32, bytes, s>>>(F, H, B, L, Lmax, R, ntiles, M, dv ? atoi(dv) : 0);
   return cudaGetLastError();
 }
 
