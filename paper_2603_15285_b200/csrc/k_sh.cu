@@ -735,9 +735,9 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   const size_t gbytes = sizeof(cplx_t<T>) * (size_t)SG * nth * L1;
   const int wbytes = (int)sizeof(T) * Jh * tab.pwp_stride;
   const T* W = (const T*)smem;
-  cplx_t<T>* Gb[2];
-  Gb[0] = (cplx_t<T>*)(smem + (((size_t)wbytes + 15) & ~size_t(15)) + (size_t)(2 * lane_id) * gbytes);
-  Gb[1] = (cplx_t<T>*)((unsigned char*)Gb[0] + gbytes);
+  // this lane's two G buffers (byte offsets into the dynamic shared memory: keeps every access an LDS/STS)
+  const int gofs = (int)((((size_t)wbytes + 15) & ~size_t(15)) + (size_t)(2 * lane_id) * gbytes);
+  auto gbuf = [&](int b) { return reinterpret_cast<cplx_t<T>*>(smem + gofs + b * (int)gbytes); };
   const int ngroups = R / SG;
   // this CTA's contiguous item range; lane l takes items l, l + 2, ...
   const int64_t i_begin = nitems * blockIdx.x / gridDim.x, i_end = nitems * (blockIdx.x + 1) / gridDim.x;
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)tab.pwp + 16 * e));
   }
   asm volatile("cp.async.commit_group;\n" ::);
-  if (i_begin + lane_id < i_end) copy_item(i_begin + lane_id, Gb[0]);
+  if (i_begin + lane_id < i_end) copy_item(i_begin + lane_id, gbuf(0));
   asm volatile("cp.async.commit_group;\n" ::);
   asm volatile("cp.async.wait_group 1;\n" ::);  // this thread's part of the weight table
   const int ntiles = leg_tiles_par(L);
@@ -786,8 +786,8 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   auto lbar = [&]() { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + lane_id), "r"(LT)); };
   int k = 0;
   for (int64_t it = i_begin + lane_id; it < i_end; it += 2, ++k) {
-    cplx_t<T>* Gs = Gb[k & 1];
-    if (it + 2 < i_end) copy_item(it + 2, Gb[(k + 1) & 1]);
+    cplx_t<T>* Gs = gbuf(k & 1);
+    if (it + 2 < i_end) copy_item(it + 2, gbuf((k + 1) & 1));
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 1;\n" ::);
     lbar();
@@ -795,8 +795,8 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
     for (int e = ltid; e < SG * half * L1; e += LT) {
       const int r = (int)__umulhi((uint32_t)e, mgL), m = e - r * L1;
       const int sh = (int)__umulhi((uint32_t)r, mgH), j = r - sh * half;
-      cplx_t<T>* a = Gs + ((size_t)sh * nth + j) * L1 + m;
-      cplx_t<T>* b = Gs + ((size_t)sh * nth + (nth - 1 - j)) * L1 + m;
+      cplx_t<T>* a = Gs + (sh * nth + j) * L1 + m;
+      cplx_t<T>* b = Gs + (sh * nth + (nth - 1 - j)) * L1 + m;
       const cplx_t<T> u = *a, v = *b;
       *a = mk<T>(u.x + v.x, u.y + v.y);
       *b = mk<T>(u.x - v.x, u.y - v.y);
@@ -816,15 +816,15 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
         for (int s2 = 0; s2 < SG; ++s2) ar[a][s2] = ai[a][s2] = T(0);
       using V = typename V4<T>::t;
       // G+ (even l - m) sits at node q, G- (odd) at node n-1-q after the fold
-      const cplx_t<T>* g0 = Gs + (par ? (size_t)(nth - 1) * L1 : 0) + m;
-      const int gstep = par ? -L1 : L1;
+      const cplx_t<T>* g0 = Gs + (par ? (nth - 1) * L1 : 0) + m;
+      const int gstep = par ? -L1 : L1, sstep = nth * L1;
 #pragma unroll 3
       for (int q = 0; q < Jh; ++q) {
         const V wv = *reinterpret_cast<const V*>(wrow + (size_t)q * tab.pwp_stride);
         const T w[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
         for (int s2 = 0; s2 < SG; ++s2) {
-          const cplx_t<T> g = g0[(size_t)s2 * nth * L1 + q * gstep];
+          const cplx_t<T> g = g0[s2 * sstep + q * gstep];
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
             ar[a][s2] = fma(w[a], g.x, ar[a][s2]);
