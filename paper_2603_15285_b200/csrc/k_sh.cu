@@ -49,7 +49,7 @@ __host__ __device__ inline int wbuf_elems(int Kh) { return 4 * (Kh + 1) * kG + 2
 
 template <typename T>
 __host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph, int R, int Kh, int MP,
-                                                   bool dft_smem = true) {
+                                                   bool dft_smem = true, int warps = kRingWarps) {
   RingLayout s;
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -62,8 +62,8 @@ __host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph
   s.dft = take(dft_smem ? sizeof(cplx_t<T>) * (size_t)(Kh + 1) * MP : 0);
   s.pl = take(sizeof(float) * (size_t)(S + 1) * N * plane_pitch(N));
   s.list = take(sizeof(int) * (size_t)R * nth);
-  s.wsum = take(sizeof(int) * (kRingWarps + 2));
-  s.wbuf = take(sizeof(T) * (size_t)kRingWarps * wbuf_elems(Kh));
+  s.wsum = take(sizeof(int) * (warps + 2));
+  s.wbuf = take(sizeof(T) * (size_t)warps * wbuf_elems(Kh));
   s.total = o;
   return s;
 }
@@ -285,7 +285,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
   const int R = tab.R, L = tab.L, nth = tab.nth, nph = tab.nph, Kh = tab.Kh, MP = tab.MP;
   const int Mp = nph / 2, K1 = Kh + 1;
   const bool mid = (Mp % 2) == 0;
-  const RingLayout lay = ring_layout<T>(N, S, nth, nph, R, Kh, MP, dft_smem);
+  const int THR = blockDim.x, NW = THR / 32;  // 512 threads, fewer when shared memory is short (large Kh)
+  const RingLayout lay = ring_layout<T>(N, S, nth, nph, R, Kh, MP, dft_smem, NW);
   cplx_t<T>* tw = (cplx_t<T>*)(smem + lay.tw);
   cplx_t<T>* node = (cplx_t<T>*)(smem + lay.node);
   const cplx_t<T>* dft = dft_smem ? (const cplx_t<T>*)(smem + lay.dft) : tab.dft;
@@ -309,8 +310,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
   //    one 16-byte column x4 and walks rows with a fixed stride (no per-element division)
   {
     const int PW = plane_pitch(N), n4 = N / 4, rows = (S + 1) * N;
-    if (kRingThreads % n4 == 0) {
-      const int x4 = tid % n4, rstride = kRingThreads / n4;
+    if (THR % n4 == 0) {
+      const int x4 = tid % n4, rstride = THR / n4;
       int row = tid / n4, pz = row / N, y = row - pz * N;
       for (; row < rows; row += rstride) {
         const int z = zs + pz;
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
         }
       }
     } else {
-      for (int t = tid; t < rows * n4; t += kRingThreads) {
+      for (int t = tid; t < rows * n4; t += THR) {
         const int row = t / n4, x4 = t - row * n4, pz = row / N, y = row - pz * N, z = zs + pz;
         const bool valid = z < N;
         cp_async16(pl + (size_t)row * PW + 4 * x4, vol + ((size_t)(valid ? z : 0) * N + y) * N + 4 * x4, valid);
@@ -331,16 +332,16 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
     }
     asm volatile("cp.async.commit_group;\n" ::);
   }
-  for (int t = tid; t < nph; t += kRingThreads) tw[t] = tab.tw[t];
-  for (int t = tid; t < nth; t += kRingThreads) node[t] = tab.node[t];
+  for (int t = tid; t < nph; t += THR) tw[t] = tab.tw[t];
+  for (int t = tid; t < nth; t += THR) node[t] = tab.node[t];
   if (dft_smem)
-    for (int t = tid; t < K1 * MP; t += kRingThreads) ((cplx_t<T>*)(smem + lay.dft))[t] = tab.dft[t];
+    for (int t = tid; t < K1 * MP; t += THR) ((cplx_t<T>*)(smem + lay.dft))[t] = tab.dft[t];
   // 2. ordered list of the rings whose floor(z) belongs to this slab: one thread per node j counts its
   //    shells (z = c_z + r_i x_j is monotone in i), then an ordered scan over j (deterministic)
   int count = 0;
   {
     const int lo = (slab == 0) ? INT_MIN : zs, hi = (slab == nslab - 1) ? INT_MAX : zs + S;
-    for (int j0 = 0; j0 < nth; j0 += kRingThreads) {
+    for (int j0 = 0; j0 < nth; j0 += THR) {
       const int j = j0 + tid;
       int cnt = 0;
       T xj = T(0);
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
       if (lane == 31) wsum[warp] = v;
       __syncthreads();
       int off = 0, tot = 0;
-      for (int w = 0; w < kRingWarps; ++w) {
+      for (int w = 0; w < NW; ++w) {
         if (w < warp) off += wsum[w];
         tot += wsum[w];
       }
@@ -378,8 +379,8 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
   __syncthreads();
   // 3. warp-local work: a balanced contiguous range of rings per warp, in groups of kG
   const T dscale = T(2.0 * kPi) / (T)nph;
-  const int r_begin = (int)(((long long)count * warp) / kRingWarps);
-  const int r_end = (int)(((long long)count * (warp + 1)) / kRingWarps);
+  const int r_begin = (int)(((long long)count * warp) / NW);
+  const int r_end = (int)(((long long)count * (warp + 1)) / NW);
   for (int g0 = r_begin; g0 < r_end; g0 += kG) {
     const int nr = min(kG, r_end - g0);
     // folds: lanes walk consecutive k in [1, Kh] along ONE ring (gathers at neighbouring points: few bank
@@ -852,33 +853,36 @@ template <typename T> size_t leg_pers_bytes(const ShTables<T>& tab) {
 }
 
 template <typename T> struct ShPlan {
-  int S, nslab;
+  int S, nslab, threads;
   bool dft_smem;
   size_t rbytes;
 };
 
 template <typename T> ShPlan<T> sh_plan(const ShTables<T>& tab) {
-  // one CTA (512 threads) per SM: the deepest slab (<= 8 planes) that fits; the DFT table moves to global
-  // memory (read through L1) only if shared memory cannot hold it
+  // one CTA per SM: the deepest slab (<= 8 planes) that fits with 16 warps; the DFT table moves to global memory
+  // (read through L1) if shared memory cannot hold it; large boxes / degrees (e.g. 128^3, L = 64) use 8 or 4 warps
   ShPlan<T> pl;
   const size_t budget = 224 * 1024;
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool ds = (pass == 0);
-    for (int S = 8; S >= 1; --S) {
-      const size_t tot = ring_layout<T>(tab.N, S, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, ds).total;
-      if (tot <= budget) {
-        pl.S = S;
-        pl.dft_smem = ds;
-        pl.nslab = (tab.N + S - 1) / S;
-        pl.rbytes = tot;
-        return pl;
+  for (int warps = kRingWarps; warps >= 2; warps /= 2)
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool ds = (pass == 0);
+      for (int S = 8; S >= 1; --S) {
+        const size_t tot = ring_layout<T>(tab.N, S, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, ds, warps).total;
+        if (tot <= budget) {
+          pl.S = S;
+          pl.dft_smem = ds;
+          pl.nslab = (tab.N + S - 1) / S;
+          pl.rbytes = tot;
+          pl.threads = 32 * warps;
+          return pl;
+        }
       }
     }
-  }
   pl.S = 1;
   pl.dft_smem = false;
   pl.nslab = tab.N;
-  pl.rbytes = ring_layout<T>(tab.N, 1, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false).total;
+  pl.threads = 128;
+  pl.rbytes = ring_layout<T>(tab.N, 1, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false, 4).total;
   return pl;
 }
 
@@ -894,7 +898,7 @@ static cudaError_t launch_rings_nt(const float* vols, int64_t nb, const T* shift
   cudaError_t e =
       cudaFuncSetAttribute(k_sh_rings<T, NT, DS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.rbytes);
   if (e != cudaSuccess) return e;
-  k_sh_rings<T, NT, DS><<<(unsigned)(nb * plan.nslab), kRingThreads, plan.rbytes, st>>>(vols, shifts, shift_stride, tab,
+  k_sh_rings<T, NT, DS><<<(unsigned)(nb * plan.nslab), plan.threads, plan.rbytes, st>>>(vols, shifts, shift_stride, tab,
                                                                                        plan.S, plan.nslab, Gws);
   return cudaGetLastError();
 }

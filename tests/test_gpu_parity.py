@@ -40,7 +40,7 @@ def handle(N, L, prec="fp32", max_batch=64):
 
 
 # ------------------------------------------------------------------ stage 1
-@pytest.mark.parametrize("N,L,B", [(32, 8, 5), (64, 32, 3), (16, 5, 7)])
+@pytest.mark.parametrize("N,L,B", [(32, 8, 5), (64, 32, 3), (16, 5, 7), (128, 64, 2)])
 def test_sh_analysis_parity(N, L, B, prec):
     b = gen.particles(N, B, 0.1, seed=21, shift_mode=gen.SHIFT_UNIFORM, shift_max=2.0)
     h = handle(N, L, prec)
