@@ -585,18 +585,17 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           }
           long long tq2 = clock64();
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[2], (unsigned long long)(tq2 - tq1));
-          // per-ring power-of-two scale (max |sample| -> [2^14, 2^15)), fp16 hi/lo split, 8-byte stores; the four
-          // rings' max reductions run interleaved
+          // per-ring power-of-two scale (max |sample| -> [2^14, 2^15)), fp16 hi/lo split, 8-byte stores
           float mxv[RPW];
 #pragma unroll
           for (int rr = 0; rr < RPW; ++rr) {
             mxv[rr] = fmaxf(fmaxf(fabsf(sv[rr][0]), fabsf(sv[rr][1])), fmaxf(fabsf(sv[rr][2]), fabsf(sv[rr][3])));
             if (xr == rr) mxv[rr] = fmaxf(mxv[rr], fabsf(ex));
           }
+          // |x| as an unsigned bit pattern orders like the value: one warp-reduce instruction (REDUX) per ring
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int rr = 0; rr < RPW; ++rr) mxv[rr] = fmaxf(mxv[rr], __shfl_xor_sync(0xffffffffu, mxv[rr], o));
+          for (int rr = 0; rr < RPW; ++rr)
+            mxv[rr] = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mxv[rr])));
 #pragma unroll
           for (int rr = 0; rr < RPW; ++rr) {
             const int r = warp + rr * kWarps;
