@@ -56,7 +56,7 @@ def test_sh_analysis_parity(N, L, B, prec):
             assert np.abs(F[p] - Fo[p]).max() <= tol, (p, np.abs(F[p] - Fo[p]).max() / scale)
 
 
-@pytest.mark.parametrize("N,L,B", [(64, 32, 150), (32, 8, 160)])
+@pytest.mark.parametrize("N,L,B", [(64, 32, 150), (32, 8, 160), (16, 5, 48), (48, 20, 40)])
 def test_sh_analysis_tensor_core_path_parity(N, L, B):
     """Batches of at least a quarter of the SMs take the persistent tensor-core ring kernel (fp16 hi/lo split DFT,
     z-sorted rings, plane ring buffer) -- compared with the oracle on sampled particles, unshifted and shifted
