@@ -605,10 +605,13 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             const float sc = __uint_as_float((uint32_t)(127 + es) << 23);
             const uint32_t rowoff = (uint32_t)((r >> 3) * 128 + (r & 7) * 16);
             if (k <= Kh) {
-              const float x0 = sv[rr][0] * sc, x1 = sv[rr][1] * sc, x2 = sv[rr][2] * sc, x3 = sv[rr][3] * sc;
-              const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+              const float2 sc2 = make_float2(sc, sc);
+              const float2 x01 = __fmul2_rn(make_float2(sv[rr][0], sv[rr][1]), sc2);
+              const float2 x23 = __fmul2_rn(make_float2(sv[rr][2], sv[rr][3]), sc2);
+              const __half2 h01 = __float22half2_rn(x01), h23 = __float22half2_rn(x23);
               const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-              const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+              const __half2 l01 = __float22half2_rn(__fadd2_rn(x01, make_float2(-f01.x, -f01.y)));
+              const __half2 l23 = __float22half2_rn(__fadd2_rn(x23, make_float2(-f23.x, -f23.y)));
               const int c = 4 * (k - 1);  // K position of the lane's first sample (8-byte aligned)
               const uint32_t off = (uint32_t)(c >> 3) * LBO + rowoff + (uint32_t)(c & 7) * 2;
               uint2 hv, lv;
