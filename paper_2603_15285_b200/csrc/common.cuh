@@ -44,6 +44,7 @@ enum : int { FLAG_NONFINITE = 1, FLAG_OVERFLOW = 2, FLAG_PLANES = 4 };
 // lnc = 1/2 ln C(2 l0, |m+n|) (seed normalisation), in double on the host.
 struct PairDesc {
   int16_t m, n;
+  int32_t off0;  // half-plane offset of M^{l0}_mn, l0 = max(m, |n|): half_offset(l0) + m (2 l0 + 1) + n + l0
 };
 
 // ------------------------------------------------------------------ kernel argument packs

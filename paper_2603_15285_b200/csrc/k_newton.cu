@@ -225,7 +225,7 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
       // M^l_mn for l = l0.. lives at half_offset(l) + m(2l+1) + n + l (consecutive l differ by (l+1)(2l+1)+2m+1).
       // The l-loop is unrolled by two so that d^{l-1} is overwritten in place by d^{l+1} (no register rotation);
       // M is loaded two degrees ahead of its use.
-      const cplx_t<T>* pM = M + ((int)half_offset(l0) + m * (2 * l0 + 1) + (n + l0));
+      const cplx_t<T>* pM = M + pd.off0;
       int inc = (l0 + 1) * (2 * l0 + 1) + 2 * m + 1;  // pointer step l0 -> l0 + 1; grows by 4l + 5
       auto next_ptr = [&](int l) {                   // advance pM from degree l to l + 1
         pM += inc;

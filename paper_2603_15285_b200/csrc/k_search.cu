@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) k_so3_search(SearchArgs<T> a) {
       T d, dd, dprev = T(0), sq = T(0);
       wigner_seed<T, false>(m, n, a.pair_lnc[pi], bl, d, dd);
       T xr = T(0), xi = T(0);
-      int off = (int)half_offset(l0) + m * (2 * l0 + 1) + (n + l0);
+      int off = pd.off0;
       for (int l = l0;; ++l) {
         const cplx_t<T> Ml = Ms[off];
         xr = fma(Ml.x, d, xr);
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc)
       cb[q] = bsl[j];
       dprev[q] = xr[q] = xi[q] = T(0);
     }
-    int off = (int)half_offset(l0) + m * (2 * l0 + 1) + (n + l0);
+    int off = pd.off0;
     T sq = T(0);
     for (int l = l0;; ++l) {
       const cplx_t<T> Ml = Ms[off];

@@ -513,7 +513,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   std::vector<double> plnc;
   for (int k = 0; k <= h->L; ++k) {
     auto add = [&](int m, int n) {
-      pairs.push_back(PairDesc{(int16_t)m, (int16_t)n});
+      pairs.push_back(PairDesc{(int16_t)m, (int16_t)n, (int32_t)(half_offset(k) + (int64_t)m * (2 * k + 1) + (n + k))});
       const int p = std::abs(m + n);
       plnc.push_back(0.5 * (std::lgamma(2.0 * k + 1.0) - std::lgamma(p + 1.0) - std::lgamma(2.0 * k - p + 1.0)));
     };
