@@ -806,6 +806,14 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
     const int64_t p = it / ngroups;
     const int i0 = (int)(it % ngroups) * SG;
     cplx_t<T>* Fp = F + p * (int64_t)ncf * R;
+    {
+      // this item's G is in shared memory now and nobody reads it again: drop its whole 128-byte L2 lines without
+      // write-back (the two partial boundary lines are shared with the neighbouring items and stay)
+      const uintptr_t g0 = reinterpret_cast<uintptr_t>(G + ((p * R + i0) * (int64_t)nth) * L1);
+      const uintptr_t a0 = (g0 + 127) & ~uintptr_t(127), a1 = (g0 + gbytes) & ~uintptr_t(127);
+      for (uintptr_t a = a0 + 128 * (uintptr_t)ltid; a < a1; a += 128 * (uintptr_t)LT)
+        asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(a) : "memory");
+    }
     for (int tile = ltid; tile < ntiles; tile += LT) {
       const int m = tmap[tile] & 0xffff, par = (tmap[tile] >> 16) & 1, lb = tmap[tile] >> 17;
       const int l0t = m + par + 8 * lb;  // degrees l0t, l0t + 2, l0t + 4, l0t + 6 (same parity of l - m)

@@ -113,6 +113,15 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool va
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n));
 }
 
+// the particle volumes are read exactly once: mark their L2 lines evict-first so that the ring coefficients G
+// (written here, read back by the Legendre kernel) stay in L2 instead of round-tripping through HBM
+__device__ __forceinline__ void cp_async16_stream(void* sdst, const void* gsrc, bool valid, uint64_t policy) {
+  const unsigned s = su32(sdst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(s), "l"(gsrc), "r"(n),
+               "l"(policy));
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
@@ -385,6 +394,8 @@ __global__ void __launch_bounds__(kThr + 32, 1)
     // ================================================================ sampler warps (512 threads)
     auto sbar = []() { asm volatile("bar.sync 1, %0;\n" ::"r"(kThr)); };
     uint32_t dph = 0u;       // bit b: parity of the next completion of done[b]
+    uint64_t l2_stream;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(l2_stream));
     uint32_t gtile = 0;      // global tile counter (buffer = gtile & 1)
     for (int64_t p = blockIdx.x; p < B; p += gridDim.x) {
       const float* vol = vols + p * (int64_t)N * N * N;
@@ -457,7 +468,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           const float* src = vol + (size_t)(valid ? z : 0) * N * N;
           for (int t = tid; t < N * n4; t += kThr) {
             const int y = t / n4, x4 = t - y * n4;
-            cp_async16(dst + y * PW + 4 * x4, src + y * N + 4 * x4, valid);
+            cp_async16_stream(dst + y * PW + 4 * x4, src + y * N + 4 * x4, valid, l2_stream);
           }
         }
         zhave = max(zhave, zto);
