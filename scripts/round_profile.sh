@@ -17,3 +17,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 for K in k_sh_rings_tc k_sh_legendre_pers k_corr_tc k_so3_grid k_newton_refine; do
   ncu --set full --clock-control none --import-source on -k "regex:$K" -s 3 -c 1 -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_$K.log 2>&1; echo full_$K=$?
 done
+# warm-cache DRAM traffic of the same launches (--cache-control none: what the pipeline really moves; the --set full
+# captures above flush the caches before every kernel)
+for K in k_sh_rings_tc k_sh_legendre_pers k_corr_tc k_so3_grid k_newton_refine; do
+  ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+      -k "regex:$K" -s 3 -c 1 --csv $CMD 2>/dev/null | grep -E "dram__|gpu__time" > gpurun_out/${TAG}_warm_$K.csv; echo warm_$K=$?
+done
