@@ -148,9 +148,11 @@ def time_oracle(vols, ref, c, n, nthreads):
 def cpu_baseline(batch, c, budget_s=20.0):
     """The FP64 oracle as it stands, on this host's cores, on a bounded sample of the same workload."""
     cores = os.cpu_count() or 1
-    t1 = time_oracle(batch.vols, batch.ref, c, 1, 1)
-    n = int(max(1, min(len(batch.vols), budget_s * cores / max(t1, 1e-3))))
-    n = max(min(n, len(batch.vols)), min(cores, len(batch.vols)))
+    # calibrate on one particle per thread (the pool's real throughput, not 1-thread time x cores)
+    n0 = min(cores, len(batch.vols))
+    t0 = time_oracle(batch.vols, batch.ref, c, n0, cores)
+    n = int(max(n0, min(len(batch.vols), budget_s * n0 / max(t0, 1e-3))))
+    n = max(n0, (n // n0) * n0)
     t = time_oracle(batch.vols, batch.ref, c, n, cores)
     return {"value": n / t, "unit": "particles/s", "cores": cores, "kind": "oracle",
             "sample": f"{n} of the {len(batch.vols)} {c['N']}^3 particles of this workload (same seed), "
@@ -163,9 +165,10 @@ def run_reference(args, c, rank, world):
         return 0
     cores = os.cpu_count() or 1
     batch = make_batch(c, 0, 1, min(c["particles"], 4096))
-    t1 = time_oracle(batch.vols, batch.ref, c, 1, 1)
+    n0 = min(cores, len(batch.vols))
+    t0 = time_oracle(batch.vols, batch.ref, c, n0, cores)  # one particle per pool thread: calibration
     per_step_budget = 150.0 / max(1, args.steps + args.warmup)
-    S = int(max(1, min(len(batch.vols), per_step_budget * cores / max(t1, 1e-3))))
+    S = int(max(n0, min(len(batch.vols), per_step_budget * n0 / max(t0, 1e-3))))
     for _ in range(args.warmup):
         time_oracle(batch.vols, batch.ref, c, S, cores)
     t = 0.0
@@ -304,12 +307,13 @@ def main():
     fl, by = work[dom]
     t_stage = dms / 1e3
     t_alu, t_hbm = fl / (alu_peak * 1e12), by / (hbm_peak * 1e9)
-    traffic = None
+    traffic = traffic_pp = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         tr = json.load(open(tp)).get(args.config, {}).get(dom)
-        if isinstance(tr, dict):
-            traffic = tr.get("bytes_per_particle")
+        if isinstance(tr, dict) and tr.get("bytes_per_particle") is not None:
+            traffic_pp = tr["bytes_per_particle"]
+            traffic = traffic_pp * units / dn  # DRAM bytes per launch, like achieved
     if t_alu >= t_hbm:
         achieved = fl * units / t_stage / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
@@ -323,8 +327,10 @@ def main():
                                  if roof["bound"] == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({src})"),
                  "launches": dn, "avg_launch_ms": dms / dn,
                  "work_per_particle": {"flop": fl, "bytes": by},
-                 "traffic_unit": "DRAM bytes per particle (ncu dram__bytes_read+write of the stage's kernels, "
-                                 "profiles/traffic.json); compare with work_per_particle.bytes",
+                 "traffic_unit": "DRAM bytes per launch of the stage (ncu dram__bytes_read+write of its kernels "
+                                 "per particle, profiles/traffic.json, x particles per launch)",
+                 "traffic_per_particle": traffic_pp,
+                 "algorithmic_bytes_per_launch": by * units / dn,
                  "hbm_gbs_achieved": by * units / t_stage / 1e9,
                  "alu_tflops_achieved": fl * units / t_stage / 1e12,
                  "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()}})
