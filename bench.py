@@ -7,7 +7,7 @@ stage 2 (Wigner coefficient tensor), stage 3 (coarse SO(3) search), stage 4 (fre
 Newton, final C_{L_J}, argmax), pose gather (all_gather over NCCL when N>1).  Weak scaling: every
 rank aligns its own --particles (default 1,000 = BASELINE configs[1], "c2").
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl matcha|reference] [--config c2|c5]
+    python bench.py [--gpus N --steps K --warmup W] [--impl matcha|reference] [--config c2|c3|c4|c5]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement" for the roofline arithmetic.
@@ -35,6 +35,10 @@ CONFIGS = {
     "c4": dict(N=64, L=32, bands=[8, 12, 16, 24, 32], ncand=10, K=2, snr=0.1, particles=12500, iters=1),
     # configs[4] (c5), high-bandwidth Newton stress
     "c5": dict(N=128, L=64, bands=[12, 16, 24, 32, 48, 64], ncand=16, K=2, snr=0.1, particles=1000, iters=1),
+    # configs[2] (c3): 96^3, SNR 0.05, shifts U[-4,4]^3, T = 3 alternations with the FFT translation update
+    # (W = 6); 1,000 particles per rank (the 10,000-particle job is 10 such steps)
+    "c3": dict(N=96, L=48, bands=[8, 12, 16, 24, 32, 48], ncand=10, K=2, snr=0.05, particles=1000, iters=1,
+               T=3, W=6, shift_max=4.0),
     # configs[0] (c1) rotation part, small
     "c1": dict(N=32, L=8, bands=[4, 6, 8], ncand=4, K=2, snr=float("inf"), particles=64, iters=1),
 }
@@ -74,8 +78,20 @@ def stage_work(c):
     srch_by = 8 * mh(L0)
     nw_fl = sum(c["iters"] * mh(Lj) * nc * 28 for Lj in c["bands"]) + mh(c["bands"][-1]) * nc * 8
     nw_by = sum(c["iters"] * 8 * mh(Lj) for Lj in c["bands"]) + 8 * mh(c["bands"][-1])
-    return {"sh_analysis": (sh_fl, sh_by), "corr_coeffs": (corr_fl, corr_by), "so3_search": (srch_fl, srch_by),
-            "newton_refine": (nw_fl, nw_by), "gather_poses": (0, 48)}
+    T = c.get("T", 1)
+    work = {"sh_analysis": (T * sh_fl, T * sh_by), "corr_coeffs": (T * corr_fl, T * corr_by),
+            "so3_search": (T * srch_fl, T * srch_by), "newton_refine": (T * nw_fl, T * nw_by),
+            "gather_poses": (0, 48)}
+    if T > 1:
+        # a11-a13 per alternation: rotated reference (~30 flop/voxel, write rho), R2C(rho) + C2R of the product
+        # (2 x 2.5 N^3 log2 N^3), the spectrum product (6 flop/bin); bytes: rho written + read, F^ read.
+        # Plus F^ = R2C(f) once per particle (f read, F^ written).
+        n3, bins = N ** 3, N * N * (N // 2 + 1)
+        lg = 3 * np.log2(N)
+        alt_fl = 30 * n3 + 2 * 2.5 * n3 * lg + 6 * bins
+        alt_by = 8 * n3 + 8 * bins
+        work["translation_update"] = (int(T * alt_fl + 2.5 * n3 * lg), int(T * alt_by + 4 * n3 + 8 * bins))
+    return work
 
 
 class ClockSampler:
@@ -130,12 +146,15 @@ class ClockSampler:
 
 def make_batch(c, rank, world, P):
     import gen
+    if c.get("shift_max"):
+        return gen.particles(c["N"], P, c["snr"], seed=SEED, first=rank * P, shift_mode=gen.SHIFT_UNIFORM,
+                             shift_max=c["shift_max"])
     return gen.particles(c["N"], P, c["snr"], seed=SEED, first=rank * P)
 
 
 def oracle_params(c):
     return dict(L=c["L"], qover=2, L0=c["bands"][0], K=c["K"], ncand=c["ncand"], bands=c["bands"],
-                iters=c["iters"], T=1, W=0)
+                iters=c["iters"], T=c.get("T", 1), W=c.get("W", 0))
 
 
 def time_oracle(vols, ref, c, n, nthreads):
@@ -177,7 +196,7 @@ def run_reference(args, c, rank, world):
     value = S * args.steps / t
     sample = (f"{S} particles per step of the {c['N']}^3 workload (same seed), std::thread pool of {cores}, "
               "FP64 C++ oracle")
-    out = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": args.gpus, "steps": args.steps,
+    out = {"metric": metric_of(args.config, c), "value": value, "unit": "particles/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
@@ -189,6 +208,14 @@ def run_reference(args, c, rank, world):
            "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
+
+
+def metric_of(name, c):
+    """BASELINE's metric for its workload (c2/c4); the same measure named for the other configs."""
+    if name in ("c2", "c4"):
+        return METRIC
+    alt = f", T={c['T']} alternations" if c.get("T", 1) > 1 else ""
+    return f"particles aligned/s (box {c['N']}³, L0={c['bands'][0]}→L={c['L']}{alt}, device-timed)"
 
 
 def main():
@@ -228,7 +255,8 @@ def main():
     vols = vols_host.to(dev)
     ref = ref_host.to(dev)
     h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=P)
-    params = mt.Params(bands=c["bands"], n_cand=c["ncand"], oversample=c["K"], newton_iters=c["iters"])
+    params = mt.Params(bands=c["bands"], n_cand=c["ncand"], oversample=c["K"], newton_iters=c["iters"],
+                       n_alternations=c.get("T", 1), shift_window=c.get("W", 0))
     from paper_2603_15285_b200 import dist as D
     H = torch.empty((ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
     counts = [P] * world
@@ -339,12 +367,15 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(batch, c)
 
-    out = {"metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
+    out = {"metric": metric_of(args.config, c), "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
            "config": {"workload": f"{args.config}: {P} particles/rank of {c['N']}^3, SNR {c['snr']}, "
                                   f"L0={c['bands'][0]}->L={c['L']} bands {c['bands']}, N_C={c['ncand']}, "
-                                  f"K={c['K']}, 1 Newton step/band, rotation only",
+                                  f"K={c['K']}, 1 Newton step/band, "
+                                  + (f"T={c['T']} alternations with the FFT translation update (W={c['W']}), "
+                                     f"shifts U[-{c['shift_max']:g},{c['shift_max']:g}]^3" if c.get("T", 1) > 1
+                                     else "rotation only"),
                       "particles_per_rank": P, "parallelism": f"dp{world}",
                       "l2": f"inputs larger than L2 ({P * c['N'] ** 3 * 4 / 2**30:.2f} GiB per rank resident)"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch, "clocks": clocks}

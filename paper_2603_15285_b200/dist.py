@@ -64,5 +64,9 @@ def align_step(handle, vols_local: torch.Tensor, ref: torch.Tensor, params, H: t
     if rank == 0:
         handle.sh_analysis(ref[None], out=H[None])
     broadcast_ref_coeffs(H, src=0, group=group)
-    poses = handle.align_batch(vols_local, None, params, ref_coeffs=H)
+    translate = getattr(params, "n_alternations", 1) > 1
+    if translate:
+        # the translation update (App. C) rotates the reference volume itself: rank 0's copy goes to every rank
+        broadcast_ref_coeffs(ref, src=0, group=group)
+    poses = handle.align_batch(vols_local, ref if translate else None, params, ref_coeffs=H)
     return gather_poses(poses, counts=counts, group=group)
