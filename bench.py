@@ -172,7 +172,7 @@ def cpu_baseline(batch, c, budget_s=20.0):
     t0 = time_oracle(batch.vols, batch.ref, c, n0, cores)
     n = int(max(n0, min(len(batch.vols), budget_s * n0 / max(t0, 1e-3))))
     n = max(n0, (n // n0) * n0)
-    t = time_oracle(batch.vols, batch.ref, c, n, cores)
+    t = t0 if n == n0 else time_oracle(batch.vols, batch.ref, c, n, cores)
     return {"value": n / t, "unit": "particles/s", "cores": cores, "kind": "oracle",
             "sample": f"{n} of the {len(batch.vols)} {c['N']}^3 particles of this workload (same seed), "
                       f"std::thread pool of {cores}, FP64 C++ oracle (oracle/oracle.cpp)"}
