@@ -37,6 +37,7 @@ class FakeHandle:
         poses = torch.zeros((n, 8), dtype=torch.float32)
         poses[:, 0] = vols.reshape(n, -1)[:, 0]          # global particle id planted in voxel 0
         poses[:, 6] = float(torch.view_as_real(ref_coeffs).sum())
+        poses[:, 7] = -1.0 if ref is None else float(ref.sum())  # the volume the translation update would rotate
         return poses
 
 
@@ -48,7 +49,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, P, q):
+class _Params:
+    def __init__(self, T):
+        self.n_alternations = T
+
+
+def _worker(rank, world, port, P, q, T=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -56,22 +62,24 @@ def _worker(rank, world, port, P, q):
         a, b = D.shard(P, world, rank)
         vols = torch.zeros((b - a, 4, 4, 4))
         vols.reshape(b - a, -1)[:, 0] = torch.arange(a, b, dtype=torch.float32)
-        ref = torch.full((4, 4, 4), 0.5)
+        # rank 1 starts with another reference volume: with translation (T > 1) it must receive rank 0's
+        ref = torch.full((4, 4, 4), 0.5 if rank == 0 else 9.0)
         H = torch.zeros((3, 2), dtype=torch.complex64)  # rank 1 starts with zeros: must receive rank 0's
-        poses = D.align_step(FakeHandle(), vols, ref, None, H, rank)
+        poses = D.align_step(FakeHandle(), vols, ref, _Params(T) if T else None, H, rank)
         t = D.max_over_ranks(float(rank + 1))
         # plain Python values only: a tensor would travel as a shared-memory handle that dies with this process
-        q.put((rank, poses[:, 0].tolist(), poses[:, 6].tolist(), torch.view_as_real(H).tolist(), t))
+        q.put((rank, poses[:, 0].tolist(), poses[:, 6].tolist(), torch.view_as_real(H).tolist(), t,
+               poses[:, 7].tolist()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("P", [10, 7])
-def test_align_step_world2_gloo(P):
+@pytest.mark.parametrize("P,T", [(10, 0), (7, 1), (7, 3)])
+def test_align_step_world2_gloo(P, T):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, P, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, P, q, T)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(2)]
@@ -80,8 +88,10 @@ def test_align_step_world2_gloo(P):
         assert p.exitcode == 0
     res.sort()
     expect_H = torch.full((3, 2), complex(0.5 * 64, 1.0), dtype=torch.complex64)
-    for rank, ids, checks, H, t in res:
+    for rank, ids, checks, H, t, refsum in res:
         assert ids == [float(i) for i in range(P)]                  # gathered in global order
         assert torch.equal(torch.view_as_complex(torch.tensor(H)), expect_H)  # broadcast from rank 0
         assert all(abs(c - float(torch.view_as_real(expect_H).sum())) < 1e-3 for c in checks)
         assert t == 2.0                                             # max over ranks
+        # rotation only: no reference volume is passed; translating: rank 0's volume on every rank
+        assert refsum == [-1.0 if T <= 1 else 0.5 * 64] * P
