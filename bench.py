@@ -83,13 +83,14 @@ def stage_work(c):
             "so3_search": (T * srch_fl, T * srch_by), "newton_refine": (T * nw_fl, T * nw_by),
             "gather_poses": (0, 48)}
     if T > 1:
-        # a11-a13 per alternation: rotated reference (~30 flop/voxel, write rho), R2C(rho) + C2R of the product
-        # (2 x 2.5 N^3 log2 N^3), the spectrum product (6 flop/bin); bytes: rho written + read, F^ read.
+        # a11-a13 per alternation (k_trans.cu): rotated reference rho (~30 flop/voxel, written once, read by the
+        # R2C), R2C(rho) (2.5 N^3 log2 N^3 flop, rho^ written), then the pruned inverse DFT on the w' = 2W+3 window
+        # (X = F^ conj(rho^) formed on chip: F^ and rho^ read once; 8 flop per complex MAC over the x, y, z passes).
         # Plus F^ = R2C(f) once per particle (f read, F^ written).
-        n3, bins = N ** 3, N * N * (N // 2 + 1)
-        lg = 3 * np.log2(N)
-        alt_fl = 30 * n3 + 2 * 2.5 * n3 * lg + 6 * bins
-        alt_by = 8 * n3 + 8 * bins
+        n3, H = N ** 3, N // 2 + 1
+        bins, lg, wp = N * N * H, 3 * np.log2(N), 2 * c["W"] + 3
+        alt_fl = 30 * n3 + 2.5 * n3 * lg + 6 * bins + 8 * (N * N * H * wp + N * N * wp * wp) + 8 * N * wp ** 3
+        alt_by = 8 * n3 + 8 * bins + 16 * bins
         work["translation_update"] = (int(T * alt_fl + 2.5 * n3 * lg), int(T * alt_by + 4 * n3 + 8 * bins))
     return work
 

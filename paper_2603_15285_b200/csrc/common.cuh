@@ -134,5 +134,9 @@ template <typename T> cudaError_t launch_cross_spectrum(const cplx_t<T>* F, cplx
 template <typename T>
 cudaError_t launch_window_peak(const T* corr, int N, int W, int64_t nb, T* shifts, int sstride, T* peak,
                                cudaStream_t s);
+size_t window_scratch_reals(int N, int W);
+template <typename T>
+cudaError_t launch_window_pruned(const cplx_t<T>* Fh, const cplx_t<T>* Rh, int N, int W, int64_t nb, T* scratch,
+                                 T* shifts, int sstride, T* peak, cudaStream_t s);
 
 }  // namespace matcha

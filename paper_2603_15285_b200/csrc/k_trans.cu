@@ -60,25 +60,87 @@ __device__ __forceinline__ T trilinear_g(const float* __restrict__ v, int N, T p
   return fma(fz, c1 - c0, c0);
 }
 
-// rho_p(x) = h(R_p^T (x - c) + c) for particles p < nb; euler rows at stride estride
+// rho_p(x) = h(R_p^T (x - c) + c) for particles p < nb; euler rows at stride estride.
+// One CTA per (8^3 output tile, particle): the tile's source region (the axis-aligned box around the rotated
+// cube, <= 16^3 voxels incl. the trilinear +1) is staged in shared memory by row loads from the L2-resident
+// reference, then every voxel gathers its 8 corners from shared memory.  (A direct gather from L2 touches a
+// separate 32-byte sector for nearly every lane of a rotated row: ~0.25 voxel per cycle per SM.)  Out-of-volume
+// corners are staged as 0, so the arithmetic is exactly trilinear_g's.  N is a multiple of 8 (matcha_create).
+constexpr int kRotTile = 8, kRotBox = 16;
 template <typename T>
 __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ ref, int N, const T* __restrict__ euler,
                                                     int estride, T* __restrict__ rho) {
   __shared__ double Rm[9];
+  __shared__ float box[kRotBox * kRotBox * kRotBox];
+  __shared__ int org[4];
   const int64_t p = blockIdx.y;
-  if (threadIdx.x == 0) rot_matrix<T>(euler + p * estride, Rm);
-  __syncthreads();
-  const int64_t n3 = (int64_t)N * N * N;
+  const int nt = N / kRotTile;
+  const int tz = blockIdx.x / (nt * nt), ty = (blockIdx.x / nt) % nt, tx = blockIdx.x % nt;
   const T c = T(0.5) * (T)(N - 1);
+  if (threadIdx.x == 0) {
+    rot_matrix<T>(euler + p * estride, Rm);
+    // source box of the tile: image of the 8 corners of [x0, x0+7]^3 under v -> R^T (v - c) + c
+    T lo[3] = {T(1e30), T(1e30), T(1e30)}, hi[3] = {T(-1e30), T(-1e30), T(-1e30)};
+    for (int k = 0; k < 8; ++k) {
+      const T vx = (T)(tx * kRotTile + (k & 1) * (kRotTile - 1)) - c;
+      const T vy = (T)(ty * kRotTile + ((k >> 1) & 1) * (kRotTile - 1)) - c;
+      const T vz = (T)(tz * kRotTile + (k >> 2) * (kRotTile - 1)) - c;
+      const T q[3] = {fma((T)Rm[0], vx, fma((T)Rm[3], vy, (T)Rm[6] * vz)) + c,
+                      fma((T)Rm[1], vx, fma((T)Rm[4], vy, (T)Rm[7] * vz)) + c,
+                      fma((T)Rm[2], vx, fma((T)Rm[5], vy, (T)Rm[8] * vz)) + c};
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = fmin(lo[d], q[d]);
+        hi[d] = fmax(hi[d], q[d]);
+      }
+    }
+    int fits = 1;
+    for (int d = 0; d < 3; ++d) {
+      org[d] = (int)floor(lo[d]);
+      fits &= (int)floor(hi[d]) + 1 - org[d] < kRotBox;  // corners floor(q) .. floor(q)+1 inside the box
+    }
+    org[3] = fits;
+  }
+  __syncthreads();
   const T r0 = (T)Rm[0], r1 = (T)Rm[1], r2 = (T)Rm[2], r3 = (T)Rm[3], r4 = (T)Rm[4], r5 = (T)Rm[5], r6 = (T)Rm[6],
           r7 = (T)Rm[7], r8 = (T)Rm[8];
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n3; v += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(v % N), y = (int)((v / N) % N), z = (int)(v / ((int64_t)N * N));
+  const int ox = org[0], oy = org[1], oz = org[2];
+  const bool staged = org[3] != 0;
+  if (staged) {
+    for (int i = threadIdx.x; i < kRotBox * kRotBox * kRotBox; i += blockDim.x) {
+      const int x = ox + (i % kRotBox), y = oy + (i / kRotBox) % kRotBox, z = oz + i / (kRotBox * kRotBox);
+      const bool in = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N;
+      box[i] = in ? __ldg(ref + ((size_t)z * N + y) * N + x) : 0.f;
+    }
+  }
+  __syncthreads();
+  T* out = rho + p * (int64_t)N * N * N;
+  for (int i = threadIdx.x; i < kRotTile * kRotTile * kRotTile; i += blockDim.x) {
+    const int x = tx * kRotTile + (i % kRotTile), y = ty * kRotTile + (i / kRotTile) % kRotTile,
+              z = tz * kRotTile + i / (kRotTile * kRotTile);
     const T vx = (T)x - c, vy = (T)y - c, vz = (T)z - c;
     const T qx = fma(r0, vx, fma(r3, vy, r6 * vz)) + c;  // R^T v
     const T qy = fma(r1, vx, fma(r4, vy, r7 * vz)) + c;
     const T qz = fma(r2, vx, fma(r5, vy, r8 * vz)) + c;
-    rho[p * n3 + v] = trilinear_g<T>(ref, N, qx, qy, qz);
+    T val;
+    if (staged) {
+      const T fx0 = floor(qx), fy0 = floor(qy), fz0 = floor(qz);
+      const int bx = (int)fx0 - ox, by = (int)fy0 - oy, bz = (int)fz0 - oz;
+      const T fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
+      const float* b0 = box + (bz * kRotBox + by) * kRotBox + bx;
+      const T c000 = b0[0], c001 = b0[1], c010 = b0[kRotBox], c011 = b0[kRotBox + 1];
+      const T c100 = b0[kRotBox * kRotBox], c101 = b0[kRotBox * kRotBox + 1];
+      const T c110 = b0[kRotBox * kRotBox + kRotBox], c111 = b0[kRotBox * kRotBox + kRotBox + 1];
+      const T c00 = fma(fx, c001 - c000, c000);
+      const T c01 = fma(fx, c011 - c010, c010);
+      const T c10 = fma(fx, c101 - c100, c100);
+      const T c11 = fma(fx, c111 - c110, c110);
+      const T c0 = fma(fy, c01 - c00, c00);
+      const T c1 = fma(fy, c11 - c10, c10);
+      val = fma(fz, c1 - c0, c0);
+    } else {
+      val = trilinear_g<T>(ref, N, qx, qy, qz);
+    }
+    out[((int64_t)z * N + y) * N + x] = val;
   }
 }
 
@@ -161,6 +223,160 @@ __global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ corr,
   }
 }
 
+// ---- windowed correlation by a pruned inverse DFT (replaces the cross spectrum + full C2R + window read) --------
+// Only c(t) for t in the window [-W-1, W+1]^3 (the argmax window plus the subpixel neighbours) is needed, so the
+// inverse transform of X = F^ conj(rho^) is evaluated directly on those w' = 2W+3 points per axis, separably:
+//   Y1[kz][ky][a]  = sum_{kx=0}^{N/2} w_kx X[kz][ky][kx] e^{+2 pi i kx tx_a / N}   (w_kx = 1 at kx = 0, N/2, else 2)
+//   Y2[kz][b][a]   = sum_ky Y1[kz][ky][a] e^{+2 pi i ky ty_b / N}
+//   cw[c][b][a]    = Re sum_kz Y2[kz][b][a] e^{+2 pi i kz tz_c / N}  = N^3 c(t)  (the unnormalised C2R value)
+// X is Hermitian (F^, rho^ are spectra of real volumes), so the half-spectrum sum with weights w_kx and Re is exact.
+// The per-(particle, kz) kernel forms X in shared memory from coalesced F^/rho^ plane loads (X is never stored).
+
+template <typename T> __device__ __forceinline__ cplx_t<T> cmul(cplx_t<T> a, cplx_t<T> b) {
+  return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+template <typename T>
+__device__ __forceinline__ void build_twiddles(cplx_t<T>* tw, int N) {
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double sn, cs;
+    sincospi(2.0 * j / N, &sn, &cs);  // e^{+2 pi i j / N}
+    tw[j] = mk<T>((T)cs, (T)sn);
+  }
+}
+
+// grid (N, nb): block (kz, p) -> Y2[p][kz][w'][w']
+template <typename T>
+__global__ void __launch_bounds__(256) k_window_xy(const cplx_t<T>* __restrict__ Fh, const cplx_t<T>* __restrict__ Rh,
+                                                   int N, int W, cplx_t<T>* __restrict__ Y2) {
+  extern __shared__ unsigned char smem_raw[];
+  const int H = N / 2 + 1, wp = 2 * W + 3;
+  cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N]
+  cplx_t<T>* X = tw + N;                                   // [N][H]
+  cplx_t<T>* Y1 = X + N * H;                               // [N][wp]
+  const int kz = blockIdx.x;
+  const int64_t p = blockIdx.y;
+  const int64_t plane = ((int64_t)p * N + kz) * N * H;
+  build_twiddles<T>(tw, N);
+  for (int i = threadIdx.x; i < N * H; i += blockDim.x) {
+    const cplx_t<T> f = Fh[plane + i], r = Rh[plane + i];
+    const int kx = i % H;
+    const T wk = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
+    X[i] = mk<T>(wk * (f.x * r.x + f.y * r.y), wk * (f.y * r.x - f.x * r.y));  // w_kx F^ conj(rho^)
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < N * wp; o += blockDim.x) {
+    const int ky = o / wp, a = o - ky * wp;
+    const int tx = a - (W + 1);
+    const int step = ((tx % N) + N) % N;
+    const cplx_t<T>* xr = X + ky * H;
+    T ar = T(0), ai = T(0);
+    int idx = 0;
+    for (int kx = 0; kx < H; ++kx) {
+      const cplx_t<T> x = xr[kx], t = tw[idx];
+      ar = fma(x.x, t.x, fma(-x.y, t.y, ar));
+      ai = fma(x.x, t.y, fma(x.y, t.x, ai));
+      idx += step;
+      if (idx >= N) idx -= N;
+    }
+    Y1[o] = mk<T>(ar, ai);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < wp * wp; o += blockDim.x) {
+    const int b = o / wp, a = o - b * wp;
+    const int ty = b - (W + 1);
+    const int step = ((ty % N) + N) % N;
+    T ar = T(0), ai = T(0);
+    int idx = 0;
+    for (int ky = 0; ky < N; ++ky) {
+      const cplx_t<T> y = Y1[ky * wp + a], t = tw[idx];
+      ar = fma(y.x, t.x, fma(-y.y, t.y, ar));
+      ai = fma(y.x, t.y, fma(y.y, t.x, ai));
+      idx += step;
+      if (idx >= N) idx -= N;
+    }
+    Y2[((int64_t)p * N + kz) * wp * wp + o] = mk<T>(ar, ai);
+  }
+}
+
+// grid nb: the z pass into cw[p][w'^3] (global scratch), then the windowed argmax (ties -> lowest window index,
+// z-major) and the per-axis parabolic subpixel (reading C18), as k_window_peak but on the pruned window
+template <typename T>
+__global__ void __launch_bounds__(256) k_window_z_peak(const cplx_t<T>* __restrict__ Y2, int N, int W,
+                                                       T* __restrict__ cw_all, T* shifts, int sstride, T* peak) {
+  __shared__ cplx_t<T> tw[512];
+  __shared__ T sv[8];
+  __shared__ int si[8];
+  const int64_t p = blockIdx.x;
+  const int wp = 2 * W + 3, w = 2 * W + 1, wp2 = wp * wp;
+  build_twiddles<T>(tw, N);
+  __syncthreads();
+  const cplx_t<T>* y2 = Y2 + p * (int64_t)N * wp2;
+  T* cw = cw_all + p * (int64_t)wp2 * wp;
+  for (int o = threadIdx.x; o < wp2 * wp; o += blockDim.x) {
+    const int c = o / wp2, ba = o - c * wp2;
+    const int tz = c - (W + 1);
+    const int step = ((tz % N) + N) % N;
+    T acc = T(0);
+    int idx = 0;
+    for (int kz = 0; kz < N; ++kz) {
+      const cplx_t<T> y = y2[(int64_t)kz * wp2 + ba], t = tw[idx];
+      acc = fma(y.x, t.x, fma(-y.y, t.y, acc));
+      idx += step;
+      if (idx >= N) idx -= N;
+    }
+    cw[o] = acc;
+  }
+  __syncthreads();
+  auto at = [&](int tx, int ty, int tz) { return cw[((tz + W + 1) * wp + (ty + W + 1)) * wp + (tx + W + 1)]; };
+  const int nw = w * w * w;
+  T bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = threadIdx.x; t < nw; t += blockDim.x) {
+    const int tx = t % w - W, ty = (t / w) % w - W, tz = t / (w * w) - W;
+    const T v = at(tx, ty, tz);
+    if (better(v, t, bv, bi)) {
+      bv = v;
+      bi = t;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(v2, i2, bv, bi)) {
+      bv = v2;
+      bi = i2;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[warp] = bv;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (better(sv[k], si[k], bv, bi)) {
+        bv = sv[k];
+        bi = si[k];
+      }
+    const int t[3] = {bi % w - W, (bi / w) % w - W, bi / (w * w) - W};
+    const T c0 = bv;
+    for (int ax = 0; ax < 3; ++ax) {
+      int tm[3] = {t[0], t[1], t[2]}, tp[3] = {t[0], t[1], t[2]};
+      tm[ax] -= 1;
+      tp[ax] += 1;
+      const T cm = at(tm[0], tm[1], tm[2]), cpl = at(tp[0], tp[1], tp[2]);
+      const T den = cm - T(2) * c0 + cpl;
+      T dl = T(0);
+      if (den < T(0)) dl = fmin(T(0.5), fmax(T(-0.5), (cm - cpl) / (T(2) * den)));
+      shifts[p * sstride + ax] = (T)t[ax] + dl;
+    }
+    if (peak) peak[p] = c0 / ((T)N * N * N);
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -168,8 +384,10 @@ cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estri
                               cudaStream_t s) {
   if (nb == 0) return cudaSuccess;
   const int64_t n3 = (int64_t)N * N * N;
-  dim3 grid((unsigned)std::min<int64_t>((n3 + 255) / 256, 4096), (unsigned)nb);
-  k_rotate_ref<T><<<grid, 256, 0, s>>>(ref, N, euler, estride, rho);
+  (void)n3;
+  if (N % kRotTile) return cudaErrorInvalidValue;
+  const int nt = N / kRotTile;
+  k_rotate_ref<T><<<dim3((unsigned)(nt * nt * nt), (unsigned)nb), 256, 0, s>>>(ref, N, euler, estride, rho);
   return cudaGetLastError();
 }
 
@@ -194,6 +412,30 @@ cudaError_t launch_window_peak(const T* corr, int N, int W, int64_t nb, T* shift
   return cudaGetLastError();
 }
 
+size_t window_scratch_reals(int N, int W) {
+  const int64_t wp = 2 * W + 3;
+  return (size_t)(2 * (int64_t)N * wp * wp + wp * wp * wp);
+}
+
+// Y2 and the c window of particle p live in scratch + p * window_scratch_reals(N, W) reals
+template <typename T>
+cudaError_t launch_window_pruned(const cplx_t<T>* Fh, const cplx_t<T>* Rh, int N, int W, int64_t nb, T* scratch,
+                                 T* shifts, int sstride, T* peak, cudaStream_t s) {
+  if (nb == 0) return cudaSuccess;
+  if (N > 512 || 2 * W + 3 > N) return cudaErrorInvalidValue;
+  const int H = N / 2 + 1, wp = 2 * W + 3;
+  const size_t smem = sizeof(cplx_t<T>) * ((size_t)N + (size_t)N * H + (size_t)N * wp);
+  cudaError_t e = cudaFuncSetAttribute(k_window_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // Y2 [nb][N][wp][wp] complex at the front of the scratch, the c windows [nb][wp^3] behind it
+  cplx_t<T>* Y2 = reinterpret_cast<cplx_t<T>*>(scratch);
+  T* cw = scratch + 2 * nb * (int64_t)N * wp * wp;
+  k_window_xy<T><<<dim3((unsigned)N, (unsigned)nb), 256, smem, s>>>(Fh, Rh, N, W, Y2);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_window_z_peak<T><<<(unsigned)nb, 256, 0, s>>>(Y2, N, W, cw, shifts, sstride, peak);
+  return cudaGetLastError();
+}
+
 template cudaError_t launch_rotate_ref<float>(const float*, int, const float*, int, int64_t, float*, cudaStream_t);
 template cudaError_t launch_rotate_ref<double>(const float*, int, const double*, int, int64_t, double*, cudaStream_t);
 template cudaError_t launch_to_real<float>(const float*, float*, int64_t, cudaStream_t);
@@ -203,5 +445,9 @@ template cudaError_t launch_cross_spectrum<double>(const double2*, double2*, int
 template cudaError_t launch_window_peak<float>(const float*, int, int, int64_t, float*, int, float*, cudaStream_t);
 template cudaError_t launch_window_peak<double>(const double*, int, int, int64_t, double*, int, double*,
                                                 cudaStream_t);
+template cudaError_t launch_window_pruned<float>(const float2*, const float2*, int, int, int64_t, float*, float*, int,
+                                                 float*, cudaStream_t);
+template cudaError_t launch_window_pruned<double>(const double2*, const double2*, int, int, int64_t, double*, double*,
+                                                  int, double*, cudaStream_t);
 
 }  // namespace matcha

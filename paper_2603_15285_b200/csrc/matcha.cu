@@ -65,6 +65,9 @@ struct matcha_ctx {
   void* ws_Xhat = nullptr;   // complex [mb][N][N][N/2+1]  rho^, then the cross spectrum
   void* ws_rho = nullptr;    // real [mb][N^3]             rotated references, then c(t)
   void* ws_peak = nullptr;   // real [mb]
+  void* ws_win = nullptr;    // real [mb][window_scratch_reals(N, W)]: pruned inverse DFT (Y2 + c window)
+  int ws_win_W = -1;
+  bool trans_fft = false;    // MATCHA_TRANS_FFT=1: full C2R + window read instead of the pruned inverse DFT
   void* ws_euler1 = nullptr; // real [mb][3]
   // per-stage event tracing
   bool prof = false;
@@ -357,6 +360,25 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
               : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
   if (!fft_r2c(h, h->ws_rho, h->ws_Xhat, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT R2C of rho failed");
+  const size_t pr_smem = (size_t)h->rsz * 2 * ((size_t)N + (size_t)N * (N / 2 + 1) + (size_t)N * (2 * W + 3));
+  if (!h->trans_fft && pr_smem <= 227 * 1024 && 2 * W + 3 <= N) {
+    // pruned inverse DFT on the window only (X = F^ conj(rho^) formed on chip, never stored)
+    if (h->ws_win_W < W) {
+      if (h->ws_win) cudaFree(h->ws_win);
+      h->ws_win = nullptr;
+      h->ws_win_W = -1;
+      e = cudaMalloc(&h->ws_win, h->rsz * window_scratch_reals(N, W) * h->cfg.max_batch);
+      if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation window scratch allocation failed");
+      h->ws_win_W = W;
+    }
+    e = h->fp64 ? launch_window_pruned<double>((const double2*)h->ws_Fhat, (const double2*)h->ws_Xhat, N, W, nb,
+                                               (double*)h->ws_win, (double*)shifts, sstride, (double*)peak, s)
+                : launch_window_pruned<float>((const float2*)h->ws_Fhat, (const float2*)h->ws_Xhat, N, W, nb,
+                                              (float*)h->ws_win, (float*)shifts, sstride, (float*)peak, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: window_pruned");
+    h->launches += 3;
+    return MATCHA_OK;
+  }
   e = h->fp64 ? launch_cross_spectrum<double>((const double2*)h->ws_Fhat, (double2*)h->ws_Xhat, nb * nc, s)
               : launch_cross_spectrum<float>((const float2*)h->ws_Fhat, (float2*)h->ws_Xhat, nb * nc, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: cross_spectrum");
@@ -419,6 +441,7 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
       h->launches++;
       if (translate) {
         if (tau == 0) {
+          ProfScope ps(h, 5, s);
           st = trans_fhat(h, vols + c0 * n3, nb, s);
           if (st != MATCHA_OK) return st;
         }
@@ -446,6 +469,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   cudaGetDevice(&h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
   if (const char* v = getenv("MATCHA_CORR_SIMT")) h->use_tc = !(v[0] == '1');
+  if (const char* v = getenv("MATCHA_TRANS_FFT")) h->trans_fft = v[0] == '1';
   h->fp64 = cfg->precision == MATCHA_FP64;
   h->rsz = h->fp64 ? 8 : 4;
   h->R = cfg->N / 2;
@@ -586,7 +610,7 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->plan_r2c) cufftDestroy(h->plan_r2c);
   if (h->plan_c2r) cufftDestroy(h->plan_c2r);
-  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1})
+  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
