@@ -66,81 +66,74 @@ __device__ __forceinline__ T trilinear_g(const float* __restrict__ v, int N, T p
 // reference, then every voxel gathers its 8 corners from shared memory.  (A direct gather from L2 touches a
 // separate 32-byte sector for nearly every lane of a rotated row: ~0.25 voxel per cycle per SM.)  Out-of-volume
 // corners are staged as 0, so the arithmetic is exactly trilinear_g's.  N is a multiple of 8 (matcha_create).
-constexpr int kRotTile = 8, kRotBox = 16;
+constexpr int kRotTile = 8, kRotBox = 16, kRotCtas = 96;
 template <typename T>
 __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ ref, int N, const T* __restrict__ euler,
                                                     int estride, T* __restrict__ rho) {
   __shared__ double Rm[9];
   __shared__ float box[kRotBox * kRotBox * kRotBox];
-  __shared__ int org[4];
   const int64_t p = blockIdx.y;
   const int nt = N / kRotTile;
-  const int tz = blockIdx.x / (nt * nt), ty = (blockIdx.x / nt) % nt, tx = blockIdx.x % nt;
   const T c = T(0.5) * (T)(N - 1);
-  if (threadIdx.x == 0) {
-    rot_matrix<T>(euler + p * estride, Rm);
-    // source box of the tile: image of the 8 corners of [x0, x0+7]^3 under v -> R^T (v - c) + c
-    T lo[3] = {T(1e30), T(1e30), T(1e30)}, hi[3] = {T(-1e30), T(-1e30), T(-1e30)};
-    for (int k = 0; k < 8; ++k) {
-      const T vx = (T)(tx * kRotTile + (k & 1) * (kRotTile - 1)) - c;
-      const T vy = (T)(ty * kRotTile + ((k >> 1) & 1) * (kRotTile - 1)) - c;
-      const T vz = (T)(tz * kRotTile + (k >> 2) * (kRotTile - 1)) - c;
-      const T q[3] = {fma((T)Rm[0], vx, fma((T)Rm[3], vy, (T)Rm[6] * vz)) + c,
-                      fma((T)Rm[1], vx, fma((T)Rm[4], vy, (T)Rm[7] * vz)) + c,
-                      fma((T)Rm[2], vx, fma((T)Rm[5], vy, (T)Rm[8] * vz)) + c};
-      for (int d = 0; d < 3; ++d) {
-        lo[d] = fmin(lo[d], q[d]);
-        hi[d] = fmax(hi[d], q[d]);
-      }
-    }
-    int fits = 1;
-    for (int d = 0; d < 3; ++d) {
-      org[d] = (int)floor(lo[d]);
-      fits &= (int)floor(hi[d]) + 1 - org[d] < kRotBox;  // corners floor(q) .. floor(q)+1 inside the box
-    }
-    org[3] = fits;
-  }
+  if (threadIdx.x == 0) rot_matrix<T>(euler + p * estride, Rm);
   __syncthreads();
   const T r0 = (T)Rm[0], r1 = (T)Rm[1], r2 = (T)Rm[2], r3 = (T)Rm[3], r4 = (T)Rm[4], r5 = (T)Rm[5], r6 = (T)Rm[6],
           r7 = (T)Rm[7], r8 = (T)Rm[8];
-  const int ox = org[0], oy = org[1], oz = org[2];
-  const bool staged = org[3] != 0;
-  if (staged) {
-    for (int i = threadIdx.x; i < kRotBox * kRotBox * kRotBox; i += blockDim.x) {
-      const int x = ox + (i % kRotBox), y = oy + (i / kRotBox) % kRotBox, z = oz + i / (kRotBox * kRotBox);
-      const bool in = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N;
-      box[i] = in ? __ldg(ref + ((size_t)z * N + y) * N + x) : 0.f;
-    }
-  }
-  __syncthreads();
+  // half extent of the image of a tile (cube of edge kRotTile-1 voxels) along each source axis
+  const T hE = T(0.5) * (T)(kRotTile - 1);
+  const T ex = hE * (fabs(r0) + fabs(r3) + fabs(r6)), ey = hE * (fabs(r1) + fabs(r4) + fabs(r7)),
+          ez = hE * (fabs(r2) + fabs(r5) + fabs(r8));
   T* out = rho + p * (int64_t)N * N * N;
-  for (int i = threadIdx.x; i < kRotTile * kRotTile * kRotTile; i += blockDim.x) {
-    const int x = tx * kRotTile + (i % kRotTile), y = ty * kRotTile + (i / kRotTile) % kRotTile,
-              z = tz * kRotTile + i / (kRotTile * kRotTile);
-    const T vx = (T)x - c, vy = (T)y - c, vz = (T)z - c;
-    const T qx = fma(r0, vx, fma(r3, vy, r6 * vz)) + c;  // R^T v
-    const T qy = fma(r1, vx, fma(r4, vy, r7 * vz)) + c;
-    const T qz = fma(r2, vx, fma(r5, vy, r8 * vz)) + c;
-    T val;
+  for (int tile = blockIdx.x; tile < nt * nt * nt; tile += gridDim.x) {
+    const int tz = tile / (nt * nt), ty = (tile / nt) % nt, tx = tile % nt;
+    // source box: image centre +- extent (+ margin against rounding), corners floor(q) .. floor(q) + 1
+    const T vx = (T)tx * kRotTile + hE - c, vy = (T)ty * kRotTile + hE - c, vz = (T)tz * kRotTile + hE - c;
+    const T qcx = fma(r0, vx, fma(r3, vy, r6 * vz)) + c, qcy = fma(r1, vx, fma(r4, vy, r7 * vz)) + c,
+            qcz = fma(r2, vx, fma(r5, vy, r8 * vz)) + c;
+    const int ox = (int)floor(qcx - ex - T(1e-3)), oy = (int)floor(qcy - ey - T(1e-3)),
+              oz = (int)floor(qcz - ez - T(1e-3));
+    const int dx = (int)floor(qcx + ex + T(1e-3)) + 2 - ox, dy = (int)floor(qcy + ey + T(1e-3)) + 2 - oy,
+              dz = (int)floor(qcz + ez + T(1e-3)) + 2 - oz;
+    const bool staged = dx <= kRotBox && dy <= kRotBox && dz <= kRotBox;  // always at kRotTile = 8 (<= 15)
+    __syncthreads();  // previous tile's gathers are done with the box
     if (staged) {
+      const int nbx = dx * dy * dz;
+      for (int i = threadIdx.x; i < nbx; i += blockDim.x) {
+        const int ix = i % dx, iy = (i / dx) % dy, iz = i / (dx * dy);
+        const int x = ox + ix, y = oy + iy, z = oz + iz;
+        const bool in = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N;
+        box[(iz * kRotBox + iy) * kRotBox + ix] = in ? __ldg(ref + ((size_t)z * N + y) * N + x) : 0.f;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kRotTile * kRotTile * kRotTile; i += blockDim.x) {
+      const int x = tx * kRotTile + (i % kRotTile), y = ty * kRotTile + (i / kRotTile) % kRotTile,
+                z = tz * kRotTile + i / (kRotTile * kRotTile);
+      const T ux = (T)x - c, uy = (T)y - c, uz = (T)z - c;
+      const T qx = fma(r0, ux, fma(r3, uy, r6 * uz)) + c;  // R^T v
+      const T qy = fma(r1, ux, fma(r4, uy, r7 * uz)) + c;
+      const T qz = fma(r2, ux, fma(r5, uy, r8 * uz)) + c;
+      T val;
       const T fx0 = floor(qx), fy0 = floor(qy), fz0 = floor(qz);
       const int bx = (int)fx0 - ox, by = (int)fy0 - oy, bz = (int)fz0 - oz;
-      const T fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
-      const float* b0 = box + (bz * kRotBox + by) * kRotBox + bx;
-      const T c000 = b0[0], c001 = b0[1], c010 = b0[kRotBox], c011 = b0[kRotBox + 1];
-      const T c100 = b0[kRotBox * kRotBox], c101 = b0[kRotBox * kRotBox + 1];
-      const T c110 = b0[kRotBox * kRotBox + kRotBox], c111 = b0[kRotBox * kRotBox + kRotBox + 1];
-      const T c00 = fma(fx, c001 - c000, c000);
-      const T c01 = fma(fx, c011 - c010, c010);
-      const T c10 = fma(fx, c101 - c100, c100);
-      const T c11 = fma(fx, c111 - c110, c110);
-      const T c0 = fma(fy, c01 - c00, c00);
-      const T c1 = fma(fy, c11 - c10, c10);
-      val = fma(fz, c1 - c0, c0);
-    } else {
-      val = trilinear_g<T>(ref, N, qx, qy, qz);
+      if (staged && bx >= 0 && by >= 0 && bz >= 0 && bx + 1 < dx && by + 1 < dy && bz + 1 < dz) {
+        const T fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
+        const float* b0 = box + (bz * kRotBox + by) * kRotBox + bx;
+        const T c000 = b0[0], c001 = b0[1], c010 = b0[kRotBox], c011 = b0[kRotBox + 1];
+        const T c100 = b0[kRotBox * kRotBox], c101 = b0[kRotBox * kRotBox + 1];
+        const T c110 = b0[kRotBox * kRotBox + kRotBox], c111 = b0[kRotBox * kRotBox + kRotBox + 1];
+        const T c00 = fma(fx, c001 - c000, c000);
+        const T c01 = fma(fx, c011 - c010, c010);
+        const T c10 = fma(fx, c101 - c100, c100);
+        const T c11 = fma(fx, c111 - c110, c110);
+        const T c0 = fma(fy, c01 - c00, c00);
+        const T c1 = fma(fy, c11 - c10, c10);
+        val = fma(fz, c1 - c0, c0);
+      } else {
+        val = trilinear_g<T>(ref, N, qx, qy, qz);
+      }
+      out[((int64_t)z * N + y) * N + x] = val;
     }
-    out[((int64_t)z * N + y) * N + x] = val;
   }
 }
 
@@ -251,13 +244,19 @@ __global__ void __launch_bounds__(256) k_window_xy(const cplx_t<T>* __restrict__
                                                    int N, int W, cplx_t<T>* __restrict__ Y2) {
   extern __shared__ unsigned char smem_raw[];
   const int H = N / 2 + 1, wp = 2 * W + 3;
-  cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N]
-  cplx_t<T>* X = tw + N;                                   // [N][H]
+  cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N][wp]: e^{+2 pi i k t_a / N}, t_a = a - (W+1)
+  cplx_t<T>* X = tw + N * wp;                              // [N][H]
   cplx_t<T>* Y1 = X + N * H;                               // [N][wp]
+  cplx_t<T>* base = Y1 + N * wp;                           // [N]: e^{+2 pi i j / N}
   const int kz = blockIdx.x;
   const int64_t p = blockIdx.y;
   const int64_t plane = ((int64_t)p * N + kz) * N * H;
-  build_twiddles<T>(tw, N);
+  build_twiddles<T>(base, N);
+  __syncthreads();
+  for (int i = threadIdx.x; i < N * wp; i += blockDim.x) {
+    const int k = i / wp, t = i - k * wp - (W + 1);
+    tw[i] = base[(((k * t) % N) + N) % N];
+  }
   for (int i = threadIdx.x; i < N * H; i += blockDim.x) {
     const cplx_t<T> f = Fh[plane + i], r = Rh[plane + i];
     const int kx = i % H;
@@ -267,33 +266,23 @@ __global__ void __launch_bounds__(256) k_window_xy(const cplx_t<T>* __restrict__
   __syncthreads();
   for (int o = threadIdx.x; o < N * wp; o += blockDim.x) {
     const int ky = o / wp, a = o - ky * wp;
-    const int tx = a - (W + 1);
-    const int step = ((tx % N) + N) % N;
     const cplx_t<T>* xr = X + ky * H;
     T ar = T(0), ai = T(0);
-    int idx = 0;
     for (int kx = 0; kx < H; ++kx) {
-      const cplx_t<T> x = xr[kx], t = tw[idx];
+      const cplx_t<T> x = xr[kx], t = tw[kx * wp + a];
       ar = fma(x.x, t.x, fma(-x.y, t.y, ar));
       ai = fma(x.x, t.y, fma(x.y, t.x, ai));
-      idx += step;
-      if (idx >= N) idx -= N;
     }
     Y1[o] = mk<T>(ar, ai);
   }
   __syncthreads();
   for (int o = threadIdx.x; o < wp * wp; o += blockDim.x) {
     const int b = o / wp, a = o - b * wp;
-    const int ty = b - (W + 1);
-    const int step = ((ty % N) + N) % N;
     T ar = T(0), ai = T(0);
-    int idx = 0;
     for (int ky = 0; ky < N; ++ky) {
-      const cplx_t<T> y = Y1[ky * wp + a], t = tw[idx];
+      const cplx_t<T> y = Y1[ky * wp + a], t = tw[ky * wp + b];
       ar = fma(y.x, t.x, fma(-y.y, t.y, ar));
       ai = fma(y.x, t.y, fma(y.y, t.x, ai));
-      idx += step;
-      if (idx >= N) idx -= N;
     }
     Y2[((int64_t)p * N + kz) * wp * wp + o] = mk<T>(ar, ai);
   }
@@ -387,7 +376,8 @@ cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estri
   (void)n3;
   if (N % kRotTile) return cudaErrorInvalidValue;
   const int nt = N / kRotTile;
-  k_rotate_ref<T><<<dim3((unsigned)(nt * nt * nt), (unsigned)nb), 256, 0, s>>>(ref, N, euler, estride, rho);
+  k_rotate_ref<T><<<dim3((unsigned)std::min(nt * nt * nt, kRotCtas), (unsigned)nb), 256, 0, s>>>(ref, N, euler,
+                                                                                                  estride, rho);
   return cudaGetLastError();
 }
 
@@ -424,7 +414,7 @@ cudaError_t launch_window_pruned(const cplx_t<T>* Fh, const cplx_t<T>* Rh, int N
   if (nb == 0) return cudaSuccess;
   if (N > 512 || 2 * W + 3 > N) return cudaErrorInvalidValue;
   const int H = N / 2 + 1, wp = 2 * W + 3;
-  const size_t smem = sizeof(cplx_t<T>) * ((size_t)N + (size_t)N * H + (size_t)N * wp);
+  const size_t smem = sizeof(cplx_t<T>) * ((size_t)N * wp + (size_t)N * H + (size_t)N * wp + (size_t)N);
   cudaError_t e = cudaFuncSetAttribute(k_window_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // Y2 [nb][N][wp][wp] complex at the front of the scratch, the c windows [nb][wp^3] behind it

@@ -360,7 +360,7 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
               : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
   if (!fft_r2c(h, h->ws_rho, h->ws_Xhat, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT R2C of rho failed");
-  const size_t pr_smem = (size_t)h->rsz * 2 * ((size_t)N + (size_t)N * (N / 2 + 1) + (size_t)N * (2 * W + 3));
+  const size_t pr_smem = (size_t)h->rsz * 2 * ((size_t)N * (N / 2 + 1) + 2 * (size_t)N * (2 * W + 3) + (size_t)N);
   if (!h->trans_fft && pr_smem <= 227 * 1024 && 2 * W + 3 <= N) {
     // pruned inverse DFT on the window only (X = F^ conj(rho^) formed on chip, never stored)
     if (h->ws_win_W < W) {
