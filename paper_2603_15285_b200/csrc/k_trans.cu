@@ -97,12 +97,18 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
     const bool staged = dx <= kRotBox && dy <= kRotBox && dz <= kRotBox;  // always at kRotTile = 8 (<= 15)
     __syncthreads();  // previous tile's gathers are done with the box
     if (staged) {
-      const int nbx = dx * dy * dz;
-      for (int i = threadIdx.x; i < nbx; i += blockDim.x) {
-        const int ix = i % dx, iy = (i / dx) % dy, iz = i / (dx * dy);
-        const int x = ox + ix, y = oy + iy, z = oz + iz;
-        const bool in = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N;
-        box[(iz * kRotBox + iy) * kRotBox + ix] = in ? __ldg(ref + ((size_t)z * N + y) * N + x) : 0.f;
+      // one (y, x) slice of the box per pass: thread -> (iy, ix) = (tid / 16, tid % 16), no index division
+      const int ix = threadIdx.x & (kRotBox - 1), iy = threadIdx.x / kRotBox;
+      const int x = ox + ix, y = oy + iy;
+      const bool inxy = ix < dx && iy < dy;
+      const bool vxy = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N;
+      if (inxy && threadIdx.x < kRotBox * kRotBox) {
+        const float* src = ref + ((int64_t)y * N + x);
+        float* dst = box + iy * kRotBox + ix;
+        for (int iz = 0; iz < dz; ++iz) {
+          const int z = oz + iz;
+          dst[iz * kRotBox * kRotBox] = (vxy && (unsigned)z < (unsigned)N) ? __ldg(src + (int64_t)z * N * N) : 0.f;
+        }
       }
     }
     __syncthreads();
@@ -257,11 +263,28 @@ __global__ void __launch_bounds__(256) k_window_xy(const cplx_t<T>* __restrict__
     const int k = i / wp, t = i - k * wp - (W + 1);
     tw[i] = base[(((k * t) % N) + N) % N];
   }
-  for (int i = threadIdx.x; i < N * H; i += blockDim.x) {
-    const cplx_t<T> f = Fh[plane + i], r = Rh[plane + i];
-    const int kx = i % H;
-    const T wk = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
-    X[i] = mk<T>(wk * (f.x * r.x + f.y * r.y), wk * (f.y * r.x - f.x * r.y));  // w_kx F^ conj(rho^)
+  // four elements per thread per pass, all eight loads issued before the first use (the loads' latency, not the
+  // arithmetic, paced the one-element loop)
+  constexpr int kU = 4;
+  for (int i0 = threadIdx.x; i0 < N * H; i0 += kU * blockDim.x) {
+    cplx_t<T> f[kU], r[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < N * H) {
+        f[u] = Fh[plane + i];
+        r[u] = Rh[plane + i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < N * H) {
+        const int kx = i % H;
+        const T wk = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
+        X[i] = mk<T>(wk * (f[u].x * r[u].x + f[u].y * r[u].y), wk * (f[u].y * r[u].x - f[u].x * r[u].y));  // w F^ conj(rho^)
+      }
+    }
   }
   __syncthreads();
   for (int o = threadIdx.x; o < N * wp; o += blockDim.x) {
