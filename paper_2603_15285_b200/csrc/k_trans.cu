@@ -105,10 +105,17 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
       if (inxy && threadIdx.x < kRotBox * kRotBox) {
         const float* src = ref + ((int64_t)y * N + x);
         float* dst = box + iy * kRotBox + ix;
-        for (int iz = 0; iz < dz; ++iz) {
+        // all of the column's loads in flight before the first store (a load -> store loop serialised ~dz L2
+        // latencies per tile)
+        float col[kRotBox];
+#pragma unroll
+        for (int iz = 0; iz < kRotBox; ++iz) {
           const int z = oz + iz;
-          dst[iz * kRotBox * kRotBox] = (vxy && (unsigned)z < (unsigned)N) ? __ldg(src + (int64_t)z * N * N) : 0.f;
+          col[iz] = (iz < dz && vxy && (unsigned)z < (unsigned)N) ? __ldg(src + (int64_t)z * N * N) : 0.f;
         }
+#pragma unroll
+        for (int iz = 0; iz < kRotBox; ++iz)
+          if (iz < dz) dst[iz * kRotBox * kRotBox] = col[iz];
       }
     }
     __syncthreads();
