@@ -103,15 +103,16 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
       const bool inxy = ix < dx && iy < dy;
       const bool vxy = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N;
       if (inxy && threadIdx.x < kRotBox * kRotBox) {
-        const float* src = ref + ((int64_t)y * N + x);
         float* dst = box + iy * kRotBox + ix;
         // all of the column's loads in flight before the first store (a load -> store loop serialised ~dz L2
-        // latencies per tile)
+        // latencies per tile); 32-bit plane offsets (N^3 < 2^31), one pointer per column
+        const int NN = N * N;
+        const float* src = ref + (vxy ? y * N + x : 0);
         float col[kRotBox];
 #pragma unroll
         for (int iz = 0; iz < kRotBox; ++iz) {
           const int z = oz + iz;
-          col[iz] = (iz < dz && vxy && (unsigned)z < (unsigned)N) ? __ldg(src + (int64_t)z * N * N) : 0.f;
+          col[iz] = (iz < dz && vxy && (unsigned)z < (unsigned)N) ? __ldg(src + z * NN) : 0.f;
         }
 #pragma unroll
         for (int iz = 0; iz < kRotBox; ++iz)
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
       } else {
         val = trilinear_g<T>(ref, N, qx, qy, qz);
       }
-      out[((int64_t)z * N + y) * N + x] = val;
+      out[(z * N + y) * N + x] = val;
     }
   }
 }
@@ -253,7 +254,7 @@ __device__ __forceinline__ void build_twiddles(cplx_t<T>* tw, int N) {
 
 // grid (N, nb): block (kz, p) -> Y2[p][kz][w'][w']
 template <typename T>
-__global__ void __launch_bounds__(256) k_window_xy(const cplx_t<T>* __restrict__ Fh, const cplx_t<T>* __restrict__ Rh,
+__global__ void __launch_bounds__(512) k_window_xy(const cplx_t<T>* __restrict__ Fh, const cplx_t<T>* __restrict__ Rh,
                                                    int N, int W, cplx_t<T>* __restrict__ Y2) {
   extern __shared__ unsigned char smem_raw[];
   const int H = N / 2 + 1, wp = 2 * W + 3;
@@ -450,7 +451,7 @@ cudaError_t launch_window_pruned(const cplx_t<T>* Fh, const cplx_t<T>* Rh, int N
   // Y2 [nb][N][wp][wp] complex at the front of the scratch, the c windows [nb][wp^3] behind it
   cplx_t<T>* Y2 = reinterpret_cast<cplx_t<T>*>(scratch);
   T* cw = scratch + 2 * nb * (int64_t)N * wp * wp;
-  k_window_xy<T><<<dim3((unsigned)N, (unsigned)nb), 256, smem, s>>>(Fh, Rh, N, W, Y2);
+  k_window_xy<T><<<dim3((unsigned)N, (unsigned)nb), 512, smem, s>>>(Fh, Rh, N, W, Y2);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_window_z_peak<T><<<(unsigned)nb, 256, 0, s>>>(Y2, N, W, cw, shifts, sstride, peak);
   return cudaGetLastError();
