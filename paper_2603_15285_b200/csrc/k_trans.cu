@@ -94,9 +94,11 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
               oz = (int)floor(qcz - ez - T(1e-3));
     const int dx = (int)floor(qcx + ex + T(1e-3)) + 2 - ox, dy = (int)floor(qcy + ey + T(1e-3)) + 2 - oy,
               dz = (int)floor(qcz + ez + T(1e-3)) + 2 - oz;
-    const bool staged = dx <= kRotBox && dy <= kRotBox && dz <= kRotBox;  // always at kRotTile = 8 (<= 15)
+    // the box always fits: each extent is 2e + 3 + 0.002 <= 7 sqrt(3) + 3.002 < 16 voxels at kRotTile = 8, and by
+    // construction every voxel's corners floor(q) .. floor(q) + 1 lie inside it (static_assert below)
+    static_assert(kRotTile == 8 && kRotBox == 16, "box bound derived for 8^3 tiles");
     __syncthreads();  // previous tile's gathers are done with the box
-    if (staged) {
+    {
       // one (y, x) slice of the box per pass: thread -> (iy, ix) = (tid / 16, tid % 16), no index division
       const int ix = threadIdx.x & (kRotBox - 1), iy = threadIdx.x / kRotBox;
       const int x = ox + ix, y = oy + iy;
@@ -127,25 +129,20 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
       const T qx = fma(r0, ux, fma(r3, uy, r6 * uz)) + c;  // R^T v
       const T qy = fma(r1, ux, fma(r4, uy, r7 * uz)) + c;
       const T qz = fma(r2, ux, fma(r5, uy, r8 * uz)) + c;
-      T val;
       const T fx0 = floor(qx), fy0 = floor(qy), fz0 = floor(qz);
       const int bx = (int)fx0 - ox, by = (int)fy0 - oy, bz = (int)fz0 - oz;
-      if (staged && bx >= 0 && by >= 0 && bz >= 0 && bx + 1 < dx && by + 1 < dy && bz + 1 < dz) {
-        const T fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
-        const float* b0 = box + (bz * kRotBox + by) * kRotBox + bx;
-        const T c000 = b0[0], c001 = b0[1], c010 = b0[kRotBox], c011 = b0[kRotBox + 1];
-        const T c100 = b0[kRotBox * kRotBox], c101 = b0[kRotBox * kRotBox + 1];
-        const T c110 = b0[kRotBox * kRotBox + kRotBox], c111 = b0[kRotBox * kRotBox + kRotBox + 1];
-        const T c00 = fma(fx, c001 - c000, c000);
-        const T c01 = fma(fx, c011 - c010, c010);
-        const T c10 = fma(fx, c101 - c100, c100);
-        const T c11 = fma(fx, c111 - c110, c110);
-        const T c0 = fma(fy, c01 - c00, c00);
-        const T c1 = fma(fy, c11 - c10, c10);
-        val = fma(fz, c1 - c0, c0);
-      } else {
-        val = trilinear_g<T>(ref, N, qx, qy, qz);
-      }
+      const T fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
+      const float* b0 = box + (bz * kRotBox + by) * kRotBox + bx;
+      const T c000 = b0[0], c001 = b0[1], c010 = b0[kRotBox], c011 = b0[kRotBox + 1];
+      const T c100 = b0[kRotBox * kRotBox], c101 = b0[kRotBox * kRotBox + 1];
+      const T c110 = b0[kRotBox * kRotBox + kRotBox], c111 = b0[kRotBox * kRotBox + kRotBox + 1];
+      const T c00 = fma(fx, c001 - c000, c000);
+      const T c01 = fma(fx, c011 - c010, c010);
+      const T c10 = fma(fx, c101 - c100, c100);
+      const T c11 = fma(fx, c111 - c110, c110);
+      const T c0 = fma(fy, c01 - c00, c00);
+      const T c1 = fma(fy, c11 - c10, c10);
+      const T val = fma(fz, c1 - c0, c0);
       out[(z * N + y) * N + x] = val;
     }
   }
