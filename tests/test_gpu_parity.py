@@ -305,7 +305,8 @@ def test_invalid_arguments_rejected():
 
 
 # ------------------------------------------------------------------ stage 5: translation (App. C)
-@pytest.mark.parametrize("N,W,shift_mode", [(32, 4, gen.SHIFT_FIXED), (32, 3, gen.SHIFT_UNIFORM), (64, 8, gen.SHIFT_UNIFORM)])
+@pytest.mark.parametrize("N,W,shift_mode", [(32, 4, gen.SHIFT_FIXED), (32, 3, gen.SHIFT_UNIFORM), (64, 8, gen.SHIFT_UNIFORM),
+                                            (32, 8, gen.SHIFT_UNIFORM), (24, 6, gen.SHIFT_FIXED)])
 def test_translation_update_parity(N, W, shift_mode, prec):
     B = 4
     b = gen.particles(N, B, 1.0, seed=41, shift_mode=shift_mode, shift_max=W - 1.0, fixed_shift=(1.0, -2.0, 1.0))
@@ -320,6 +321,24 @@ def test_translation_update_parity(N, W, shift_mode, prec):
         assert np.abs(sh[p] - so).max() < (1e-6 if prec == "fp64" else 2e-3), (p, sh[p], so)
         assert abs(pk[p] - po) <= (1e-9 if prec == "fp64" else 1e-4) * abs(po)
         assert np.abs(sh[p] - b.truth_t[p]).max() < 0.6  # near the planted shift
+
+
+def test_translation_pruned_window_matches_full_c2r_at_c3_shape(monkeypatch):
+    """The pruned inverse DFT on the (2W+3)^3 window and the full cuFFT C2R + window read (MATCHA_TRANS_FFT=1)
+    evaluate the same circular correlation (C18): same integer peaks, subpixel shifts and peak values to FP32
+    rounding, at c3's 96^3 / W = 6 on a batch that spans several CTAs."""
+    N, W, B = 96, 6, 6
+    b = gen.particles(N, B, 0.05, seed=43, shift_mode=gen.SHIFT_UNIFORM, shift_max=4.0)
+    eul = cuda(np.array([O.matrix_to_euler(R) for R in b.truth_R]))
+    vols, ref = cuda(b.vols), cuda(b.ref)
+    sh_p, pk_p = handle(N, 8).translation_update(vols, ref, eul, W)
+    monkeypatch.setenv("MATCHA_TRANS_FFT", "1")
+    sh_f, pk_f = handle(N, 8).translation_update(vols, ref, eul, W)
+    sh_p, sh_f, pk_p, pk_f = to_np(sh_p), to_np(sh_f), to_np(pk_p), to_np(pk_f)
+    assert np.array_equal(np.round(sh_p), np.round(sh_f))
+    assert np.abs(sh_p - sh_f).max() < 2e-3
+    assert np.all(np.abs(pk_p - pk_f) <= 1e-4 * np.abs(pk_f))
+    assert np.abs(sh_p - b.truth_t).max() < 0.6
 
 
 def test_translation_integer_shifts_exact_gpu():
