@@ -84,8 +84,19 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
   const T ex = hE * (fabs(r0) + fabs(r3) + fabs(r6)), ey = hE * (fabs(r1) + fabs(r4) + fabs(r7)),
           ez = hE * (fabs(r2) + fabs(r5) + fabs(r8));
   T* out = rho + p * (int64_t)N * N * N;
-  for (int tile = blockIdx.x; tile < nt * nt * nt; tile += gridDim.x) {
-    const int tz = tile / (nt * nt), ty = (tile / nt) % nt, tx = tile % nt;
+  // tile coordinates advanced by gridDim.x with carries (no per-tile integer division)
+  int tx = blockIdx.x % nt, ty = (blockIdx.x / nt) % nt, tz = blockIdx.x / (nt * nt);
+  const int sx = gridDim.x % nt, sy = (gridDim.x / nt) % nt, sz = gridDim.x / (nt * nt);
+  for (; tz < nt; tx += sx, ty += sy, tz += sz) {
+    if (tx >= nt) {
+      tx -= nt;
+      ++ty;
+    }
+    if (ty >= nt) {
+      ty -= nt;
+      ++tz;
+    }
+    if (tz >= nt) break;
     // source box: image centre +- extent (+ margin against rounding), corners floor(q) .. floor(q) + 1
     const T vx = (T)tx * kRotTile + hE - c, vy = (T)ty * kRotTile + hE - c, vz = (T)tz * kRotTile + hE - c;
     const T qcx = fma(r0, vx, fma(r3, vy, r6 * vz)) + c, qcy = fma(r1, vx, fma(r4, vy, r7 * vz)) + c,
