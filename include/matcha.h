@@ -82,8 +82,9 @@ typedef struct {
   int32_t newton_iters;    /* M_iter Newton steps per band (default 1) */
   int32_t n_cand;          /* N_C candidates kept from the coarse search, 1..32 */
   int32_t oversample;      /* K, SO(3)-grid oversampling (default 2) */
-  int32_t n_alternations;  /* T rotation/translation alternations (App. C); 1 = rotation only */
-  int32_t shift_window;    /* W: translation search window [-W,W]^3 voxels; 0 = no translation update */
+  int32_t n_alternations;  /* T rotation/translation alternations (App. C); used only when
+                              shift_window > 0 (without a translation update one rotation pass is run) */
+  int32_t shift_window;    /* W: translation search window [-W,W]^3 voxels, W <= N/4; 0 = rotation only */
   double tol_grad;         /* early stop: ||grad|| < tol_grad*|C|; 0 = off */
   double tol_step;         /* early stop: ||delta|| < tol_step (rad); 0 = off */
   double tol_obj;          /* early stop: |dC| < tol_obj*|C|; 0 = off */

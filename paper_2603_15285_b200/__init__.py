@@ -120,7 +120,6 @@ class Params:
 def _ptr(t: Optional[torch.Tensor]):
     if t is None:
         return None
-    assert t.is_cuda and t.is_contiguous(), "device tensors must be contiguous CUDA tensors"
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -150,6 +149,26 @@ class Handle:
             _lib.matcha_destroy(h)
             self._h = None
 
+    def _arg(self, t: Optional[torch.Tensor], name: str, dtype, shape=None, optional: bool = False):
+        """Validate a tensor argument before its pointer crosses the C ABI: the library reads raw bytes, so a wrong
+        dtype (e.g. float64 angles handed to an FP32 handle), device, layout or shape would be reinterpreted
+        silently.  Raises TypeError / ValueError; returns the tensor."""
+        if t is None:
+            if optional:
+                return None
+            raise ValueError(f"{name} is required")
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+        if t.dtype != dtype:
+            raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+        if not t.is_cuda or t.device != self.device:
+            raise ValueError(f"{name} must live on {self.device}, got {t.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+        return t
+
     def _check(self, st, h=None):
         if st != MATCHA_OK:
             msg = _lib.matcha_last_error_string(h if h is not None else self._h).decode() if (
@@ -174,68 +193,96 @@ class Handle:
         return {name: (ms[i], n[i]) for i, name in enumerate(STAGES) if n[i] > 0}
 
     # ---------------------------------------------------------------- stages
+    def _vols(self, vols: torch.Tensor, name: str = "vols") -> int:
+        if not isinstance(vols, torch.Tensor) or vols.dim() != 4:
+            raise ValueError(f"{name} must be a [B, N, N, N] tensor")
+        self._arg(vols, name, torch.float32, (vols.shape[0], self.N, self.N, self.N))
+        return vols.shape[0]
+
     def sh_analysis(self, vols: torch.Tensor, shifts: Optional[torch.Tensor] = None, out=None) -> torch.Tensor:
-        B = vols.shape[0]
-        assert vols.dtype == torch.float32 and tuple(vols.shape[1:]) == (self.N,) * 3
+        B = self._vols(vols)
+        shape = (B, ncoef(self.L_max), self.R)
         if out is None:
-            out = torch.empty((B, ncoef(self.L_max), self.R), dtype=self.cplx, device=vols.device)
-        if shifts is not None:
-            assert shifts.dtype == self.real and tuple(shifts.shape) == (B, 3)
+            out = torch.empty(shape, dtype=self.cplx, device=self.device)
+        self._arg(out, "out", self.cplx, shape)
+        self._arg(shifts, "shifts", self.real, (B, 3), optional=True)
         self._check(_lib.matcha_sh_analysis(self._h, _ptr(vols), B, _ptr(shifts), _ptr(out), _stream()))
         return out
 
     def corr_coeffs(self, f: torch.Tensor, href: torch.Tensor, L: Optional[int] = None, out=None) -> torch.Tensor:
         L = self.L_max if L is None else L
         B = f.shape[0]
-        assert f.dtype == self.cplx and href.dtype == self.cplx
+        self._arg(f, "f", self.cplx, (B, ncoef(self.L_max), self.R))
+        self._arg(href, "href", self.cplx, (ncoef(self.L_max), self.R))
         if out is None:
-            out = torch.empty((B, corr_count(L)), dtype=self.cplx, device=f.device)
+            out = torch.empty((B, corr_count(L)), dtype=self.cplx, device=self.device)
+        self._arg(out, "out", self.cplx, (B, corr_count(L)))
         self._check(_lib.matcha_corr_coeffs(self._h, _ptr(f), _ptr(href), B, L, _ptr(out), _stream()))
         return out
 
+    def _M(self, M: torch.Tensor, L_M: int) -> int:
+        if not isinstance(M, torch.Tensor) or M.dim() != 2:
+            raise ValueError("M must be a [B, Mh(L_M)] tensor")
+        self._arg(M, "M", self.cplx, (M.shape[0], corr_count(L_M)))
+        return M.shape[0]
+
     def so3_search(self, M: torch.Tensor, L_M: int, L0: int, oversample: int = 2, n_cand: int = 10):
-        B = M.shape[0]
-        euler = torch.empty((B, n_cand, 3), dtype=self.real, device=M.device)
-        score = torch.empty((B, n_cand), dtype=self.real, device=M.device)
-        idx = torch.empty((B, n_cand), dtype=torch.int32, device=M.device)
+        B = self._M(M, L_M)
+        euler = torch.empty((B, n_cand, 3), dtype=self.real, device=self.device)
+        score = torch.empty((B, n_cand), dtype=self.real, device=self.device)
+        idx = torch.empty((B, n_cand), dtype=torch.int32, device=self.device)
         self._check(_lib.matcha_so3_search(self._h, _ptr(M), L_M, B, L0, oversample, n_cand, _ptr(euler),
                                            _ptr(score), _ptr(idx), _stream()))
         return euler, score, idx
 
     def eval_corr(self, M: torch.Tensor, L_M: int, L: int, euler: torch.Tensor, derivs: bool = True):
-        B, Q = euler.shape[0], euler.shape[1]
-        val = torch.empty((B, Q), dtype=self.real, device=M.device)
-        grad = torch.empty((B, Q, 3), dtype=self.real, device=M.device) if derivs else None
-        hess = torch.empty((B, Q, 6), dtype=self.real, device=M.device) if derivs else None
-        self._check(_lib.matcha_eval_corr(self._h, _ptr(M), L_M, B, Q, L, _ptr(euler.contiguous()), _ptr(val),
+        B = self._M(M, L_M)
+        if not isinstance(euler, torch.Tensor) or euler.dim() != 3:
+            raise ValueError("euler must be a [B, Q, 3] tensor")
+        Q = euler.shape[1]
+        self._arg(euler, "euler", self.real, (B, Q, 3))
+        val = torch.empty((B, Q), dtype=self.real, device=self.device)
+        grad = torch.empty((B, Q, 3), dtype=self.real, device=self.device) if derivs else None
+        hess = torch.empty((B, Q, 6), dtype=self.real, device=self.device) if derivs else None
+        self._check(_lib.matcha_eval_corr(self._h, _ptr(M), L_M, B, Q, L, _ptr(euler), _ptr(val),
                                           _ptr(grad), _ptr(hess), _stream()))
         return val, grad, hess
 
     def newton_refine(self, M: torch.Tensor, L_M: int, euler: torch.Tensor, params: Params,
                       grid_idx: Optional[torch.Tensor] = None):
-        B, Q = euler.shape[0], euler.shape[1]
-        euler = euler.clone().contiguous()
-        score = torch.empty((B, Q), dtype=self.real, device=M.device)
-        best = torch.empty((B,), dtype=torch.int32, device=M.device)
+        B = self._M(M, L_M)
+        if not isinstance(euler, torch.Tensor) or euler.dim() != 3:
+            raise ValueError("euler must be a [B, n_cand, 3] tensor")
+        Q = euler.shape[1]
+        self._arg(euler, "euler", self.real, (B, Q, 3))
+        self._arg(grid_idx, "grid_idx", torch.int32, (B, Q), optional=True)
+        euler = euler.clone()
+        score = torch.empty((B, Q), dtype=self.real, device=self.device)
+        best = torch.empty((B,), dtype=torch.int32, device=self.device)
         p = params.c()
         self._check(_lib.matcha_newton_refine(self._h, _ptr(M), L_M, B, Q, ctypes.byref(p), _ptr(euler),
                                               _ptr(grid_idx), _ptr(score), _ptr(best), _stream()))
         return euler, score, best
 
     def translation_update(self, vols: torch.Tensor, ref: torch.Tensor, euler: torch.Tensor, window: int):
-        B = vols.shape[0]
-        shifts = torch.empty((B, 3), dtype=self.real, device=vols.device)
-        peak = torch.empty((B,), dtype=self.real, device=vols.device)
-        self._check(_lib.matcha_translation_update(self._h, _ptr(vols), B, _ptr(ref), _ptr(euler.contiguous()),
+        B = self._vols(vols)
+        self._arg(ref, "ref", torch.float32, (self.N, self.N, self.N))
+        self._arg(euler, "euler", self.real, (B, 3))
+        shifts = torch.empty((B, 3), dtype=self.real, device=self.device)
+        peak = torch.empty((B,), dtype=self.real, device=self.device)
+        self._check(_lib.matcha_translation_update(self._h, _ptr(vols), B, _ptr(ref), _ptr(euler),
                                                    window, _ptr(shifts), _ptr(peak), _stream()))
         return shifts, peak
 
     def align_batch(self, vols: torch.Tensor, ref: Optional[torch.Tensor], params: Params,
                     ref_coeffs: Optional[torch.Tensor] = None, out=None) -> torch.Tensor:
         """poses [B, 8] = (alpha, beta, gamma, t_x, t_y, t_z, score, best_cand)."""
-        B = vols.shape[0]
+        B = self._vols(vols)
+        self._arg(ref, "ref", torch.float32, (self.N, self.N, self.N), optional=True)
+        self._arg(ref_coeffs, "ref_coeffs", self.cplx, (ncoef(self.L_max), self.R), optional=True)
         if out is None:
-            out = torch.empty((B, 8), dtype=self.real, device=vols.device)
+            out = torch.empty((B, 8), dtype=self.real, device=self.device)
+        self._arg(out, "out", self.real, (B, 8))
         p = params.c()
         self._check(_lib.matcha_align_batch(self._h, _ptr(vols), B, _ptr(ref), _ptr(ref_coeffs), ctypes.byref(p),
                                             _ptr(out), _stream()))
@@ -244,10 +291,20 @@ class Handle:
     def align_batch_host(self, vols_host: torch.Tensor, ref_host: torch.Tensor, params: Params,
                          out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """End-to-end on host (ideally pinned) buffers: H2D chunks overlapped with compute; syncs."""
+        n3 = (self.N,) * 3
+
+        def host(t, name, dtype, shape):
+            if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_contiguous() or t.dtype != dtype:
+                raise TypeError(f"{name} must be a contiguous host {dtype} tensor")
+            if tuple(t.shape) != tuple(shape):
+                raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
         B = vols_host.shape[0]
-        assert not vols_host.is_cuda and vols_host.is_contiguous() and vols_host.dtype == torch.float32
+        host(vols_host, "vols_host", torch.float32, (B,) + n3)
+        host(ref_host, "ref_host", torch.float32, n3)
         if out is None:
             out = torch.empty((B, 8), dtype=self.real, pin_memory=True)
+        host(out, "out", self.real, (B, 8))
         p = params.c()
         self._check(_lib.matcha_align_batch_host(self._h, ctypes.c_void_p(vols_host.data_ptr()), B,
                                                  ctypes.c_void_p(ref_host.data_ptr()), ctypes.byref(p),

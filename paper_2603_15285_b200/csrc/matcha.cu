@@ -404,8 +404,8 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
     if (st != MATCHA_OK) return st;
     H = h->ws_H;
   }
-  const int T = p->n_alternations;
   const bool translate = p->shift_window > 0;
+  const int T = translate ? p->n_alternations : 1;  // without a translation update the T passes are identical
   for (int64_t c0 = 0; c0 < B; c0 += h->cfg.max_batch) {
     const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
     char* pc = (char*)poses + c0 * 8 * h->rsz;
@@ -806,6 +806,9 @@ MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const floa
     return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch_host: bad arguments");
   std::string why;
   if (!valid_params(params, h->L, why)) return fail(h, MATCHA_ERR_CUTOFF, "align_batch_host: " + why);
+  if (params->shift_window > h->cfg.N / 4) return fail(h, MATCHA_ERR_WINDOW, "align_batch_host: W > N/4");
+  if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch_host: coarse grid too large for one CTA");
   cudaStream_t s = (cudaStream_t)stream;
   const int N = h->cfg.N;
   const int64_t n3 = (int64_t)N * N * N, mb = h->cfg.max_batch;

@@ -64,7 +64,8 @@ def align_step(handle, vols_local: torch.Tensor, ref: torch.Tensor, params, H: t
     if rank == 0:
         handle.sh_analysis(ref[None], out=H[None])
     broadcast_ref_coeffs(H, src=0, group=group)
-    translate = getattr(params, "n_alternations", 1) > 1
+    # the library translates iff shift_window > 0 (include/matcha.h, matcha_params_t.shift_window)
+    translate = getattr(params, "shift_window", 0) > 0
     if translate:
         # the translation update (App. C) rotates the reference volume itself: rank 0's copy goes to every rank
         broadcast_ref_coeffs(ref, src=0, group=group)

@@ -33,6 +33,9 @@ class FakeHandle:
         return out
 
     def align_batch(self, vols, ref, params, ref_coeffs=None):
+        # the library's contract: a translation update (shift_window > 0) needs the reference volume
+        if params is not None and params.shift_window > 0 and ref is None:
+            raise RuntimeError("matcha WINDOW: shift window needs ref")
         n = vols.shape[0]
         poses = torch.zeros((n, 8), dtype=torch.float32)
         poses[:, 0] = vols.reshape(n, -1)[:, 0]          # global particle id planted in voxel 0
@@ -50,11 +53,12 @@ def _free_port():
 
 
 class _Params:
-    def __init__(self, T):
+    def __init__(self, T, W):
         self.n_alternations = T
+        self.shift_window = W
 
 
-def _worker(rank, world, port, P, q, T=1):
+def _worker(rank, world, port, P, q, T=1, W=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -62,10 +66,10 @@ def _worker(rank, world, port, P, q, T=1):
         a, b = D.shard(P, world, rank)
         vols = torch.zeros((b - a, 4, 4, 4))
         vols.reshape(b - a, -1)[:, 0] = torch.arange(a, b, dtype=torch.float32)
-        # rank 1 starts with another reference volume: with translation (T > 1) it must receive rank 0's
+        # rank 1 starts with another reference volume: with translation (W > 0) it must receive rank 0's
         ref = torch.full((4, 4, 4), 0.5 if rank == 0 else 9.0)
         H = torch.zeros((3, 2), dtype=torch.complex64)  # rank 1 starts with zeros: must receive rank 0's
-        poses = D.align_step(FakeHandle(), vols, ref, _Params(T) if T else None, H, rank)
+        poses = D.align_step(FakeHandle(), vols, ref, _Params(T, W) if T else None, H, rank)
         t = D.max_over_ranks(float(rank + 1))
         # plain Python values only: a tensor would travel as a shared-memory handle that dies with this process
         q.put((rank, poses[:, 0].tolist(), poses[:, 6].tolist(), torch.view_as_real(H).tolist(), t,
@@ -74,12 +78,14 @@ def _worker(rank, world, port, P, q, T=1):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("P,T", [(10, 0), (7, 1), (7, 3)])
-def test_align_step_world2_gloo(P, T):
+@pytest.mark.parametrize("P,T,W", [(10, 0, 0), (7, 1, 0), (7, 3, 2), (7, 1, 2), (7, 3, 0)])
+def test_align_step_world2_gloo(P, T, W):
+    """The translation predicate is the library's (shift_window > 0), not n_alternations > 1: T=1 with W>0 still
+    translates (the reference volume is broadcast), T>1 with W=0 is rotation only."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, P, q, T)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, P, q, T, W)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(2)]
@@ -94,4 +100,4 @@ def test_align_step_world2_gloo(P, T):
         assert all(abs(c - float(torch.view_as_real(expect_H).sum())) < 1e-3 for c in checks)
         assert t == 2.0                                             # max over ranks
         # rotation only: no reference volume is passed; translating: rank 0's volume on every rank
-        assert refsum == [-1.0 if T <= 1 else 0.5 * 64] * P
+        assert refsum == [-1.0 if (not T or W == 0) else 0.5 * 64] * P

@@ -323,23 +323,59 @@ def test_translation_update_parity(N, W, shift_mode, prec):
         assert np.abs(sh[p] - b.truth_t[p]).max() < 0.6  # near the planted shift
 
 
-def test_translation_pruned_window_matches_full_c2r_at_c3_shape(monkeypatch):
-    """The pruned inverse DFT on the (2W+3)^3 window and the full cuFFT C2R + window read (MATCHA_TRANS_FFT=1)
-    evaluate the same circular correlation (C18): same integer peaks, subpixel shifts and peak values to FP32
-    rounding, at c3's 96^3 / W = 6 on a batch that spans several CTAs."""
+def test_translation_c3_shape_vs_oracle_and_truth():
+    """c3's 96^3 / W = 6 at SNR 0.05 on a batch that spans several CTAs, at the TRUE rotations (FP32 angles, the
+    handle's precision): the shifts recover the planted U[-4,4]^3 shifts (< 0.6 voxel), and 2 particles are
+    compared with the oracle's direct windowed correlation (App. C; reading C18).  (Round 1 fed float64
+    angles to the FP32 handle here; the binding now rejects that, see test_binding_rejects_wrong_dtypes.)"""
     N, W, B = 96, 6, 6
     b = gen.particles(N, B, 0.05, seed=43, shift_mode=gen.SHIFT_UNIFORM, shift_max=4.0)
-    eul = cuda(np.array([O.matrix_to_euler(R) for R in b.truth_R]))
-    vols, ref = cuda(b.vols), cuda(b.ref)
-    sh_p, pk_p = handle(N, 8).translation_update(vols, ref, eul, W)
-    monkeypatch.setenv("MATCHA_TRANS_FFT", "1")
-    sh_f, pk_f = handle(N, 8).translation_update(vols, ref, eul, W)
-    sh_p, sh_f, pk_p, pk_f = to_np(sh_p), to_np(sh_f), to_np(pk_p), to_np(pk_f)
-    assert np.array_equal(np.round(sh_p), np.round(sh_f))
-    assert np.abs(sh_p - sh_f).max() < 2e-3
-    assert np.all(np.abs(pk_p - pk_f) <= 1e-4 * np.abs(pk_f))
-    # (no ground-truth check: at SNR 0.05 the whole-box correlation of one particle is noise-dominated; the
-    # alternation tests check recovery)
+    h = handle(N, 8)
+    eul = np.array([O.matrix_to_euler(R) for R in b.truth_R])
+    sh, pk = h.translation_update(cuda(b.vols), cuda(b.ref), cuda(eul, h.real), W)
+    sh, pk = to_np(sh), to_np(pk)
+    assert np.abs(sh - b.truth_t).max() < 0.6, np.abs(sh - b.truth_t).max()
+    eul_used = to_np(cuda(eul, h.real)).astype(np.float64)
+    for p in (0, 4):
+        so, po = O.translation(b.vols[p], b.ref, eul_used[p], W)
+        assert np.abs(sh[p] - so).max() < 2e-3, (p, sh[p], so)
+        assert abs(pk[p] - po) <= 1e-4 * abs(po)
+
+
+def test_binding_rejects_wrong_dtypes():
+    """Tensors cross the C ABI as raw pointers: the binding must refuse a float64 tensor handed to an FP32 handle
+    (and wrong shapes / devices / int64 indices) instead of letting the kernel reinterpret its bytes."""
+    N = 32
+    h = handle(N, 8)
+    vols = torch.zeros((2, N, N, N), device=DEV)
+    ref = torch.zeros((N, N, N), device=DEV)
+    with pytest.raises(TypeError):
+        h.translation_update(vols, ref, torch.zeros((2, 3), dtype=torch.float64, device=DEV), 4)
+    with pytest.raises(ValueError):
+        h.translation_update(vols, ref, torch.zeros((2, 4), device=DEV), 4)
+    with pytest.raises(ValueError):
+        h.translation_update(vols, ref.cpu(), torch.zeros((2, 3), device=DEV), 4)
+    M = torch.zeros((2, mt.corr_count(8)), dtype=torch.complex64, device=DEV)
+    with pytest.raises(TypeError):
+        h.eval_corr(M, 8, 8, torch.zeros((2, 3, 3), dtype=torch.float64, device=DEV))
+    with pytest.raises(TypeError):
+        h.newton_refine(M, 8, torch.zeros((2, 4, 3), device=DEV), mt.Params(bands=[4, 8], n_cand=4),
+                        grid_idx=torch.zeros((2, 4), dtype=torch.int64, device=DEV))
+    with pytest.raises(TypeError):
+        h.eval_corr(M.to(torch.complex128), 8, 8, torch.zeros((2, 3, 3), device=DEV))
+    with pytest.raises(TypeError):
+        h.align_batch(vols.double(), ref, mt.Params(bands=[4, 8], n_cand=4))
+    with pytest.raises(TypeError):
+        h.align_batch(vols, ref, mt.Params(bands=[4, 8], n_cand=4),
+                      ref_coeffs=torch.zeros((mt.ncoef(8), N // 2), dtype=torch.complex128, device=DEV))
+    with pytest.raises(TypeError):
+        h.sh_analysis(vols, torch.zeros((2, 3), dtype=torch.float64, device=DEV))
+    h64 = handle(N, 8, "fp64")
+    with pytest.raises(TypeError):
+        h64.translation_update(vols, ref, torch.zeros((2, 3), dtype=torch.float32, device=DEV), 4)
+    with pytest.raises(mt.MatchaError):  # W > N/4 (SPEC WindowTooLarge)
+        h.align_batch_host(torch.zeros((2, N, N, N)), torch.zeros((N, N, N)),
+                           mt.Params(bands=[4, 8], n_cand=4, n_alternations=2, shift_window=N // 4 + 1))
 
 
 def test_translation_integer_shifts_exact_gpu():
