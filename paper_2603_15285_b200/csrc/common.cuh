@@ -84,8 +84,6 @@ template <typename T> struct NewtonArgs {
   double tol_grad, tol_step, tol_obj;
   T* score;
   int32_t* best;
-  int qsplit;            // CTAs per particle (candidate groups of CG); > 1: FP64 final scores to cfinal, argmax later
-  double* cfinal;        // [B][Q] FP64 C_{L_J} of every candidate (-inf = inactive), used when qsplit > 1
   const PairDesc* pairs;
   const T* pair_lnc;
   int* flags;

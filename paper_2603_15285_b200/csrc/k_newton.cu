@@ -379,17 +379,14 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
 }
 
 // ------------------------------------------------------------------ matcha_newton_refine kernel
-// One CTA per (particle, group of up to CG candidates) when a.qsplit > 1 (more, smaller CTAs: the last wave of
-// the grid is fuller); the candidates are independent, so the result equals the one-CTA-per-particle run.
+// One CTA per particle: all of its candidates share every read of M (ALU-bound, not HBM-bound).
 template <typename T, int CG>
 __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1) k_newton_refine(NewtonArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int QT = a.Q, G = a.qsplit;
-  const int64_t p = blockIdx.x / G;
-  const int q0 = (int)(blockIdx.x % G) * ((QT + G - 1) / G);
-  const int Q = min(QT - q0, (QT + G - 1) / G);  // candidates of this CTA: q0 .. q0 + Q - 1
+  const int Q = a.Q;
+  const int64_t p = blockIdx.x;
   const int Lmax_b = a.bands[a.nbands - 1];
-  const SmemLayout lay = smem_layout<T>((QT + G - 1) / G, Lmax_b, CG);
+  const SmemLayout lay = smem_layout<T>(Q, Lmax_b, CG);
   double* theta = (double*)(smem + lay.theta);
   CandShared<T>* cs = (CandShared<T>*)(smem + lay.cand);
   cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
@@ -403,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   int* run = act + Q;                    // [Q] still iterating in this band
   int* any = run + Q;                    // [1]
   const cplx_t<T>* M = a.M + p * a.strideM;
-  const int64_t cb0 = p * QT + q0;       // global index of this CTA's first candidate
+  const int64_t cb0 = p * Q;             // global index of this particle's first candidate
   for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) theta[t] = (double)a.euler[cb0 * 3 + t];
   for (int c = threadIdx.x; c < Q; c += blockDim.x) act[c] = a.idx ? (a.idx[cb0 + c] >= 0) : 1;
   load_inv_tables(inv_l, inv_ll);
@@ -458,10 +455,9 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   for (int c = threadIdx.x; c < Q; c += blockDim.x) {
     const double v = act[c] ? sums[c * 10] : -INFINITY;
     a.score[cb0 + c] = (T)v;
-    if (G > 1) a.cfinal[cb0 + c] = v;
     if (act[c] && !isfinite(v)) atomicOr(a.flags, FLAG_NONFINITE);
   }
-  if (G == 1 && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     int b = -1;
     double bv = -INFINITY;
     for (int c = 0; c < Q; ++c)
@@ -473,24 +469,6 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   }
 }
 
-// argmax over the FP64 final scores when the candidates were split over CTAs (first maximum: reading C23)
-__global__ void k_best_of(const double* __restrict__ cfinal, const int32_t* __restrict__ idx, int64_t B, int Q,
-                          int32_t* __restrict__ best) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= B) return;
-  int b = -1;
-  double bv = -INFINITY;
-  for (int c = 0; c < Q; ++c) {
-    const bool act = idx ? idx[p * Q + c] >= 0 : true;
-    const double v = cfinal[p * Q + c];
-    if (act && (b < 0 || v > bv)) {
-      b = c;
-      bv = v;
-    }
-  }
-  best[p] = b;
-}
-
 template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a, bool derivs, cudaStream_t s) {
   const SmemLayout lay = smem_layout<T>(a.Q, a.L_eval, CG);
   cudaError_t e = cudaFuncSetAttribute(k_eval_corr<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
@@ -499,19 +477,12 @@ template <typename T, int CG> cudaError_t launch_eval_cg(const NewtonArgs<T>& a,
   return cudaGetLastError();
 }
 
-template <typename T, int CG> cudaError_t launch_newton_cg(NewtonArgs<T> a, cudaStream_t s) {
-  // optionally split the candidates over ceil(Q / CG) CTAs per particle (MATCHA_NEWTON_SPLIT; measured slower at c2:
-  // 0.93 vs 0.89 ms -- the duplicated per-CTA band setup outweighs the fuller last wave)
-  const int G = (a.cfinal && a.Q > CG && getenv("MATCHA_NEWTON_SPLIT")) ? (a.Q + CG - 1) / CG : 1;
-  a.qsplit = G;
-  const SmemLayout lay = smem_layout<T>((a.Q + G - 1) / G, a.bands[a.nbands - 1], CG);
+template <typename T, int CG> cudaError_t launch_newton_cg(const NewtonArgs<T>& a, cudaStream_t s) {
+  const SmemLayout lay = smem_layout<T>(a.Q, a.bands[a.nbands - 1], CG);
   cudaError_t e =
       cudaFuncSetAttribute(k_newton_refine<T, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
   if (e != cudaSuccess) return e;
-  k_newton_refine<T, CG><<<(unsigned)(a.B * G), kThreads, lay.total, s>>>(a);
-  e = cudaGetLastError();
-  if (e != cudaSuccess || G == 1) return e;
-  k_best_of<<<(unsigned)((a.B + 127) / 128), 128, 0, s>>>(a.cfinal, a.idx, a.B, a.Q, a.best);
+  k_newton_refine<T, CG><<<(unsigned)a.B, kThreads, lay.total, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -520,7 +491,6 @@ template <typename T> int pick_cg(int Q) {
   if (sizeof(T) == 8) return Q >= 2 ? 2 : 1;
   if (Q <= 2) return Q;
   if (Q <= 4) return 4;
-  if (Q == 10 && getenv("MATCHA_NEWTON_CG10")) return 10;
   if (Q % 5 == 0 || Q == 9) return 5;
   return 4;
 }
@@ -533,7 +503,6 @@ template <typename T> cudaError_t launch_eval_corr(const NewtonArgs<T>& a, bool 
     case 1: return launch_eval_cg<T, 1>(a, derivs, s);
     case 2: return launch_eval_cg<T, 2>(a, derivs, s);
     case 4: return launch_eval_cg<T, 4>(a, derivs, s);
-    case 10: return launch_eval_cg<T, 10>(a, derivs, s);
     default: return launch_eval_cg<T, 5>(a, derivs, s);
   }
 }
@@ -544,7 +513,6 @@ template <typename T> cudaError_t launch_newton_refine(const NewtonArgs<T>& a, c
     case 1: return launch_newton_cg<T, 1>(a, s);
     case 2: return launch_newton_cg<T, 2>(a, s);
     case 4: return launch_newton_cg<T, 4>(a, s);
-    case 10: return launch_newton_cg<T, 10>(a, s);
     default: return launch_newton_cg<T, 5>(a, s);
   }
 }

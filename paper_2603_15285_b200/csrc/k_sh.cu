@@ -941,9 +941,8 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
   if (tab.R % 8 == 0 && leg_full_bytes<T>(8, tab.nth, tab.L) + wtab <= 220 * 1024) lsg = 8;
   else if (tab.R % 4 == 0 && leg_full_bytes<T>(4, tab.nth, tab.L) <= 110 * 1024) lsg = 4;
   else if (tab.R % 2 == 0 && leg_full_bytes<T>(2, tab.nth, tab.L) <= 200 * 1024) lsg = 2;
-  if (getenv("MATCHA_LEG_OLD")) lsg = 0;
   const bool lpers = sizeof(T) == 4 && tab.R % kLegSG == 0 && leg_tiles_par(tab.L) <= kLegLaneThreads &&
-                     leg_pers_bytes<T>(tab) <= 226 * 1024 && !getenv("MATCHA_LEG_NOPERS");
+                     leg_pers_bytes<T>(tab) <= 226 * 1024;
   if (lpers) {
     e = cudaFuncSetAttribute(k_sh_legendre_pers<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)leg_pers_bytes<T>(tab));

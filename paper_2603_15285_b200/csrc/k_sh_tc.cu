@@ -1,25 +1,29 @@
 // k_sh_tc.cu -- stage 1 (shell SH analysis), ring sampling + ring DFT with the DFT on the 5th-generation tensor
-// cores (tcgen05, kind::tf32 3-pass split, TMEM operands), FP32 handles.
+// cores (tcgen05.mma kind::f16, fp16 hi/lo split, A operand in TMEM), FP32 handles.
 //
 // north_star stage (1); readings C2-C5:
 //   G_ijm = (2 pi / n_phi) sum_k u(c + t + r_i w_jk) e^{-i m phi_k}     (ring (i, j): shell r_i, polar node theta_j)
-// followed by the Legendre contraction f_lm(r_i) = sum_j W_j Pbar_lm(x_j) G_ijm (k_sh_legendre in k_sh.cu).
+// followed by the Legendre contraction f_lm(r_i) = sum_j W_j Pbar_lm(x_j) G_ijm (k_sh_legendre_pers in k_sh.cu).
 //
 // The ring DFT is a dense real contraction  D[o][ring] = sum_k A[o][k] S[ring][k]  with o = 2m + (0: Re, 1: Im),
-// A[2m][k] = (2 pi / n_phi) cos(m phi_k), A[2m+1][k] = -(2 pi / n_phi) sin(m phi_k), S = the ring samples.  It runs as
-// tcgen05.mma with M = 128 DFT rows (2(L+1) <= 128 used), N = 32 rings, K = n_phi (padded to a multiple of 8):
-//   A_hi, A_lo  in TMEM (written once per CTA; constant),
-//   S_hi, S_lo  in shared memory (K-major, SWIZZLE_NONE; the K-chunk stride is padded by 16 B so that a warp's 32
-//               consecutive-k stores along one ring hit 32 different banks), double-buffered,
-//   D           in TMEM (double-buffered), read back with tcgen05.ld: TMEM lane o = output row, column = ring; lane o
-//               of a warp stores G[ring][o] -> 32 consecutive floats per ring (coalesced).
+// A[2m][k] = (2 pi / n_phi) cos(m phi_k), A[2m+1][k] = -(2 pi / n_phi) sin(m phi_k), S = the ring samples (folded
+// over the real-data symmetry to Kh + 1 k-columns per parity class).  It runs as tcgen05.mma with M = 128 DFT rows
+// (2(L+1) <= 128 used), N = 64 rings per tile, K-steps of 16 fp16:
+//   A_hi, A_lo  the DFT matrix x 2^10 split into fp16 hi + lo, in TMEM (written once per CTA; constant),
+//   S_hi, S_lo  each ring's samples scaled by a power of two and split into fp16 hi + lo, in shared memory
+//               (K-major, SWIZZLE_NONE; the K-chunk stride is padded by 16 B so that a warp's consecutive-k stores
+//               along one ring hit different banks), double-buffered,
+//   D           FP32 accumulator in TMEM (double-buffered), read back with tcgen05.ld: TMEM lane o = output row,
+//               column = ring; lane o of a warp stores G[ring][o] (coalesced), undoing the two scales.
 //   D = A_hi S_hi + A_hi S_lo + A_lo S_hi  (FP32-level accuracy; lo*lo dropped).
+// The MMAs are issued by a dedicated warp (kThr sampler threads + 1 MMA warp), so the ~1.7 k issue cycles per tile
+// overlap the sampling of the next tile.
 //
 // Persistent CTAs (one per SM) take whole particles.  Per particle the rings are sorted by the plane index of their
-// z (deterministic counting sort), so consecutive tiles of 32 rings need a small window of z-planes (max span ~6 at
-// 64^3): the planes live in a P-slot ring buffer in shared memory, prefetched one tile ahead with cp.async (the
-// particle crosses HBM once).  Per tile: sample (trilinear from shared memory) -> S[buf]; one thread issues the
-// 3 x K/8 MMAs into D[buf]; meanwhile the CTA drains D[buf^1] of the previous tile and samples the next one.
+// z (deterministic counting sort), so consecutive tiles of 64 rings need a small window of z-planes: the planes live
+// in a P-slot ring buffer in shared memory, prefetched one tile ahead with cp.async (the particle crosses HBM once).
+// Per tile: sample (trilinear from shared memory) -> S[buf]; the MMA warp issues 3 x K/16 MMAs into D[buf];
+// meanwhile the CTA drains D[buf^1] of the previous tile and samples the next one.
 // Deterministic: fixed summation orders, no atomics on data.
 #include <algorithm>
 #include <climits>

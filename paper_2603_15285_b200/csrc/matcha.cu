@@ -48,7 +48,6 @@ struct matcha_ctx {
   void* ws_score = nullptr;
   int32_t* ws_idx = nullptr;
   int32_t* ws_best = nullptr;
-  double* ws_cfinal = nullptr;  // [max_batch][kMaxCand] FP64 final scores (stage 4 split over CTAs)
   // host-buffer path
   float* ws_vols[2] = {nullptr, nullptr};
   void* ws_poses = nullptr;
@@ -289,8 +288,6 @@ static cudaError_t do_refine(matcha_handle_t h, const void* M, int32_t L_M, int6
   a.tol_obj = p->tol_obj;
   a.score = (T*)score;
   a.best = best;
-  a.qsplit = 1;
-  a.cfinal = (B <= h->cfg.max_batch) ? h->ws_cfinal : nullptr;
   return launch_newton_refine<T>(a, s);
 }
 
@@ -591,7 +588,6 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   if (e == cudaSuccess) e = cudaMalloc(&h->ws_score, h->rsz * mb * kMaxCand);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->ws_idx, sizeof(int32_t) * mb * kMaxCand);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->ws_best, sizeof(int32_t) * mb);
-  if (e == cudaSuccess) e = cudaMalloc((void**)&h->ws_cfinal, sizeof(double) * mb * kMaxCand);
   if (e != cudaSuccess) {
     matcha_destroy(h);
     return e == cudaErrorMemoryAllocation ? MATCHA_ERR_ALLOC : MATCHA_ERR_CUDA;
@@ -602,7 +598,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
 
 MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (!h) return MATCHA_ERR_INVALID_ARG;
-  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G, h->ws_cfinal,
+  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
                   h->ws_euler, h->ws_score, h->ws_idx, h->ws_best, h->ws_vols[0], h->ws_vols[1], h->ws_poses,
                   h->ws_ref};
   for (void* p : ptrs)
