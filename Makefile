@@ -29,7 +29,7 @@ build/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 $(PKG)/libmatcha.so: $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcufft
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS)
 
 clean:
 	rm -rf gen/*.so oracle/*.so $(PKG)/*.so build

@@ -127,14 +127,18 @@ cudaError_t launch_corr_coeffs_tc(const float2* F, const float2* H, int64_t B, i
                                   int num_sms, cudaStream_t s);
 template <typename T>
 cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estride, int64_t nb, T* rho, cudaStream_t s);
-template <typename T> cudaError_t launch_to_real(const float* in, T* out, int64_t n, cudaStream_t s);
-template <typename T> cudaError_t launch_cross_spectrum(const cplx_t<T>* F, cplx_t<T>* X, int64_t n, cudaStream_t s);
-template <typename T>
-cudaError_t launch_window_peak(const T* corr, int N, int W, int64_t nb, T* shifts, int sstride, T* peak,
-                               cudaStream_t s);
+// stage 5 without an FFT library (k_trans.cu): mixed-radix factorisation of a transform length
+struct FftRadix {
+  int n, nst;
+  int rad[16];
+};
+FftRadix fft_radix(int n);
+bool trans_supported(int N, int W, bool fp64);  // shared-memory limits of the stage-5 kernels
+template <typename T, typename Tin>
+cudaError_t launch_plane_r2c(const Tin* vol, int N, int64_t nb, cplx_t<T>* out, cudaStream_t s);
 size_t window_scratch_reals(int N, int W);
 template <typename T>
-cudaError_t launch_window_pruned(const cplx_t<T>* Fh, const cplx_t<T>* Rh, int N, int W, int64_t nb, T* scratch,
-                                 T* shifts, int sstride, T* peak, cudaStream_t s);
+cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N, int W, int64_t nb, T* scratch,
+                                T* shifts, int sstride, T* peak, cudaStream_t s);
 
 }  // namespace matcha

@@ -7,10 +7,17 @@
 // per axis clamped to 1/2, trilinear rotation of the reference, zero outside):
 //   rho(x) = h(R^T (x - c) + c),   c(t) = sum_x f(x) rho((x - t) mod N) = IFFT(F^ conj(rho^))(t) / N^3.
 //
-// B200 mapping: the rotated references of a chunk are produced by one gather kernel (the reference is
-// shared by every particle and stays L2-resident), the 3-D transforms are batched cuFFT R2C/C2R plans
-// (library, like cuBLAS), the cross spectrum is an in-place elementwise kernel, and the windowed argmax +
-// subpixel fit is one CTA per particle with a deterministic (value desc, index asc) block reduction.
+// B200 mapping (no FFT library): the inverse transform is needed only on the window, and its kz part at integer
+// tz is a circular correlation ALONG z of the 2-D (x, y) plane spectra, so no z transform is ever done:
+//   5a k_plane_r2c   2-D R2C of every z-plane (hand-written mixed-radix Stockham FFTs in shared memory, two real
+//                    rows per complex line): f~ of the particles once per chunk, rho~ of the rotated references
+//                    (k_rotate_ref, the reference is L2-resident) every alternation;
+//   5b k_zcorr       Y1(kx, ky, tz) = sum_z f~(kx, ky, z + tz) conj(rho~(kx, ky, z)) for the w' = 2W + 3 window tz;
+//   5c k_window_xy   the (x, y) inverse onto the window (tx, ty) from Y1, Hermitian half spectrum, Re;
+//   5d k_window_peak the windowed argmax and the per-axis parabolic subpixel fit (deterministic block reduction).
+// N^2 c(t) = Re sum_{kx,ky} w_kx e^{2 pi i (kx tx + ky ty)/N} Y1(kx, ky, tz)   (exact: Parseval in x, y + the z shift).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace matcha {
@@ -159,203 +166,260 @@ __global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ re
   }
 }
 
-template <typename T>
-__global__ void k_to_real(const float* __restrict__ in, T* __restrict__ out, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (T)in[i];
-}
-
-// X <- F^ . conj(X), elementwise
-template <typename T>
-__global__ void k_cross_spectrum(const cplx_t<T>* __restrict__ F, cplx_t<T>* __restrict__ X, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const cplx_t<T> f = F[i], x = X[i];
-    X[i] = mk<T>(f.x * x.x + f.y * x.y, f.y * x.x - f.x * x.y);
-  }
-}
-
 template <typename T> __device__ __forceinline__ bool better(T v1, int i1, T v2, int i2) {
   return v1 > v2 || (v1 == v2 && i1 < i2);
 }
 
-// windowed argmax (ties -> lowest window index, z-major) + per-axis parabolic subpixel; corr = N^3 c(t)
-template <typename T>
-__global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ corr, int N, int W, T* shifts, int sstride,
-                                                     T* peak) {
-  __shared__ T sv[8];
-  __shared__ int si[8];
-  const int64_t p = blockIdx.x;
-  const T* cp = corr + p * (int64_t)N * N * N;
-  const int w = 2 * W + 1, nw = w * w * w;
-  auto at = [&](int tx, int ty, int tz) {
-    const int x = ((tx % N) + N) % N, y = ((ty % N) + N) % N, z = ((tz % N) + N) % N;
-    return cp[((size_t)z * N + y) * N + x];
-  };
-  T bv = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int t = threadIdx.x; t < nw; t += blockDim.x) {
-    const int tx = t % w - W, ty = (t / w) % w - W, tz = t / (w * w) - W;
-    const T v = at(tx, ty, tz);
-    if (better(v, t, bv, bi)) {
-      bv = v;
-      bi = t;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (better(v2, i2, bv, bi)) {
-      bv = v2;
-      bi = i2;
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    sv[warp] = bv;
-    si[warp] = bi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
-      if (better(sv[k], si[k], bv, bi)) {
-        bv = sv[k];
-        bi = si[k];
-      }
-    const int t[3] = {bi % w - W, (bi / w) % w - W, bi / (w * w) - W};
-    const T c0 = bv;
-    for (int ax = 0; ax < 3; ++ax) {
-      int tm[3] = {t[0], t[1], t[2]}, tp[3] = {t[0], t[1], t[2]};
-      tm[ax] -= 1;
-      tp[ax] += 1;
-      const T cm = at(tm[0], tm[1], tm[2]), cpl = at(tp[0], tp[1], tp[2]);
-      const T den = cm - T(2) * c0 + cpl;
-      T dl = T(0);
-      if (den < T(0)) dl = fmin(T(0.5), fmax(T(-0.5), (cm - cpl) / (T(2) * den)));
-      shifts[p * sstride + ax] = (T)t[ax] + dl;
-    }
-    if (peak) peak[p] = c0 / ((T)N * N * N);
-  }
-}
-
-// ---- windowed correlation by a pruned inverse DFT (replaces the cross spectrum + full C2R + window read) --------
-// Only c(t) for t in the window [-W-1, W+1]^3 (the argmax window plus the subpixel neighbours) is needed, so the
-// inverse transform of X = F^ conj(rho^) is evaluated directly on those w' = 2W+3 points per axis, separably:
-//   Y1[kz][ky][a]  = sum_{kx=0}^{N/2} w_kx X[kz][ky][kx] e^{+2 pi i kx tx_a / N}   (w_kx = 1 at kx = 0, N/2, else 2)
-//   Y2[kz][b][a]   = sum_ky Y1[kz][ky][a] e^{+2 pi i ky ty_b / N}
-//   cw[c][b][a]    = Re sum_kz Y2[kz][b][a] e^{+2 pi i kz tz_c / N}  = N^3 c(t)  (the unnormalised C2R value)
-// X is Hermitian (F^, rho^ are spectra of real volumes), so the half-spectrum sum with weights w_kx and Re is exact.
-// The per-(particle, kz) kernel forms X in shared memory from coalesced F^/rho^ plane loads (X is never stored).
-
 template <typename T> __device__ __forceinline__ cplx_t<T> cmul(cplx_t<T> a, cplx_t<T> b) {
   return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+template <typename T> __device__ __forceinline__ cplx_t<T> cadd(cplx_t<T> a, cplx_t<T> b) {
+  return mk<T>(a.x + b.x, a.y + b.y);
+}
+template <typename T> __device__ __forceinline__ cplx_t<T> csub(cplx_t<T> a, cplx_t<T> b) {
+  return mk<T>(a.x - b.x, a.y - b.y);
+}
+// a * (-i)
+template <typename T> __device__ __forceinline__ cplx_t<T> cmi(cplx_t<T> a) { return mk<T>(a.y, -a.x); }
 
-template <typename T>
-__device__ __forceinline__ void build_twiddles(cplx_t<T>* tw, int N) {
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+// tw[m] = e^{sign 2 pi i m / n}, m < n (FP64 sincospi, cast)
+template <typename T> __device__ __forceinline__ void build_roots(cplx_t<T>* tw, int n, int sign) {
+  for (int m = threadIdx.x; m < n; m += blockDim.x) {
     double sn, cs;
-    sincospi(2.0 * j / N, &sn, &cs);  // e^{+2 pi i j / N}
-    tw[j] = mk<T>((T)cs, (T)sn);
+    sincospi(2.0 * m / n, &sn, &cs);
+    tw[m] = mk<T>((T)cs, (T)(sign * sn));
   }
 }
 
-// grid (N, nb): block (kz, p) -> Y2[p][kz][w'][w']
+// ---- batched 1-D FFTs in shared memory (mixed-radix Stockham autosort, forward e^{-2 pi i k n / N}) ----------
+// nl independent lines of length n = fr.n, line l at a[l * n + i].  Stage s (radix R = fr.rad[s], Ns = product of the
+// previous radices) combines R sub-transforms of length Ns: butterfly j (< n / R) reads a[j + r n / R], twiddles input
+// r by e^{-2 pi i r (j mod Ns) / (Ns R)} = tw[r (j mod Ns) n / (Ns R)], applies the R-point DFT and writes
+// b[(j - j mod Ns) R + j mod Ns + q Ns].  Radix 4, 2, 3 are specialised; any other prime factor (N is a multiple of 8,
+// so only N with factors 5, 7, 11, ... reach it) runs the direct R-point DFT.  All threads of the CTA must call it;
+// it ends with __syncthreads() after every stage and returns the buffer that holds the result (a or b).
 template <typename T>
-__global__ void __launch_bounds__(512) k_window_xy(const cplx_t<T>* __restrict__ Fh, const cplx_t<T>* __restrict__ Rh,
-                                                   int N, int W, cplx_t<T>* __restrict__ Y2) {
-  extern __shared__ unsigned char smem_raw[];
-  const int H = N / 2 + 1, wp = 2 * W + 3;
-  cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N][wp]: e^{+2 pi i k t_a / N}, t_a = a - (W+1)
-  cplx_t<T>* X = tw + N * wp;                              // [N][H]
-  cplx_t<T>* Y1 = X + N * H;                               // [N][wp]
-  cplx_t<T>* base = Y1 + N * wp;                           // [N]: e^{+2 pi i j / N}
-  const int kz = blockIdx.x;
+__device__ cplx_t<T>* stockham(cplx_t<T>* a, cplx_t<T>* b, int nl, const FftRadix& fr, const cplx_t<T>* __restrict__ tw) {
+  const int n = fr.n;
+  int Ns = 1;
+  for (int s = 0; s < fr.nst; ++s) {
+    const int R = fr.rad[s], nb = n / R, ts = n / (Ns * R);
+    for (int t = threadIdx.x; t < nl * nb; t += blockDim.x) {
+      const int l = t / nb, j = t - l * nb, k = j % Ns;
+      const cplx_t<T>* in = a + l * n + j;
+      cplx_t<T>* out = b + l * n + (j - k) * R + k;
+      if (R == 4) {
+        const cplx_t<T> v0 = in[0], v1 = cmul<T>(in[nb], tw[k * ts]), v2 = cmul<T>(in[2 * nb], tw[2 * k * ts]),
+                        v3 = cmul<T>(in[3 * nb], tw[3 * k * ts]);
+        const cplx_t<T> s02 = cadd<T>(v0, v2), d02 = csub<T>(v0, v2), s13 = cadd<T>(v1, v3), d13 = cmi<T>(csub<T>(v1, v3));
+        out[0] = cadd<T>(s02, s13);
+        out[Ns] = cadd<T>(d02, d13);
+        out[2 * Ns] = csub<T>(s02, s13);
+        out[3 * Ns] = csub<T>(d02, d13);
+      } else if (R == 2) {
+        const cplx_t<T> v0 = in[0], v1 = cmul<T>(in[nb], tw[k * ts]);
+        out[0] = cadd<T>(v0, v1);
+        out[Ns] = csub<T>(v0, v1);
+      } else if (R == 3) {
+        const cplx_t<T> v0 = in[0], v1 = cmul<T>(in[nb], tw[k * ts]), v2 = cmul<T>(in[2 * nb], tw[2 * k * ts]);
+        const T h = T(0.86602540378443864676);  // sin(2 pi / 3)
+        const cplx_t<T> sm = cadd<T>(v1, v2), df = csub<T>(v1, v2);
+        const cplx_t<T> m = mk<T>(v0.x - T(0.5) * sm.x, v0.y - T(0.5) * sm.y);
+        out[0] = cadd<T>(v0, sm);
+        out[Ns] = mk<T>(m.x + h * df.y, m.y - h * df.x);      // m - i h df
+        out[2 * Ns] = mk<T>(m.x - h * df.y, m.y + h * df.x);  // m + i h df
+      } else {
+        const int nR = n / R;
+        for (int q = 0; q < R; ++q) {
+          cplx_t<T> acc = mk<T>(T(0), T(0));
+          for (int r = 0; r < R; ++r) {
+            const cplx_t<T> v = r ? cmul<T>(in[r * nb], tw[r * k * ts]) : in[0];
+            acc = cadd<T>(acc, cmul<T>(v, tw[((r * q) % R) * nR]));
+          }
+          out[q * Ns] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    cplx_t<T>* x = a;
+    a = b;
+    b = x;
+    Ns *= R;
+  }
+  return a;
+}
+
+// ---- stage 5a: 2-D R2C transform of every z-plane of a real volume -----------------------------------------------
+//   U~[p][z][ky][kx] = sum_{y,x} u_p(x, y, z) e^{-2 pi i (kx x + ky y) / N},   kx in [0, N/2]
+// One CTA per (plane, particle).  x pass: rows 2y', 2y'+1 packed as one complex line a + i b, transformed together,
+// then unpacked, A(k) = (Z(k) + conj Z(N-k)) / 2, B(k) = (Z(k) - conj Z(N-k)) / (2i); the half rows land in the plane
+// buffer P[N][H].  y pass: columns of P in chunks of cwl lines, transformed back into P.  P is written out linearly.
+// Used for the particles (once per chunk: f~) and for the rotated references (every alternation: rho~).
+template <typename T, typename Tin>
+__global__ void __launch_bounds__(256) k_plane_r2c(const Tin* __restrict__ vol, const __grid_constant__ FftRadix fr,
+                                                   int cwl,
+                                                   cplx_t<T>* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = fr.n, H = N / 2 + 1;
+  cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);
+  cplx_t<T>* P = tw + N;
+  cplx_t<T>* S0 = P + N * H;
+  cplx_t<T>* S1 = S0 + cwl * N;
+  const int z = blockIdx.x;
   const int64_t p = blockIdx.y;
-  const int64_t plane = ((int64_t)p * N + kz) * N * H;
-  build_twiddles<T>(base, N);
+  const Tin* u = vol + (p * N + z) * (int64_t)N * N;
+  build_roots<T>(tw, N, -1);
+  for (int y0 = 0; y0 < N / 2; y0 += cwl) {
+    const int nl = min(cwl, N / 2 - y0);
+    for (int i = threadIdx.x; i < nl * N; i += blockDim.x) {
+      const int l = i / N, x = i - l * N;
+      const Tin* r0 = u + (2 * (y0 + l)) * N + x;
+      S0[i] = mk<T>((T)__ldg(r0), (T)__ldg(r0 + N));
+    }
+    __syncthreads();
+    const cplx_t<T>* res = stockham<T>(S0, S1, nl, fr, tw);
+    for (int i = threadIdx.x; i < nl * H; i += blockDim.x) {
+      const int l = i / H, k = i - l * H;
+      const cplx_t<T> Z = res[l * N + k], Zc = res[l * N + (N - k) % N];
+      const int y = 2 * (y0 + l);
+      P[y * H + k] = mk<T>(T(0.5) * (Z.x + Zc.x), T(0.5) * (Z.y - Zc.y));          // (Z + conj Zc) / 2
+      P[(y + 1) * H + k] = mk<T>(T(0.5) * (Z.y + Zc.y), -T(0.5) * (Z.x - Zc.x));   // (Z - conj Zc) / (2i)
+    }
+    __syncthreads();
+  }
+  for (int k0 = 0; k0 < H; k0 += cwl) {
+    const int nl = min(cwl, H - k0);
+    for (int i = threadIdx.x; i < nl * N; i += blockDim.x) {
+      const int l = i % nl, y = i / nl;
+      S0[l * N + y] = P[y * H + k0 + l];
+    }
+    __syncthreads();
+    const cplx_t<T>* res = stockham<T>(S0, S1, nl, fr, tw);
+    for (int i = threadIdx.x; i < nl * N; i += blockDim.x) {
+      const int l = i % nl, ky = i / nl;
+      P[ky * H + k0 + l] = res[l * N + ky];
+    }
+    __syncthreads();
+  }
+  cplx_t<T>* o = out + (p * N + z) * (int64_t)N * H;
+  for (int i = threadIdx.x; i < N * H; i += blockDim.x) o[i] = P[i];
+}
+
+// ---- stage 5b: correlation along z of the plane spectra, on the window only --------------------------------------
+// With f~, rho~ the 2-D (x, y) spectra of the planes, the kz part of IFFT(F^ conj(rho^)) at integer tz is a circular
+// correlation along z (no z transform needed):
+//   Y1[p][a][ky][kx] = sum_z f~(kx, ky, (z + tz_a) mod N) conj(rho~(kx, ky, z)),   tz_a = a - (W + 1), a < w' = 2W+3
+// One CTA per (ky row, kx chunk of hc, particle): both rows of every z are staged transposed ([kx][z], padded) and
+// each output (kx, a) is an N-term complex dot product; outputs are staged and written as contiguous rows.
+template <typename T>
+__global__ void __launch_bounds__(256) k_zcorr(const cplx_t<T>* __restrict__ ft, const cplx_t<T>* __restrict__ rt,
+                                               int N, int W, int hc, cplx_t<T>* __restrict__ Y1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int H = N / 2 + 1, wp = 2 * W + 3, nkc = (H + hc - 1) / hc, ld = N + 1;
+  cplx_t<T>* fs = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [hc][N+1]
+  cplx_t<T>* rs = fs + hc * ld;                             // [hc][N+1]
+  const int ky = blockIdx.x / nkc, kx0 = (blockIdx.x - ky * nkc) * hc, nk = min(hc, H - kx0);
+  const int64_t p = blockIdx.y;
+  for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
+    const int zz = i / nk, kl = i - zz * nk;
+    const int64_t g = ((p * N + zz) * N + ky) * (int64_t)H + kx0 + kl;
+    fs[kl * ld + zz] = ft[g];
+    rs[kl * ld + zz] = rt[g];
+  }
+  __syncthreads();
+  cplx_t<T> acc[4];  // nk * wp <= 4 * blockDim.x (zcorr_chunk)
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int o = threadIdx.x + u * blockDim.x;
+    if (o >= nk * wp) break;
+    const int kl = o / wp, a = o - kl * wp;
+    const cplx_t<T>* fr = fs + kl * ld;
+    const cplx_t<T>* rr = rs + kl * ld;
+    int zz = ((a - (W + 1)) % N + N) % N;
+    T ar = T(0), ai = T(0);
+    for (int zi = 0; zi < N; ++zi) {
+      const cplx_t<T> f = fr[zz], r = rr[zi];
+      ar = fma(f.x, r.x, fma(f.y, r.y, ar));   // f conj(r)
+      ai = fma(f.y, r.x, fma(-f.x, r.y, ai));
+      if (++zz == N) zz = 0;
+    }
+    acc[u] = mk<T>(ar, ai);
+  }
+  __syncthreads();
+  // stage [a][kl] in fs, then contiguous row writes Y1[p][a][ky][kx0 .. kx0 + nk)
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int o = threadIdx.x + u * blockDim.x;
+    if (o >= nk * wp) break;
+    const int kl = o / wp, a = o - kl * wp;
+    fs[a * hc + kl] = acc[u];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < wp * nk; i += blockDim.x) {
+    const int a = i / nk, kl = i - a * nk;
+    Y1[((p * wp + a) * N + ky) * (int64_t)H + kx0 + kl] = fs[a * hc + kl];
+  }
+}
+
+// ---- stage 5c: the (x, y) part of the window inverse, one CTA per (tz plane, particle) ----------------------------
+//   cw[p][a][b][c] = Re sum_{ky} e^{+2 pi i ky ty_b / N} sum_{kx <= N/2} w_kx Y1[p][a][ky][kx] e^{+2 pi i kx tx_c / N}
+// (w_kx = 1 at kx = 0 and N/2, else 2: the Hermitian half spectrum) = N^2 c(t) for t = (tx_c, ty_b, tz_a).
+template <typename T>
+__global__ void __launch_bounds__(512) k_window_xy(const cplx_t<T>* __restrict__ Y1, int N, int W, T* __restrict__ cw) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int H = N / 2 + 1, wp = 2 * W + 3;
+  cplx_t<T>* base = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N] e^{+2 pi i j / N}
+  cplx_t<T>* tw = base + N;                                  // [N][wp] e^{+2 pi i k t_a / N}
+  cplx_t<T>* Y = tw + N * wp;                                // [N][H]
+  cplx_t<T>* Z = Y + N * H;                                  // [N][wp]
+  const int a = blockIdx.x;
+  const int64_t p = blockIdx.y;
+  build_roots<T>(base, N, +1);
+  const cplx_t<T>* y1 = Y1 + (p * wp + a) * (int64_t)N * H;
+  for (int i = threadIdx.x; i < N * H; i += blockDim.x) {
+    const int kx = i % H;
+    const T wk = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
+    const cplx_t<T> v = y1[i];
+    Y[i] = mk<T>(wk * v.x, wk * v.y);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < N * wp; i += blockDim.x) {
     const int k = i / wp, t = i - k * wp - (W + 1);
     tw[i] = base[(((k * t) % N) + N) % N];
   }
-  // four elements per thread per pass, all eight loads issued before the first use (the loads' latency, not the
-  // arithmetic, paced the one-element loop)
-  constexpr int kU = 4;
-  for (int i0 = threadIdx.x; i0 < N * H; i0 += kU * blockDim.x) {
-    cplx_t<T> f[kU], r[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < N * H) {
-        f[u] = Fh[plane + i];
-        r[u] = Rh[plane + i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = i0 + u * blockDim.x;
-      if (i < N * H) {
-        const int kx = i % H;
-        const T wk = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
-        X[i] = mk<T>(wk * (f[u].x * r[u].x + f[u].y * r[u].y), wk * (f[u].y * r[u].x - f[u].x * r[u].y));  // w F^ conj(rho^)
-      }
-    }
-  }
   __syncthreads();
   for (int o = threadIdx.x; o < N * wp; o += blockDim.x) {
-    const int ky = o / wp, a = o - ky * wp;
-    const cplx_t<T>* xr = X + ky * H;
+    const int ky = o / wp, c = o - ky * wp;
+    const cplx_t<T>* yr = Y + ky * H;
     T ar = T(0), ai = T(0);
     for (int kx = 0; kx < H; ++kx) {
-      const cplx_t<T> x = xr[kx], t = tw[kx * wp + a];
-      ar = fma(x.x, t.x, fma(-x.y, t.y, ar));
-      ai = fma(x.x, t.y, fma(x.y, t.x, ai));
+      const cplx_t<T> v = yr[kx], t = tw[kx * wp + c];
+      ar = fma(v.x, t.x, fma(-v.y, t.y, ar));
+      ai = fma(v.x, t.y, fma(v.y, t.x, ai));
     }
-    Y1[o] = mk<T>(ar, ai);
+    Z[o] = mk<T>(ar, ai);
   }
   __syncthreads();
   for (int o = threadIdx.x; o < wp * wp; o += blockDim.x) {
-    const int b = o / wp, a = o - b * wp;
-    T ar = T(0), ai = T(0);
+    const int b = o / wp, c = o - b * wp;
+    T ar = T(0);
     for (int ky = 0; ky < N; ++ky) {
-      const cplx_t<T> y = Y1[ky * wp + a], t = tw[ky * wp + b];
-      ar = fma(y.x, t.x, fma(-y.y, t.y, ar));
-      ai = fma(y.x, t.y, fma(y.y, t.x, ai));
+      const cplx_t<T> v = Z[ky * wp + c], t = tw[ky * wp + b];
+      ar = fma(v.x, t.x, fma(-v.y, t.y, ar));
     }
-    Y2[((int64_t)p * N + kz) * wp * wp + o] = mk<T>(ar, ai);
+    cw[(p * wp + a) * (int64_t)wp * wp + o] = ar;
   }
 }
 
-// grid nb: the z pass into cw[p][w'^3] (global scratch), then the windowed argmax (ties -> lowest window index,
-// z-major) and the per-axis parabolic subpixel (reading C18), as k_window_peak but on the pruned window
+// ---- stage 5d: windowed argmax (ties -> lowest window index, z-major) + per-axis parabolic subpixel (C18) -------
 template <typename T>
-__global__ void __launch_bounds__(256) k_window_z_peak(const cplx_t<T>* __restrict__ Y2, int N, int W,
-                                                       T* __restrict__ cw_all, T* shifts, int sstride, T* peak) {
-  __shared__ cplx_t<T> tw[512];
+__global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ cw_all, int N, int W, T* shifts,
+                                                     int sstride, T* peak) {
   __shared__ T sv[8];
   __shared__ int si[8];
   const int64_t p = blockIdx.x;
-  const int wp = 2 * W + 3, w = 2 * W + 1, wp2 = wp * wp;
-  build_twiddles<T>(tw, N);
-  __syncthreads();
-  const cplx_t<T>* y2 = Y2 + p * (int64_t)N * wp2;
-  T* cw = cw_all + p * (int64_t)wp2 * wp;
-  for (int o = threadIdx.x; o < wp2 * wp; o += blockDim.x) {
-    const int c = o / wp2, ba = o - c * wp2;
-    const int tz = c - (W + 1);
-    const int step = ((tz % N) + N) % N;
-    T acc = T(0);
-    int idx = 0;
-    for (int kz = 0; kz < N; ++kz) {
-      const cplx_t<T> y = y2[(int64_t)kz * wp2 + ba], t = tw[idx];
-      acc = fma(y.x, t.x, fma(-y.y, t.y, acc));
-      idx += step;
-      if (idx >= N) idx -= N;
-    }
-    cw[o] = acc;
-  }
-  __syncthreads();
+  const int wp = 2 * W + 3, w = 2 * W + 1;
+  const T* cw = cw_all + p * (int64_t)wp * wp * wp;
   auto at = [&](int tx, int ty, int tz) { return cw[((tz + W + 1) * wp + (ty + W + 1)) * wp + (tx + W + 1)]; };
   const int nw = w * w * w;
   T bv = -INFINITY;
@@ -401,10 +465,9 @@ __global__ void __launch_bounds__(256) k_window_z_peak(const cplx_t<T>* __restri
       if (den < T(0)) dl = fmin(T(0.5), fmax(T(-0.5), (cm - cpl) / (T(2) * den)));
       shifts[p * sstride + ax] = (T)t[ax] + dl;
     }
-    if (peak) peak[p] = c0 / ((T)N * N * N);
+    if (peak) peak[p] = c0 / ((T)N * N);
   }
 }
-
 }  // namespace
 
 template <typename T>
@@ -420,63 +483,101 @@ cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estri
   return cudaGetLastError();
 }
 
-template <typename T> cudaError_t launch_to_real(const float* in, T* out, int64_t n, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  k_to_real<T><<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s>>>(in, out, n);
-  return cudaGetLastError();
+FftRadix fft_radix(int n) {
+  FftRadix f;
+  f.n = n;
+  f.nst = 0;
+  int m = n;
+  for (int r : {4, 2, 3}) {
+    while (m % r == 0 && f.nst < 16) {
+      f.rad[f.nst++] = r;
+      m /= r;
+    }
+  }
+  for (int r = 5; m > 1 && f.nst < 16; r += 2)
+    while (m % r == 0 && f.nst < 16) {
+      f.rad[f.nst++] = r;
+      m /= r;
+    }
+  return f;
 }
 
-template <typename T>
-cudaError_t launch_cross_spectrum(const cplx_t<T>* F, cplx_t<T>* X, int64_t n, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  k_cross_spectrum<T><<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s>>>(F, X, n);
-  return cudaGetLastError();
+static int plane_lines(int N, size_t csz) {
+  const int H = N / 2 + 1;
+  for (int cwl : {16, 8, 4, 2})
+    if (csz * ((size_t)N + (size_t)N * H + 2 * (size_t)cwl * N) <= 227 * 1024) return cwl;
+  return 0;
+}
+static size_t plane_smem(int N, int cwl, size_t csz) {
+  return csz * ((size_t)N + (size_t)N * (N / 2 + 1) + 2 * (size_t)cwl * N);
+}
+static int zcorr_chunk(int N, int W, size_t csz) {
+  const int H = N / 2 + 1, wp = 2 * W + 3;
+  int hc = std::min(H, 1024 / wp);
+  while (hc > 1 && 2 * csz * (size_t)hc * (N + 1) > 160 * 1024) --hc;
+  return hc;
+}
+static size_t window_xy_smem(int N, int W, size_t csz) {
+  const int wp = 2 * W + 3;
+  return csz * ((size_t)N + 2 * (size_t)N * wp + (size_t)N * (N / 2 + 1));
 }
 
-template <typename T>
-cudaError_t launch_window_peak(const T* corr, int N, int W, int64_t nb, T* shifts, int sstride, T* peak,
-                               cudaStream_t s) {
+bool trans_supported(int N, int W, bool fp64) {
+  const size_t csz = fp64 ? 16 : 8;
+  return plane_lines(N, csz) > 0 && 2 * W + 3 <= N && window_xy_smem(N, W, csz) <= 227 * 1024 &&
+         zcorr_chunk(N, W, csz) >= 1;
+}
+
+template <typename T, typename Tin>
+cudaError_t launch_plane_r2c(const Tin* vol, int N, int64_t nb, cplx_t<T>* out, cudaStream_t s) {
   if (nb == 0) return cudaSuccess;
-  k_window_peak<T><<<(unsigned)nb, 256, 0, s>>>(corr, N, W, shifts, sstride, peak);
+  const size_t csz = sizeof(cplx_t<T>);
+  const int cwl = plane_lines(N, csz);
+  if (!cwl) return cudaErrorInvalidValue;
+  const size_t smem = plane_smem(N, cwl, csz);
+  cudaError_t e = cudaFuncSetAttribute(k_plane_r2c<T, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_plane_r2c<T, Tin><<<dim3((unsigned)N, (unsigned)nb), 256, smem, s>>>(vol, fft_radix(N), cwl, out);
   return cudaGetLastError();
 }
 
 size_t window_scratch_reals(int N, int W) {
-  const int64_t wp = 2 * W + 3;
-  return (size_t)(2 * (int64_t)N * wp * wp + wp * wp * wp);
+  const int64_t wp = 2 * W + 3, H = N / 2 + 1;
+  return (size_t)(2 * wp * N * H + wp * wp * wp);
 }
 
-// Y2 and the c window of particle p live in scratch + p * window_scratch_reals(N, W) reals
+// Y1 [nb][wp][N][H] complex at the front of the scratch, the c windows [nb][wp^3] behind it
 template <typename T>
-cudaError_t launch_window_pruned(const cplx_t<T>* Fh, const cplx_t<T>* Rh, int N, int W, int64_t nb, T* scratch,
-                                 T* shifts, int sstride, T* peak, cudaStream_t s) {
+cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N, int W, int64_t nb, T* scratch,
+                                T* shifts, int sstride, T* peak, cudaStream_t s) {
   if (nb == 0) return cudaSuccess;
-  if (N > 512 || 2 * W + 3 > N) return cudaErrorInvalidValue;
+  const size_t csz = sizeof(cplx_t<T>);
+  if (!trans_supported(N, W, sizeof(T) == 8)) return cudaErrorInvalidValue;
   const int H = N / 2 + 1, wp = 2 * W + 3;
-  const size_t smem = sizeof(cplx_t<T>) * ((size_t)N * wp + (size_t)N * H + (size_t)N * wp + (size_t)N);
-  cudaError_t e = cudaFuncSetAttribute(k_window_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int hc = zcorr_chunk(N, W, csz), nkc = (H + hc - 1) / hc;
+  cplx_t<T>* Y1 = reinterpret_cast<cplx_t<T>*>(scratch);
+  T* cw = scratch + 2 * nb * (int64_t)wp * N * H;
+  const size_t zsm = 2 * csz * (size_t)hc * (N + 1);
+  cudaError_t e = cudaFuncSetAttribute(k_zcorr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
   if (e != cudaSuccess) return e;
-  // Y2 [nb][N][wp][wp] complex at the front of the scratch, the c windows [nb][wp^3] behind it
-  cplx_t<T>* Y2 = reinterpret_cast<cplx_t<T>*>(scratch);
-  T* cw = scratch + 2 * nb * (int64_t)N * wp * wp;
-  k_window_xy<T><<<dim3((unsigned)N, (unsigned)nb), 512, smem, s>>>(Fh, Rh, N, W, Y2);
+  k_zcorr<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, N, W, hc, Y1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k_window_z_peak<T><<<(unsigned)nb, 256, 0, s>>>(Y2, N, W, cw, shifts, sstride, peak);
+  const size_t xsm = window_xy_smem(N, W, csz);
+  e = cudaFuncSetAttribute(k_window_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
+  if (e != cudaSuccess) return e;
+  k_window_xy<T><<<dim3((unsigned)wp, (unsigned)nb), 512, xsm, s>>>(Y1, N, W, cw);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_window_peak<T><<<(unsigned)nb, 256, 0, s>>>(cw, N, W, shifts, sstride, peak);
   return cudaGetLastError();
 }
-
 template cudaError_t launch_rotate_ref<float>(const float*, int, const float*, int, int64_t, float*, cudaStream_t);
 template cudaError_t launch_rotate_ref<double>(const float*, int, const double*, int, int64_t, double*, cudaStream_t);
-template cudaError_t launch_to_real<float>(const float*, float*, int64_t, cudaStream_t);
-template cudaError_t launch_to_real<double>(const float*, double*, int64_t, cudaStream_t);
-template cudaError_t launch_cross_spectrum<float>(const float2*, float2*, int64_t, cudaStream_t);
-template cudaError_t launch_cross_spectrum<double>(const double2*, double2*, int64_t, cudaStream_t);
-template cudaError_t launch_window_peak<float>(const float*, int, int, int64_t, float*, int, float*, cudaStream_t);
-template cudaError_t launch_window_peak<double>(const double*, int, int, int64_t, double*, int, double*,
-                                                cudaStream_t);
-template cudaError_t launch_window_pruned<float>(const float2*, const float2*, int, int, int64_t, float*, float*, int,
-                                                 float*, cudaStream_t);
-template cudaError_t launch_window_pruned<double>(const double2*, const double2*, int, int, int64_t, double*, double*,
-                                                  int, double*, cudaStream_t);
+template cudaError_t launch_plane_r2c<float, float>(const float*, int, int64_t, float2*, cudaStream_t);
+template cudaError_t launch_plane_r2c<double, float>(const float*, int, int64_t, double2*, cudaStream_t);
+template cudaError_t launch_plane_r2c<double, double>(const double*, int, int64_t, double2*, cudaStream_t);
+template cudaError_t launch_window_zcorr<float>(const float2*, const float2*, int, int, int64_t, float*, float*, int,
+                                                float*, cudaStream_t);
+template cudaError_t launch_window_zcorr<double>(const double2*, const double2*, int, int, int64_t, double*, double*,
+                                                 int, double*, cudaStream_t);
 
 }  // namespace matcha

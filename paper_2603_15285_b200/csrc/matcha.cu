@@ -4,7 +4,6 @@
 // Tables are computed here in double precision (own Gauss-Legendre Newton solve and normalised
 // associated-Legendre recurrence; no code is shared with oracle/) and cast to the handle precision.
 #include <cuda_runtime.h>
-#include <cufft.h>
 
 #include <algorithm>
 #include <cmath>
@@ -57,16 +56,13 @@ struct matcha_ctx {
   cudaEvent_t ev_used[2] = {nullptr, nullptr};
   int64_t launches = 0;
   std::string err;
-  // stage 5 (translation): batched cuFFT plans and workspaces, allocated on first use
-  cufftHandle plan_r2c = 0, plan_c2r = 0;
-  int64_t plan_batch = 0;
-  void* ws_Fhat = nullptr;   // complex [mb][N][N][N/2+1]  F^ of the chunk's particles
-  void* ws_Xhat = nullptr;   // complex [mb][N][N][N/2+1]  rho^, then the cross spectrum
-  void* ws_rho = nullptr;    // real [mb][N^3]             rotated references, then c(t)
+  // stage 5 (translation): workspaces, allocated on first use
+  void* ws_Fhat = nullptr;   // complex [mb][N][N][N/2+1]  f~: 2-D spectra of the particles' z-planes
+  void* ws_Xhat = nullptr;   // complex [mb][N][N][N/2+1]  rho~: 2-D spectra of the rotated references' planes
+  void* ws_rho = nullptr;    // real [mb][N^3]             rotated references
   void* ws_peak = nullptr;   // real [mb]
-  void* ws_win = nullptr;    // real [mb][window_scratch_reals(N, W)]: pruned inverse DFT (Y2 + c window)
+  void* ws_win = nullptr;    // real [mb][window_scratch_reals(N, W)]: Y1 (z correlation) + the c window
   int ws_win_W = -1;
-  bool trans_fft = false;    // MATCHA_TRANS_FFT=1: full C2R + window read instead of the pruned inverse DFT
   void* ws_euler1 = nullptr; // real [mb][3]
   // per-stage event tracing
   bool prof = false;
@@ -292,9 +288,11 @@ static cudaError_t do_refine(matcha_handle_t h, const void* M, int32_t L_M, int6
 }
 
 // ---------------------------------------------------------------- stage 5 helpers
-static matcha_status_t trans_prepare(matcha_handle_t h, int64_t nb) {
+static matcha_status_t trans_prepare(matcha_handle_t h, int W) {
   const int N = h->cfg.N;
   const int64_t nr = (int64_t)N * N * N, nc = (int64_t)N * N * (N / 2 + 1), mb = h->cfg.max_batch;
+  if (!trans_supported(N, W, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "translation: box/window exceed the stage-5 shared-memory limits");
   if (!h->ws_Fhat) {
     cudaError_t e = cudaMalloc(&h->ws_Fhat, 2 * h->rsz * nc * mb);
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_Xhat, 2 * h->rsz * nc * mb);
@@ -303,88 +301,49 @@ static matcha_status_t trans_prepare(matcha_handle_t h, int64_t nb) {
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_euler1, 3 * h->rsz * mb);
     if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation workspace allocation failed");
   }
-  if (h->plan_batch != nb) {
-    if (h->plan_r2c) cufftDestroy(h->plan_r2c);
-    if (h->plan_c2r) cufftDestroy(h->plan_c2r);
-    h->plan_r2c = h->plan_c2r = 0;
-    int n[3] = {N, N, N};
-    if (cufftPlanMany(&h->plan_r2c, 3, n, nullptr, 1, 0, nullptr, 1, 0, h->fp64 ? CUFFT_D2Z : CUFFT_R2C, (int)nb) !=
-            CUFFT_SUCCESS ||
-        cufftPlanMany(&h->plan_c2r, 3, n, nullptr, 1, 0, nullptr, 1, 0, h->fp64 ? CUFFT_Z2D : CUFFT_C2R, (int)nb) !=
-            CUFFT_SUCCESS)
-      return fail(h, MATCHA_ERR_CUDA, "cuFFT plan creation failed");
-    h->plan_batch = nb;
+  if (h->ws_win_W < W) {
+    if (h->ws_win) cudaFree(h->ws_win);
+    h->ws_win = nullptr;
+    h->ws_win_W = -1;
+    if (cudaMalloc(&h->ws_win, h->rsz * window_scratch_reals(N, W) * mb) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "translation window scratch allocation failed");
+    h->ws_win_W = W;
   }
   return MATCHA_OK;
 }
 
-static bool fft_r2c(matcha_handle_t h, void* in, void* out, cudaStream_t s) {
-  cufftSetStream(h->plan_r2c, s);
-  return (h->fp64 ? cufftExecD2Z(h->plan_r2c, (cufftDoubleReal*)in, (cufftDoubleComplex*)out)
-                  : cufftExecR2C(h->plan_r2c, (cufftReal*)in, (cufftComplex*)out)) == CUFFT_SUCCESS;
-}
-static bool fft_c2r(matcha_handle_t h, void* in, void* out, cudaStream_t s) {
-  cufftSetStream(h->plan_c2r, s);
-  return (h->fp64 ? cufftExecZ2D(h->plan_c2r, (cufftDoubleComplex*)in, (cufftDoubleReal*)out)
-                  : cufftExecC2R(h->plan_c2r, (cufftComplex*)in, (cufftReal*)out)) == CUFFT_SUCCESS;
-}
-
-// F^ of nb particle volumes into ws_Fhat (once per chunk; the particles do not change across alternations)
-static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t nb, cudaStream_t s) {
-  const int N = h->cfg.N;
-  const int64_t nr = (int64_t)N * N * N;
-  matcha_status_t st = trans_prepare(h, nb);
+// f~ (2-D plane spectra) of nb particle volumes into ws_Fhat (once per chunk: the particles do not change across
+// alternations)
+static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t nb, int W, cudaStream_t s) {
+  matcha_status_t st = trans_prepare(h, W);
   if (st != MATCHA_OK) return st;
-  void* in = (void*)vols;
-  if (h->fp64) {
-    cudaError_t e = launch_to_real<double>(vols, (double*)h->ws_rho, nb * nr, s);
-    if (e != cudaSuccess) return cuda_fail(h, e, "translation: to_real");
-    h->launches++;
-    in = h->ws_rho;
-  }
-  if (!fft_r2c(h, in, h->ws_Fhat, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT R2C of the particles failed");
+  cudaError_t e = h->fp64 ? launch_plane_r2c<double, float>(vols, h->cfg.N, nb, (double2*)h->ws_Fhat, s)
+                          : launch_plane_r2c<float, float>(vols, h->cfg.N, nb, (float2*)h->ws_Fhat, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of the particles");
+  h->launches++;
   return MATCHA_OK;
 }
 
-// t = windowed argmax of c(t) = IFFT(F^ conj(rho^)) for the rotations `euler` (stride estride)
+// t = windowed argmax of c(t) = sum_x f(x) rho(x - t) for the rotations `euler` (stride estride)
 static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* ref, const void* euler, int estride,
                                     int W, void* shifts, int sstride, void* peak, cudaStream_t s) {
   const int N = h->cfg.N;
-  const int64_t nc = (int64_t)N * N * (N / 2 + 1);
   cudaError_t e;
   ProfScope ps(h, 5, s);
+  matcha_status_t st = trans_prepare(h, W);
+  if (st != MATCHA_OK) return st;
   e = h->fp64 ? launch_rotate_ref<double>(ref, N, (const double*)euler, estride, nb, (double*)h->ws_rho, s)
               : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
-  if (!fft_r2c(h, h->ws_rho, h->ws_Xhat, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT R2C of rho failed");
-  const size_t pr_smem = (size_t)h->rsz * 2 * ((size_t)N * (N / 2 + 1) + 2 * (size_t)N * (2 * W + 3) + (size_t)N);
-  if (!h->trans_fft && pr_smem <= 227 * 1024 && 2 * W + 3 <= N) {
-    // pruned inverse DFT on the window only (X = F^ conj(rho^) formed on chip, never stored)
-    if (h->ws_win_W < W) {
-      if (h->ws_win) cudaFree(h->ws_win);
-      h->ws_win = nullptr;
-      h->ws_win_W = -1;
-      e = cudaMalloc(&h->ws_win, h->rsz * window_scratch_reals(N, W) * h->cfg.max_batch);
-      if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation window scratch allocation failed");
-      h->ws_win_W = W;
-    }
-    e = h->fp64 ? launch_window_pruned<double>((const double2*)h->ws_Fhat, (const double2*)h->ws_Xhat, N, W, nb,
-                                               (double*)h->ws_win, (double*)shifts, sstride, (double*)peak, s)
-                : launch_window_pruned<float>((const float2*)h->ws_Fhat, (const float2*)h->ws_Xhat, N, W, nb,
-                                              (float*)h->ws_win, (float*)shifts, sstride, (float*)peak, s);
-    if (e != cudaSuccess) return cuda_fail(h, e, "translation: window_pruned");
-    h->launches += 3;
-    return MATCHA_OK;
-  }
-  e = h->fp64 ? launch_cross_spectrum<double>((const double2*)h->ws_Fhat, (double2*)h->ws_Xhat, nb * nc, s)
-              : launch_cross_spectrum<float>((const float2*)h->ws_Fhat, (float2*)h->ws_Xhat, nb * nc, s);
-  if (e != cudaSuccess) return cuda_fail(h, e, "translation: cross_spectrum");
-  if (!fft_c2r(h, h->ws_Xhat, h->ws_rho, s)) return fail(h, MATCHA_ERR_CUDA, "cuFFT C2R failed");
-  e = h->fp64 ? launch_window_peak<double>((const double*)h->ws_rho, N, W, nb, (double*)shifts, sstride,
-                                           (double*)peak, s)
-              : launch_window_peak<float>((const float*)h->ws_rho, N, W, nb, (float*)shifts, sstride, (float*)peak, s);
-  if (e != cudaSuccess) return cuda_fail(h, e, "translation: window_peak");
-  h->launches += 3;
+  e = h->fp64 ? launch_plane_r2c<double, double>((const double*)h->ws_rho, N, nb, (double2*)h->ws_Xhat, s)
+              : launch_plane_r2c<float, float>((const float*)h->ws_rho, N, nb, (float2*)h->ws_Xhat, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of rho");
+  e = h->fp64 ? launch_window_zcorr<double>((const double2*)h->ws_Fhat, (const double2*)h->ws_Xhat, N, W, nb,
+                                            (double*)h->ws_win, (double*)shifts, sstride, (double*)peak, s)
+              : launch_window_zcorr<float>((const float2*)h->ws_Fhat, (const float2*)h->ws_Xhat, N, W, nb,
+                                           (float*)h->ws_win, (float*)shifts, sstride, (float*)peak, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "translation: window_zcorr");
+  h->launches += 5;
   return MATCHA_OK;
 }
 
@@ -439,7 +398,7 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
       if (translate) {
         if (tau == 0) {
           ProfScope ps(h, 5, s);
-          st = trans_fhat(h, vols + c0 * n3, nb, s);
+          st = trans_fhat(h, vols + c0 * n3, nb, p->shift_window, s);
           if (st != MATCHA_OK) return st;
         }
         // t^tau from the rotation just estimated (poses[b][0..2]) -> poses[b][3..5]
@@ -466,7 +425,6 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   cudaGetDevice(&h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
   if (const char* v = getenv("MATCHA_CORR_SIMT")) h->use_tc = !(v[0] == '1');
-  if (const char* v = getenv("MATCHA_TRANS_FFT")) h->trans_fft = v[0] == '1';
   h->fp64 = cfg->precision == MATCHA_FP64;
   h->rsz = h->fp64 ? 8 : 4;
   h->R = cfg->N / 2;
@@ -604,8 +562,6 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  if (h->plan_r2c) cufftDestroy(h->plan_r2c);
-  if (h->plan_c2r) cufftDestroy(h->plan_c2r);
   for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -769,7 +725,7 @@ MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const fl
   const int64_t n3 = (int64_t)h->cfg.N * h->cfg.N * h->cfg.N;
   for (int64_t c0 = 0; c0 < B; c0 += h->cfg.max_batch) {
     const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
-    matcha_status_t st = trans_fhat(h, vols + c0 * n3, nb, s);
+    matcha_status_t st = trans_fhat(h, vols + c0 * n3, nb, window, s);
     if (st != MATCHA_OK) return st;
     st = trans_update(h, nb, ref, (const char*)euler + c0 * 3 * h->rsz, 3, window, (char*)shifts + c0 * 3 * h->rsz, 3,
                       peak ? (char*)peak + c0 * h->rsz : h->ws_peak, s);
@@ -789,6 +745,8 @@ MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vo
   if (!ref_coeffs && !ref) return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: need ref or ref_coeffs");
   if (params->shift_window > 0 && (!ref || params->shift_window > h->cfg.N / 4))
     return fail(h, MATCHA_ERR_WINDOW, "align_batch: shift window needs ref and W <= N/4");
+  if (params->shift_window > 0 && !trans_supported(h->cfg.N, params->shift_window, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: box too large for the stage-5 kernels");
   if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
     return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: coarse grid too large for one CTA");
   return align_device(h, vols, B, ref, ref_coeffs, params, poses, (cudaStream_t)stream);
@@ -803,6 +761,8 @@ MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const floa
   std::string why;
   if (!valid_params(params, h->L, why)) return fail(h, MATCHA_ERR_CUTOFF, "align_batch_host: " + why);
   if (params->shift_window > h->cfg.N / 4) return fail(h, MATCHA_ERR_WINDOW, "align_batch_host: W > N/4");
+  if (params->shift_window > 0 && !trans_supported(h->cfg.N, params->shift_window, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch_host: box too large for the stage-5 kernels");
   if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
     return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch_host: coarse grid too large for one CTA");
   cudaStream_t s = (cudaStream_t)stream;

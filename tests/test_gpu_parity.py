@@ -306,7 +306,8 @@ def test_invalid_arguments_rejected():
 
 # ------------------------------------------------------------------ stage 5: translation (App. C)
 @pytest.mark.parametrize("N,W,shift_mode", [(32, 4, gen.SHIFT_FIXED), (32, 3, gen.SHIFT_UNIFORM), (64, 8, gen.SHIFT_UNIFORM),
-                                            (32, 8, gen.SHIFT_UNIFORM), (24, 6, gen.SHIFT_FIXED)])
+                                            (32, 8, gen.SHIFT_UNIFORM), (24, 6, gen.SHIFT_FIXED),
+                                            (40, 4, gen.SHIFT_UNIFORM), (56, 5, gen.SHIFT_FIXED)])
 def test_translation_update_parity(N, W, shift_mode, prec):
     B = 4
     b = gen.particles(N, B, 1.0, seed=41, shift_mode=shift_mode, shift_max=W - 1.0, fixed_shift=(1.0, -2.0, 1.0))
