@@ -136,6 +136,12 @@ FftRadix fft_radix(int n);
 bool trans_supported(int N, int W, bool fp64);  // shared-memory limits of the stage-5 kernels
 template <typename T, typename Tin>
 cudaError_t launch_plane_r2c(const Tin* vol, int N, int64_t nb, cplx_t<T>* out, cudaStream_t s);
+// FP32 fast path (N = 32, 64, 96, 128): compile-time FFTs; rot = true fuses the rotation of the reference (read
+// through `tex`, a 2-D texture over launch_pad_ref's zero-padded plane stack) into the transform of rho
+bool plane_fast_supported(int N);
+cudaError_t launch_plane_fft_f32(const float* vol, cudaTextureObject_t tex, const float* euler, int estride, int N,
+                                 int64_t nb, float2* out, bool rot, cudaStream_t s);
+cudaError_t launch_pad_ref(const float* ref, int N, int pitch, float* pad, cudaStream_t s);
 size_t window_scratch_reals(int N, int W);
 template <typename T>
 cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N, int W, int64_t nb, T* scratch,

@@ -468,6 +468,241 @@ __global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ cw_al
     if (peak) peak[p] = c0 / ((T)N * N);
   }
 }
+
+// ==== FP32 fast path for the common box edges (N = 32, 64, 96, 128): compile-time FFT stages, the rotation fused
+// into the transform of rho (texture gathers), register-blocked z correlation ====================================
+__host__ __device__ constexpr int ct_nst(int n) {
+  int s = 0;
+  while (n % 4 == 0) { n /= 4; ++s; }
+  while (n % 2 == 0) { n /= 2; ++s; }
+  while (n % 3 == 0) { n /= 3; ++s; }
+  for (int r = 5; n > 1; r += 2)
+    while (n % r == 0) { n /= r; ++s; }
+  return s;
+}
+// k-th radix (same order as fft_radix) and the product of the radices before it
+__host__ __device__ constexpr int ct_rad(int n, int k) {
+  int s = 0;
+  while (n % 4 == 0) { if (s++ == k) return 4; n /= 4; }
+  while (n % 2 == 0) { if (s++ == k) return 2; n /= 2; }
+  while (n % 3 == 0) { if (s++ == k) return 3; n /= 3; }
+  for (int r = 5; n > 1; r += 2)
+    while (n % r == 0) { if (s++ == k) return r; n /= r; }
+  return 1;
+}
+__host__ __device__ constexpr int ct_ns(int n, int k) {
+  int p = 1;
+  for (int i = 0; i < k; ++i) p *= ct_rad(n, i);
+  return p;
+}
+
+constexpr int kFftThreads = 512;
+
+// one Stockham stage on NL lines of length N at line stride LS (compile time: the index divisions are shifts/mults)
+template <int N, int NL, int LS, int S>
+__device__ __forceinline__ void ct_stage(const float2* __restrict__ a, float2* __restrict__ b,
+                                         const float2* __restrict__ tw) {
+  constexpr int R = ct_rad(N, S), Ns = ct_ns(N, S), NB = N / R, TS = N / (Ns * R), TOT = NL * NB;
+#pragma unroll
+  for (int t0 = 0; t0 < TOT; t0 += kFftThreads) {
+    const int t = t0 + (int)threadIdx.x;
+    if (TOT % kFftThreads != 0 && t >= TOT) break;
+    const int l = t / NB, j = t - l * NB, k = j % Ns;
+    const float2* in = a + l * LS + j;
+    float2* out = b + l * LS + (j - k) * R + k;
+    if constexpr (R == 4) {
+      const float2 v0 = in[0], v1 = cmul<float>(in[NB], tw[k * TS]), v2 = cmul<float>(in[2 * NB], tw[2 * k * TS]),
+                   v3 = cmul<float>(in[3 * NB], tw[3 * k * TS]);
+      const float2 s02 = cadd<float>(v0, v2), d02 = csub<float>(v0, v2), s13 = cadd<float>(v1, v3),
+                   d13 = cmi<float>(csub<float>(v1, v3));
+      out[0] = cadd<float>(s02, s13);
+      out[Ns] = cadd<float>(d02, d13);
+      out[2 * Ns] = csub<float>(s02, s13);
+      out[3 * Ns] = csub<float>(d02, d13);
+    } else if constexpr (R == 2) {
+      const float2 v0 = in[0], v1 = cmul<float>(in[NB], tw[k * TS]);
+      out[0] = cadd<float>(v0, v1);
+      out[Ns] = csub<float>(v0, v1);
+    } else {
+      static_assert(R == 3, "fast path: radices 4, 2, 3");
+      const float2 v0 = in[0], v1 = cmul<float>(in[NB], tw[k * TS]), v2 = cmul<float>(in[2 * NB], tw[2 * k * TS]);
+      const float h = 0.86602540378443864676f;
+      const float2 sm = cadd<float>(v1, v2), df = csub<float>(v1, v2);
+      const float2 m = make_float2(v0.x - 0.5f * sm.x, v0.y - 0.5f * sm.y);
+      out[0] = cadd<float>(v0, sm);
+      out[Ns] = make_float2(m.x + h * df.y, m.y - h * df.x);
+      out[2 * Ns] = make_float2(m.x - h * df.y, m.y + h * df.x);
+    }
+  }
+}
+template <int N, int NL, int LS, int S = 0>
+__device__ __forceinline__ float2* ct_fft(float2* a, float2* b, const float2* tw) {
+  if constexpr (S == ct_nst(N)) {
+    return a;
+  } else {
+    ct_stage<N, NL, LS, S>(a, b, tw);
+    __syncthreads();
+    return ct_fft<N, NL, LS, S + 1>(b, a, tw);
+  }
+}
+
+template <int N> constexpr size_t plane_fast_smem() {
+  constexpr int H = N / 2 + 1, LP = N + 1;
+  return sizeof(float2) * ((size_t)N + (size_t)N * N + (size_t)H * LP);
+}
+
+// 2-D R2C of every z-plane, FP32, compile-time N.  ROT = false: u = the particle volume (float [N][N][N]);
+// ROT = true: u = rho_p(x) = h(R_p^T (x - c) + c) computed here from the reference through a 2-D texture over the
+// zero-padded plane stack (row z (N+1) + y; row z (N+1) + N is zero; border = 0), two tld4 gathers per voxel (the
+// 2 x 2 footprints of planes z0 and z0 + 1), with k_rotate_ref's exact trilinear arithmetic; rho never touches HBM.
+template <int N, bool ROT>
+__global__ void __launch_bounds__(kFftThreads, 1) k_plane_fft(const float* __restrict__ vol, cudaTextureObject_t tex,
+                                                              const float* __restrict__ euler, int estride,
+                                                              float2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int H = N / 2 + 1, LP = N + 1;
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* A = tw + N;              // [N/2][N] x-pass lines, then (with B) the y-pass ping-pong buffer
+  float2* B = A + (N / 2) * N;
+  float2* C = B + (N / 2) * N;     // [H][LP]: y-pass lines (column kx of the half rows)
+  __shared__ double Rm[9];
+  const int z = blockIdx.x;
+  const int64_t p = blockIdx.y;
+  build_roots<float>(tw, N, -1);
+  if (ROT) {
+    if (threadIdx.x == 0) rot_matrix<float>(euler + p * estride, Rm);
+    __syncthreads();
+    const float c = 0.5f * (float)(N - 1);
+    const float r0 = (float)Rm[0], r1 = (float)Rm[1], r2 = (float)Rm[2], r3 = (float)Rm[3], r4 = (float)Rm[4],
+                r5 = (float)Rm[5], r6 = (float)Rm[6], r7 = (float)Rm[7], r8 = (float)Rm[8];
+    const float uz = (float)z - c;
+    for (int i = threadIdx.x; i < (N / 2) * N; i += kFftThreads) {
+      const int l = i / N, x = i - l * N;
+      float v2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float ux = (float)x - c, uy = (float)(2 * l + h) - c;
+        const float qx = fmaf(r0, ux, fmaf(r3, uy, r6 * uz)) + c;  // R^T v
+        const float qy = fmaf(r1, ux, fmaf(r4, uy, r7 * uz)) + c;
+        const float qz = fmaf(r2, ux, fmaf(r5, uy, r8 * uz)) + c;
+        const float fx0 = floorf(qx), fy0 = floorf(qy), fz0 = floorf(qz);
+        const int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
+        const float fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
+        const float tu = (float)x0 + 1.0f;
+        float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
+        if ((unsigned)z0 < (unsigned)N) g0 = tex2Dgather<float4>(tex, tu, (float)(z0 * (N + 1) + y0) + 1.0f, 0);
+        if ((unsigned)(z0 + 1) < (unsigned)N)
+          g1 = tex2Dgather<float4>(tex, tu, (float)((z0 + 1) * (N + 1) + y0) + 1.0f, 0);
+        // gather order: x = (x0, y0+1), y = (x0+1, y0+1), z = (x0+1, y0), w = (x0, y0)
+        const float c00 = fmaf(fx, g0.z - g0.w, g0.w);
+        const float c01 = fmaf(fx, g0.y - g0.x, g0.x);
+        const float c10 = fmaf(fx, g1.z - g1.w, g1.w);
+        const float c11 = fmaf(fx, g1.y - g1.x, g1.x);
+        const float c0 = fmaf(fy, c01 - c00, c00);
+        const float c1 = fmaf(fy, c11 - c10, c10);
+        v2[h] = fmaf(fz, c1 - c0, c0);
+      }
+      A[i] = make_float2(v2[0], v2[1]);
+    }
+  } else {
+    const float* u = vol + (p * N + z) * (int64_t)N * N;
+    for (int i = threadIdx.x; i < (N / 2) * N; i += kFftThreads) {
+      const int l = i / N, x = i - l * N;
+      A[i] = make_float2(__ldg(u + 2 * l * N + x), __ldg(u + (2 * l + 1) * N + x));
+    }
+  }
+  __syncthreads();
+  const float2* res = ct_fft<N, N / 2, N>(A, B, tw);
+  for (int i = threadIdx.x; i < (N / 2) * H; i += kFftThreads) {
+    const int l = i / H, k = i - l * H;
+    const float2 Z = res[l * N + k], Zc = res[l * N + (N - k) % N];
+    C[k * LP + 2 * l] = make_float2(0.5f * (Z.x + Zc.x), 0.5f * (Z.y - Zc.y));
+    C[k * LP + 2 * l + 1] = make_float2(0.5f * (Z.y + Zc.y), -0.5f * (Z.x - Zc.x));
+  }
+  __syncthreads();
+  const float2* res2 = ct_fft<N, H, LP>(C, A, tw);
+  float2* o = out + (p * N + z) * (int64_t)N * H;
+  for (int i = threadIdx.x; i < N * H; i += kFftThreads) {
+    const int ky = i / H, kx = i - ky * H;
+    o[i] = res2[kx * LP + ky];
+  }
+}
+
+// zero-padded plane stack of the reference for the gathers: pad[(z (N+1) + y) * pitch + x] (row z (N+1) + N = 0)
+__global__ void k_pad_ref(const float* __restrict__ ref, int N, int pitch, float* __restrict__ pad) {
+  const int64_t n = (int64_t)N * (N + 1) * pitch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % pitch);
+    const int64_t row = i / pitch;
+    const int z = (int)(row / (N + 1)), y = (int)(row % (N + 1));
+    pad[i] = (x < N && y < N) ? ref[((int64_t)z * N + y) * N + x] : 0.f;
+  }
+}
+
+// register-blocked z correlation: thread (z segment s, tz block bk of TB, kx): TB accumulators, a rolling window of
+// TB f~ values (one new shared-memory load and one rho~ load per z for TB complex MACs); the S segment partials are
+// summed in a fixed order (deterministic).
+template <int TB>
+__global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft, const float2* __restrict__ rt, int N,
+                                                  int W, int hc, int S, float2* __restrict__ Y1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int H = N / 2 + 1, wp = 2 * W + 3, nkc = (H + hc - 1) / hc, ld = N + 1, nblk = (wp + TB - 1) / TB;
+  float2* fs = reinterpret_cast<float2*>(smem_raw);  // [hc][N+1]
+  float2* rs = fs + hc * ld;                          // [hc][N+1]
+  const int ky = blockIdx.x / nkc, kx0 = (blockIdx.x - ky * nkc) * hc, nk = min(hc, H - kx0);
+  const int64_t p = blockIdx.y;
+  for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
+    const int zz = i / nk, kl = i - zz * nk;
+    const int64_t g = ((p * N + zz) * N + ky) * (int64_t)H + kx0 + kl;
+    fs[kl * ld + zz] = ft[g];
+    rs[kl * ld + zz] = rt[g];
+  }
+  __syncthreads();
+  const int kl = threadIdx.x % hc, rest = threadIdx.x / hc, bk = rest % nblk, s = rest / nblk;
+  const bool live = s < S && kl < nk;
+  const int zseg = N / S, z0 = s * zseg, a0 = bk * TB;
+  float2 acc[TB];
+#pragma unroll
+  for (int u = 0; u < TB; ++u) acc[u] = make_float2(0.f, 0.f);
+  if (live) {
+    const float2* fr = fs + kl * ld;
+    const float2* rr = rs + kl * ld;
+    float2 fw[TB];
+    int zi = ((z0 + a0 - (W + 1)) % N + N) % N;
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      fw[u] = fr[zi];
+      if (++zi == N) zi = 0;
+    }
+    for (int zz = z0; zz < z0 + zseg; ++zz) {
+      const float2 r = rr[zz];
+#pragma unroll
+      for (int u = 0; u < TB; ++u) {
+        acc[u].x = fmaf(fw[u].x, r.x, fmaf(fw[u].y, r.y, acc[u].x));  // f conj(r)
+        acc[u].y = fmaf(fw[u].y, r.x, fmaf(-fw[u].x, r.y, acc[u].y));
+      }
+#pragma unroll
+      for (int u = 0; u + 1 < TB; ++u) fw[u] = fw[u + 1];
+      fw[TB - 1] = fr[zi];
+      if (++zi == N) zi = 0;
+    }
+  }
+  __syncthreads();
+  float2* part = fs;  // [S][wp][hc]
+  if (live) {
+#pragma unroll
+    for (int u = 0; u < TB; ++u)
+      if (a0 + u < wp) part[(s * wp + a0 + u) * hc + kl] = acc[u];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < wp * nk; i += blockDim.x) {
+    const int a = i / nk, k = i - a * nk;
+    float2 v = part[a * hc + k];
+    for (int q = 1; q < S; ++q) v = cadd<float>(v, part[(q * wp + a) * hc + k]);
+    Y1[((p * wp + a) * N + ky) * (int64_t)H + kx0 + k] = v;
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -541,6 +776,37 @@ cudaError_t launch_plane_r2c(const Tin* vol, int N, int64_t nb, cplx_t<T>* out, 
   return cudaGetLastError();
 }
 
+bool plane_fast_supported(int N) { return N == 32 || N == 64 || N == 96 || N == 128; }
+
+template <int N>
+static cudaError_t launch_plane_fast(const float* vol, cudaTextureObject_t tex, const float* euler, int estride,
+                                     int64_t nb, float2* out, bool rot, cudaStream_t s) {
+  constexpr size_t smem = plane_fast_smem<N>();
+  static_assert(smem <= 227 * 1024, "plane buffers exceed shared memory");
+  auto kern = rot ? k_plane_fft<N, true> : k_plane_fft<N, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3((unsigned)N, (unsigned)nb), kFftThreads, smem, s>>>(vol, tex, euler, estride, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plane_fft_f32(const float* vol, cudaTextureObject_t tex, const float* euler, int estride, int N,
+                                 int64_t nb, float2* out, bool rot, cudaStream_t s) {
+  if (nb == 0) return cudaSuccess;
+  switch (N) {
+    case 32: return launch_plane_fast<32>(vol, tex, euler, estride, nb, out, rot, s);
+    case 64: return launch_plane_fast<64>(vol, tex, euler, estride, nb, out, rot, s);
+    case 96: return launch_plane_fast<96>(vol, tex, euler, estride, nb, out, rot, s);
+    case 128: return launch_plane_fast<128>(vol, tex, euler, estride, nb, out, rot, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_pad_ref(const float* ref, int N, int pitch, float* pad, cudaStream_t s) {
+  k_pad_ref<<<592, 256, 0, s>>>(ref, N, pitch, pad);
+  return cudaGetLastError();
+}
+
 size_t window_scratch_reals(int N, int W) {
   const int64_t wp = 2 * W + 3, H = N / 2 + 1;
   return (size_t)(2 * wp * N * H + wp * wp * wp);
@@ -558,9 +824,26 @@ cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N,
   cplx_t<T>* Y1 = reinterpret_cast<cplx_t<T>*>(scratch);
   T* cw = scratch + 2 * nb * (int64_t)wp * N * H;
   const size_t zsm = 2 * csz * (size_t)hc * (N + 1);
-  cudaError_t e = cudaFuncSetAttribute(k_zcorr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
-  if (e != cudaSuccess) return e;
-  k_zcorr<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, N, W, hc, Y1);
+  cudaError_t e;
+  if constexpr (sizeof(T) == 4) {
+    constexpr int TB = 5;
+    const int nblk = (wp + TB - 1) / TB;
+    int S = 1;
+    for (int q : {4, 3, 2})
+      if (N % q == 0 && q * nblk * hc <= 512 && q * wp <= 2 * (N + 1)) {
+        S = q;
+        break;
+      }
+    const int thr = std::min(512, (S * nblk * hc + 31) / 32 * 32);
+    if (S * nblk * hc > 512) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(k_zcorr_rb<TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
+    if (e != cudaSuccess) return e;
+    k_zcorr_rb<TB><<<dim3((unsigned)(N * nkc), (unsigned)nb), thr, zsm, s>>>(ft, rt, N, W, hc, S, Y1);
+  } else {
+    e = cudaFuncSetAttribute(k_zcorr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
+    if (e != cudaSuccess) return e;
+    k_zcorr<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, N, W, hc, Y1);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t xsm = window_xy_smem(N, W, csz);
   e = cudaFuncSetAttribute(k_window_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);

@@ -63,6 +63,10 @@ struct matcha_ctx {
   void* ws_peak = nullptr;   // real [mb]
   void* ws_win = nullptr;    // real [mb][window_scratch_reals(N, W)]: Y1 (z correlation) + the c window
   int ws_win_W = -1;
+  bool trans_fast = false;   // FP32 and N in {32, 64, 96, 128}: compile-time FFTs, rotation fused into rho's transform
+  float* ws_refpad = nullptr;  // zero-padded plane stack of the reference (texture source of the fused rotation)
+  int refpad_pitch = 0;        // floats per row
+  cudaTextureObject_t tex_ref = 0;
   void* ws_euler1 = nullptr; // real [mb][3]
   // per-stage event tracing
   bool prof = false;
@@ -296,10 +300,35 @@ static matcha_status_t trans_prepare(matcha_handle_t h, int W) {
   if (!h->ws_Fhat) {
     cudaError_t e = cudaMalloc(&h->ws_Fhat, 2 * h->rsz * nc * mb);
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_Xhat, 2 * h->rsz * nc * mb);
-    if (e == cudaSuccess) e = cudaMalloc(&h->ws_rho, h->rsz * nr * mb);
+    h->trans_fast = !h->fp64 && plane_fast_supported(N);
+    if (e == cudaSuccess && !h->trans_fast) e = cudaMalloc(&h->ws_rho, h->rsz * nr * mb);
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_peak, h->rsz * mb);
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_euler1, 3 * h->rsz * mb);
     if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation workspace allocation failed");
+    if (h->trans_fast) {
+      int align = 32;
+      cudaDeviceGetAttribute(&align, cudaDevAttrTexturePitchAlignment, h->device);
+      const int af = std::max(1, align / (int)sizeof(float));
+      h->refpad_pitch = (N + af - 1) / af * af;
+      e = cudaMalloc((void**)&h->ws_refpad, sizeof(float) * (size_t)h->refpad_pitch * N * (N + 1));
+      if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation reference texture allocation failed");
+      cudaResourceDesc rd;
+      std::memset(&rd, 0, sizeof(rd));
+      rd.resType = cudaResourceTypePitch2D;
+      rd.res.pitch2D.devPtr = h->ws_refpad;
+      rd.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+      rd.res.pitch2D.width = N;
+      rd.res.pitch2D.height = (size_t)N * (N + 1);
+      rd.res.pitch2D.pitchInBytes = sizeof(float) * (size_t)h->refpad_pitch;
+      cudaTextureDesc td;
+      std::memset(&td, 0, sizeof(td));
+      td.addressMode[0] = td.addressMode[1] = cudaAddressModeBorder;  // border colour 0: zero outside the box
+      td.filterMode = cudaFilterModePoint;
+      td.readMode = cudaReadModeElementType;
+      td.normalizedCoords = 0;
+      e = cudaCreateTextureObject(&h->tex_ref, &rd, &td, nullptr);
+      if (e != cudaSuccess) return cuda_fail(h, e, "translation: reference texture");
+    }
   }
   if (h->ws_win_W < W) {
     if (h->ws_win) cudaFree(h->ws_win);
@@ -318,7 +347,9 @@ static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t 
   matcha_status_t st = trans_prepare(h, W);
   if (st != MATCHA_OK) return st;
   cudaError_t e = h->fp64 ? launch_plane_r2c<double, float>(vols, h->cfg.N, nb, (double2*)h->ws_Fhat, s)
-                          : launch_plane_r2c<float, float>(vols, h->cfg.N, nb, (float2*)h->ws_Fhat, s);
+                  : h->trans_fast
+                      ? launch_plane_fft_f32(vols, 0, nullptr, 0, h->cfg.N, nb, (float2*)h->ws_Fhat, false, s)
+                      : launch_plane_r2c<float, float>(vols, h->cfg.N, nb, (float2*)h->ws_Fhat, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of the particles");
   h->launches++;
   return MATCHA_OK;
@@ -332,12 +363,20 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
   ProfScope ps(h, 5, s);
   matcha_status_t st = trans_prepare(h, W);
   if (st != MATCHA_OK) return st;
-  e = h->fp64 ? launch_rotate_ref<double>(ref, N, (const double*)euler, estride, nb, (double*)h->ws_rho, s)
-              : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
-  if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
-  e = h->fp64 ? launch_plane_r2c<double, double>((const double*)h->ws_rho, N, nb, (double2*)h->ws_Xhat, s)
-              : launch_plane_r2c<float, float>((const float*)h->ws_rho, N, nb, (float2*)h->ws_Xhat, s);
-  if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of rho");
+  if (h->trans_fast) {
+    // rho~ straight from the reference texture: the rotated references never touch HBM
+    e = launch_pad_ref(ref, N, h->refpad_pitch, h->ws_refpad, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: pad_ref");
+    e = launch_plane_fft_f32(nullptr, h->tex_ref, (const float*)euler, estride, N, nb, (float2*)h->ws_Xhat, true, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_fft of rho");
+  } else {
+    e = h->fp64 ? launch_rotate_ref<double>(ref, N, (const double*)euler, estride, nb, (double*)h->ws_rho, s)
+                : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
+    e = h->fp64 ? launch_plane_r2c<double, double>((const double*)h->ws_rho, N, nb, (double2*)h->ws_Xhat, s)
+                : launch_plane_r2c<float, float>((const float*)h->ws_rho, N, nb, (float2*)h->ws_Xhat, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of rho");
+  }
   e = h->fp64 ? launch_window_zcorr<double>((const double2*)h->ws_Fhat, (const double2*)h->ws_Xhat, N, W, nb,
                                             (double*)h->ws_win, (double*)shifts, sstride, (double*)peak, s)
               : launch_window_zcorr<float>((const float2*)h->ws_Fhat, (const float2*)h->ws_Xhat, N, W, nb,
@@ -562,7 +601,8 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win})
+  if (h->tex_ref) cudaDestroyTextureObject(h->tex_ref);
+  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
