@@ -590,8 +590,11 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_plane_fft(const float* __res
         const float fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
         const float tu = (float)x0 + 1.0f;
         float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
-        if ((unsigned)z0 < (unsigned)N) g0 = tex2Dgather<float4>(tex, tu, (float)(z0 * (N + 1) + y0) + 1.0f, 0);
-        if ((unsigned)(z0 + 1) < (unsigned)N)
+        // rows y0, y0 + 1 stay inside plane z0's N + 1 rows (the zero row / the border) only for -1 <= y0 <= N - 1;
+        // beyond that both rows are outside the box
+        const bool yin = (unsigned)(y0 + 1) <= (unsigned)N;
+        if (yin && (unsigned)z0 < (unsigned)N) g0 = tex2Dgather<float4>(tex, tu, (float)(z0 * (N + 1) + y0) + 1.0f, 0);
+        if (yin && (unsigned)(z0 + 1) < (unsigned)N)
           g1 = tex2Dgather<float4>(tex, tu, (float)((z0 + 1) * (N + 1) + y0) + 1.0f, 0);
         // gather order: x = (x0, y0+1), y = (x0+1, y0+1), z = (x0+1, y0), w = (x0, y0)
         const float c00 = fmaf(fx, g0.z - g0.w, g0.w);
