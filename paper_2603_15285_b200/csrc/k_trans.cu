@@ -576,6 +576,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_plane_fft(const float* __res
     const float r0 = (float)Rm[0], r1 = (float)Rm[1], r2 = (float)Rm[2], r3 = (float)Rm[3], r4 = (float)Rm[4],
                 r5 = (float)Rm[5], r6 = (float)Rm[6], r7 = (float)Rm[7], r8 = (float)Rm[8];
     const float uz = (float)z - c;
+#pragma unroll 3
     for (int i = threadIdx.x; i < (N / 2) * N; i += kFftThreads) {
       const int l = i / N, x = i - l * N;
       float v2[2];
@@ -608,11 +609,19 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_plane_fft(const float* __res
       A[i] = make_float2(v2[0], v2[1]);
     }
   } else {
+    // all of the plane's loads in flight before the first shared-memory store (a load -> store loop is latency bound)
     const float* u = vol + (p * N + z) * (int64_t)N * N;
-    for (int i = threadIdx.x; i < (N / 2) * N; i += kFftThreads) {
-      const int l = i / N, x = i - l * N;
-      A[i] = make_float2(__ldg(u + 2 * l * N + x), __ldg(u + (2 * l + 1) * N + x));
+    constexpr int IT = (N / 2) * N / kFftThreads;
+    static_assert(IT * kFftThreads == (N / 2) * N, "plane tiles the CTA");
+    float e0[IT], e1[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = (int)threadIdx.x + it * kFftThreads, l = i / N, x = i - l * N;
+      e0[it] = __ldg(u + 2 * l * N + x);
+      e1[it] = __ldg(u + (2 * l + 1) * N + x);
     }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) A[(int)threadIdx.x + it * kFftThreads] = make_float2(e0[it], e1[it]);
   }
   __syncthreads();
   const float2* res = ct_fft<N, N / 2, N>(A, B, tw);
@@ -649,16 +658,23 @@ template <int TB>
 __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft, const float2* __restrict__ rt, int N,
                                                   int W, int hc, int S, float2* __restrict__ Y1) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int H = N / 2 + 1, wp = 2 * W + 3, nkc = (H + hc - 1) / hc, ld = N + 1, nblk = (wp + TB - 1) / TB;
-  float2* fs = reinterpret_cast<float2*>(smem_raw);  // [hc][N+1]
-  float2* rs = fs + hc * ld;                          // [hc][N+1]
+  const int H = N / 2 + 1, wp = 2 * W + 3, nkc = (H + hc - 1) / hc, nblk = (wp + TB - 1) / TB;
+  float2* fs = reinterpret_cast<float2*>(smem_raw);  // [N][hc]  (natural layout: lanes own consecutive kx)
+  float2* rs = fs + N * hc;                           // [N][hc]
   const int ky = blockIdx.x / nkc, kx0 = (blockIdx.x - ky * nkc) * hc, nk = min(hc, H - kx0);
   const int64_t p = blockIdx.y;
-  for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
-    const int zz = i / nk, kl = i - zz * nk;
-    const int64_t g = ((p * N + zz) * N + ky) * (int64_t)H + kx0 + kl;
-    fs[kl * ld + zz] = ft[g];
-    rs[kl * ld + zz] = rt[g];
+  {
+    // asynchronous 8-byte copies of the N row segments (one in flight per element, no register round trip)
+    const int64_t row0 = (p * N * N + ky) * (int64_t)H + kx0;  // z = 0
+    for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
+      const int zz = i / nk, kl = i - zz * nk;
+      const int64_t g = row0 + (int64_t)zz * N * H + kl;
+      const unsigned df = (unsigned)__cvta_generic_to_shared(fs + zz * hc + kl);
+      const unsigned dr = (unsigned)__cvta_generic_to_shared(rs + zz * hc + kl);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(df), "l"(ft + g));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dr), "l"(rt + g));
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
   }
   __syncthreads();
   const int kl = threadIdx.x % hc, rest = threadIdx.x / hc, bk = rest % nblk, s = rest / nblk;
@@ -668,17 +684,17 @@ __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft,
 #pragma unroll
   for (int u = 0; u < TB; ++u) acc[u] = make_float2(0.f, 0.f);
   if (live) {
-    const float2* fr = fs + kl * ld;
-    const float2* rr = rs + kl * ld;
+    const float2* fr = fs + kl;
+    const float2* rr = rs + kl;
     float2 fw[TB];
     int zi = ((z0 + a0 - (W + 1)) % N + N) % N;
 #pragma unroll
     for (int u = 0; u < TB; ++u) {
-      fw[u] = fr[zi];
+      fw[u] = fr[zi * hc];
       if (++zi == N) zi = 0;
     }
     for (int zz = z0; zz < z0 + zseg; ++zz) {
-      const float2 r = rr[zz];
+      const float2 r = rr[zz * hc];
 #pragma unroll
       for (int u = 0; u < TB; ++u) {
         acc[u].x = fmaf(fw[u].x, r.x, fmaf(fw[u].y, r.y, acc[u].x));  // f conj(r)
@@ -686,12 +702,12 @@ __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft,
       }
 #pragma unroll
       for (int u = 0; u + 1 < TB; ++u) fw[u] = fw[u + 1];
-      fw[TB - 1] = fr[zi];
+      fw[TB - 1] = fr[zi * hc];
       if (++zi == N) zi = 0;
     }
   }
   __syncthreads();
-  float2* part = fs;  // [S][wp][hc]
+  float2* part = fs;  // [S][wp][hc] (S wp <= 2 N: fits fs + rs)
   if (live) {
 #pragma unroll
     for (int u = 0; u < TB; ++u)
@@ -833,7 +849,7 @@ cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N,
     const int nblk = (wp + TB - 1) / TB;
     int S = 1;
     for (int q : {4, 3, 2})
-      if (N % q == 0 && q * nblk * hc <= 512 && q * wp <= 2 * (N + 1)) {
+      if (N % q == 0 && q * nblk * hc <= 512 && q * wp <= 2 * N) {
         S = q;
         break;
       }
