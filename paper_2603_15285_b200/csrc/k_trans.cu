@@ -497,6 +497,9 @@ __host__ __device__ constexpr int ct_ns(int n, int k) {
 }
 
 constexpr int kFftThreads = 512;
+// shared-memory index padding of the FFT line buffers: one float2 of slack every 16 (the radix-R stage writes at
+// stride R and the transposes at stride N + 1; without it a warp's 8-byte stores hit 4 banks 4-way)
+__host__ __device__ constexpr int fpad(int i) { return i + (i >> 4); }
 
 // one Stockham stage on NL lines of length N at line stride LS (compile time: the index divisions are shifts/mults)
 template <int N, int NL, int LS, int S>
@@ -508,30 +511,31 @@ __device__ __forceinline__ void ct_stage(const float2* __restrict__ a, float2* _
     const int t = t0 + (int)threadIdx.x;
     if (TOT % kFftThreads != 0 && t >= TOT) break;
     const int l = t / NB, j = t - l * NB, k = j % Ns;
-    const float2* in = a + l * LS + j;
-    float2* out = b + l * LS + (j - k) * R + k;
+    const int ib = l * LS + j, ob = l * LS + (j - k) * R + k;
     if constexpr (R == 4) {
-      const float2 v0 = in[0], v1 = cmul<float>(in[NB], tw[k * TS]), v2 = cmul<float>(in[2 * NB], tw[2 * k * TS]),
-                   v3 = cmul<float>(in[3 * NB], tw[3 * k * TS]);
+      const float2 v0 = a[fpad(ib)], v1 = cmul<float>(a[fpad(ib + NB)], tw[k * TS]),
+                   v2 = cmul<float>(a[fpad(ib + 2 * NB)], tw[2 * k * TS]),
+                   v3 = cmul<float>(a[fpad(ib + 3 * NB)], tw[3 * k * TS]);
       const float2 s02 = cadd<float>(v0, v2), d02 = csub<float>(v0, v2), s13 = cadd<float>(v1, v3),
                    d13 = cmi<float>(csub<float>(v1, v3));
-      out[0] = cadd<float>(s02, s13);
-      out[Ns] = cadd<float>(d02, d13);
-      out[2 * Ns] = csub<float>(s02, s13);
-      out[3 * Ns] = csub<float>(d02, d13);
+      b[fpad(ob)] = cadd<float>(s02, s13);
+      b[fpad(ob + Ns)] = cadd<float>(d02, d13);
+      b[fpad(ob + 2 * Ns)] = csub<float>(s02, s13);
+      b[fpad(ob + 3 * Ns)] = csub<float>(d02, d13);
     } else if constexpr (R == 2) {
-      const float2 v0 = in[0], v1 = cmul<float>(in[NB], tw[k * TS]);
-      out[0] = cadd<float>(v0, v1);
-      out[Ns] = csub<float>(v0, v1);
+      const float2 v0 = a[fpad(ib)], v1 = cmul<float>(a[fpad(ib + NB)], tw[k * TS]);
+      b[fpad(ob)] = cadd<float>(v0, v1);
+      b[fpad(ob + Ns)] = csub<float>(v0, v1);
     } else {
       static_assert(R == 3, "fast path: radices 4, 2, 3");
-      const float2 v0 = in[0], v1 = cmul<float>(in[NB], tw[k * TS]), v2 = cmul<float>(in[2 * NB], tw[2 * k * TS]);
+      const float2 v0 = a[fpad(ib)], v1 = cmul<float>(a[fpad(ib + NB)], tw[k * TS]),
+                   v2 = cmul<float>(a[fpad(ib + 2 * NB)], tw[2 * k * TS]);
       const float h = 0.86602540378443864676f;
       const float2 sm = cadd<float>(v1, v2), df = csub<float>(v1, v2);
       const float2 m = make_float2(v0.x - 0.5f * sm.x, v0.y - 0.5f * sm.y);
-      out[0] = cadd<float>(v0, sm);
-      out[Ns] = make_float2(m.x + h * df.y, m.y - h * df.x);
-      out[2 * Ns] = make_float2(m.x - h * df.y, m.y + h * df.x);
+      b[fpad(ob)] = cadd<float>(v0, sm);
+      b[fpad(ob + Ns)] = make_float2(m.x + h * df.y, m.y - h * df.x);
+      b[fpad(ob + 2 * Ns)] = make_float2(m.x - h * df.y, m.y + h * df.x);
     }
   }
 }
@@ -546,9 +550,15 @@ __device__ __forceinline__ float2* ct_fft(float2* a, float2* b, const float2* tw
   }
 }
 
+// buffer sizes (float2) with the fpad slack: the x pass runs in two halves of N/4 row pairs (A <-> B); the y pass
+// ping-pongs C with A + B
+template <int N> constexpr int plane_c() { return fpad((N / 2 + 1) * (N + 1)); }
+template <int N> constexpr int plane_ab() {
+  return fpad((N / 4) * N) > (plane_c<N>() + 1) / 2 ? fpad((N / 4) * N) : (plane_c<N>() + 1) / 2;
+}
 template <int N> constexpr size_t plane_fast_smem() {
-  constexpr int H = N / 2 + 1, LP = N + 1;
-  return sizeof(float2) * ((size_t)N + (size_t)N * N + (size_t)H * LP);
+  static_assert(2 * plane_ab<N>() >= plane_c<N>(), "the y pass ping-pongs C with A + B");
+  return sizeof(float2) * ((size_t)N + 2 * (size_t)plane_ab<N>() + (size_t)plane_c<N>());
 }
 
 // 2-D R2C of every z-plane, FP32, compile-time N.  ROT = false: u = the particle volume (float [N][N][N]);
@@ -556,87 +566,97 @@ template <int N> constexpr size_t plane_fast_smem() {
 // zero-padded plane stack (row z (N+1) + y; row z (N+1) + N is zero; border = 0), two tld4 gathers per voxel (the
 // 2 x 2 footprints of planes z0 and z0 + 1), with k_rotate_ref's exact trilinear arithmetic; rho never touches HBM.
 template <int N, bool ROT>
-__global__ void __launch_bounds__(kFftThreads, 1) k_plane_fft(const float* __restrict__ vol, cudaTextureObject_t tex,
+__global__ void __launch_bounds__(kFftThreads, 2) k_plane_fft(const float* __restrict__ vol, cudaTextureObject_t tex,
                                                               const float* __restrict__ euler, int estride,
                                                               float2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int H = N / 2 + 1, LP = N + 1;
+  constexpr int H = N / 2 + 1, LP = N + 1, NQ = N / 4;  // NQ row pairs per x half
   float2* tw = reinterpret_cast<float2*>(smem_raw);
-  float2* A = tw + N;              // [N/2][N] x-pass lines, then (with B) the y-pass ping-pong buffer
-  float2* B = A + (N / 2) * N;
-  float2* C = B + (N / 2) * N;     // [H][LP]: y-pass lines (column kx of the half rows)
+  float2* A = tw + N;              // [N/4][N] x-pass lines, then (with B) the y-pass ping-pong buffer (fpad indices)
+  float2* B = A + plane_ab<N>();
+  float2* C = B + plane_ab<N>();   // [H][LP]: y-pass lines (column kx of the half rows)
   __shared__ double Rm[9];
   const int z = blockIdx.x;
   const int64_t p = blockIdx.y;
   build_roots<float>(tw, N, -1);
+  float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f, r4 = 0.f, r5 = 0.f, r6 = 0.f, r7 = 0.f, r8 = 0.f;
+  const float c = 0.5f * (float)(N - 1), uz = (float)z - c;
   if (ROT) {
     if (threadIdx.x == 0) rot_matrix<float>(euler + p * estride, Rm);
     __syncthreads();
-    const float c = 0.5f * (float)(N - 1);
-    const float r0 = (float)Rm[0], r1 = (float)Rm[1], r2 = (float)Rm[2], r3 = (float)Rm[3], r4 = (float)Rm[4],
-                r5 = (float)Rm[5], r6 = (float)Rm[6], r7 = (float)Rm[7], r8 = (float)Rm[8];
-    const float uz = (float)z - c;
-#pragma unroll 3
-    for (int i = threadIdx.x; i < (N / 2) * N; i += kFftThreads) {
-      const int l = i / N, x = i - l * N;
-      float v2[2];
+    r0 = (float)Rm[0], r1 = (float)Rm[1], r2 = (float)Rm[2], r3 = (float)Rm[3], r4 = (float)Rm[4],
+    r5 = (float)Rm[5], r6 = (float)Rm[6], r7 = (float)Rm[7], r8 = (float)Rm[8];
+  }
+  const float* u = vol + (p * N + z) * (int64_t)N * N;
+  for (int half = 0; half < 2; ++half) {
+    const int lb = half * NQ;  // first row pair of this half
+    if (ROT) {
+      for (int i = threadIdx.x; i < NQ * N; i += kFftThreads) {
+        const int l = i / N, x = i - l * N;
+        float v2[2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float ux = (float)x - c, uy = (float)(2 * l + h) - c;
-        const float qx = fmaf(r0, ux, fmaf(r3, uy, r6 * uz)) + c;  // R^T v
-        const float qy = fmaf(r1, ux, fmaf(r4, uy, r7 * uz)) + c;
-        const float qz = fmaf(r2, ux, fmaf(r5, uy, r8 * uz)) + c;
-        const float fx0 = floorf(qx), fy0 = floorf(qy), fz0 = floorf(qz);
-        const int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
-        const float fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
-        const float tu = (float)x0 + 1.0f;
-        float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
-        // rows y0, y0 + 1 stay inside plane z0's N + 1 rows (the zero row / the border) only for -1 <= y0 <= N - 1;
-        // beyond that both rows are outside the box
-        const bool yin = (unsigned)(y0 + 1) <= (unsigned)N;
-        if (yin && (unsigned)z0 < (unsigned)N) g0 = tex2Dgather<float4>(tex, tu, (float)(z0 * (N + 1) + y0) + 1.0f, 0);
-        if (yin && (unsigned)(z0 + 1) < (unsigned)N)
-          g1 = tex2Dgather<float4>(tex, tu, (float)((z0 + 1) * (N + 1) + y0) + 1.0f, 0);
-        // gather order: x = (x0, y0+1), y = (x0+1, y0+1), z = (x0+1, y0), w = (x0, y0)
-        const float c00 = fmaf(fx, g0.z - g0.w, g0.w);
-        const float c01 = fmaf(fx, g0.y - g0.x, g0.x);
-        const float c10 = fmaf(fx, g1.z - g1.w, g1.w);
-        const float c11 = fmaf(fx, g1.y - g1.x, g1.x);
-        const float c0 = fmaf(fy, c01 - c00, c00);
-        const float c1 = fmaf(fy, c11 - c10, c10);
-        v2[h] = fmaf(fz, c1 - c0, c0);
+        for (int h = 0; h < 2; ++h) {
+          const float ux = (float)x - c, uy = (float)(2 * (lb + l) + h) - c;
+          const float qx = fmaf(r0, ux, fmaf(r3, uy, r6 * uz)) + c;  // R^T v
+          const float qy = fmaf(r1, ux, fmaf(r4, uy, r7 * uz)) + c;
+          const float qz = fmaf(r2, ux, fmaf(r5, uy, r8 * uz)) + c;
+          const float fx0 = floorf(qx), fy0 = floorf(qy), fz0 = floorf(qz);
+          const int x0 = (int)fx0, y0 = (int)fy0, z0 = (int)fz0;
+          const float fx = qx - fx0, fy = qy - fy0, fz = qz - fz0;
+          const float tu = (float)x0 + 1.0f;
+          float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
+          // rows y0, y0 + 1 stay inside plane z0's N + 1 rows (the zero row / the border) only for -1 <= y0 <= N - 1;
+          // beyond that both rows are outside the box
+          const bool yin = (unsigned)(y0 + 1) <= (unsigned)N;
+          if (yin && (unsigned)z0 < (unsigned)N)
+            g0 = tex2Dgather<float4>(tex, tu, (float)(z0 * (N + 1) + y0) + 1.0f, 0);
+          if (yin && (unsigned)(z0 + 1) < (unsigned)N)
+            g1 = tex2Dgather<float4>(tex, tu, (float)((z0 + 1) * (N + 1) + y0) + 1.0f, 0);
+          // gather order (scripts/tld4_probe.cu): x = (x0, y0+1), y = (x0+1, y0+1), z = (x0+1, y0), w = (x0, y0)
+          const float c00 = fmaf(fx, g0.z - g0.w, g0.w);
+          const float c01 = fmaf(fx, g0.y - g0.x, g0.x);
+          const float c10 = fmaf(fx, g1.z - g1.w, g1.w);
+          const float c11 = fmaf(fx, g1.y - g1.x, g1.x);
+          const float c0 = fmaf(fy, c01 - c00, c00);
+          const float c1 = fmaf(fy, c11 - c10, c10);
+          v2[h] = fmaf(fz, c1 - c0, c0);
+        }
+        A[fpad(i)] = make_float2(v2[0], v2[1]);
       }
-      A[i] = make_float2(v2[0], v2[1]);
-    }
-  } else {
-    // all of the plane's loads in flight before the first shared-memory store (a load -> store loop is latency bound)
-    const float* u = vol + (p * N + z) * (int64_t)N * N;
-    constexpr int IT = (N / 2) * N / kFftThreads;
-    static_assert(IT * kFftThreads == (N / 2) * N, "plane tiles the CTA");
-    float e0[IT], e1[IT];
+    } else {
+      // all of the half plane's loads in flight before the first shared-memory store
+      constexpr int IT = (NQ * N + kFftThreads - 1) / kFftThreads;
+      float e0[IT], e1[IT];
 #pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int i = (int)threadIdx.x + it * kFftThreads, l = i / N, x = i - l * N;
-      e0[it] = __ldg(u + 2 * l * N + x);
-      e1[it] = __ldg(u + (2 * l + 1) * N + x);
-    }
+      for (int it = 0; it < IT; ++it) {
+        const int i = (int)threadIdx.x + it * kFftThreads, l = i / N, x = i - l * N;
+        if (i < NQ * N) {
+          e0[it] = __ldg(u + 2 * (lb + l) * N + x);
+          e1[it] = __ldg(u + (2 * (lb + l) + 1) * N + x);
+        }
+      }
 #pragma unroll
-    for (int it = 0; it < IT; ++it) A[(int)threadIdx.x + it * kFftThreads] = make_float2(e0[it], e1[it]);
+      for (int it = 0; it < IT; ++it) {
+        const int i = (int)threadIdx.x + it * kFftThreads;
+        if (i < NQ * N) A[fpad(i)] = make_float2(e0[it], e1[it]);
+      }
+    }
+    __syncthreads();
+    const float2* res = ct_fft<N, NQ, N>(A, B, tw);
+    for (int i = threadIdx.x; i < NQ * H; i += kFftThreads) {
+      const int l = i / H, k = i - l * H;
+      const float2 Z = res[fpad(l * N + k)], Zc = res[fpad(l * N + (N - k) % N)];
+      const int y = 2 * (lb + l);
+      C[fpad(k * LP + y)] = make_float2(0.5f * (Z.x + Zc.x), 0.5f * (Z.y - Zc.y));
+      C[fpad(k * LP + y + 1)] = make_float2(0.5f * (Z.y + Zc.y), -0.5f * (Z.x - Zc.x));
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  const float2* res = ct_fft<N, N / 2, N>(A, B, tw);
-  for (int i = threadIdx.x; i < (N / 2) * H; i += kFftThreads) {
-    const int l = i / H, k = i - l * H;
-    const float2 Z = res[l * N + k], Zc = res[l * N + (N - k) % N];
-    C[k * LP + 2 * l] = make_float2(0.5f * (Z.x + Zc.x), 0.5f * (Z.y - Zc.y));
-    C[k * LP + 2 * l + 1] = make_float2(0.5f * (Z.y + Zc.y), -0.5f * (Z.x - Zc.x));
-  }
-  __syncthreads();
   const float2* res2 = ct_fft<N, H, LP>(C, A, tw);
   float2* o = out + (p * N + z) * (int64_t)N * H;
   for (int i = threadIdx.x; i < N * H; i += kFftThreads) {
     const int ky = i / H, kx = i - ky * H;
-    o[i] = res2[kx * LP + ky];
+    o[i] = res2[fpad(kx * LP + ky)];
   }
 }
 
