@@ -54,6 +54,8 @@ def _lib():
             "orc_refine": [_dp, _ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64p, _d, _d, _d, _dp, _dp, _ip],
             "orc_rotate_volume": [_fp, ctypes.c_int, _dp, _dp],
             "orc_translation": [_fp, _fp, ctypes.c_int, _dp, ctypes.c_int, _dp, _dp],
+            "orc_translation_upsampled": [_fp, _fp, ctypes.c_int, _dp, ctypes.c_int, ctypes.c_int, _dp, _dp],
+            "orc_upsampled_corr_at": [_fp, _fp, ctypes.c_int, _dp, _dp],
             "orc_energy": [_dp, _dp, ctypes.c_int, ctypes.c_int],
             "orc_align_batch": [_fp, ctypes.c_int64, _fp, _dp, ctypes.c_int, _ip, _dp, _dp, ctypes.c_int],
         }
@@ -61,6 +63,7 @@ def _lib():
             getattr(lib, name).argtypes = args
         lib.orc_find_maxima.restype = ctypes.c_int
         lib.orc_energy.restype = ctypes.c_double
+        lib.orc_upsampled_corr_at.restype = ctypes.c_double
         _LIB = lib
     return _LIB
 
@@ -280,22 +283,42 @@ def translation(vol, ref, e, W):
     return sh, float(pk[0])
 
 
+def translation_upsampled(vol, ref, e, W, kappa=16):
+    """Integer windowed peak, then the upsampled-DFT refinement (Guizar-Sicairos; App. C remark iii)."""
+    vol = np.ascontiguousarray(vol, np.float32)
+    ref = np.ascontiguousarray(ref, np.float32)
+    sh, pk = np.zeros(3), np.zeros(1)
+    _lib().orc_translation_upsampled(_p(vol, _fp), _p(ref, _fp), vol.shape[-1],
+                                     _p(np.ascontiguousarray(e, np.float64)), W, kappa, _p(sh), _p(pk))
+    return sh, float(pk[0])
+
+
+def upsampled_corr_at(vol, ref, e, t):
+    """c~(t) = (1/N^3) Re sum_{k in [-N/2, N/2)^3} F^ conj(rho^) e^{2 pi i k.t/N} at one point (full triple sum)."""
+    vol = np.ascontiguousarray(vol, np.float32)
+    ref = np.ascontiguousarray(ref, np.float32)
+    return _lib().orc_upsampled_corr_at(_p(vol, _fp), _p(ref, _fp), vol.shape[-1],
+                                        _p(np.ascontiguousarray(e, np.float64)),
+                                        _p(np.ascontiguousarray(t, np.float64)))
+
+
 def energy(F, H, Lc):
     F, H = _c128(F), _c128(H)
     return _lib().orc_energy(_p(F.view(np.float64)), _p(H.view(np.float64)), Lc, F.shape[1])
 
 
 def align_batch(vols, ref, params, H=None, nthreads=0):
-    """params: dict with L, qover, L0, K, ncand, bands, iters, T, W, tol_grad, tol_step, tol_obj.
+    """params: dict with L, qover, L0, K, ncand, bands, iters, T, W, ups (0: parabolic subpixel, kappa: upsampled
+    DFT), tol_grad, tol_step, tol_obj.
     -> poses [B, 8] = (alpha, beta, gamma, tx, ty, tz, score, best)."""
     vols = np.ascontiguousarray(vols, np.float32)
     ref = np.ascontiguousarray(ref, np.float32)
     B, N = vols.shape[0], vols.shape[-1]
     bands = list(params["bands"])
-    ip = np.zeros(25, np.int32)
+    ip = np.zeros(26, np.int32)
     ip[0:6] = [params["L"], params.get("qover", 2), params["L0"], params.get("K", 2), params["ncand"], len(bands)]
     ip[6:6 + len(bands)] = bands
-    ip[22:25] = [params.get("iters", 1), params.get("T", 1), params.get("W", 0)]
+    ip[22:26] = [params.get("iters", 1), params.get("T", 1), params.get("W", 0), params.get("ups", 0)]
     dp = np.array([params.get("tol_grad", 0.0), params.get("tol_step", 0.0), params.get("tol_obj", 0.0)])
     Hc = None if H is None else _c128(H)
     poses = np.zeros((B, 8))

@@ -21,6 +21,8 @@
  *
  * Parity-unpinned parts (only GPU-vs-oracle parity checks them): noisy-landscape Newton
  * paths, noise aliasing in stage 1, parabolic-subpixel bias on noisy peaks.
+ * translation_upsampled is pinned by: c~ at integer points = the direct circular correlation, the
+ * separable contraction = the full triple sum at arbitrary points, planted fractional shifts recovered to 1/kappa.
  */
 #include <algorithm>
 #include <atomic>
@@ -620,8 +622,102 @@ void translation(const float* vol, const float* ref, int N, const double* e, int
   }
 }
 
+/* ---------------- stage 5, subpixel by an upsampled DFT (App. C remark iii) ----------------
+   Guizar-Sicairos's scheme: the integer peak t0 of the windowed correlation (as translation() above), then the
+   correlation's trigonometric interpolant on a kappa-times finer grid over +-1.5 voxel around t0, evaluated by
+   matrix-multiply DFTs (reading C27):
+     c~(t) = (1/N^3) Re sum_{k in K^3} F^(k) conj(rho^(k)) e^{+2 pi i k.t / N},   K = {-N/2, ..., N/2 - 1},
+   F^, rho^ the 3-D DFTs of f and rho (here by a plain separable DFT in FP64), t = t0 + u / kappa,
+   u in [-h, h]^3 with h = ceil(1.5 kappa); the result is the argmax (ties -> lowest index, z-major) and c~ there.
+   At integer t, c~(t) = c(t) = sum_x f(x) rho(x - t) exactly (circular correlation). */
+void dft_axis(vector<cd>& a, int N, int axis) {
+  /* a: [z][y][x] complex N^3; forward DFT e^{-2 pi i k n / N} along one axis, by the definition */
+  vector<cd> w(N);
+  for (int m = 0; m < N; ++m) w[m] = std::polar(1.0, -2.0 * PI * m / N);
+  vector<cd> line(N), out(N);
+  const size_t st = axis == 0 ? 1 : axis == 1 ? (size_t)N : (size_t)N * N;
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < N; ++j) {
+      size_t base;
+      if (axis == 0) base = ((size_t)i * N + j) * N;
+      else if (axis == 1) base = (size_t)i * N * N + j;
+      else base = (size_t)i * N + j;
+      for (int n = 0; n < N; ++n) line[n] = a[base + n * st];
+      for (int k = 0; k < N; ++k) {
+        cd s(0, 0);
+        for (int n = 0; n < N; ++n) s += line[n] * w[((size_t)k * n) % N];
+        out[k] = s;
+      }
+      for (int k = 0; k < N; ++k) a[base + k * st] = out[k];
+    }
+}
+
+void translation_upsampled(const float* vol, const float* ref, int N, const double* e, int W, int kappa,
+                           double* shift, double* peak) {
+  double tpar[3], pk;
+  translation(vol, ref, N, e, W, tpar, &pk);  /* parabolic result; its integer part is recomputed below */
+  vector<double> rho;
+  rotate_volume(ref, N, e, rho);
+  /* integer window argmax t0 (same scan as translation) */
+  double best = -std::numeric_limits<double>::infinity();
+  int t0[3] = {0, 0, 0};
+  for (int tz = -W; tz <= W; ++tz)
+    for (int ty = -W; ty <= W; ++ty)
+      for (int tx = -W; tx <= W; ++tx) {
+        double v = circ_corr(vol, rho, N, tx, ty, tz);
+        if (v > best) { best = v; t0[0] = tx; t0[1] = ty; t0[2] = tz; }
+      }
+  const size_t n3 = (size_t)N * N * N;
+  vector<cd> F(n3), R(n3);
+  for (size_t i = 0; i < n3; ++i) { F[i] = cd(vol[i], 0.0); R[i] = cd(rho[i], 0.0); }
+  for (int ax = 0; ax < 3; ++ax) { dft_axis(F, N, ax); dft_axis(R, N, ax); }
+  vector<cd> X(n3);
+  for (size_t i = 0; i < n3; ++i) X[i] = F[i] * std::conj(R[i]);
+  const int h = (int)std::ceil(1.5 * kappa), U = 2 * h + 1;
+  /* phase matrices E_ax[k][u] = e^{2 pi i k' (t0_ax + (u - h)/kappa) / N}, k' = k (k < N/2) or k - N (k >= N/2) */
+  vector<cd> E[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    E[ax].resize((size_t)N * U);
+    for (int k = 0; k < N; ++k) {
+      const int kp = k < N / 2 ? k : k - N;
+      for (int u = 0; u < U; ++u) {
+        const double t = t0[ax] + (double)(u - h) / kappa;
+        E[ax][(size_t)k * U + u] = std::polar(1.0, 2.0 * PI * kp * t / N);
+      }
+    }
+  }
+  /* separable contraction: x, then y, then z (matrix-multiply DFTs) */
+  vector<cd> A((size_t)N * N * U), B((size_t)N * U * U);
+  for (int z = 0; z < N; ++z)
+    for (int y = 0; y < N; ++y)
+      for (int u = 0; u < U; ++u) {
+        cd s(0, 0);
+        for (int kx = 0; kx < N; ++kx) s += X[((size_t)z * N + y) * N + kx] * E[0][(size_t)kx * U + u];
+        A[((size_t)z * N + y) * U + u] = s;
+      }
+  for (int z = 0; z < N; ++z)
+    for (int v = 0; v < U; ++v)
+      for (int u = 0; u < U; ++u) {
+        cd s(0, 0);
+        for (int ky = 0; ky < N; ++ky) s += A[((size_t)z * N + ky) * U + u] * E[1][(size_t)ky * U + v];
+        B[((size_t)z * U + v) * U + u] = s;
+      }
+  double bv = -std::numeric_limits<double>::infinity();
+  int bu[3] = {h, h, h};
+  for (int w = 0; w < U; ++w)
+    for (int v = 0; v < U; ++v)
+      for (int u = 0; u < U; ++u) {
+        cd s(0, 0);
+        for (int kz = 0; kz < N; ++kz) s += B[((size_t)kz * U + v) * U + u] * E[2][(size_t)kz * U + w];
+        const double c = std::real(s) / (double)n3;
+        if (c > bv) { bv = c; bu[0] = u; bu[1] = v; bu[2] = w; } /* scan order = z-major index order */
+      }
+  for (int ax = 0; ax < 3; ++ax) shift[ax] = t0[ax] + (double)(bu[ax] - h) / kappa;
+  *peak = bv;
+}
+
 struct Params {
-  int L, qover, L0, K, ncand, nbands, bands[16], iters, T, W;
+  int L, qover, L0, K, ncand, nbands, bands[16], iters, T, W, ups;
   double tol_grad, tol_step, tol_obj;
 };
 
@@ -656,7 +752,8 @@ void align_one(const float* vol, const float* ref, const double* H, int N, const
     }
     if (p.W > 0) {
       double pk;
-      translation(vol, ref, N, rot, p.W, t, &pk);
+      if (p.ups > 0) translation_upsampled(vol, ref, N, rot, p.W, p.ups, t, &pk);
+      else translation(vol, ref, N, rot, p.W, t, &pk);
     }
   }
   pose[0] = rot[0]; pose[1] = rot[1]; pose[2] = rot[2];
@@ -759,6 +856,29 @@ void orc_rotate_volume(const float* ref, int N, const double* e, double* out) {
 void orc_translation(const float* vol, const float* ref, int N, const double* e, int W, double* shift, double* peak) {
   translation(vol, ref, N, e, W, shift, peak);
 }
+void orc_translation_upsampled(const float* vol, const float* ref, int N, const double* e, int W, int kappa,
+                               double* shift, double* peak) {
+  translation_upsampled(vol, ref, N, e, W, kappa, shift, peak);
+}
+/* c~(t) of the upsampled scheme at ONE arbitrary point t, by the full triple sum over k in K^3 (no separation):
+   the pin of the separable contraction above */
+double orc_upsampled_corr_at(const float* vol, const float* ref, int N, const double* e, const double* t) {
+  vector<double> rho;
+  rotate_volume(ref, N, e, rho);
+  const size_t n3 = (size_t)N * N * N;
+  vector<cd> F(n3), R(n3);
+  for (size_t i = 0; i < n3; ++i) { F[i] = cd(vol[i], 0.0); R[i] = cd(rho[i], 0.0); }
+  for (int ax = 0; ax < 3; ++ax) { dft_axis(F, N, ax); dft_axis(R, N, ax); }
+  cd s(0, 0);
+  for (int kz = 0; kz < N; ++kz)
+    for (int ky = 0; ky < N; ++ky)
+      for (int kx = 0; kx < N; ++kx) {
+        const int px = kx < N / 2 ? kx : kx - N, py = ky < N / 2 ? ky : ky - N, pz = kz < N / 2 ? kz : kz - N;
+        const size_t i = ((size_t)kz * N + ky) * N + kx;
+        s += F[i] * std::conj(R[i]) * std::polar(1.0, 2.0 * PI * (px * t[0] + py * t[1] + pz * t[2]) / N);
+      }
+  return std::real(s) / (double)n3;
+}
 /* E_L = ||F_{<=L}||_w ||H_{<=L}||_w (SURVEY 8(c) tolerance scale; Cauchy-Schwarz bound on |C_L|) */
 double orc_energy(const double* F, const double* H, int Lc, int R) {
   double ef = 0, eh = 0;
@@ -771,7 +891,8 @@ double orc_energy(const double* F, const double* H, int Lc, int R) {
       }
   return std::sqrt(ef * eh);
 }
-/* params: ints [L, qover, L0, K, ncand, nbands, bands[16], iters, T, W]; dbl [tol_grad, tol_step, tol_obj]
+/* params: ints [L, qover, L0, K, ncand, nbands, bands[16], iters, T, W, ups]; dbl [tol_grad, tol_step, tol_obj]
+   (ups = 0: parabolic subpixel; ups = kappa > 0: the upsampled DFT of translation_upsampled)
    H: complex [ncoef(L)][R] reference coefficients (NULL -> analysed from ref at t = 0).
    poses [B][8] = {alpha, beta, gamma, tx, ty, tz, score, best}. */
 void orc_align_batch(const float* vols, int64_t B, const float* ref, const double* H, int N, const int* ip,
@@ -779,7 +900,7 @@ void orc_align_batch(const float* vols, int64_t B, const float* ref, const doubl
   Params p;
   p.L = ip[0]; p.qover = ip[1]; p.L0 = ip[2]; p.K = ip[3]; p.ncand = ip[4]; p.nbands = ip[5];
   for (int k = 0; k < 16; ++k) p.bands[k] = ip[6 + k];
-  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24];
+  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24]; p.ups = ip[25];
   p.tol_grad = dp[0]; p.tol_step = dp[1]; p.tol_obj = dp[2];
   const int R = N / 2;
   vector<double> Hl;

@@ -570,3 +570,49 @@ def test_alternation_exact_recovery_c1():
     err = O.geodesic_deg_matrix(O.euler_to_matrix(pose[:3]), b.truth_R[0])
     assert err < 0.05, err
     assert np.abs(pose[3:6] - b.truth_t[0]).max() < 0.01
+
+
+# ------------------------------------------------------------------ stage 5: upsampled-DFT subpixel
+def test_upsampled_corr_equals_circular_correlation_at_integer_points():
+    """c~(t) (App. C remark iii; reading C27: the correlation's trigonometric interpolant over the symmetric
+    frequency range) equals the direct circular correlation sum_x f(x) rho(x - t) at every integer t: pins the phase
+    sign, the symmetric range and the 1/N^3 normalisation of the oracle's upsampled scheme."""
+    N = 16
+    bl = _wide_blobs()
+    ref = gen.render(bl, N)[0]
+    vol = gen.particles(N, 1, 0.5, seed=3).vols[0]
+    e = np.array([0.4, 1.2, 2.5])
+    rho = O.rotate_volume(ref, e)
+    for t in [(0, 0, 0), (1, -2, 3), (-4, 5, -1), (7, 0, -8)]:
+        d = np.sum(vol.astype(np.float64) * np.roll(rho, (t[2], t[1], t[0]), axis=(0, 1, 2)))
+        assert abs(O.upsampled_corr_at(vol, ref, e, np.array(t, float)) - d) <= 1e-11 * np.abs(vol).sum() * np.abs(rho).max()
+
+
+def test_upsampled_separable_matches_full_sum_and_is_a_local_max():
+    """The oracle's separable matrix-multiply DFT (x, then y, then z) gives the same c~ as the full triple sum at
+    its argmax, and that point is a maximum of c~ on the 1/kappa grid around it."""
+    N, kappa = 16, 16
+    bl = _wide_blobs()
+    ref = gen.render(bl, N)[0]
+    vol = gen.render(bl, N, t=np.array([0.3, -1.2, 0.55]))[0]
+    e = np.zeros(3)
+    sh, pk = O.translation_upsampled(vol, ref, e, 3, kappa)
+    assert abs(O.upsampled_corr_at(vol, ref, e, sh) - pk) <= 1e-10 * abs(pk)
+    for ax in range(3):
+        for d in (-1.0 / kappa, 1.0 / kappa):
+            t = sh.copy()
+            t[ax] += d
+            assert O.upsampled_corr_at(vol, ref, e, t) <= pk + 1e-10 * abs(pk)
+
+
+@pytest.mark.parametrize("t", [(0.25, -0.4, 0.0), (-0.3125, 0.4, 1.45), (1.4, -2.25, 0.75), (-0.55, 0.1, -1.9)])
+def test_upsampled_recovers_planted_fractional_shifts(t):
+    """Noise-free volume rendered at a planted fractional shift: the upsampled DFT (kappa = 16, +-1.5 voxel)
+    recovers it to the 1/kappa grid (error <= 1/(2 kappa) + 0.01 per axis), where the parabola is off by up to
+    ~0.12 voxel (test_translation_parabolic_subpixel_fractional_shifts)."""
+    N, kappa = 24, 16
+    bl = _wide_blobs()
+    ref = gen.render(bl, N)[0]
+    vol = gen.render(bl, N, t=np.array(t))[0]
+    sh, _ = O.translation_upsampled(vol, ref, np.zeros(3), 4, kappa)
+    assert np.abs(sh - np.array(t)).max() <= 0.5 / kappa + 0.01, (sh, t)
