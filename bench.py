@@ -39,6 +39,9 @@ CONFIGS = {
     # (W = 6); 1,000 particles per rank (the 10,000-particle job is 10 such steps)
     "c3": dict(N=96, L=48, bands=[8, 12, 16, 24, 32, 48], ncand=10, K=2, snr=0.05, particles=1000, iters=1,
                T=3, W=6, shift_max=4.0),
+    # c3 with the upsampled-DFT subpixel refinement (kappa = 16 over +-1.5 voxel, App. C remark iii)
+    "c3u": dict(N=96, L=48, bands=[8, 12, 16, 24, 32, 48], ncand=10, K=2, snr=0.05, particles=1000, iters=1,
+                T=3, W=6, shift_max=4.0, ups=16),
     # configs[0] (c1) rotation part, small
     "c1": dict(N=32, L=8, bands=[4, 6, 8], ncand=4, K=2, snr=float("inf"), particles=64, iters=1),
 }
@@ -82,16 +85,24 @@ def stage_work(c):
     work = {"sh_analysis": (T * sh_fl, T * sh_by), "corr_coeffs": (T * corr_fl, T * corr_by),
             "so3_search": (T * srch_fl, T * srch_by), "newton_refine": (T * nw_fl, T * nw_by),
             "gather_poses": (0, 48)}
-    if T > 1:
-        # a11-a13 per alternation (k_trans.cu): rotated reference rho (~30 flop/voxel, written once, read by the
-        # R2C), R2C(rho) (2.5 N^3 log2 N^3 flop, rho^ written), then the pruned inverse DFT on the w' = 2W+3 window
-        # (X = F^ conj(rho^) formed on chip: F^ and rho^ read once; 8 flop per complex MAC over the x, y, z passes).
-        # Plus F^ = R2C(f) once per particle (f read, F^ written).
-        n3, H = N ** 3, N // 2 + 1
-        bins, lg, wp = N * N * H, 3 * np.log2(N), 2 * c["W"] + 3
-        alt_fl = 30 * n3 + 2.5 * n3 * lg + 6 * bins + 8 * (N * N * H * wp + N * N * wp * wp) + 8 * N * wp ** 3
-        alt_by = 8 * n3 + 8 * bins + 16 * bins
-        work["translation_update"] = (int(T * alt_fl + 2.5 * n3 * lg), int(T * alt_by + 4 * n3 + 8 * bins))
+    if c.get("W", 0) > 0:
+        # a11-a13 per alternation (k_trans.cu, no FFT library): rho~ = 2-D R2C of every z-plane of the rotated
+        # reference (rotation fused: ~30 flop/voxel, 2.5 N^2 log2 N^2 flop per plane), the z correlation of the plane
+        # spectra onto the w' = 2W+3 window (8 flop per complex MAC, N^2 H w' MACs), the (x, y) window inverse;
+        # once per particle f~ (the particle's plane spectra).  Bytes: f~ read + rho~ written and read + Y1 written
+        # and read per alternation; f read and f~ written once.
+        n3, H, wp = N ** 3, N // 2 + 1, 2 * c["W"] + 3
+        lg2 = 2 * np.log2(N)
+        plane_fft = 2.5 * n3 * lg2
+        alt_fl = 30 * n3 + plane_fft + 8 * N * N * H * wp + 8 * wp * (N * H * wp + N * wp * wp)
+        alt_by = 3 * 8 * N * N * H + 2 * 16 * wp * N * H
+        once_fl, once_by = plane_fft, 4 * n3 + 8 * N * N * H
+        if c.get("ups"):
+            # f3: z FFTs of f~ and rho~ -> X, then the three matrix-multiply DFTs onto the U^3 grid
+            U = 2 * int(np.ceil(1.5 * c["ups"])) + 1
+            alt_fl += 2 * 5 * N * N * H * np.log2(N) + 6 * N * N * H + 8 * N * (N * H * U + N * U * U) + 4 * N * U ** 3
+            alt_by += 4 * 8 * N * N * H + 2 * 8 * N * U * U
+        work["translation_update"] = (int(T * alt_fl + once_fl), int(T * alt_by + once_by))
     return work
 
 
@@ -155,7 +166,7 @@ def make_batch(c, rank, world, P):
 
 def oracle_params(c):
     return dict(L=c["L"], qover=2, L0=c["bands"][0], K=c["K"], ncand=c["ncand"], bands=c["bands"],
-                iters=c["iters"], T=c.get("T", 1), W=c.get("W", 0))
+                iters=c["iters"], T=c.get("T", 1), W=c.get("W", 0), ups=c.get("ups", 0))
 
 
 def time_oracle(vols, ref, c, n, nthreads):
@@ -216,6 +227,8 @@ def metric_of(name, c):
     if name in ("c2", "c4"):
         return METRIC
     alt = f", T={c['T']} alternations" if c.get("T", 1) > 1 else ""
+    if c.get("ups"):
+        alt += f", upsampled subpixel kappa={c['ups']}"
     return f"particles aligned/s (box {c['N']}³, L0={c['bands'][0]}→L={c['L']}{alt}, device-timed)"
 
 
@@ -257,7 +270,7 @@ def main():
     ref = ref_host.to(dev)
     h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=P)
     params = mt.Params(bands=c["bands"], n_cand=c["ncand"], oversample=c["K"], newton_iters=c["iters"],
-                       n_alternations=c.get("T", 1), shift_window=c.get("W", 0))
+                       n_alternations=c.get("T", 1), shift_window=c.get("W", 0), upsample=c.get("ups", 0))
     from paper_2603_15285_b200 import dist as D
     H = torch.empty((ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
     counts = [P] * world
@@ -374,9 +387,10 @@ def main():
            "config": {"workload": f"{args.config}: {P} particles/rank of {c['N']}^3, SNR {c['snr']}, "
                                   f"L0={c['bands'][0]}->L={c['L']} bands {c['bands']}, N_C={c['ncand']}, "
                                   f"K={c['K']}, 1 Newton step/band, "
-                                  + (f"T={c['T']} alternations with the FFT translation update (W={c['W']}), "
-                                     f"shifts U[-{c['shift_max']:g},{c['shift_max']:g}]^3" if c.get("T", 1) > 1
-                                     else "rotation only"),
+                                  + (f"T={c['T']} alternations with the FFT translation update (W={c['W']}, "
+                                     + (f"upsampled-DFT subpixel kappa={c['ups']}" if c.get("ups") else
+                                        "parabolic subpixel") + f"), shifts U[-{c['shift_max']:g},{c['shift_max']:g}]^3"
+                                     if c.get("T", 1) > 1 else "rotation only"),
                       "particles_per_rank": P, "parallelism": f"dp{world}",
                       "l2": f"inputs larger than L2 ({P * c['N'] ** 3 * 4 / 2**30:.2f} GiB per rank resident)"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch, "clocks": clocks}

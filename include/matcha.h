@@ -85,6 +85,10 @@ typedef struct {
   int32_t n_alternations;  /* T rotation/translation alternations (App. C); used only when
                               shift_window > 0 (without a translation update one rotation pass is run) */
   int32_t shift_window;    /* W: translation search window [-W,W]^3 voxels, W <= N/4; 0 = rotation only */
+  int32_t upsample;        /* subpixel step of the translation update: 0 = per-axis parabola (reading C18);
+                              kappa >= 1 = upsampled DFT (Guizar-Sicairos, App. C remark iii; reading C27):
+                              the correlation's trigonometric interpolant on a 1/kappa grid over +-1.5 voxel around
+                              the integer peak (kappa <= 21; 16 in SURVEY f3) */
   double tol_grad;         /* early stop: ||grad|| < tol_grad*|C|; 0 = off */
   double tol_step;         /* early stop: ||delta|| < tol_step (rad); 0 = off */
   double tol_obj;          /* early stop: |dC| < tol_obj*|C|; 0 = off */
@@ -146,13 +150,17 @@ MATCHA_API matcha_status_t matcha_newton_refine(matcha_handle_t h, const void* M
                                                 const int32_t* grid_idx, void* score, int32_t* best, void* stream);
 
 /* Stage 5 -- translation update (App. C; readings C17, C18): rho = g o h (trilinear rotation
-   of the reference, zero outside), c(t) = sum_x f(x) rho((x - t) mod N) by 3-D FFT, argmax over the
-   window [-W,W]^3 (ties -> lowest window index, z-major), parabolic subpixel per axis clamped to 1/2.
+   of the reference, zero outside), c(t) = sum_x f(x) rho((x - t) mod N) (the FFT correlation of P:1797, evaluated
+   on the window from 2-D plane spectra: hand-written FFTs, no library), argmax over the window [-W,W]^3 (ties ->
+   lowest window index, z-major); subpixel step: upsample = 0 -> parabola per axis clamped to 1/2; upsample = kappa
+   -> upsampled DFT around the integer peak (see matcha_params_t.upsample; reading C27).
    vols: float32 [B][N^3]; ref: float32 [N^3]; euler: real [B][3]; shifts (out): real [B][3] (x,y,z
-   voxels, particle frame: f ~ S_t(g o h)); peak (out): real [B] (c at the integer argmax), may be NULL. */
+   voxels, particle frame: f ~ S_t(g o h)); peak (out): real [B] (c at the integer argmax, or c~ at the upsampled
+   argmax), may be NULL.  Errors: WINDOW if W > N/4; NOT_IMPLEMENTED if the box/window/kappa exceed the kernels'
+   shared-memory limits (FP32 boxes up to ~200 voxels). */
 MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const float* vols, int64_t B,
                                                      const float* ref, const void* euler, int32_t window,
-                                                     void* shifts, void* peak, void* stream);
+                                                     int32_t upsample, void* shifts, void* peak, void* stream);
 
 /* Whole path -- App. C alternation around Algorithm 1, chunked by max_batch:
    t = 0; repeat T times { stage 1 at centre c + t; stage 2; stage 3 (L_0); stage 4; if W > 0 stage 5 }.

@@ -44,7 +44,7 @@ class _Config(ctypes.Structure):
 class _Params(ctypes.Structure):
     _fields_ = [("n_bands", ctypes.c_int32), ("bands", ctypes.c_int32 * 16), ("newton_iters", ctypes.c_int32),
                 ("n_cand", ctypes.c_int32), ("oversample", ctypes.c_int32), ("n_alternations", ctypes.c_int32),
-                ("shift_window", ctypes.c_int32), ("tol_grad", ctypes.c_double), ("tol_step", ctypes.c_double),
+                ("shift_window", ctypes.c_int32), ("upsample", ctypes.c_int32), ("tol_grad", ctypes.c_double), ("tol_step", ctypes.c_double),
                 ("tol_obj", ctypes.c_double)]
 
 
@@ -61,7 +61,7 @@ _SIGS = {
     "matcha_eval_corr": ([_H, _vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "matcha_newton_refine": ([_H, _vp, _i32, _i64, _i32, ctypes.POINTER(_Params), _vp, _vp, _vp, _vp, _vp],
                              ctypes.c_int),
-    "matcha_translation_update": ([_H, _vp, _i64, _vp, _vp, _i32, _vp, _vp, _vp], ctypes.c_int),
+    "matcha_translation_update": ([_H, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp], ctypes.c_int),
     "matcha_align_batch": ([_H, _vp, _i64, _vp, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_align_batch_host": ([_H, _vp, _i64, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_get_status": ([_H, _vp], ctypes.c_int),
@@ -102,6 +102,7 @@ class Params:
     oversample: int = 2
     n_alternations: int = 1
     shift_window: int = 0
+    upsample: int = 0          # 0: parabolic subpixel; kappa: upsampled-DFT subpixel
     tol_grad: float = 0.0
     tol_step: float = 0.0
     tol_obj: float = 0.0
@@ -112,7 +113,7 @@ class Params:
         for i, b in enumerate(self.bands):
             p.bands[i] = int(b)
         p.newton_iters, p.n_cand, p.oversample = self.newton_iters, self.n_cand, self.oversample
-        p.n_alternations, p.shift_window = self.n_alternations, self.shift_window
+        p.n_alternations, p.shift_window, p.upsample = self.n_alternations, self.shift_window, self.upsample
         p.tol_grad, p.tol_step, p.tol_obj = self.tol_grad, self.tol_step, self.tol_obj
         return p
 
@@ -264,14 +265,15 @@ class Handle:
                                               _ptr(grid_idx), _ptr(score), _ptr(best), _stream()))
         return euler, score, best
 
-    def translation_update(self, vols: torch.Tensor, ref: torch.Tensor, euler: torch.Tensor, window: int):
+    def translation_update(self, vols: torch.Tensor, ref: torch.Tensor, euler: torch.Tensor, window: int,
+                           upsample: int = 0):
         B = self._vols(vols)
         self._arg(ref, "ref", torch.float32, (self.N, self.N, self.N))
         self._arg(euler, "euler", self.real, (B, 3))
         shifts = torch.empty((B, 3), dtype=self.real, device=self.device)
         peak = torch.empty((B,), dtype=self.real, device=self.device)
         self._check(_lib.matcha_translation_update(self._h, _ptr(vols), B, _ptr(ref), _ptr(euler),
-                                                   window, _ptr(shifts), _ptr(peak), _stream()))
+                                                   window, upsample, _ptr(shifts), _ptr(peak), _stream()))
         return shifts, peak
 
     def align_batch(self, vols: torch.Tensor, ref: Optional[torch.Tensor], params: Params,

@@ -145,6 +145,13 @@ cudaError_t launch_pad_ref(const float* ref, int N, int pitch, float* pad, cudaS
 size_t window_scratch_reals(int N, int W);
 template <typename T>
 cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N, int W, int64_t nb, T* scratch,
-                                T* shifts, int sstride, T* peak, cudaStream_t s);
+                                T* shifts, int sstride, T* peak, int* tint, cudaStream_t s);
+// upsampled-DFT subpixel refinement around the integer peaks tint (overwrites rt with X = F^ conj(rho^))
+int ups_points(int kappa);
+bool ups_supported(int N, int kappa, bool fp64);
+size_t ups_scratch_bytes(int N, int kappa, size_t csz);  // per particle
+template <typename T>
+cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
+                             void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s);
 
 }  // namespace matcha

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(512) k_window_xy(const cplx_t<T>* __restrict__
 // ---- stage 5d: windowed argmax (ties -> lowest window index, z-major) + per-axis parabolic subpixel (C18) -------
 template <typename T>
 __global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ cw_all, int N, int W, T* shifts,
-                                                     int sstride, T* peak) {
+                                                     int sstride, T* peak, int* __restrict__ tint) {
   __shared__ T sv[8];
   __shared__ int si[8];
   const int64_t p = blockIdx.x;
@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ cw_al
       T dl = T(0);
       if (den < T(0)) dl = fmin(T(0.5), fmax(T(-0.5), (cm - cpl) / (T(2) * den)));
       shifts[p * sstride + ax] = (T)t[ax] + dl;
+      if (tint) tint[p * 3 + ax] = t[ax];
     }
     if (peak) peak[p] = c0 / ((T)N * N);
   }
@@ -742,6 +743,219 @@ __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft,
   }
 }
 
+
+// ==== stage 5e: subpixel refinement by an upsampled DFT (Guizar-Sicairos; App. C remark iii) ===
+// Around the integer window peak t0 the correlation's trigonometric interpolant (reading C27)
+//   c~(t) = (1/N^3) Re sum_{k in [-N/2, N/2)^3} F^(k) conj(rho^(k)) e^{+2 pi i k.t / N}
+// is evaluated on t = t0 + (u - h) / kappa, u in [0, U)^3, U = 2h + 1, h = ceil(1.5 kappa), by three matrix-multiply
+// DFTs; the result is the grid argmax (ties -> lowest index, z-major).
+//   k_zfft_cross  3-D spectra from the plane spectra: the z FFT of f~ and rho~ pencils (Stockham in shared memory),
+//                 X = F^ conj(rho^) written over rho~ (never needed again this alternation);
+//   k_ups_xy      per (kz plane, particle): Z2[kz][uy][ux] = sum_ky Ey[ky][uy] sum_kx wx Ex[kx][ux] X[kz][ky][kx]
+//                 (half spectrum in kx: w = 1 at kx = 0, the Nyquist column as -N/2 with w = 1, else w = 2; Re taken
+//                 at the end makes the half sum exact for the Hermitian X);
+//   k_ups_z       per (block of (uy, ux), particle): c~ = Re sum_kz Ez[kz][uz] Z2[kz][uy][ux] for all uz, block argmax;
+//   k_ups_final   per particle: argmax over the blocks, t = t0 + (u - h)/kappa, peak = c~ / ... (already 1/N^3).
+
+// z FFT of the plane spectra of one (ky row, kx chunk) -> X over rt
+template <typename T>
+__global__ void __launch_bounds__(256) k_zfft_cross(const cplx_t<T>* __restrict__ ft, cplx_t<T>* __restrict__ rt,
+                                                    const __grid_constant__ FftRadix fr, int hc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = fr.n, H = N / 2 + 1, nkc = (H + hc - 1) / hc;
+  cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);
+  cplx_t<T>* f0 = tw + N;          // [hc][N] lines along z
+  cplx_t<T>* f1 = f0 + hc * N;
+  cplx_t<T>* r0 = f1 + hc * N;
+  cplx_t<T>* r1 = r0 + hc * N;
+  const int ky = blockIdx.x / nkc, kx0 = (blockIdx.x - ky * nkc) * hc, nk = min(hc, H - kx0);
+  const int64_t p = blockIdx.y;
+  build_roots<T>(tw, N, -1);
+  for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
+    const int zz = i / nk, kl = i - zz * nk;
+    const int64_t g = ((p * N + zz) * N + ky) * (int64_t)H + kx0 + kl;
+    f0[kl * N + zz] = ft[g];
+    r0[kl * N + zz] = rt[g];
+  }
+  __syncthreads();
+  const cplx_t<T>* Fz = stockham<T>(f0, f1, nk, fr, tw);
+  const cplx_t<T>* Rz = stockham<T>(r0, r1, nk, fr, tw);
+  for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
+    const int kz = i / nk, kl = i - kz * nk;
+    const cplx_t<T> f = Fz[kl * N + kz], r = Rz[kl * N + kz];
+    rt[((p * N + kz) * N + ky) * (int64_t)H + kx0 + kl] = mk<T>(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
+  }
+}
+
+// e^{+2 pi i k' t / N} with k' the symmetric frequency of index k (k' = k - N for k >= N/2)
+template <typename T> __device__ __forceinline__ cplx_t<T> ups_phase(int k, int N, int t0, int u, int h, int kappa) {
+  const int kp = k < N / 2 ? k : k - N;
+  const T t = (T)t0 + (T)(u - h) / (T)kappa;
+  T sn, cs;
+  if constexpr (sizeof(T) == 8) sincospi(2.0 * kp * t / N, &sn, &cs);
+  else sincospif(2.0f * (float)kp * t / (float)N, &sn, &cs);
+  return mk<T>(cs, sn);
+}
+
+constexpr int kUpsRows = 16;  // ky rows per chunk in k_ups_xy
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_ups_xy(const cplx_t<T>* __restrict__ X, int N, int kappa,
+                                                const int* __restrict__ tint, cplx_t<T>* __restrict__ Z2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int H = N / 2 + 1, h = (int)ceil(1.5 * kappa), U = 2 * h + 1;
+  cplx_t<T>* Ex = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [H][U] (weights folded in)
+  cplx_t<T>* Ey = Ex + H * U;                               // [N][U]
+  cplx_t<T>* Xc = Ey + N * U;                               // [kUpsRows][H]
+  cplx_t<T>* Z1 = Xc + kUpsRows * H;                        // [kUpsRows][U]
+  const int kz = blockIdx.x;
+  const int64_t p = blockIdx.y;
+  const int tx0 = tint[p * 3 + 0], ty0 = tint[p * 3 + 1];
+  for (int i = threadIdx.x; i < H * U; i += blockDim.x) {
+    const int kx = i / U, u = i - kx * U;
+    // kx = N/2 is the symmetric range's -N/2 (weight 1); 1 <= kx < N/2 stand for +-kx (weight 2)
+    const int kk = (2 * kx == N) ? N / 2 : kx;  // ups_phase maps N/2 to -N/2
+    const T w = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
+    const cplx_t<T> e = ups_phase<T>(kk, N, tx0, u, h, kappa);
+    Ex[i] = mk<T>(w * e.x, w * e.y);
+  }
+  for (int i = threadIdx.x; i < N * U; i += blockDim.x) {
+    const int ky = i / U, u = i - ky * U;
+    Ey[i] = ups_phase<T>(ky, N, ty0, u, h, kappa);
+  }
+  // Z2 accumulators: thread o owns (uy, ux) = o, o + blockDim.x, ...  (U^2 <= 6 * 512)
+  constexpr int kAcc = 6;
+  cplx_t<T> acc[kAcc];
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) acc[q] = mk<T>(T(0), T(0));
+  const cplx_t<T>* xp = X + (p * N + kz) * (int64_t)N * H;
+  for (int ky0 = 0; ky0 < N; ky0 += kUpsRows) {
+    const int nr = min(kUpsRows, N - ky0);
+    __syncthreads();  // previous chunk's Z1 consumed; tables written
+    for (int i = threadIdx.x; i < nr * H; i += blockDim.x) Xc[i] = xp[(int64_t)ky0 * H + i];
+    __syncthreads();
+    for (int o = threadIdx.x; o < nr * U; o += blockDim.x) {
+      const int r = o / U, u = o - r * U;
+      T ar = T(0), ai = T(0);
+      for (int kx = 0; kx < H; ++kx) {
+        const cplx_t<T> x = Xc[r * H + kx], e = Ex[kx * U + u];
+        ar = fma(x.x, e.x, fma(-x.y, e.y, ar));
+        ai = fma(x.x, e.y, fma(x.y, e.x, ai));
+      }
+      Z1[o] = mk<T>(ar, ai);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kAcc; ++q) {
+      const int o = threadIdx.x + q * blockDim.x;
+      if (o < U * U) {
+        const int uy = o / U, ux = o - uy * U;
+        T ar = acc[q].x, ai = acc[q].y;
+        for (int r = 0; r < nr; ++r) {
+          const cplx_t<T> z = Z1[r * U + ux], e = Ey[(ky0 + r) * U + uy];
+          ar = fma(z.x, e.x, fma(-z.y, e.y, ar));
+          ai = fma(z.x, e.y, fma(z.y, e.x, ai));
+        }
+        acc[q] = mk<T>(ar, ai);
+      }
+    }
+  }
+  cplx_t<T>* zo = Z2 + (p * N + kz) * (int64_t)U * U;
+#pragma unroll
+  for (int q = 0; q < kAcc; ++q) {
+    const int o = threadIdx.x + q * blockDim.x;
+    if (o < U * U) zo[o] = acc[q];
+  }
+}
+
+constexpr int kUpsZThreads = 128;
+constexpr int kUpsMaxU = 65;  // kappa <= 21
+
+// grid (ceil(U^2 / 128), nb): thread (uy, ux), all U values of uz in registers
+template <typename T>
+__global__ void __launch_bounds__(kUpsZThreads) k_ups_z(const cplx_t<T>* __restrict__ Z2, int N, int kappa,
+                                                        const int* __restrict__ tint, T* __restrict__ bval,
+                                                        int* __restrict__ bidx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int h = (int)ceil(1.5 * kappa), U = 2 * h + 1;
+  cplx_t<T>* Ez = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N][U]
+  __shared__ T sv[kUpsZThreads / 32];
+  __shared__ int si[kUpsZThreads / 32];
+  const int64_t p = blockIdx.y;
+  const int tz0 = tint[p * 3 + 2];
+  for (int i = threadIdx.x; i < N * U; i += blockDim.x) {
+    const int kz = i / U, u = i - kz * U;
+    Ez[i] = ups_phase<T>(kz, N, tz0, u, h, kappa);
+  }
+  __syncthreads();
+  const int o = blockIdx.x * kUpsZThreads + threadIdx.x;  // (uy, ux)
+  T bv = -INFINITY;
+  int bi = 0x7fffffff;
+  if (o < U * U) {
+    T acc[kUpsMaxU];
+#pragma unroll
+    for (int w = 0; w < kUpsMaxU; ++w) acc[w] = T(0);
+    const cplx_t<T>* zp = Z2 + p * (int64_t)N * U * U + o;
+    for (int kz = 0; kz < N; ++kz) {
+      const cplx_t<T> z = zp[(int64_t)kz * U * U];
+      const cplx_t<T>* er = Ez + kz * U;
+#pragma unroll
+      for (int w = 0; w < kUpsMaxU; ++w)
+        if (w < U) acc[w] = fma(z.x, er[w].x, fma(-z.y, er[w].y, acc[w]));  // Re(z e)
+    }
+#pragma unroll
+    for (int w = 0; w < kUpsMaxU; ++w)
+      if (w < U) {
+        const int idx = w * U * U + o;  // z-major grid index
+        if (better(acc[w], idx, bv, bi)) {
+          bv = acc[w];
+          bi = idx;
+        }
+      }
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const T v2 = __shfl_xor_sync(0xffffffffu, bv, s);
+    const int i2 = __shfl_xor_sync(0xffffffffu, bi, s);
+    if (better(v2, i2, bv, bi)) {
+      bv = v2;
+      bi = i2;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < kUpsZThreads / 32; ++k)
+      if (better(sv[k], si[k], bv, bi)) {
+        bv = sv[k];
+        bi = si[k];
+      }
+    bval[p * gridDim.x + blockIdx.x] = bv;
+    bidx[p * gridDim.x + blockIdx.x] = bi;
+  }
+}
+
+template <typename T>
+__global__ void k_ups_final(const T* __restrict__ bval, const int* __restrict__ bidx, int nblk, int N, int kappa,
+                            const int* __restrict__ tint, int64_t nb, T* shifts, int sstride, T* peak) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nb) return;
+  const int h = (int)ceil(1.5 * kappa), U = 2 * h + 1;
+  T bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int k = 0; k < nblk; ++k)
+    if (better(bval[p * nblk + k], bidx[p * nblk + k], bv, bi)) {
+      bv = bval[p * nblk + k];
+      bi = bidx[p * nblk + k];
+    }
+  const int u[3] = {bi % U, (bi / U) % U, bi / (U * U)};
+  for (int ax = 0; ax < 3; ++ax) shifts[p * sstride + ax] = (T)tint[p * 3 + ax] + (T)(u[ax] - h) / (T)kappa;
+  if (peak) peak[p] = bv / ((T)N * N * N);
+}
+
 }  // namespace
 
 template <typename T>
@@ -854,7 +1068,7 @@ size_t window_scratch_reals(int N, int W) {
 // Y1 [nb][wp][N][H] complex at the front of the scratch, the c windows [nb][wp^3] behind it
 template <typename T>
 cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N, int W, int64_t nb, T* scratch,
-                                T* shifts, int sstride, T* peak, cudaStream_t s) {
+                                T* shifts, int sstride, T* peak, int* tint, cudaStream_t s) {
   if (nb == 0) return cudaSuccess;
   const size_t csz = sizeof(cplx_t<T>);
   if (!trans_supported(N, W, sizeof(T) == 8)) return cudaErrorInvalidValue;
@@ -889,17 +1103,78 @@ cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N,
   if (e != cudaSuccess) return e;
   k_window_xy<T><<<dim3((unsigned)wp, (unsigned)nb), 512, xsm, s>>>(Y1, N, W, cw);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  k_window_peak<T><<<(unsigned)nb, 256, 0, s>>>(cw, N, W, shifts, sstride, peak);
+  k_window_peak<T><<<(unsigned)nb, 256, 0, s>>>(cw, N, W, shifts, sstride, peak, tint);
   return cudaGetLastError();
 }
+
+int ups_points(int kappa) { return 2 * (int)std::ceil(1.5 * kappa) + 1; }
+
+size_t ups_scratch_bytes(int N, int kappa, size_t csz) {
+  const size_t U = (size_t)ups_points(kappa);
+  const size_t nblk = (U * U + kUpsZThreads - 1) / kUpsZThreads;
+  return csz * (size_t)N * U * U + nblk * (csz / 2 + sizeof(int)) + 3 * sizeof(int) + 256;
+}
+
+static int zfft_chunk(int N, size_t csz) {
+  const int H = N / 2 + 1;
+  int hc = H;
+  while (hc > 1 && csz * ((size_t)N + 4 * (size_t)hc * N) > 200 * 1024) --hc;
+  return hc;
+}
+
+bool ups_supported(int N, int kappa, bool fp64) {
+  const size_t csz = fp64 ? 16 : 8;
+  const int U = ups_points(kappa), H = N / 2 + 1;
+  const size_t xy = csz * ((size_t)H * U + (size_t)N * U + (size_t)kUpsRows * H + (size_t)kUpsRows * U);
+  return kappa >= 1 && U <= kUpsMaxU && U * U <= 6 * 512 && xy <= 227 * 1024 && csz * (size_t)N * U <= 200 * 1024 &&
+         csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
+}
+
+// per-particle scratch: Z2 [N][U][U] complex, then the block bests; tint [nb][3] from k_window_peak
+template <typename T>
+cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
+                             void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s) {
+  if (nb == 0) return cudaSuccess;
+  const size_t csz = sizeof(cplx_t<T>);
+  if (!ups_supported(N, kappa, sizeof(T) == 8)) return cudaErrorInvalidValue;
+  const int H = N / 2 + 1, U = ups_points(kappa);
+  const int hc = zfft_chunk(N, csz), nkc = (H + hc - 1) / hc;
+  const size_t zsm = csz * ((size_t)N + 4 * (size_t)hc * N);
+  cudaError_t e = cudaFuncSetAttribute(k_zfft_cross<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
+  if (e != cudaSuccess) return e;
+  k_zfft_cross<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, fft_radix(N), hc);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cplx_t<T>* Z2 = reinterpret_cast<cplx_t<T>*>(scratch);
+  const int nblk = (U * U + kUpsZThreads - 1) / kUpsZThreads;
+  T* bval = reinterpret_cast<T*>(Z2 + nb * (int64_t)N * U * U);
+  int* bidx = reinterpret_cast<int*>(bval + nb * nblk);
+  const size_t xsm = csz * ((size_t)H * U + (size_t)N * U + (size_t)kUpsRows * H + (size_t)kUpsRows * U);
+  e = cudaFuncSetAttribute(k_ups_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
+  if (e != cudaSuccess) return e;
+  k_ups_xy<T><<<dim3((unsigned)N, (unsigned)nb), 512, xsm, s>>>(rt, N, kappa, tint, Z2);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t esm = csz * (size_t)N * U;
+  e = cudaFuncSetAttribute(k_ups_z<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+  if (e != cudaSuccess) return e;
+  k_ups_z<T><<<dim3((unsigned)nblk, (unsigned)nb), kUpsZThreads, esm, s>>>(Z2, N, kappa, tint, bval, bidx);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_ups_final<T><<<(unsigned)((nb + 127) / 128), 128, 0, s>>>(bval, bidx, nblk, N, kappa, tint, nb, shifts, sstride,
+                                                               peak);
+  return cudaGetLastError();
+}
+
 template cudaError_t launch_rotate_ref<float>(const float*, int, const float*, int, int64_t, float*, cudaStream_t);
 template cudaError_t launch_rotate_ref<double>(const float*, int, const double*, int, int64_t, double*, cudaStream_t);
+template cudaError_t launch_upsampled<float>(const float2*, float2*, int, int, int64_t, const int*, void*, float*, int,
+                                             float*, cudaStream_t);
+template cudaError_t launch_upsampled<double>(const double2*, double2*, int, int, int64_t, const int*, void*, double*,
+                                              int, double*, cudaStream_t);
 template cudaError_t launch_plane_r2c<float, float>(const float*, int, int64_t, float2*, cudaStream_t);
 template cudaError_t launch_plane_r2c<double, float>(const float*, int, int64_t, double2*, cudaStream_t);
 template cudaError_t launch_plane_r2c<double, double>(const double*, int, int64_t, double2*, cudaStream_t);
 template cudaError_t launch_window_zcorr<float>(const float2*, const float2*, int, int, int64_t, float*, float*, int,
-                                                float*, cudaStream_t);
+                                                float*, int*, cudaStream_t);
 template cudaError_t launch_window_zcorr<double>(const double2*, const double2*, int, int, int64_t, double*, double*,
-                                                 int, double*, cudaStream_t);
+                                                 int, double*, int*, cudaStream_t);
 
 }  // namespace matcha

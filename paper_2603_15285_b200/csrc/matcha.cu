@@ -63,6 +63,9 @@ struct matcha_ctx {
   void* ws_peak = nullptr;   // real [mb]
   void* ws_win = nullptr;    // real [mb][window_scratch_reals(N, W)]: Y1 (z correlation) + the c window
   int ws_win_W = -1;
+  int* ws_tint = nullptr;    // int [mb][3]: integer window peaks (upsampled subpixel)
+  void* ws_ups = nullptr;    // [mb] x ups_scratch_bytes(N, kappa): upsampled-DFT scratch
+  int ws_ups_kappa = -1;
   bool trans_fast = false;   // FP32 and N in {32, 64, 96, 128}: compile-time FFTs, rotation fused into rho's transform
   float* ws_refpad = nullptr;  // zero-padded plane stack of the reference (texture source of the fused rotation)
   int refpad_pitch = 0;        // floats per row
@@ -196,6 +199,7 @@ bool valid_params(const matcha_params_t* p, int LM, std::string& why) {
   if (p->n_cand < 1 || p->n_cand > kMaxCand) { why = "n_cand must be in [1,32]"; return false; }
   if (p->oversample < 1 || p->oversample > 8) { why = "oversample must be in [1,8]"; return false; }
   if (p->n_alternations < 1 || p->n_alternations > 64) { why = "n_alternations must be in [1,64]"; return false; }
+  if (p->upsample < 0) { why = "upsample must be >= 0"; return false; }
   return true;
 }
 
@@ -292,7 +296,7 @@ static cudaError_t do_refine(matcha_handle_t h, const void* M, int32_t L_M, int6
 }
 
 // ---------------------------------------------------------------- stage 5 helpers
-static matcha_status_t trans_prepare(matcha_handle_t h, int W) {
+static matcha_status_t trans_prepare(matcha_handle_t h, int W, int kappa) {
   const int N = h->cfg.N;
   const int64_t nr = (int64_t)N * N * N, nc = (int64_t)N * N * (N / 2 + 1), mb = h->cfg.max_batch;
   if (!trans_supported(N, W, h->fp64))
@@ -338,13 +342,28 @@ static matcha_status_t trans_prepare(matcha_handle_t h, int W) {
       return fail(h, MATCHA_ERR_ALLOC, "translation window scratch allocation failed");
     h->ws_win_W = W;
   }
+  if (kappa > 0) {
+    if (!ups_supported(N, kappa, h->fp64))
+      return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "translation: upsample factor / box exceed the kernels' limits");
+    if (!h->ws_tint && cudaMalloc((void**)&h->ws_tint, sizeof(int) * 3 * mb) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "translation: peak index allocation failed");
+    if (h->ws_ups_kappa < kappa) {
+      if (h->ws_ups) cudaFree(h->ws_ups);
+      h->ws_ups = nullptr;
+      h->ws_ups_kappa = -1;
+      if (cudaMalloc(&h->ws_ups, ups_scratch_bytes(N, kappa, 2 * h->rsz) * mb) != cudaSuccess)
+        return fail(h, MATCHA_ERR_ALLOC, "translation: upsampled-DFT scratch allocation failed");
+      h->ws_ups_kappa = kappa;
+    }
+  }
   return MATCHA_OK;
 }
 
 // f~ (2-D plane spectra) of nb particle volumes into ws_Fhat (once per chunk: the particles do not change across
 // alternations)
-static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t nb, int W, cudaStream_t s) {
-  matcha_status_t st = trans_prepare(h, W);
+static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t nb, int W, int kappa,
+                                  cudaStream_t s) {
+  matcha_status_t st = trans_prepare(h, W, kappa);
   if (st != MATCHA_OK) return st;
   cudaError_t e = h->fp64 ? launch_plane_r2c<double, float>(vols, h->cfg.N, nb, (double2*)h->ws_Fhat, s)
                   : h->trans_fast
@@ -357,11 +376,11 @@ static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t 
 
 // t = windowed argmax of c(t) = sum_x f(x) rho(x - t) for the rotations `euler` (stride estride)
 static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* ref, const void* euler, int estride,
-                                    int W, void* shifts, int sstride, void* peak, cudaStream_t s) {
+                                    int W, int kappa, void* shifts, int sstride, void* peak, cudaStream_t s) {
   const int N = h->cfg.N;
   cudaError_t e;
   ProfScope ps(h, 5, s);
-  matcha_status_t st = trans_prepare(h, W);
+  matcha_status_t st = trans_prepare(h, W, kappa);
   if (st != MATCHA_OK) return st;
   if (h->trans_fast) {
     // rho~ straight from the reference texture: the rotated references never touch HBM
@@ -377,12 +396,21 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
                 : launch_plane_r2c<float, float>((const float*)h->ws_rho, N, nb, (float2*)h->ws_Xhat, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of rho");
   }
+  int* tint = kappa > 0 ? h->ws_tint : nullptr;
   e = h->fp64 ? launch_window_zcorr<double>((const double2*)h->ws_Fhat, (const double2*)h->ws_Xhat, N, W, nb,
-                                            (double*)h->ws_win, (double*)shifts, sstride, (double*)peak, s)
+                                            (double*)h->ws_win, (double*)shifts, sstride, (double*)peak, tint, s)
               : launch_window_zcorr<float>((const float2*)h->ws_Fhat, (const float2*)h->ws_Xhat, N, W, nb,
-                                           (float*)h->ws_win, (float*)shifts, sstride, (float*)peak, s);
+                                           (float*)h->ws_win, (float*)shifts, sstride, (float*)peak, tint, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: window_zcorr");
-  h->launches += 5;
+  h->launches += h->trans_fast ? 5 : 6;
+  if (kappa > 0) {
+    e = h->fp64 ? launch_upsampled<double>((const double2*)h->ws_Fhat, (double2*)h->ws_Xhat, N, kappa, nb, tint,
+                                           h->ws_ups, (double*)shifts, sstride, (double*)peak, s)
+                : launch_upsampled<float>((const float2*)h->ws_Fhat, (float2*)h->ws_Xhat, N, kappa, nb, tint,
+                                          h->ws_ups, (float*)shifts, sstride, (float*)peak, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "translation: upsampled DFT");
+    h->launches += 4;
+  }
   return MATCHA_OK;
 }
 
@@ -437,11 +465,11 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
       if (translate) {
         if (tau == 0) {
           ProfScope ps(h, 5, s);
-          st = trans_fhat(h, vols + c0 * n3, nb, p->shift_window, s);
+          st = trans_fhat(h, vols + c0 * n3, nb, p->shift_window, p->upsample, s);
           if (st != MATCHA_OK) return st;
         }
         // t^tau from the rotation just estimated (poses[b][0..2]) -> poses[b][3..5]
-        st = trans_update(h, nb, ref, pc, 8, p->shift_window, pc + 3 * h->rsz, 8, h->ws_peak, s);
+        st = trans_update(h, nb, ref, pc, 8, p->shift_window, p->upsample, pc + 3 * h->rsz, 8, h->ws_peak, s);
         if (st != MATCHA_OK) return st;
       }
     }
@@ -602,7 +630,8 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
     if (p) cudaFree(p);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->tex_ref) cudaDestroyTextureObject(h->tex_ref);
-  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad})
+  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad,
+                  (void*)h->ws_tint, h->ws_ups})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -756,19 +785,23 @@ MATCHA_API matcha_status_t matcha_newton_refine(matcha_handle_t h, const void* M
 
 MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const float* vols, int64_t B,
                                                      const float* ref, const void* euler, int32_t window,
-                                                     void* shifts, void* peak, void* stream) {
+                                                     int32_t upsample, void* shifts, void* peak, void* stream) {
   if (!h) return MATCHA_ERR_INVALID_ARG;
   if (B < 0 || (B > 0 && (!vols || !ref || !euler || !shifts)))
     return fail(h, MATCHA_ERR_INVALID_ARG, "translation_update: bad arguments");
   if (window < 0 || window > h->cfg.N / 4) return fail(h, MATCHA_ERR_WINDOW, "translation_update: W > N/4");
+  if (upsample < 0 || (upsample > 0 && !ups_supported(h->cfg.N, upsample, h->fp64)))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "translation_update: upsample factor outside the supported range");
+  if (!trans_supported(h->cfg.N, window, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "translation_update: box too large for the stage-5 kernels");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n3 = (int64_t)h->cfg.N * h->cfg.N * h->cfg.N;
   for (int64_t c0 = 0; c0 < B; c0 += h->cfg.max_batch) {
     const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
-    matcha_status_t st = trans_fhat(h, vols + c0 * n3, nb, window, s);
+    matcha_status_t st = trans_fhat(h, vols + c0 * n3, nb, window, upsample, s);
     if (st != MATCHA_OK) return st;
-    st = trans_update(h, nb, ref, (const char*)euler + c0 * 3 * h->rsz, 3, window, (char*)shifts + c0 * 3 * h->rsz, 3,
-                      peak ? (char*)peak + c0 * h->rsz : h->ws_peak, s);
+    st = trans_update(h, nb, ref, (const char*)euler + c0 * 3 * h->rsz, 3, window, upsample,
+                      (char*)shifts + c0 * 3 * h->rsz, 3, peak ? (char*)peak + c0 * h->rsz : h->ws_peak, s);
     if (st != MATCHA_OK) return st;
   }
   return MATCHA_OK;
@@ -787,6 +820,8 @@ MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vo
     return fail(h, MATCHA_ERR_WINDOW, "align_batch: shift window needs ref and W <= N/4");
   if (params->shift_window > 0 && !trans_supported(h->cfg.N, params->shift_window, h->fp64))
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: box too large for the stage-5 kernels");
+  if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: upsample factor / box exceed the kernels' limits");
   if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
     return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: coarse grid too large for one CTA");
   return align_device(h, vols, B, ref, ref_coeffs, params, poses, (cudaStream_t)stream);
@@ -803,6 +838,8 @@ MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const floa
   if (params->shift_window > h->cfg.N / 4) return fail(h, MATCHA_ERR_WINDOW, "align_batch_host: W > N/4");
   if (params->shift_window > 0 && !trans_supported(h->cfg.N, params->shift_window, h->fp64))
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch_host: box too large for the stage-5 kernels");
+  if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch_host: upsample factor / box exceed the kernels' limits");
   if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
     return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch_host: coarse grid too large for one CTA");
   cudaStream_t s = (cudaStream_t)stream;

@@ -420,3 +420,65 @@ def test_alternation_c3_shape_sampled():
         assert np.abs(poses[p, 3:6] - po[i, 3:6]).max() < 0.1
     errs = [O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) for p in range(B)]
     assert np.median(errs) < 2.0
+
+
+# ------------------------------------------------------------------ stage 5: upsampled-DFT subpixel
+@pytest.mark.parametrize("N,W", [(32, 4), (24, 5), (40, 4), (64, 6)])
+def test_translation_upsampled_parity(N, W, prec):
+    """matcha_translation_update with upsample = 16 (Guizar-Sicairos refinement, App. C remark iii) vs the oracle's
+    separable matrix-multiply DFT in FP64: same integer peak, the same 1/16-grid point (or a neighbour when two grid
+    values tie within FP32 rounding: <= 0.1 voxel, north_star's shift tolerance), same c~ at that point."""
+    B = 4
+    b = gen.particles(N, B, 2.0, seed=45, shift_mode=gen.SHIFT_UNIFORM, shift_max=W - 1.5)
+    eul = np.array([O.matrix_to_euler(R) for R in b.truth_R])
+    eul[1] += 0.01
+    h = handle(N, 8, prec)
+    sh, pk = h.translation_update(cuda(b.vols), cuda(b.ref), cuda(eul, h.real), W, upsample=16)
+    sh, pk = to_np(sh), to_np(pk)
+    eul_used = to_np(cuda(eul, h.real)).astype(np.float64)
+    same = 0
+    for p in range(B):
+        so, po = O.translation_upsampled(b.vols[p], b.ref, eul_used[p], W, 16)
+        d = np.abs(sh[p] - so).max()
+        assert d <= 0.1, (p, sh[p], so)
+        if d < 1e-6:
+            same += 1
+            assert abs(pk[p] - po) <= (1e-9 if prec == "fp64" else 1e-4) * abs(po), (p, pk[p], po)
+        assert np.abs(sh[p] - b.truth_t[p]).max() < 0.3
+    assert same >= B - 1
+
+
+def test_alternation_fractional_shift_upsampled_c1_gpu():
+    """SURVEY f3 done-criterion: the c1 fixture with a fractional planted shift reaches <= 0.05 deg and <= 0.01 voxel
+    by T = 4 with the upsampled subpixel, and matches the oracle."""
+    b = gen.particles(32, 2, float("inf"), seed=12, shift_mode=gen.SHIFT_FIXED, fixed_shift=(1.25, -1.5, 0.75))
+    h = handle(32, 8)
+    params = mt.Params(bands=[4, 6, 8], n_cand=4, oversample=2, n_alternations=4, shift_window=4, upsample=16)
+    poses = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    h.status()
+    po = O.align_batch(b.vols, b.ref, dict(L=8, qover=2, L0=4, K=2, ncand=4, bands=[4, 6, 8], iters=1, T=4, W=4,
+                                           ups=16))
+    for p in range(2):
+        assert rot_err_deg(poses[p, :3], po[p, :3]) < TOL_ROT_DEG
+        assert np.abs(poses[p, 3:6] - po[p, 3:6]).max() < 0.1
+        assert O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) <= 0.05
+        assert np.abs(poses[p, 3:6] - b.truth_t[p]).max() <= 0.01
+
+
+def test_alternation_c3_shape_upsampled():
+    """c3 shape (96^3, SNR 0.05, L0=8 -> 48, T=3, W=6) with the upsampled subpixel: 3 particles of a 32-particle
+    batch vs the oracle, and the recovered shifts vs the planted U[-4,4]^3 ones."""
+    B = 32
+    b = gen.particles(96, B, 0.05, seed=47, shift_mode=gen.SHIFT_UNIFORM, shift_max=4.0)
+    bands = [8, 12, 16, 24, 32, 48]
+    h = handle(96, 48, max_batch=B)
+    params = mt.Params(bands=bands, n_cand=10, oversample=2, n_alternations=3, shift_window=6, upsample=16)
+    poses = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    h.status()
+    sel = [0, 13, 31]
+    po = O.align_batch(b.vols[sel], b.ref, dict(L=48, qover=2, L0=8, K=2, ncand=10, bands=bands, iters=1, T=3, W=6,
+                                                 ups=16))
+    for i, p in enumerate(sel):
+        assert rot_err_deg(poses[p, :3], po[i, :3]) < TOL_ROT_DEG, (p, rot_err_deg(poses[p, :3], po[i, :3]))
+        assert np.abs(poses[p, 3:6] - po[i, 3:6]).max() <= 0.1
+    assert np.median(np.abs(poses[:, 3:6] - b.truth_t).max(axis=1)) < 0.5
