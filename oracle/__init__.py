@@ -294,7 +294,8 @@ def translation_upsampled(vol, ref, e, W, kappa=16):
 
 
 def upsampled_corr_at(vol, ref, e, t):
-    """c~(t) = (1/N^3) Re sum_{k in [-N/2, N/2)^3} F^ conj(rho^) e^{2 pi i k.t/N} at one point (full triple sum)."""
+    """c~(t) = (1/N^3) Re sum_k F^ conj(rho^) D(kx,tx) D(ky,ty) D(kz,tz) at one point (full triple sum; D(k,t) =
+    e^{2 pi i k' t/N}, k' the symmetric frequency, D(N/2, t) = cos(pi t): reading C27)."""
     vol = np.ascontiguousarray(vol, np.float32)
     ref = np.ascontiguousarray(ref, np.float32)
     return _lib().orc_upsampled_corr_at(_p(vol, _fp), _p(ref, _fp), vol.shape[-1],

@@ -625,8 +625,10 @@ void translation(const float* vol, const float* ref, int N, const double* e, int
 /* ---------------- stage 5, subpixel by an upsampled DFT (App. C remark iii) ----------------
    Guizar-Sicairos's scheme: the integer peak t0 of the windowed correlation (as translation() above), then the
    correlation's trigonometric interpolant on a kappa-times finer grid over +-1.5 voxel around t0, evaluated by
-   matrix-multiply DFTs (reading C27):
-     c~(t) = (1/N^3) Re sum_{k in K^3} F^(k) conj(rho^(k)) e^{+2 pi i k.t / N},   K = {-N/2, ..., N/2 - 1},
+   matrix-multiply DFTs (reading C27: the REAL trigonometric interpolant, the Nyquist index N/2 split evenly
+   between +-N/2, i.e. D(N/2, t) = cos(pi t)):
+     c~(t) = (1/N^3) sum_{k in [0,N)^3} F^(k) conj(rho^(k)) D(kx, tx) D(ky, ty) D(kz, tz),
+     D(k, t) = e^{+2 pi i k' t / N} with k' = k (k < N/2) or k - N (k > N/2), D(N/2, t) = cos(pi t),
    F^, rho^ the 3-D DFTs of f and rho (here by a plain separable DFT in FP64), t = t0 + u / kappa,
    u in [-h, h]^3 with h = ceil(1.5 kappa); the result is the argmax (ties -> lowest index, z-major) and c~ there.
    At integer t, c~(t) = c(t) = sum_x f(x) rho(x - t) exactly (circular correlation). */
@@ -652,6 +654,12 @@ void dft_axis(vector<cd>& a, int N, int axis) {
     }
 }
 
+cd interp_kernel(int k, int N, double t) {
+  if (2 * k == N) return cd(std::cos(PI * t), 0.0);
+  const int kp = k < N / 2 ? k : k - N;
+  return std::polar(1.0, 2.0 * PI * kp * t / N);
+}
+
 void translation_upsampled(const float* vol, const float* ref, int N, const double* e, int W, int kappa,
                            double* shift, double* peak) {
   double tpar[3], pk;
@@ -674,17 +682,12 @@ void translation_upsampled(const float* vol, const float* ref, int N, const doub
   vector<cd> X(n3);
   for (size_t i = 0; i < n3; ++i) X[i] = F[i] * std::conj(R[i]);
   const int h = (int)std::ceil(1.5 * kappa), U = 2 * h + 1;
-  /* phase matrices E_ax[k][u] = e^{2 pi i k' (t0_ax + (u - h)/kappa) / N}, k' = k (k < N/2) or k - N (k >= N/2) */
+  /* phase matrices E_ax[k][u] = D(k, t0_ax + (u - h)/kappa) */
   vector<cd> E[3];
   for (int ax = 0; ax < 3; ++ax) {
     E[ax].resize((size_t)N * U);
-    for (int k = 0; k < N; ++k) {
-      const int kp = k < N / 2 ? k : k - N;
-      for (int u = 0; u < U; ++u) {
-        const double t = t0[ax] + (double)(u - h) / kappa;
-        E[ax][(size_t)k * U + u] = std::polar(1.0, 2.0 * PI * kp * t / N);
-      }
-    }
+    for (int k = 0; k < N; ++k)
+      for (int u = 0; u < U; ++u) E[ax][(size_t)k * U + u] = interp_kernel(k, N, t0[ax] + (double)(u - h) / kappa);
   }
   /* separable contraction: x, then y, then z (matrix-multiply DFTs) */
   vector<cd> A((size_t)N * N * U), B((size_t)N * U * U);
@@ -709,7 +712,7 @@ void translation_upsampled(const float* vol, const float* ref, int N, const doub
       for (int u = 0; u < U; ++u) {
         cd s(0, 0);
         for (int kz = 0; kz < N; ++kz) s += B[((size_t)kz * U + v) * U + u] * E[2][(size_t)kz * U + w];
-        const double c = std::real(s) / (double)n3;
+        const double c = std::real(s) / (double)n3;  /* imaginary part 0 up to rounding (Hermitian X, real D) */
         if (c > bv) { bv = c; bu[0] = u; bu[1] = v; bu[2] = w; } /* scan order = z-major index order */
       }
   for (int ax = 0; ax < 3; ++ax) shift[ax] = t0[ax] + (double)(bu[ax] - h) / kappa;
@@ -873,9 +876,8 @@ double orc_upsampled_corr_at(const float* vol, const float* ref, int N, const do
   for (int kz = 0; kz < N; ++kz)
     for (int ky = 0; ky < N; ++ky)
       for (int kx = 0; kx < N; ++kx) {
-        const int px = kx < N / 2 ? kx : kx - N, py = ky < N / 2 ? ky : ky - N, pz = kz < N / 2 ? kz : kz - N;
         const size_t i = ((size_t)kz * N + ky) * N + kx;
-        s += F[i] * std::conj(R[i]) * std::polar(1.0, 2.0 * PI * (px * t[0] + py * t[1] + pz * t[2]) / N);
+        s += F[i] * std::conj(R[i]) * interp_kernel(kx, N, t[0]) * interp_kernel(ky, N, t[1]) * interp_kernel(kz, N, t[2]);
       }
   return std::real(s) / (double)n3;
 }

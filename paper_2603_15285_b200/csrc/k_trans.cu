@@ -745,15 +745,15 @@ __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft,
 
 
 // ==== stage 5e: subpixel refinement by an upsampled DFT (Guizar-Sicairos; App. C remark iii) ===
-// Around the integer window peak t0 the correlation's trigonometric interpolant (reading C27)
-//   c~(t) = (1/N^3) Re sum_{k in [-N/2, N/2)^3} F^(k) conj(rho^(k)) e^{+2 pi i k.t / N}
+// Around the integer window peak t0 the correlation's real trigonometric interpolant (reading C27)
+//   c~(t) = (1/N^3) sum_{k in [0,N)^3} F^(k) conj(rho^(k)) D(kx,tx) D(ky,ty) D(kz,tz)   (see ups_phase)
 // is evaluated on t = t0 + (u - h) / kappa, u in [0, U)^3, U = 2h + 1, h = ceil(1.5 kappa), by three matrix-multiply
 // DFTs; the result is the grid argmax (ties -> lowest index, z-major).
 //   k_zfft_cross  3-D spectra from the plane spectra: the z FFT of f~ and rho~ pencils (Stockham in shared memory),
 //                 X = F^ conj(rho^) written over rho~ (never needed again this alternation);
 //   k_ups_xy      per (kz plane, particle): Z2[kz][uy][ux] = sum_ky Ey[ky][uy] sum_kx wx Ex[kx][ux] X[kz][ky][kx]
-//                 (half spectrum in kx: w = 1 at kx = 0, the Nyquist column as -N/2 with w = 1, else w = 2; Re taken
-//                 at the end makes the half sum exact for the Hermitian X);
+//                 (half spectrum in kx: w = 1 at kx = 0 and N/2, else w = 2; Re taken at the end makes the half sum
+//                 exact for the Hermitian X);
 //   k_ups_z       per (block of (uy, ux), particle): c~ = Re sum_kz Ez[kz][uz] Z2[kz][uy][ux] for all uz, block argmax;
 //   k_ups_final   per particle: argmax over the blocks, t = t0 + (u - h)/kappa, peak = c~ / ... (already 1/N^3).
 
@@ -787,10 +787,15 @@ __global__ void __launch_bounds__(256) k_zfft_cross(const cplx_t<T>* __restrict_
   }
 }
 
-// e^{+2 pi i k' t / N} with k' the symmetric frequency of index k (k' = k - N for k >= N/2)
+// interpolation kernel D(k, t) of reading C27: e^{+2 pi i k' t / N} with k' the symmetric frequency of index k
+// (k' = k - N for k > N/2), and the real cos(pi t) at the Nyquist index k = N/2 (split evenly between +-N/2)
 template <typename T> __device__ __forceinline__ cplx_t<T> ups_phase(int k, int N, int t0, int u, int h, int kappa) {
-  const int kp = k < N / 2 ? k : k - N;
   const T t = (T)t0 + (T)(u - h) / (T)kappa;
+  if (2 * k == N) {
+    if constexpr (sizeof(T) == 8) return mk<T>(cospi(t), T(0));
+    else return mk<T>(cospif(t), T(0));
+  }
+  const int kp = k < N / 2 ? k : k - N;
   T sn, cs;
   if constexpr (sizeof(T) == 8) sincospi(2.0 * kp * t / N, &sn, &cs);
   else sincospif(2.0f * (float)kp * t / (float)N, &sn, &cs);
@@ -813,10 +818,10 @@ __global__ void __launch_bounds__(512) k_ups_xy(const cplx_t<T>* __restrict__ X,
   const int tx0 = tint[p * 3 + 0], ty0 = tint[p * 3 + 1];
   for (int i = threadIdx.x; i < H * U; i += blockDim.x) {
     const int kx = i / U, u = i - kx * U;
-    // kx = N/2 is the symmetric range's -N/2 (weight 1); 1 <= kx < N/2 stand for +-kx (weight 2)
-    const int kk = (2 * kx == N) ? N / 2 : kx;  // ups_phase maps N/2 to -N/2
+    // Hermitian half spectrum: 1 <= kx < N/2 stand for +-kx (weight 2, Re at the end); kx = 0 and the Nyquist
+    // column (real kernel cos(pi t)) count once -- exact because D(-k, t) = conj D(k, t) for every index
     const T w = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
-    const cplx_t<T> e = ups_phase<T>(kk, N, tx0, u, h, kappa);
+    const cplx_t<T> e = ups_phase<T>(kx, N, tx0, u, h, kappa);
     Ex[i] = mk<T>(w * e.x, w * e.y);
   }
   for (int i = threadIdx.x; i < N * U; i += blockDim.x) {
