@@ -787,6 +787,42 @@ __global__ void __launch_bounds__(256) k_zfft_cross(const cplx_t<T>* __restrict_
   }
 }
 
+// FP32, compile-time N: the same z FFTs with ct_fft, cp.async-staged lines, one CTA per (ky row, particle)
+template <int N>
+__global__ void __launch_bounds__(kFftThreads, 1) k_zfft_cross_fast(const float2* __restrict__ ft,
+                                                                    float2* __restrict__ rt) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int H = N / 2 + 1, LB = fpad(H * N);
+  float2* tw = reinterpret_cast<float2*>(smem_raw);
+  float2* f0 = tw + N;  // [H][N] lines along z (fpad indices)
+  float2* r0 = f0 + LB;
+  float2* t1 = r0 + LB;  // ping-pong buffer shared by the two transforms
+  const int ky = blockIdx.x;
+  const int64_t p = blockIdx.y;
+  build_roots<float>(tw, N, -1);
+  const int64_t row0 = (p * N * N + ky) * (int64_t)H;
+  for (int i = threadIdx.x; i < N * H; i += kFftThreads) {
+    const int zz = i / H, kx = i - zz * H;
+    const int64_t g = row0 + (int64_t)zz * N * H + kx;
+    const unsigned df = (unsigned)__cvta_generic_to_shared(f0 + fpad(kx * N + zz));
+    const unsigned dr = (unsigned)__cvta_generic_to_shared(r0 + fpad(kx * N + zz));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(df), "l"(ft + g));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dr), "l"(rt + g));
+  }
+  asm volatile("cp.async.wait_all;\n" ::);
+  __syncthreads();
+  float2* Fz = ct_fft<N, H, N>(f0, t1, tw);  // result in f0 or t1
+  float2* rin = r0;
+  float2* rtmp = (Fz == f0) ? t1 : f0;        // the buffer not holding F^
+  // r0 -> rtmp -> r0 ...: ct_fft alternates the two buffers it is given
+  const float2* Rz = ct_fft<N, H, N>(rin, rtmp, tw);
+  for (int i = threadIdx.x; i < N * H; i += kFftThreads) {
+    const int kz = i / H, kx = i - kz * H;
+    const float2 f = Fz[fpad(kx * N + kz)], r = Rz[fpad(kx * N + kz)];
+    rt[row0 + (int64_t)kz * N * H + kx] = make_float2(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
+  }
+}
+
 // interpolation kernel D(k, t) of reading C27: e^{+2 pi i k' t / N} with k' the symmetric frequency of index k
 // (k' = k - N for k > N/2), and the real cos(pi t) at the Nyquist index k = N/2 (split evenly between +-N/2)
 template <typename T> __device__ __forceinline__ cplx_t<T> ups_phase(int k, int N, int t0, int u, int h, int kappa) {
@@ -802,74 +838,87 @@ template <typename T> __device__ __forceinline__ cplx_t<T> ups_phase(int k, int 
   return mk<T>(cs, sn);
 }
 
-constexpr int kUpsRows = 16;  // ky rows per chunk in k_ups_xy
-
+// register-tiled complex GEMM in shared memory: C[m][n] (+)= sum_k A[m*lda + k] B[k*ldb + n] for m < M, n < NP
+// (NP a multiple of 4; columns beyond the valid range are computed on zero-padded B and discarded by the caller).
+// Each thread owns 4 x 4 outputs: per k, 8 shared-memory loads for 16 complex MACs.
 template <typename T>
-__global__ void __launch_bounds__(512) k_ups_xy(const cplx_t<T>* __restrict__ X, int N, int kappa,
+__device__ __forceinline__ void cgemm_4x4(const cplx_t<T>* __restrict__ A, int lda, const cplx_t<T>* __restrict__ B,
+                                          int ldb, int M, int K, int NP, cplx_t<T>* __restrict__ C, int ldc) {
+  const int tn = NP / 4, ntile = ((M + 3) / 4) * tn;
+  for (int t = threadIdx.x; t < ntile; t += blockDim.x) {
+    const int m0 = (t / tn) * 4, n0 = (t - (t / tn) * tn) * 4;
+    T ar[4][4], ai[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ar[i][j] = ai[i][j] = T(0);
+    for (int k = 0; k < K; ++k) {
+      cplx_t<T> a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = (m0 + i < M) ? A[(m0 + i) * lda + k] : mk<T>(T(0), T(0));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = B[k * ldb + n0 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          ar[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, ar[i][j]));
+          ai[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, ai[i][j]));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (m0 + i < M)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) C[(m0 + i) * ldc + n0 + j] = mk<T>(ar[i][j], ai[i][j]);
+  }
+}
+
+__host__ __device__ inline int ups_pad4(int U) { return (U + 3) / 4 * 4; }
+
+template <typename T> __host__ __device__ inline size_t ups_xy_smem(int N, int U) {
+  const int H = N / 2 + 1, UP = ups_pad4(U);
+  // X plane [N][H] | Ex [H][UP] | Ey^T [UP][N] | Z1 [N][UP]   (Z2 [UP][UP] reuses the X plane + Ex)
+  return sizeof(cplx_t<T>) * ((size_t)N * H + (size_t)H * UP + (size_t)UP * N + (size_t)N * UP);
+}
+
+// per (kz plane, particle): Z1 = X Ex  ([N][H] x [H][U]),  Z2 = Ey^T Z1  ([U][N] x [N][U]), two register-tiled GEMMs
+template <typename T>
+__global__ void __launch_bounds__(256) k_ups_xy(const cplx_t<T>* __restrict__ X, int N, int kappa,
                                                 const int* __restrict__ tint, cplx_t<T>* __restrict__ Z2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int H = N / 2 + 1, h = (int)ceil(1.5 * kappa), U = 2 * h + 1;
-  cplx_t<T>* Ex = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [H][U] (weights folded in)
-  cplx_t<T>* Ey = Ex + H * U;                               // [N][U]
-  cplx_t<T>* Xc = Ey + N * U;                               // [kUpsRows][H]
-  cplx_t<T>* Z1 = Xc + kUpsRows * H;                        // [kUpsRows][U]
+  const int H = N / 2 + 1, h = (int)ceil(1.5 * kappa), U = 2 * h + 1, UP = ups_pad4(U);
+  cplx_t<T>* Xs = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N][H]
+  cplx_t<T>* Ex = Xs + N * H;                               // [H][UP] (weights folded in, zero padded)
+  cplx_t<T>* EyT = Ex + H * UP;                             // [UP][N] (zero padded rows)
+  cplx_t<T>* Z1 = EyT + UP * N;                             // [N][UP]
+  cplx_t<T>* Zs = Xs;                                       // [UP][UP] after the first GEMM
   const int kz = blockIdx.x;
   const int64_t p = blockIdx.y;
   const int tx0 = tint[p * 3 + 0], ty0 = tint[p * 3 + 1];
-  for (int i = threadIdx.x; i < H * U; i += blockDim.x) {
-    const int kx = i / U, u = i - kx * U;
+  const cplx_t<T>* xp = X + (p * N + kz) * (int64_t)N * H;
+  for (int i = threadIdx.x; i < N * H; i += blockDim.x) Xs[i] = xp[i];
+  for (int i = threadIdx.x; i < H * UP; i += blockDim.x) {
+    const int kx = i / UP, u = i - kx * UP;
     // Hermitian half spectrum: 1 <= kx < N/2 stand for +-kx (weight 2, Re at the end); kx = 0 and the Nyquist
     // column (real kernel cos(pi t)) count once -- exact because D(-k, t) = conj D(k, t) for every index
     const T w = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
-    const cplx_t<T> e = ups_phase<T>(kx, N, tx0, u, h, kappa);
+    const cplx_t<T> e = u < U ? ups_phase<T>(kx, N, tx0, u, h, kappa) : mk<T>(T(0), T(0));
     Ex[i] = mk<T>(w * e.x, w * e.y);
   }
-  for (int i = threadIdx.x; i < N * U; i += blockDim.x) {
-    const int ky = i / U, u = i - ky * U;
-    Ey[i] = ups_phase<T>(ky, N, ty0, u, h, kappa);
+  for (int i = threadIdx.x; i < UP * N; i += blockDim.x) {
+    const int u = i / N, ky = i - u * N;
+    EyT[i] = u < U ? ups_phase<T>(ky, N, ty0, u, h, kappa) : mk<T>(T(0), T(0));
   }
-  // Z2 accumulators: thread o owns (uy, ux) = o, o + blockDim.x, ...  (U^2 <= 6 * 512)
-  constexpr int kAcc = 6;
-  cplx_t<T> acc[kAcc];
-#pragma unroll
-  for (int q = 0; q < kAcc; ++q) acc[q] = mk<T>(T(0), T(0));
-  const cplx_t<T>* xp = X + (p * N + kz) * (int64_t)N * H;
-  for (int ky0 = 0; ky0 < N; ky0 += kUpsRows) {
-    const int nr = min(kUpsRows, N - ky0);
-    __syncthreads();  // previous chunk's Z1 consumed; tables written
-    for (int i = threadIdx.x; i < nr * H; i += blockDim.x) Xc[i] = xp[(int64_t)ky0 * H + i];
-    __syncthreads();
-    for (int o = threadIdx.x; o < nr * U; o += blockDim.x) {
-      const int r = o / U, u = o - r * U;
-      T ar = T(0), ai = T(0);
-      for (int kx = 0; kx < H; ++kx) {
-        const cplx_t<T> x = Xc[r * H + kx], e = Ex[kx * U + u];
-        ar = fma(x.x, e.x, fma(-x.y, e.y, ar));
-        ai = fma(x.x, e.y, fma(x.y, e.x, ai));
-      }
-      Z1[o] = mk<T>(ar, ai);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kAcc; ++q) {
-      const int o = threadIdx.x + q * blockDim.x;
-      if (o < U * U) {
-        const int uy = o / U, ux = o - uy * U;
-        T ar = acc[q].x, ai = acc[q].y;
-        for (int r = 0; r < nr; ++r) {
-          const cplx_t<T> z = Z1[r * U + ux], e = Ey[(ky0 + r) * U + uy];
-          ar = fma(z.x, e.x, fma(-z.y, e.y, ar));
-          ai = fma(z.x, e.y, fma(z.y, e.x, ai));
-        }
-        acc[q] = mk<T>(ar, ai);
-      }
-    }
-  }
+  __syncthreads();
+  cgemm_4x4<T>(Xs, H, Ex, UP, N, H, UP, Z1, UP);
+  __syncthreads();
+  cgemm_4x4<T>(EyT, N, Z1, UP, UP, N, UP, Zs, UP);
+  __syncthreads();
   cplx_t<T>* zo = Z2 + (p * N + kz) * (int64_t)U * U;
-#pragma unroll
-  for (int q = 0; q < kAcc; ++q) {
-    const int o = threadIdx.x + q * blockDim.x;
-    if (o < U * U) zo[o] = acc[q];
+  for (int i = threadIdx.x; i < U * U; i += blockDim.x) {
+    const int uy = i / U, ux = i - uy * U;
+    zo[i] = Zs[uy * UP + ux];
   }
 }
 
@@ -1129,10 +1178,10 @@ static int zfft_chunk(int N, size_t csz) {
 
 bool ups_supported(int N, int kappa, bool fp64) {
   const size_t csz = fp64 ? 16 : 8;
-  const int U = ups_points(kappa), H = N / 2 + 1;
-  const size_t xy = csz * ((size_t)H * U + (size_t)N * U + (size_t)kUpsRows * H + (size_t)kUpsRows * U);
-  return kappa >= 1 && U <= kUpsMaxU && U * U <= 6 * 512 && xy <= 227 * 1024 && csz * (size_t)N * U <= 200 * 1024 &&
-         csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
+  const int U = ups_points(kappa), H = N / 2 + 1, UP = ups_pad4(U);
+  const size_t xy = fp64 ? ups_xy_smem<double>(N, U) : ups_xy_smem<float>(N, U);
+  return kappa >= 1 && U <= kUpsMaxU && xy <= 227 * 1024 && (size_t)UP * UP <= (size_t)N * H + (size_t)H * UP &&
+         csz * (size_t)N * U <= 200 * 1024 && csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
 }
 
 // per-particle scratch: Z2 [N][U][U] complex, then the block bests; tint [nb][3] from k_window_peak
@@ -1145,18 +1194,34 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
   const int H = N / 2 + 1, U = ups_points(kappa);
   const int hc = zfft_chunk(N, csz), nkc = (H + hc - 1) / hc;
   const size_t zsm = csz * ((size_t)N + 4 * (size_t)hc * N);
-  cudaError_t e = cudaFuncSetAttribute(k_zfft_cross<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
-  if (e != cudaSuccess) return e;
-  k_zfft_cross<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, fft_radix(N), hc);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  bool fast = false;
+  if constexpr (sizeof(T) == 4) {
+    auto go = [&](auto kern, int NN) {
+      const size_t sm = sizeof(float2) * ((size_t)NN + 3 * (size_t)fpad((NN / 2 + 1) * NN));
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e == cudaSuccess) kern<<<dim3((unsigned)NN, (unsigned)nb), kFftThreads, sm, s>>>(ft, rt);
+      fast = true;
+    };
+    if (N == 32) go(k_zfft_cross_fast<32>, 32);
+    else if (N == 64) go(k_zfft_cross_fast<64>, 64);
+    else if (N == 96) go(k_zfft_cross_fast<96>, 96);
+    else if (N == 128) go(k_zfft_cross_fast<128>, 128);
+  }
+  if (!fast) {
+    e = cudaFuncSetAttribute(k_zfft_cross<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
+    if (e != cudaSuccess) return e;
+    k_zfft_cross<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, fft_radix(N), hc);
+  }
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
   cplx_t<T>* Z2 = reinterpret_cast<cplx_t<T>*>(scratch);
   const int nblk = (U * U + kUpsZThreads - 1) / kUpsZThreads;
   T* bval = reinterpret_cast<T*>(Z2 + nb * (int64_t)N * U * U);
   int* bidx = reinterpret_cast<int*>(bval + nb * nblk);
-  const size_t xsm = csz * ((size_t)H * U + (size_t)N * U + (size_t)kUpsRows * H + (size_t)kUpsRows * U);
+  const size_t xsm = ups_xy_smem<T>(N, U);
   e = cudaFuncSetAttribute(k_ups_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
   if (e != cudaSuccess) return e;
-  k_ups_xy<T><<<dim3((unsigned)N, (unsigned)nb), 512, xsm, s>>>(rt, N, kappa, tint, Z2);
+  k_ups_xy<T><<<dim3((unsigned)N, (unsigned)nb), 256, xsm, s>>>(rt, N, kappa, tint, Z2);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t esm = csz * (size_t)N * U;
   e = cudaFuncSetAttribute(k_ups_z<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
