@@ -876,13 +876,16 @@ __device__ __forceinline__ void cgemm_4x4(const cplx_t<T>* __restrict__ A, int l
 
 __host__ __device__ inline int ups_pad4(int U) { return (U + 3) / 4 * 4; }
 
+constexpr int kUpsPlanes = 4;  // kz planes per CTA (the per-particle phase tables are built once per CTA)
+
 template <typename T> __host__ __device__ inline size_t ups_xy_smem(int N, int U) {
   const int H = N / 2 + 1, UP = ups_pad4(U);
-  // X plane [N][H] | Ex [H][UP] | Ey^T [UP][N] | Z1 [N][UP]   (Z2 [UP][UP] reuses the X plane + Ex)
-  return sizeof(cplx_t<T>) * ((size_t)N * H + (size_t)H * UP + (size_t)UP * N + (size_t)N * UP);
+  // X plane [N][H] | Ex [H][UP] | Ey^T [UP][N] | Z1 [N][UP] | Z2 [UP][UP]
+  return sizeof(cplx_t<T>) * ((size_t)N * H + (size_t)H * UP + (size_t)UP * N + (size_t)N * UP + (size_t)UP * UP);
 }
 
-// per (kz plane, particle): Z1 = X Ex  ([N][H] x [H][U]),  Z2 = Ey^T Z1  ([U][N] x [N][U]), two register-tiled GEMMs
+// per (kUpsPlanes kz planes, particle): Z1 = X Ex  ([N][H] x [H][U]),  Z2 = Ey^T Z1  ([U][N] x [N][U]), two
+// register-tiled GEMMs per plane; the phase tables Ex, Ey depend only on the particle and are built once per CTA
 template <typename T>
 __global__ void __launch_bounds__(256) k_ups_xy(const cplx_t<T>* __restrict__ X, int N, int kappa,
                                                 const int* __restrict__ tint, cplx_t<T>* __restrict__ Z2) {
@@ -892,12 +895,9 @@ __global__ void __launch_bounds__(256) k_ups_xy(const cplx_t<T>* __restrict__ X,
   cplx_t<T>* Ex = Xs + N * H;                               // [H][UP] (weights folded in, zero padded)
   cplx_t<T>* EyT = Ex + H * UP;                             // [UP][N] (zero padded rows)
   cplx_t<T>* Z1 = EyT + UP * N;                             // [N][UP]
-  cplx_t<T>* Zs = Xs;                                       // [UP][UP] after the first GEMM
-  const int kz = blockIdx.x;
+  cplx_t<T>* Zs = Z1 + N * UP;                              // [UP][UP]
   const int64_t p = blockIdx.y;
   const int tx0 = tint[p * 3 + 0], ty0 = tint[p * 3 + 1];
-  const cplx_t<T>* xp = X + (p * N + kz) * (int64_t)N * H;
-  for (int i = threadIdx.x; i < N * H; i += blockDim.x) Xs[i] = xp[i];
   for (int i = threadIdx.x; i < H * UP; i += blockDim.x) {
     const int kx = i / UP, u = i - kx * UP;
     // Hermitian half spectrum: 1 <= kx < N/2 stand for +-kx (weight 2, Re at the end); kx = 0 and the Nyquist
@@ -910,15 +910,19 @@ __global__ void __launch_bounds__(256) k_ups_xy(const cplx_t<T>* __restrict__ X,
     const int u = i / N, ky = i - u * N;
     EyT[i] = u < U ? ups_phase<T>(ky, N, ty0, u, h, kappa) : mk<T>(T(0), T(0));
   }
-  __syncthreads();
-  cgemm_4x4<T>(Xs, H, Ex, UP, N, H, UP, Z1, UP);
-  __syncthreads();
-  cgemm_4x4<T>(EyT, N, Z1, UP, UP, N, UP, Zs, UP);
-  __syncthreads();
-  cplx_t<T>* zo = Z2 + (p * N + kz) * (int64_t)U * U;
-  for (int i = threadIdx.x; i < U * U; i += blockDim.x) {
-    const int uy = i / U, ux = i - uy * U;
-    zo[i] = Zs[uy * UP + ux];
+  for (int kz = blockIdx.x * kUpsPlanes; kz < min(N, (int)(blockIdx.x + 1) * kUpsPlanes); ++kz) {
+    const cplx_t<T>* xp = X + (p * N + kz) * (int64_t)N * H;
+    for (int i = threadIdx.x; i < N * H; i += blockDim.x) Xs[i] = xp[i];
+    __syncthreads();
+    cgemm_4x4<T>(Xs, H, Ex, UP, N, H, UP, Z1, UP);
+    __syncthreads();
+    cgemm_4x4<T>(EyT, N, Z1, UP, UP, N, UP, Zs, UP);
+    __syncthreads();
+    cplx_t<T>* zo = Z2 + (p * N + kz) * (int64_t)U * U;
+    for (int i = threadIdx.x; i < U * U; i += blockDim.x) {
+      const int uy = i / U, ux = i - uy * U;
+      zo[i] = Zs[uy * UP + ux];
+    }
   }
 }
 
@@ -1180,8 +1184,10 @@ bool ups_supported(int N, int kappa, bool fp64) {
   const size_t csz = fp64 ? 16 : 8;
   const int U = ups_points(kappa), H = N / 2 + 1, UP = ups_pad4(U);
   const size_t xy = fp64 ? ups_xy_smem<double>(N, U) : ups_xy_smem<float>(N, U);
-  return kappa >= 1 && U <= kUpsMaxU && xy <= 227 * 1024 && (size_t)UP * UP <= (size_t)N * H + (size_t)H * UP &&
-         csz * (size_t)N * U <= 200 * 1024 && csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
+  (void)H;
+  (void)UP;
+  return kappa >= 1 && U <= kUpsMaxU && xy <= 227 * 1024 && csz * (size_t)N * U <= 200 * 1024 &&
+         csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
 }
 
 // per-particle scratch: Z2 [N][U][U] complex, then the block bests; tint [nb][3] from k_window_peak
@@ -1221,7 +1227,8 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
   const size_t xsm = ups_xy_smem<T>(N, U);
   e = cudaFuncSetAttribute(k_ups_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
   if (e != cudaSuccess) return e;
-  k_ups_xy<T><<<dim3((unsigned)N, (unsigned)nb), 256, xsm, s>>>(rt, N, kappa, tint, Z2);
+  k_ups_xy<T><<<dim3((unsigned)((N + kUpsPlanes - 1) / kUpsPlanes), (unsigned)nb), 256, xsm, s>>>(rt, N, kappa, tint,
+                                                                                                 Z2);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t esm = csz * (size_t)N * U;
   e = cudaFuncSetAttribute(k_ups_z<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
