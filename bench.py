@@ -42,6 +42,9 @@ CONFIGS = {
     # c3 with the upsampled-DFT subpixel refinement (kappa = 16 over +-1.5 voxel, App. C remark iii)
     "c3u": dict(N=96, L=48, bands=[8, 12, 16, 24, 32, 48], ncand=10, K=2, snr=0.05, particles=1000, iters=1,
                 T=3, W=6, shift_max=4.0, ups=16),
+    # the paper's operating point: N = 200, coarse grid at L0 = 30 with K = 2
+    # (953k nodes), N_C = 10, one Newton step per band at {30, 40, 60, L_max}, L_max = 100; 0 dB (SNR 1.0)
+    "paper": dict(N=200, L=100, bands=[30, 40, 60, 100], ncand=10, K=2, snr=1.0, particles=500, iters=1),
     # configs[0] (c1) rotation part, small
     "c1": dict(N=32, L=8, bands=[4, 6, 8], ncand=4, K=2, snr=float("inf"), particles=64, iters=1),
 }

@@ -380,17 +380,24 @@ void grid_dims(int L0, int K, int& nb, int& na, int& ng) {
   nb = K * (L0 + 1);
   na = ng = 2 * K * (L0 + 1);
 }
+/* worker threads a single particle's grid evaluation may use (set by orc_align_batch when particles are fewer
+   than cores; the beta rows are independent, so the result does not depend on it) */
+int g_inner_threads = 1;
+
+template <class Fn> void parallel_for(int64_t n, int nthreads, Fn fn);
+
 void grid_eval(const double* Mfull, int L0, int K, double* grid) {
   const cd* M = reinterpret_cast<const cd*>(Mfull);
   int nb, na, ng;
   grid_dims(L0, K, nb, na, ng);
-  vector<vector<double>> d;
   vector<cd> ea((size_t)(2 * L0 + 1) * na), eg((size_t)(2 * L0 + 1) * ng);
   for (int m = -L0; m <= L0; ++m)
     for (int a = 0; a < na; ++a) ea[(size_t)(m + L0) * na + a] = std::polar(1.0, -m * 2.0 * PI * a / na);
   for (int n = -L0; n <= L0; ++n)
     for (int c = 0; c < ng; ++c) eg[(size_t)(n + L0) * ng + c] = std::polar(1.0, -n * 2.0 * PI * c / ng);
-  for (int j = 0; j < nb; ++j) {
+  parallel_for(nb, g_inner_threads, [&](int64_t jj) {
+    const int j = (int)jj;
+    vector<vector<double>> d;
     const double beta = (j + 0.5) * PI / nb;
     wigner_d_all(L0, beta, d);
     for (int a = 0; a < na; ++a)
@@ -406,7 +413,7 @@ void grid_eval(const double* Mfull, int L0, int K, double* grid) {
         }
         grid[((size_t)j * na + a) * ng + c] = s;
       }
-  }
+  });
 }
 
 /* local maxima ("N_C strongest local maxima"; readings C10, C11): node p is kept iff
@@ -766,6 +773,10 @@ void align_one(const float* vol, const float* ref, const double* H, int N, const
 
 template <class Fn>
 void parallel_for(int64_t n, int nthreads, Fn fn) {
+  if (nthreads == 1 || n <= 1) {
+    for (int64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
   if (nthreads <= 0) nthreads = (int)std::max(1u, std::thread::hardware_concurrency());
   nthreads = (int)std::min<int64_t>(nthreads, std::max<int64_t>(1, n));
   std::atomic<int64_t> next(0);
@@ -841,7 +852,11 @@ void orc_corr_full(const double* F, const double* H, int L, int Lc, int R, doubl
   corr_full(F, H, R, Lc, M);
 }
 void orc_eval_corr(const double* M, int L, const double* e, double* out10) { eval_corr(M, L, e, out10); }
-void orc_grid_eval(const double* M, int L0, int K, double* grid) { grid_eval(M, L0, K, grid); }
+void orc_grid_eval(const double* M, int L0, int K, double* grid) {
+  g_inner_threads = (int)std::max(1u, std::thread::hardware_concurrency());  /* rows are independent */
+  grid_eval(M, L0, K, grid);
+  g_inner_threads = 1;
+}
 int orc_find_maxima(const double* grid, int nb, int na, int ng, int ncand, int64_t* idx, double* score) {
   return find_maxima(grid, nb, na, ng, ncand, idx, score);
 }
@@ -912,7 +927,11 @@ void orc_align_batch(const float* vols, int64_t B, const float* ref, const doubl
     H = Hl.data();
   }
   const size_t n3 = (size_t)N * N * N;
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int outer = nthreads > 0 ? nthreads : hw;
+  g_inner_threads = (int)std::max<int64_t>(1, outer / std::max<int64_t>(1, std::min<int64_t>(B, outer)));
   parallel_for(B, nthreads, [&](int64_t b) { align_one(vols + b * n3, ref, H, N, p, poses + 8 * b); });
+  g_inner_threads = 1;
 }
 
 }  // extern "C"

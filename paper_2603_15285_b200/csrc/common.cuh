@@ -117,6 +117,11 @@ template <typename T>
 cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
                                 T* poses, cudaStream_t s);
 size_t search_smem_bytes(int L0, int K, bool fp64);
+// coarse grids too large for one CTA (L0 = 30 at K = 2): three passes over a global grid workspace of
+// so3_large_workspace_bytes per particle
+bool so3_large_needed(int L0, int K, bool fp64);
+size_t so3_large_workspace_bytes(int L0, int K, int ncand, bool fp64);
+template <typename T> cudaError_t launch_so3_search_large(const SearchArgs<T>& a, void* ws, cudaStream_t s);
 int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode);
 cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shifts, int shift_stride,
                                const ShTables<float>& tab, int P, float2* G, int* flags, int num_sms,

@@ -613,6 +613,248 @@ __global__ void __launch_bounds__(kGThreads) k_so3_grid(SearchArgs<T> a, int jc)
   }
 }
 
+
+// ------------------------------------------------------------------ large grids (L0 = 30, K = 2)
+// The paper's operating point has a 62 x 124 x 124 grid (953k nodes, 3.8 MB per particle in FP32):
+// no CTA can hold it, so the search runs in three passes over a global grid workspace:
+//   k_so3_slice     one CTA per (beta slice, particle): X (M read through L1/L2), Y, C as in k_so3_search; C -> grid
+//   k_so3_slice_max one CTA per (beta slice, particle): strict 26-neighbour maxima of slice j by the key order
+//                   (score desc, index asc), the slice's best n_cand written to a [slice][n_cand] list
+//   k_so3_merge     one CTA per particle: the n_cand best of the nb * n_cand slice winners (deterministic)
+// The global top-n_cand of the local maxima is contained in the union of the per-slice top-n_cand lists.
+constexpr int kBThreads = 256;
+constexpr int kSliceCap = 3072;
+
+template <typename T>
+__global__ void __launch_bounds__(kBThreads) k_so3_slice(SearchArgs<T> a, T* __restrict__ grid) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L0 = a.L0, K = a.K, nb = K * (L0 + 1), na = 2 * K * (L0 + 1), ng = na, w0 = 2 * L0 + 1;
+  cplx_t<T>* X = reinterpret_cast<cplx_t<T>*>(smem);     // [L0+1][2L0+1]
+  cplx_t<T>* Y = X + (L0 + 1) * w0;                       // [L0+1][ng]
+  cplx_t<T>* tw = Y + (L0 + 1) * ng;                      // [na]
+  T* inv_l = reinterpret_cast<T*>(tw + na);               // [kMaxL+2]
+  T* inv_ll = inv_l + kMaxL + 2;
+  const int j = blockIdx.x, tid = threadIdx.x;
+  const int64_t p = blockIdx.y;
+  const cplx_t<T>* Mp = a.M + p * a.strideM;
+  for (int t = tid; t < na; t += kBThreads) {
+    double sn, cs;
+    sincospi(2.0 * t / na, &sn, &cs);
+    tw[t] = mk<T>((T)cs, (T)(-sn));  // e^{-2 pi i t/na}
+  }
+  for (int l = tid; l <= kMaxL + 1; l += kBThreads) {
+    inv_l[l] = l ? (T)(1.0 / l) : T(0);
+    inv_ll[l] = l ? (T)(1.0 / ((double)l * (l + 1))) : T(0);
+  }
+  const double beta = (j + 0.5) * kPi / nb;
+  const BetaLogs<T> bl = beta_logs<T>(beta);
+  const T cb = (T)cos(beta);
+  __syncthreads();
+  for (int pi = tid; pi < pair_count(L0); pi += kBThreads) {
+    const PairDesc pd = a.pairs[pi];
+    const int m = pd.m, n = pd.n, l0 = max(m, abs(n));
+    T d, dd, dprev = T(0), sq = T(0);
+    wigner_seed<T, false>(m, n, a.pair_lnc[pi], bl, d, dd);
+    T xr = T(0), xi = T(0);
+    int off = pd.off0;
+    for (int l = l0;; ++l) {
+      const cplx_t<T> Ml = Mp[off];
+      xr = fma(Ml.x, d, xr);
+      xi = fma(-Ml.y, d, xi);
+      if (l == L0) break;
+      T A, Bc, Cc;
+      rec_coef<T>(l, m * n, m * m, n * n, inv_l, inv_ll, A, Bc, Cc, sq);
+      const T dn = fma(A * d, cb, -fma(Bc, d, Cc * dprev));
+      dprev = d;
+      d = dn;
+      off += (l + 1) * (2 * l + 1) + 2 * m + 1;
+    }
+    X[m * w0 + (n + L0)] = mk<T>(xr, xi);
+  }
+  __syncthreads();
+  for (int t = tid; t < (L0 + 1) * ng; t += kBThreads) {
+    const int m = t / ng, c = t - m * ng;
+    T yr = T(0), yi = T(0);
+    int k = (ng - (L0 * c) % ng) % ng;  // (n c) mod ng at n = -L0, then + c per step
+    for (int n = -L0; n <= L0; ++n) {
+      const cplx_t<T> x = X[m * w0 + (n + L0)], e = tw[k];
+      k += c;
+      if (k >= ng) k -= ng;
+      yr = fma(x.x, e.x, fma(-x.y, e.y, yr));
+      yi = fma(x.x, e.y, fma(x.y, e.x, yi));
+    }
+    Y[m * ng + c] = mk<T>(yr, yi);
+  }
+  __syncthreads();
+  T* out = grid + (p * nb + j) * (int64_t)na * ng;
+  for (int t = tid; t < na * ng; t += kBThreads) {
+    const int aa = t / ng, c = t - aa * ng;
+    T s2 = T(0);
+    int k = 0;
+    for (int m = 1; m <= L0; ++m) {
+      k += aa;
+      if (k >= na) k -= na;
+      const cplx_t<T> y = Y[m * ng + c], e = tw[k];
+      s2 = fma(y.x, e.x, fma(-y.y, e.y, s2));
+    }
+    out[t] = fma(T(2), s2, Y[c].x);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBThreads) k_so3_slice_max(SearchArgs<T> a, const T* __restrict__ grid,
+                                                             T* __restrict__ lval, int* __restrict__ lidx) {
+  __shared__ T cs[kSliceCap];
+  __shared__ int ci[kSliceCap];
+  __shared__ int cnt;
+  __shared__ T red_s[kBThreads / 32];
+  __shared__ int red_i[kBThreads / 32];
+  const int L0 = a.L0, K = a.K, nb = K * (L0 + 1), na = 2 * K * (L0 + 1), ng = na;
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t p = blockIdx.y;
+  const T* g = grid + p * (int64_t)nb * na * ng;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  for (int t = tid; t < na * ng; t += kBThreads) {
+    const int aa = t / ng, c = t - aa * ng;
+    const int ip = j * na * ng + t;
+    const T v = g[ip];
+    bool mx = true;
+    for (int dj = -1; dj <= 1 && mx; ++dj) {
+      const int jj = j + dj;
+      if (jj < 0 || jj >= nb) continue;
+      for (int da = -1; da <= 1 && mx; ++da) {
+        const int a2 = aa + da < 0 ? na - 1 : (aa + da >= na ? 0 : aa + da);
+        for (int dc = -1; dc <= 1; ++dc) {
+          if (!dj && !da && !dc) continue;
+          const int c2 = c + dc < 0 ? ng - 1 : (c + dc >= ng ? 0 : c + dc);
+          const int iq = (jj * na + a2) * ng + c2;
+          if (iq == ip) continue;
+          if (!before(v, ip, g[iq], iq)) {
+            mx = false;
+            break;
+          }
+        }
+      }
+    }
+    if (mx) {
+      const int slot = atomicAdd(&cnt, 1);
+      if (slot < kSliceCap) {
+        cs[slot] = v;
+        ci[slot] = ip;
+      } else {
+        atomicOr(a.flags, FLAG_OVERFLOW);
+      }
+    }
+  }
+  __syncthreads();
+  const int total = min(cnt, kSliceCap);
+  for (int k = 0; k < a.ncand; ++k) {
+    T bs = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int t = tid; t < total; t += kBThreads)
+      if (ci[t] >= 0 && before(cs[t], ci[t], bs, bi)) {
+        bs = cs[t];
+        bi = ci[t];
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (before(s2, i2, bs, bi)) {
+        bs = s2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      red_s[warp] = bs;
+      red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      T s = red_s[0];
+      int i = red_i[0];
+      for (int w = 1; w < kBThreads / 32; ++w)
+        if (before(red_s[w], red_i[w], s, i)) {
+          s = red_s[w];
+          i = red_i[w];
+        }
+      const int64_t o = (p * nb + j) * a.ncand + k;
+      lval[o] = s;
+      lidx[o] = (i == 0x7fffffff) ? -1 : i;
+      for (int t = 0; t < total; ++t)
+        if (ci[t] == i) ci[t] = -1;  // taken
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBThreads) k_so3_merge(SearchArgs<T> a, const T* __restrict__ lval,
+                                                         const int* __restrict__ lidx) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L0 = a.L0, K = a.K, nb = K * (L0 + 1), na = 2 * K * (L0 + 1), ng = na;
+  const int n = nb * a.ncand, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* cs = reinterpret_cast<T*>(smem);
+  int* ci = reinterpret_cast<int*>(cs + n);
+  __shared__ T red_s[kBThreads / 32];
+  __shared__ int red_i[kBThreads / 32];
+  const int64_t p = blockIdx.x;
+  for (int t = tid; t < n; t += kBThreads) {
+    cs[t] = lval[p * n + t];
+    ci[t] = lidx[p * n + t];
+  }
+  __syncthreads();
+  for (int k = 0; k < a.ncand; ++k) {
+    T bs = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int t = tid; t < n; t += kBThreads)
+      if (ci[t] >= 0 && before(cs[t], ci[t], bs, bi)) {
+        bs = cs[t];
+        bi = ci[t];
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (before(s2, i2, bs, bi)) {
+        bs = s2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      red_s[warp] = bs;
+      red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      T s = red_s[0];
+      int i = red_i[0];
+      for (int w = 1; w < kBThreads / 32; ++w)
+        if (before(red_s[w], red_i[w], s, i)) {
+          s = red_s[w];
+          i = red_i[w];
+        }
+      const int64_t o = p * a.ncand + k;
+      if (i != 0x7fffffff) {
+        const int c = i % ng, aa = (i / ng) % na, jj = i / (ng * na);
+        a.euler[o * 3 + 0] = (T)(2.0 * kPi * aa / na);
+        a.euler[o * 3 + 1] = (T)((jj + 0.5) * kPi / nb);
+        a.euler[o * 3 + 2] = (T)(2.0 * kPi * c / ng);
+        a.score[o] = s;
+        a.idx[o] = i;
+        for (int t = 0; t < n; ++t)
+          if (ci[t] == i) ci[t] = -1;
+      } else {
+        a.euler[o * 3 + 0] = a.euler[o * 3 + 1] = a.euler[o * 3 + 2] = T(0);
+        a.score[o] = -INFINITY;
+        a.idx[o] = -1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // slices per Y chunk for the full-grid kernel (0 = the grid does not fit: use the rolling-window kernel)
 template <typename T> int grid_chunk(int L0, int K) {
   const int nb = K * (L0 + 1);
@@ -623,9 +865,44 @@ template <typename T> int grid_chunk(int L0, int K) {
 
 }  // namespace
 
+size_t so3_large_workspace_bytes(int L0, int K, int ncand, bool fp64) {
+  const size_t nb = (size_t)K * (L0 + 1), na = 2 * (size_t)K * (L0 + 1), rs = fp64 ? 8 : 4;
+  return rs * nb * na * na + nb * ncand * (rs + sizeof(int)) + 64;
+}
+
+bool so3_large_needed(int L0, int K, bool fp64) {
+  return search_smem_bytes(L0, K, fp64) > 220 * 1024;
+}
+
+template <typename T> cudaError_t launch_so3_search_large(const SearchArgs<T>& a, void* ws, cudaStream_t s) {
+  if (a.B == 0) return cudaSuccess;
+  const int nb = a.K * (a.L0 + 1), na = 2 * a.K * (a.L0 + 1);
+  if (a.L0 > kMaxL || (int64_t)nb * na * na >= (1ll << 31)) return cudaErrorInvalidValue;
+  const size_t per = so3_large_workspace_bytes(a.L0, a.K, a.ncand, sizeof(T) == 8);
+  T* grid = reinterpret_cast<T*>(ws);
+  T* lval = grid + a.B * (int64_t)nb * na * na;
+  int* lidx = reinterpret_cast<int*>(lval + a.B * (int64_t)nb * a.ncand);
+  (void)per;
+  const size_t s1 = sizeof(cplx_t<T>) * ((size_t)(a.L0 + 1) * (2 * a.L0 + 1) + (size_t)(a.L0 + 1) * na + na) +
+                    2 * sizeof(T) * (kMaxL + 2);
+  cudaError_t e = cudaFuncSetAttribute(k_so3_slice<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+  if (e != cudaSuccess) return e;
+  k_so3_slice<T><<<dim3((unsigned)nb, (unsigned)a.B), kBThreads, s1, s>>>(a, grid);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_so3_slice_max<T><<<dim3((unsigned)nb, (unsigned)a.B), kBThreads, 0, s>>>(a, grid, lval, lidx);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t s3 = (sizeof(T) + sizeof(int)) * (size_t)nb * a.ncand;
+  e = cudaFuncSetAttribute(k_so3_merge<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
+  if (e != cudaSuccess) return e;
+  k_so3_merge<T><<<(unsigned)a.B, kBThreads, s3, s>>>(a, lval, lidx);
+  return cudaGetLastError();
+}
+template cudaError_t launch_so3_search_large<float>(const SearchArgs<float>&, void*, cudaStream_t);
+template cudaError_t launch_so3_search_large<double>(const SearchArgs<double>&, void*, cudaStream_t);
+
 template <typename T> cudaError_t launch_so3_search(const SearchArgs<T>& a, cudaStream_t s) {
   if (a.B == 0) return cudaSuccess;
-  const int jc = getenv("MATCHA_SEARCH_WINDOW") ? 0 : grid_chunk<T>(a.L0, a.K);
+  const int jc = grid_chunk<T>(a.L0, a.K);
   if (jc > 0) {
     const size_t bytes = grid_layout<T>(a.L0, a.K, jc).total;
     auto kern = (a.L0 == 8 && a.K == 2) ? k_so3_grid<T, 8, 2> : (a.L0 == 4 && a.K == 2) ? k_so3_grid<T, 4, 2>

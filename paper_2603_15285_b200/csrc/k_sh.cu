@@ -49,7 +49,7 @@ __host__ __device__ inline int wbuf_elems(int Kh) { return 4 * (Kh + 1) * kG + 2
 
 template <typename T>
 __host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph, int R, int Kh, int MP,
-                                                   bool dft_smem = true, int warps = kRingWarps) {
+                                                   bool dft_smem = true, int warps = kRingWarps, bool staged = true) {
   RingLayout s;
   size_t o = 0;
   auto take = [&](size_t b) {
@@ -60,7 +60,7 @@ __host__ __device__ inline RingLayout ring_layout(int N, int S, int nth, int nph
   s.tw = take(sizeof(cplx_t<T>) * nph);
   s.node = take(sizeof(cplx_t<T>) * nth);
   s.dft = take(dft_smem ? sizeof(cplx_t<T>) * (size_t)(Kh + 1) * MP : 0);
-  s.pl = take(sizeof(float) * (size_t)(S + 1) * N * plane_pitch(N));
+  s.pl = take(staged ? sizeof(float) * (size_t)(S + 1) * N * plane_pitch(N) : 0);
   s.list = take(sizeof(int) * (size_t)R * nth);
   s.wsum = take(sizeof(int) * (warps + 2));
   s.wbuf = take(sizeof(T) * (size_t)warps * wbuf_elems(Kh));
@@ -99,6 +99,34 @@ __device__ __forceinline__ T tri_smem(const float* __restrict__ pl, int Nr, int 
           c[dz][dy][dx] = in ? (T)pl[z * P + y * W + x] : T(0);
         }
   }
+  const T c00 = fma(fx, c[0][0][1] - c[0][0][0], c[0][0][0]);
+  const T c01 = fma(fx, c[0][1][1] - c[0][1][0], c[0][1][0]);
+  const T c10 = fma(fx, c[1][0][1] - c[1][0][0], c[1][0][0]);
+  const T c11 = fma(fx, c[1][1][1] - c[1][1][0], c[1][1][0]);
+  const T c0 = fma(fy, c01 - c00, c00);
+  const T c1 = fma(fy, c11 - c10, c10);
+  return fma(fz, c1 - c0, c0);
+}
+
+// large boxes (e.g. the paper's N = 200) whose plane slab does not fit shared memory: trilinear
+// interpolation straight from the volume in global memory (read-only path; a ring's samples lie in one plane pair,
+// so its gathers share L1 lines); z0 absolute, zero outside the box (reading C5)
+template <typename T>
+__device__ __forceinline__ T tri_glob(const float* __restrict__ v, int N, T px, T py, int z0, T fz) {
+  const T fx0 = floor(px), fy0 = floor(py);
+  const int x0 = (int)fx0, y0 = (int)fy0;
+  const T fx = px - fx0, fy = py - fy0;
+  T c[2][2][2];
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const int x = x0 + dx, y = y0 + dy, z = z0 + dz;
+        const bool in = (unsigned)x < (unsigned)N && (unsigned)y < (unsigned)N && (unsigned)z < (unsigned)N;
+        c[dz][dy][dx] = in ? (T)__ldg(v + ((size_t)z * N + y) * N + x) : T(0);
+      }
   const T c00 = fma(fx, c[0][0][1] - c[0][0][0], c[0][0][0]);
   const T c01 = fma(fx, c[0][1][1] - c[0][1][0], c[0][1][0]);
   const T c10 = fma(fx, c[1][0][1] - c[1][0][0], c[1][0][0]);
@@ -281,12 +309,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
                                                               cplx_t<T>* __restrict__ G) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool dft_smem = DFT_SMEM;
-  const int N = NT ? NT : tab.N;
+  constexpr bool GD = NT < 0;  // no plane staging: gathers straight from global memory (large boxes)
+  const int N = NT > 0 ? NT : tab.N;
   const int R = tab.R, L = tab.L, nth = tab.nth, nph = tab.nph, Kh = tab.Kh, MP = tab.MP;
   const int Mp = nph / 2, K1 = Kh + 1;
   const bool mid = (Mp % 2) == 0;
   const int THR = blockDim.x, NW = THR / 32;  // 512 threads, fewer when shared memory is short (large Kh)
-  const RingLayout lay = ring_layout<T>(N, S, nth, nph, R, Kh, MP, dft_smem, NW);
+  const RingLayout lay = ring_layout<T>(N, S, nth, nph, R, Kh, MP, dft_smem, NW, !GD);
   cplx_t<T>* tw = (cplx_t<T>*)(smem + lay.tw);
   cplx_t<T>* node = (cplx_t<T>*)(smem + lay.node);
   const cplx_t<T>* dft = dft_smem ? (const cplx_t<T>*)(smem + lay.dft) : tab.dft;
@@ -308,7 +337,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
   }
   // 1. stage planes zs..zs+S asynchronously (cp.async 16 B, zero fill beyond the volume); each thread owns
   //    one 16-byte column x4 and walks rows with a fixed stride (no per-element division)
-  {
+  if (!GD) {
     const int PW = plane_pitch(N), n4 = N / 4, rows = (S + 1) * N;
     if (THR % n4 == 0) {
       const int x4 = tid % n4, rstride = THR / n4;
@@ -408,7 +437,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
           px[q] = fma(rs, ph.x, cx);
           py[q] = fma(rs, ph.y, cy);
         }
-        tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
+        if constexpr (GD) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sv[q] = tri_glob<T>(vol, N, px[q], py[q], pz0 + zs, fz);
+        } else {
+          tri4<T, NT>(pl, N, S, px, py, pz0, fz, sv);
+        }
         const T ap = sv[0] + sv[1], am = sv[0] - sv[1], bp = sv[2] + sv[3], bm = sv[2] - sv[3];
         v[0] = ap + bp;  // even m, cos
         v[1] = ap - bp;  // even m, sin
@@ -464,10 +498,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_sh_rings(const float* __res
           int pz0;
           ring_geom(r, rs, fz, pz0);
           const cplx_t<T> ph = tw[q ? Mp : 0];
-          s0 = tri_smem<T, NT>(pl, N, S, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0, fz);
+          if constexpr (GD) s0 = tri_glob<T>(vol, N, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0 + zs, fz);
+          else s0 = tri_smem<T, NT>(pl, N, S, fma(rs, ph.x, cx), fma(rs, ph.y, cy), pz0, fz);
           if (mid) {
             const cplx_t<T> pm = tw[Mp / 2 + (q ? Mp : 0)];
-            sm = tri_smem<T, NT>(pl, N, S, fma(rs, pm.x, cx), fma(rs, pm.y, cy), pz0, fz);
+            if constexpr (GD) sm = tri_glob<T>(vol, N, fma(rs, pm.x, cx), fma(rs, pm.y, cy), pz0 + zs, fz);
+            else sm = tri_smem<T, NT>(pl, N, S, fma(rs, pm.x, cx), fma(rs, pm.y, cy), pz0, fz);
           }
         }
         const T s1 = __shfl_xor_sync(0xffffffffu, s0, 1);
@@ -863,6 +899,7 @@ template <typename T> size_t leg_pers_bytes(const ShTables<T>& tab) {
 template <typename T> struct ShPlan {
   int S, nslab, threads;
   bool dft_smem;
+  bool gd;  // no plane staging (box too large for a shared-memory slab)
   size_t rbytes;
 };
 
@@ -879,6 +916,7 @@ template <typename T> ShPlan<T> sh_plan(const ShTables<T>& tab) {
         if (tot <= budget) {
           pl.S = S;
           pl.dft_smem = ds;
+          pl.gd = false;
           pl.nslab = (tab.N + S - 1) / S;
           pl.rbytes = tot;
           pl.threads = 32 * warps;
@@ -886,11 +924,27 @@ template <typename T> ShPlan<T> sh_plan(const ShTables<T>& tab) {
         }
       }
     }
-  pl.S = 1;
+  // no slab fits: gathers straight from global memory (slabs of 8 planes only group the rings)
+  for (int warps = kRingWarps; warps >= 2; warps /= 2)
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool ds = (pass == 0);
+      const size_t tot = ring_layout<T>(tab.N, 8, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, ds, warps, false).total;
+      if (tot <= budget) {
+        pl.S = 8;
+        pl.dft_smem = ds;
+        pl.gd = true;
+        pl.nslab = (tab.N + 7) / 8;
+        pl.rbytes = tot;
+        pl.threads = 32 * warps;
+        return pl;
+      }
+    }
+  pl.S = 8;
   pl.dft_smem = false;
-  pl.nslab = tab.N;
-  pl.threads = 128;
-  pl.rbytes = ring_layout<T>(tab.N, 1, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false, 4).total;
+  pl.gd = true;
+  pl.nslab = (tab.N + 7) / 8;
+  pl.threads = 64;
+  pl.rbytes = ring_layout<T>(tab.N, 8, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false, 2, false).total;
   return pl;
 }
 
@@ -914,6 +968,7 @@ static cudaError_t launch_rings_nt(const float* vols, int64_t nb, const T* shift
 template <typename T, bool DS>
 static cudaError_t launch_rings(const float* vols, int64_t nb, const T* shifts, int shift_stride,
                                 const ShTables<T>& tab, const ShPlan<T>& plan, cplx_t<T>* Gws, cudaStream_t st) {
+  if (plan.gd) return launch_rings_nt<T, -1, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
   switch (tab.N) {  // compile-time box edges: immediate shared-memory offsets in the trilinear gathers
     case 16: return launch_rings_nt<T, 16, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);
     case 32: return launch_rings_nt<T, 32, DS>(vols, nb, shifts, shift_stride, tab, plan, Gws, st);

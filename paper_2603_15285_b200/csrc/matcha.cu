@@ -63,6 +63,8 @@ struct matcha_ctx {
   void* ws_peak = nullptr;   // real [mb]
   void* ws_win = nullptr;    // real [mb][window_scratch_reals(N, W)]: Y1 (z correlation) + the c window
   int ws_win_W = -1;
+  void* ws_grid = nullptr;   // large coarse grids (f1): [chunk] x so3_large_workspace_bytes
+  size_t ws_grid_bytes = 0;
   int* ws_tint = nullptr;    // int [mb][3]: integer window peaks (upsampled subpixel)
   void* ws_ups = nullptr;    // [mb] x ups_scratch_bytes(N, kappa): upsampled-DFT scratch
   int ws_ups_kappa = -1;
@@ -631,7 +633,7 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   if (h->tex_ref) cudaDestroyTextureObject(h->tex_ref);
   for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad,
-                  (void*)h->ws_tint, h->ws_ups})
+                  (void*)h->ws_tint, h->ws_ups, h->ws_grid})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -735,10 +737,49 @@ MATCHA_API matcha_status_t matcha_so3_search(matcha_handle_t h, const void* M, i
   if (L0 < 1 || L0 > L_M) return fail(h, MATCHA_ERR_CUTOFF, "so3_search: L0 outside [1, L_M]");
   if (oversample < 1 || oversample > 8 || n_cand < 1 || n_cand > kMaxCand)
     return fail(h, MATCHA_ERR_INVALID_ARG, "so3_search: oversample in [1,8], n_cand in [1,32]");
-  if (search_smem_bytes(L0, oversample, h->fp64) > 220 * 1024)
-    return fail(h, MATCHA_ERR_INVALID_ARG, "so3_search: grid too large for one CTA (reduce L0*K)");
+  if ((int64_t)oversample * (L0 + 1) * 4 * oversample * (L0 + 1) * oversample * (L0 + 1) >= (1ll << 31))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "so3_search: grid exceeds 2^31 nodes");
   cudaStream_t s = (cudaStream_t)stream;
   ProfScope ps(h, 2, s);
+  if (so3_large_needed(L0, oversample, h->fp64)) {
+    // three-pass search over a global grid workspace, in chunks of max_batch particles
+    const int64_t mb = h->cfg.max_batch;
+    const size_t per = so3_large_workspace_bytes(L0, oversample, n_cand, h->fp64);
+    const size_t need = per * (size_t)std::min<int64_t>(mb, B);
+    if (h->ws_grid_bytes < need) {
+      if (h->ws_grid) cudaFree(h->ws_grid);
+      h->ws_grid = nullptr;
+      h->ws_grid_bytes = 0;
+      if (cudaMalloc(&h->ws_grid, need) != cudaSuccess)
+        return fail(h, MATCHA_ERR_ALLOC, "so3_search: coarse-grid workspace allocation failed");
+      h->ws_grid_bytes = need;
+    }
+    for (int64_t c0 = 0; c0 < B; c0 += mb) {
+      const int64_t nb = std::min<int64_t>(mb, B - c0);
+      cudaError_t e;
+      const size_t rs = h->rsz;
+      if (h->fp64) {
+        SearchArgs<double> a;
+        a.M = (const double2*)((const char*)M + c0 * half_size(L_M) * 2 * rs);
+        a.strideM = half_size(L_M); a.B = nb; a.L0 = L0; a.K = oversample; a.ncand = n_cand;
+        a.euler = (double*)((char*)euler + c0 * n_cand * 3 * rs); a.score = (double*)((char*)score + c0 * n_cand * rs);
+        a.idx = grid_idx + c0 * n_cand; a.pairs = h->d_pairs; a.pair_lnc = (const double*)h->d_pair_lnc;
+        a.flags = h->d_flags;
+        e = launch_so3_search_large<double>(a, h->ws_grid, s);
+      } else {
+        SearchArgs<float> a;
+        a.M = (const float2*)((const char*)M + c0 * half_size(L_M) * 2 * rs);
+        a.strideM = half_size(L_M); a.B = nb; a.L0 = L0; a.K = oversample; a.ncand = n_cand;
+        a.euler = (float*)((char*)euler + c0 * n_cand * 3 * rs); a.score = (float*)((char*)score + c0 * n_cand * rs);
+        a.idx = grid_idx + c0 * n_cand; a.pairs = h->d_pairs; a.pair_lnc = (const float*)h->d_pair_lnc;
+        a.flags = h->d_flags;
+        e = launch_so3_search_large<float>(a, h->ws_grid, s);
+      }
+      if (e != cudaSuccess) return cuda_fail(h, e, "so3_search (large grid) launch");
+      h->launches += 3;
+    }
+    return MATCHA_OK;
+  }
   cudaError_t e = h->fp64 ? do_search<double>(h, M, L_M, B, L0, oversample, n_cand, euler, score, grid_idx, s)
                           : do_search<float>(h, M, L_M, B, L0, oversample, n_cand, euler, score, grid_idx, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "so3_search launch");
@@ -822,8 +863,6 @@ MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vo
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: box too large for the stage-5 kernels");
   if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: upsample factor / box exceed the kernels' limits");
-  if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
-    return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch: coarse grid too large for one CTA");
   return align_device(h, vols, B, ref, ref_coeffs, params, poses, (cudaStream_t)stream);
 }
 
@@ -840,8 +879,6 @@ MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const floa
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch_host: box too large for the stage-5 kernels");
   if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch_host: upsample factor / box exceed the kernels' limits");
-  if (search_smem_bytes(params->bands[0], params->oversample, h->fp64) > 220 * 1024)
-    return fail(h, MATCHA_ERR_INVALID_ARG, "align_batch_host: coarse grid too large for one CTA");
   cudaStream_t s = (cudaStream_t)stream;
   const int N = h->cfg.N;
   const int64_t n3 = (int64_t)N * N * N, mb = h->cfg.max_batch;
