@@ -85,12 +85,62 @@ __global__ void __launch_bounds__(kThreads) k_corr_coeffs(const cplx_t<T>* __res
   }
 }
 
+// one CTA per (particle, l) when the whole block fits shared memory (all of c3 / c5): F^l and Ht^l staged once
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_corr_coeffs_whole(const cplx_t<T>* __restrict__ F,
+                                                          const cplx_t<T>* __restrict__ H, int L, int Lmax, int R,
+                                                          cplx_t<T>* __restrict__ M) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int l = L - (int)(blockIdx.x % (L + 1));  // big blocks first
+  const int64_t p = blockIdx.x / (L + 1);
+  const int w = 2 * l + 1;
+  const int ncf = ncoef(Lmax);
+  cplx_t<T>* Fl = (cplx_t<T>*)smem;   // [(l+1)][R]
+  cplx_t<T>* Ht = Fl + (l + 1) * R;   // [R][w]
+  const cplx_t<T>* Fp = F + p * (int64_t)ncf * R + (int64_t)lm_index(l, 0) * R;
+  const cplx_t<T>* Hl = H + (int64_t)lm_index(l, 0) * R;
+  for (int t = threadIdx.x; t < (l + 1) * R; t += kThreads) Fl[t] = Fp[t];
+  for (int t = threadIdx.x; t < R * w; t += kThreads) {
+    const int n = t / R - l, i = t % R;  // read H coalesced along r
+    const T r = (T)i + T(0.5), wr = r * r;
+    const cplx_t<T> h = Hl[(size_t)abs(n) * R + i];
+    cplx_t<T> v;
+    if (n >= 0) v = mk<T>(wr * h.x, -wr * h.y);                  // w conj(h_{l,n})
+    else v = (n & 1) ? mk<T>(-wr * h.x, -wr * h.y) : mk<T>(wr * h.x, wr * h.y);  // w (-1)^n h_{l,|n|}
+    Ht[i * w + (n + l)] = v;
+  }
+  __syncthreads();
+  cplx_t<T>* Mo = M + p * half_size(L) + half_offset(l);
+  for (int o = threadIdx.x; o < (l + 1) * w; o += kThreads) {
+    const int m = o / w, nn = o - m * w;
+    const cplx_t<T>* fr = Fl + m * R;
+    T ar = T(0), ai = T(0);
+#pragma unroll 4
+    for (int i = 0; i < R; ++i) {
+      const cplx_t<T> f = fr[i], h = Ht[i * w + nn];
+      ar = fma(f.x, h.x, ar);
+      ar = fma(-f.y, h.y, ar);
+      ai = fma(f.x, h.y, ai);
+      ai = fma(f.y, h.x, ai);
+    }
+    Mo[o] = mk<T>(ar, ai);
+  }
+}
+
 }  // namespace
 
 template <typename T>
 cudaError_t launch_corr_coeffs(const cplx_t<T>* F, const cplx_t<T>* H, int64_t B, int L, int Lmax, int R,
                                cplx_t<T>* M, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
+  const size_t whole = sizeof(cplx_t<T>) * (size_t)R * ((L + 1) + (2 * L + 1));
+  if (whole <= 200 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_corr_coeffs_whole<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)whole);
+    if (e != cudaSuccess) return e;
+    k_corr_coeffs_whole<T><<<(unsigned)(B * (L + 1)), kThreads, whole, s>>>(F, H, L, Lmax, R, M);
+    return cudaGetLastError();
+  }
   const int w = 2 * L + 1;
   const int mb = std::max(1, std::min(L + 1, kOut * kThreads / w));  // rows of the widest block per CTA
   const size_t cs = sizeof(cplx_t<T>), budget = 200 * 1024;
