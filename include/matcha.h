@@ -171,6 +171,29 @@ MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vo
                                               const void* ref_coeffs, const matcha_params_t* params, void* poses,
                                               void* stream);
 
+/* Multi-template alignment ("evaluate alignment against multiple candidate templates per
+   iteration"): per alternation, stage 1 once per particle, stages 2-4 against every template, the template whose
+   final C_{L_J} is highest (ties -> lowest template index) is kept, and the translation update (W > 0) rotates that
+   template.  refs: float32 [n_templates][N^3] (needed when ref_coeffs is NULL or W > 0); ref_coeffs: complex
+   [n_templates][ncoef(L_max)][R] or NULL; n_templates in [1, 16].
+   poses (out): real [B][9] = {alpha, beta, gamma, t_x, t_y, t_z, score, best_cand, template}. */
+MATCHA_API matcha_status_t matcha_align_multi(matcha_handle_t h, const float* vols, int64_t B, const float* refs,
+                                              int32_t n_templates, const void* ref_coeffs,
+                                              const matcha_params_t* params, void* poses, void* stream);
+
+/* Reference update of subtomogram averaging (P:1184 half-set split; reading C28): the aligned
+   particles summed in the reference frame per class and half set,
+     sums[k][s][y] = sum_{p: class(p) = k, (first_index + p) mod 2 = s} f_p(g_p (y - c) + c + t_p)   (trilinear)
+   vols: float32 [B][N^3]; poses: real [B][pose_stride] with {alpha, beta, gamma, t_x, t_y, t_z} in columns 0..5 and
+   the class in column class_col (class_col < 0: one class; n_classes must then be 1; particles whose class is outside
+   [0, n_classes) are skipped); first_index: global index of particle 0 (half set = parity of the global index).
+   sums (out): real [n_classes][2][N^3]; counts (out): int32 [n_classes][2] (device).  The half maps are sums / counts;
+   across GPUs all-reduce sums and counts first (paper_2603_15285_b200.dist.reconstruct_step).  Deterministic (fixed
+   particle order per voxel, no atomics). */
+MATCHA_API matcha_status_t matcha_reconstruct(matcha_handle_t h, const float* vols, int64_t B, const void* poses,
+                                              int32_t pose_stride, int32_t class_col, int32_t n_classes,
+                                              int64_t first_index, void* sums, int32_t* counts, void* stream);
+
 /* End-to-end variant on HOST buffers: vols_host float32 [B][N^3] (pinned memory recommended), ref_host float32
    [N^3]; poses_host (out) real [B][8].  Copies chunks host->device on a second stream overlapped with compute,
    and synchronises before returning. */
@@ -185,8 +208,8 @@ MATCHA_API const char* matcha_last_error_string(matcha_handle_t h);
 MATCHA_API int64_t matcha_launch_count(matcha_handle_t h);
 
 /* Per-stage tracing with CUDA events recorded on the launching stream around every stage launch.
-   Stage ids: 0 sh_analysis, 1 corr_coeffs, 2 so3_search, 3 newton_refine/eval_corr, 4 pose gather,
-   5 translation_update.  matcha_profile_end synchronises on the last event and returns, per stage,
+   Stage ids: 0 sh_analysis, 1 corr_coeffs, 2 so3_search, 3 newton_refine/eval_corr, 4 pose gather / template
+   selection, 5 translation_update, 6 reconstruct.  matcha_profile_end synchronises on the last event and returns, per stage,
    the summed device milliseconds and the number of launches since matcha_profile_begin
    (stage_ms, stage_launches: host arrays of MATCHA_NUM_STAGES entries; either may be NULL). */
 #define MATCHA_NUM_STAGES 8

@@ -58,6 +58,10 @@ def _lib():
             "orc_upsampled_corr_at": [_fp, _fp, ctypes.c_int, _dp, _dp],
             "orc_energy": [_dp, _dp, ctypes.c_int, ctypes.c_int],
             "orc_align_batch": [_fp, ctypes.c_int64, _fp, _dp, ctypes.c_int, _ip, _dp, _dp, ctypes.c_int],
+            "orc_align_batch_multi": [_fp, ctypes.c_int64, _fp, ctypes.c_int, _dp, ctypes.c_int, _ip, _dp, _dp,
+                                      ctypes.c_int],
+            "orc_reconstruct": [_fp, ctypes.c_int64, ctypes.c_int, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_int64, _dp, _ip],
         }
         for name, args in sig.items():
             getattr(lib, name).argtypes = args
@@ -326,3 +330,37 @@ def align_batch(vols, ref, params, H=None, nthreads=0):
     _lib().orc_align_batch(_p(vols, _fp), B, _p(ref, _fp), None if Hc is None else _p(Hc.view(np.float64)), N,
                            _p(ip, _ip), _p(dp), _p(poses), nthreads)
     return poses
+
+
+def _param_arrays(params):
+    bands = list(params["bands"])
+    ip = np.zeros(26, np.int32)
+    ip[0:6] = [params["L"], params.get("qover", 2), params["L0"], params.get("K", 2), params["ncand"], len(bands)]
+    ip[6:6 + len(bands)] = bands
+    ip[22:26] = [params.get("iters", 1), params.get("T", 1), params.get("W", 0), params.get("ups", 0)]
+    dp = np.array([params.get("tol_grad", 0.0), params.get("tol_step", 0.0), params.get("tol_obj", 0.0)])
+    return ip, dp
+
+
+def align_batch_multi(vols, refs, params, nthreads=0):
+    """Multi-template alignment: refs [T, N, N, N] -> poses [B, 9] (..., template index)."""
+    vols = np.ascontiguousarray(vols, np.float32)
+    refs = np.ascontiguousarray(refs, np.float32)
+    B, N = vols.shape[0], vols.shape[-1]
+    ip, dp = _param_arrays(params)
+    poses = np.zeros((B, 9))
+    _lib().orc_align_batch_multi(_p(vols, _fp), B, _p(refs, _fp), refs.shape[0], None, N, _p(ip, _ip), _p(dp),
+                                 _p(poses), nthreads)
+    return poses
+
+
+def reconstruct(vols, poses, n_classes=1, class_col=-1, first_index=0):
+    """Half-map sums: -> (sums [n_classes, 2, N, N, N], counts [n_classes, 2])."""
+    vols = np.ascontiguousarray(vols, np.float32)
+    poses = np.ascontiguousarray(poses, np.float64)
+    B, N = vols.shape[0], vols.shape[-1]
+    sums = np.zeros((n_classes, 2, N, N, N))
+    counts = np.zeros((n_classes, 2), np.int32)
+    _lib().orc_reconstruct(_p(vols, _fp), B, N, _p(poses), poses.shape[1], class_col, n_classes, first_index,
+                           _p(sums), _p(counts, _ip))
+    return sums, counts

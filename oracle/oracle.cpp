@@ -771,6 +771,104 @@ void align_one(const float* vol, const float* ref, const double* H, int N, const
   pose[6] = score; pose[7] = best;
 }
 
+/* ||H_{<=L}||_w = sqrt(sum_i w_i sum_{l<=L} sum_{m=-l..l} |h_lm(r_i)|^2): the template's band-limited norm (the
+   Cauchy-Schwarz scale of C_L, SURVEY 8(c) tolerances) */
+double template_norm(const double* H, int L, int R) {
+  double e = 0;
+  for (int l = 0; l <= L; ++l)
+    for (int m = -l; m <= l; ++m)
+      for (int i = 0; i < R; ++i) {
+        const double r = i + 0.5;
+        e += r * r * std::norm(coef(H, R, l, m, i));
+      }
+  return std::sqrt(e);
+}
+
+/* whole path for one particle against nt templates: per alternation the rotation search of
+   align_one against every template; the template with the highest C_{L_J} / ||H_{<=L_J}||_w wins (reading C29: the
+   raw inner product grows with the template's energy, the particle's norm is common to all templates; ties -> the
+   lowest template index); the translation update rotates the winning template.
+   pose [9] = {alpha, beta, gamma, tx, ty, tz, score (raw C_{L_J}), best, template}. */
+void align_one_multi(const float* vol, const float* refs, int nt, const double* Hs, int N, const Params& p,
+                     double* pose) {
+  const int R = N / 2;
+  const size_t n3 = (size_t)N * N * N, hsz = (size_t)2 * ncoef(p.L) * R;
+  const double c = 0.5 * (N - 1);
+  double t[3] = {0, 0, 0};
+  vector<double> F(hsz), M((size_t)2 * full_size(p.L));
+  int nb, na, ng;
+  grid_dims(p.L0, p.K, nb, na, ng);
+  vector<double> grid((size_t)nb * na * ng);
+  vector<int64_t> idx(p.ncand);
+  vector<double> sc(p.ncand), eu((size_t)3 * p.ncand);
+  double rot[3] = {0, 0, 0}, score = 0, nbest = 0;
+  int best = -1, tbest = 0;
+  for (int tau = 0; tau < std::max(1, p.T); ++tau) {
+    double centre[3] = {c + t[0], c + t[1], c + t[2]};
+    sh_analysis(VolSampler{vol, N}, N, p.L, p.qover, centre, F.data());
+    bool have = false;
+    for (int k = 0; k < nt; ++k) {
+      corr_full(F.data(), Hs + k * hsz, R, p.L, M.data());
+      grid_eval(M.data(), p.L0, p.K, grid.data());
+      find_maxima(grid.data(), nb, na, ng, p.ncand, idx.data(), sc.data());
+      for (int n = 0; n < p.ncand; ++n) {
+        if (idx[n] >= 0) grid_node_euler(idx[n], p.L0, p.K, &eu[3 * n]);
+        else eu[3 * n] = eu[3 * n + 1] = eu[3 * n + 2] = 0.0;
+      }
+      int b = -1;
+      refine(M.data(), p.bands, p.nbands, p.iters, p.ncand, idx.data(), p.tol_grad, p.tol_step, p.tol_obj, eu.data(),
+             sc.data(), &b);
+      const double nk = sc[b >= 0 ? b : 0] / template_norm(Hs + k * hsz, p.bands[p.nbands - 1], R);
+      if (b >= 0 && (!have || nk > nbest)) {
+        have = true;
+        nbest = nk;
+        score = sc[b];
+        best = b;
+        tbest = k;
+        for (int q = 0; q < 3; ++q) rot[q] = eu[3 * b + q];
+      }
+    }
+    if (p.W > 0) {
+      double pk;
+      if (p.ups > 0) translation_upsampled(vol, refs + tbest * n3, N, rot, p.W, p.ups, t, &pk);
+      else translation(vol, refs + tbest * n3, N, rot, p.W, t, &pk);
+    }
+  }
+  pose[0] = rot[0]; pose[1] = rot[1]; pose[2] = rot[2];
+  pose[3] = t[0]; pose[4] = t[1]; pose[5] = t[2];
+  pose[6] = score; pose[7] = best; pose[8] = tbest;
+}
+
+/* reference update (P:1184 half sets; reading C28): sums[k][s][y] = sum over particles p of class k and
+   half s = (first + p) mod 2 of f_p(g_p (y - c) + c + t_p) (trilinear, zero outside), counts[k][s]. */
+void reconstruct(const float* vols, int64_t B, int N, const double* poses, int stride, int ccol, int ncls,
+                 int64_t first, double* sums, int* counts) {
+  const size_t n3 = (size_t)N * N * N;
+  const double c = 0.5 * (N - 1);
+  std::fill(sums, sums + (size_t)ncls * 2 * n3, 0.0);
+  std::fill(counts, counts + 2 * ncls, 0);
+  for (int64_t p = 0; p < B; ++p) {
+    const double* ps = poses + p * stride;
+    const int k = ccol >= 0 ? (int)ps[ccol] : 0;
+    if (k < 0 || k >= ncls) continue;
+    const int half = (int)((first + p) % 2);
+    counts[2 * k + half] += 1;
+    double Rm[9];
+    euler_to_matrix(ps, Rm);
+    VolSampler f{vols + p * n3, N};
+    double* out = sums + (size_t)(2 * k + half) * n3;
+    for (int z = 0; z < N; ++z)
+      for (int y = 0; y < N; ++y)
+        for (int x = 0; x < N; ++x) {
+          const double u0 = x - c, u1 = y - c, u2 = z - c;
+          const double q0 = Rm[0] * u0 + Rm[1] * u1 + Rm[2] * u2 + c + ps[3];
+          const double q1 = Rm[3] * u0 + Rm[4] * u1 + Rm[5] * u2 + c + ps[4];
+          const double q2 = Rm[6] * u0 + Rm[7] * u1 + Rm[8] * u2 + c + ps[5];
+          out[((size_t)z * N + y) * N + x] += f(q0, q1, q2);
+        }
+  }
+}
+
 template <class Fn>
 void parallel_for(int64_t n, int nthreads, Fn fn) {
   if (nthreads == 1 || n <= 1) {
@@ -932,6 +1030,33 @@ void orc_align_batch(const float* vols, int64_t B, const float* ref, const doubl
   g_inner_threads = (int)std::max<int64_t>(1, outer / std::max<int64_t>(1, std::min<int64_t>(B, outer)));
   parallel_for(B, nthreads, [&](int64_t b) { align_one(vols + b * n3, ref, H, N, p, poses + 8 * b); });
   g_inner_threads = 1;
+}
+
+/* multi-template: refs float [nt][N^3]; Hs complex [nt][ncoef(L)][R] or NULL (analysed here); poses [B][9] */
+void orc_align_batch_multi(const float* vols, int64_t B, const float* refs, int nt, const double* Hs, int N,
+                           const int* ip, const double* dp, double* poses, int nthreads) {
+  Params p;
+  p.L = ip[0]; p.qover = ip[1]; p.L0 = ip[2]; p.K = ip[3]; p.ncand = ip[4]; p.nbands = ip[5];
+  for (int k = 0; k < 16; ++k) p.bands[k] = ip[6 + k];
+  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24]; p.ups = ip[25];
+  p.tol_grad = dp[0]; p.tol_step = dp[1]; p.tol_obj = dp[2];
+  const int R = N / 2;
+  const size_t n3 = (size_t)N * N * N, hsz = (size_t)2 * ncoef(p.L) * R;
+  vector<double> Hl;
+  if (!Hs) {
+    Hl.resize(hsz * nt);
+    for (int k = 0; k < nt; ++k) orc_sh_analysis_vol(refs + k * n3, N, p.L, p.qover, nullptr, Hl.data() + k * hsz);
+    Hs = Hl.data();
+  }
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int outer = nthreads > 0 ? nthreads : hw;
+  g_inner_threads = (int)std::max<int64_t>(1, outer / std::max<int64_t>(1, std::min<int64_t>(B, outer)));
+  parallel_for(B, nthreads, [&](int64_t b) { align_one_multi(vols + b * n3, refs, nt, Hs, N, p, poses + 9 * b); });
+  g_inner_threads = 1;
+}
+void orc_reconstruct(const float* vols, int64_t B, int N, const double* poses, int stride, int ccol, int ncls,
+                     int64_t first, double* sums, int* counts) {
+  reconstruct(vols, B, N, poses, stride, ccol, ncls, first, sums, counts);
 }
 
 }  // extern "C"

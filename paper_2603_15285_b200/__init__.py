@@ -64,6 +64,8 @@ _SIGS = {
     "matcha_translation_update": ([_H, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp], ctypes.c_int),
     "matcha_align_batch": ([_H, _vp, _i64, _vp, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_align_batch_host": ([_H, _vp, _i64, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
+    "matcha_align_multi": ([_H, _vp, _i64, _vp, _i32, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
+    "matcha_reconstruct": ([_H, _vp, _i64, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _vp], ctypes.c_int),
     "matcha_get_status": ([_H, _vp], ctypes.c_int),
     "matcha_last_error_string": ([_H], ctypes.c_char_p),
     "matcha_launch_count": ([_H], ctypes.c_int64),
@@ -71,7 +73,8 @@ _SIGS = {
     "matcha_profile_end": ([_H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
 }
 NUM_STAGES = 8
-STAGES = ("sh_analysis", "corr_coeffs", "so3_search", "newton_refine", "gather_poses", "translation_update")
+STAGES = ("sh_analysis", "corr_coeffs", "so3_search", "newton_refine", "gather_poses", "translation_update",
+          "reconstruct")
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args
@@ -289,6 +292,35 @@ class Handle:
         self._check(_lib.matcha_align_batch(self._h, _ptr(vols), B, _ptr(ref), _ptr(ref_coeffs), ctypes.byref(p),
                                             _ptr(out), _stream()))
         return out
+
+    def align_multi(self, vols: torch.Tensor, refs: Optional[torch.Tensor], params: Params,
+                    ref_coeffs: Optional[torch.Tensor] = None, out=None) -> torch.Tensor:
+        """Multi-template alignment: refs [T, N, N, N] -> poses [B, 9] (..., template index)."""
+        B = self._vols(vols)
+        nt = refs.shape[0] if refs is not None else ref_coeffs.shape[0]
+        self._arg(refs, "refs", torch.float32, (nt, self.N, self.N, self.N), optional=True)
+        self._arg(ref_coeffs, "ref_coeffs", self.cplx, (nt, ncoef(self.L_max), self.R), optional=True)
+        if out is None:
+            out = torch.empty((B, 9), dtype=self.real, device=self.device)
+        self._arg(out, "out", self.real, (B, 9))
+        p = params.c()
+        self._check(_lib.matcha_align_multi(self._h, _ptr(vols), B, _ptr(refs), nt, _ptr(ref_coeffs), ctypes.byref(p),
+                                            _ptr(out), _stream()))
+        return out
+
+    def reconstruct(self, vols: torch.Tensor, poses: torch.Tensor, n_classes: int = 1, class_col: int = -1,
+                    first_index: int = 0):
+        """Half-map sums of the aligned particles: -> (sums [n_classes, 2, N, N, N] real,
+        counts [n_classes, 2] int32).  poses [B, stride]: columns 0..5 = (alpha, beta, gamma, tx, ty, tz)."""
+        B = self._vols(vols)
+        if not isinstance(poses, torch.Tensor) or poses.dim() != 2:
+            raise ValueError("poses must be a [B, stride] tensor")
+        self._arg(poses, "poses", self.real, (B, poses.shape[1]))
+        sums = torch.empty((n_classes, 2, self.N, self.N, self.N), dtype=self.real, device=self.device)
+        counts = torch.empty((n_classes, 2), dtype=torch.int32, device=self.device)
+        self._check(_lib.matcha_reconstruct(self._h, _ptr(vols), B, _ptr(poses), poses.shape[1], class_col, n_classes,
+                                            first_index, _ptr(sums), _ptr(counts), _stream()))
+        return sums, counts
 
     def align_batch_host(self, vols_host: torch.Tensor, ref_host: torch.Tensor, params: Params,
                          out: Optional[torch.Tensor] = None) -> torch.Tensor:

@@ -36,6 +36,7 @@ __host__ __device__ __forceinline__ int pair_count(int L) { return (L + 1) * (2 
 constexpr double kPi = 3.14159265358979323846264338327950288;
 constexpr int kMaxL = 128;
 constexpr int kMaxCand = 32;
+constexpr int kMaxTemplates = 16;  // multi-template alignment
 
 // device error flags
 enum : int { FLAG_NONFINITE = 1, FLAG_OVERFLOW = 2, FLAG_PLANES = 4 };
@@ -113,6 +114,16 @@ cudaError_t launch_corr_coeffs(const cplx_t<T>* F, const cplx_t<T>* H, int64_t B
 template <typename T> cudaError_t launch_so3_search(const SearchArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_eval_corr(const NewtonArgs<T>& a, bool derivs, cudaStream_t s);
 template <typename T> cudaError_t launch_newton_refine(const NewtonArgs<T>& a, cudaStream_t s);
+// per particle, the template whose pose scores highest relative to the template's norm (reading C29;
+// ties -> lowest template index):
+// cand [nt][B][8] poses per template -> poses [B][pstride] (columns 0..7 copied, column 8 = template index unless
+// pstride < 9), tsel [B]; shifts (columns 3..5) are taken from `poses` itself when keep_shift
+template <typename T>
+cudaError_t launch_select_template(const T* cand, const double* tnorm, int nt, int64_t B, bool keep_shift, T* poses,
+                                   int pstride, int* tsel, cudaStream_t s);
+// ||H_{<=L}||_w of nt templates (reading C29), H complex [nt][ncoef(Lmax)][R] -> out double [nt]
+template <typename T>
+cudaError_t launch_template_norms(const cplx_t<T>* H, int nt, int Lmax, int L, int R, double* out, cudaStream_t s);
 template <typename T>
 cudaError_t launch_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,
                                 T* poses, cudaStream_t s);
@@ -130,8 +141,10 @@ size_t corr_tc_smem_bytes(int L, int R);
 bool corr_tc_supported(int L, int R);
 cudaError_t launch_corr_coeffs_tc(const float2* F, const float2* H, int64_t B, int L, int Lmax, int R, float2* M,
                                   int num_sms, cudaStream_t s);
+// tsel: per-particle template index into refs [T][N^3] (multi-template alignment) or NULL (one reference)
 template <typename T>
-cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estride, int64_t nb, T* rho, cudaStream_t s);
+cudaError_t launch_rotate_ref(const float* refs, int N, const T* euler, int estride, const int* tsel, int64_t nb, T* rho,
+                              cudaStream_t s);
 // stage 5 without an FFT library (k_trans.cu): mixed-radix factorisation of a transform length
 struct FftRadix {
   int n, nst;
@@ -144,8 +157,9 @@ cudaError_t launch_plane_r2c(const Tin* vol, int N, int64_t nb, cplx_t<T>* out, 
 // FP32 fast path (N = 32, 64, 96, 128): compile-time FFTs; rot = true fuses the rotation of the reference (read
 // through `tex`, a 2-D texture over launch_pad_ref's zero-padded plane stack) into the transform of rho
 bool plane_fast_supported(int N);
-cudaError_t launch_plane_fft_f32(const float* vol, cudaTextureObject_t tex, const float* euler, int estride, int N,
-                                 int64_t nb, float2* out, bool rot, cudaStream_t s);
+cudaError_t launch_plane_fft_f32(const float* vol, const cudaTextureObject_t* tex, const int* tsel,
+                                 const float* euler, int estride, int N, int64_t nb, float2* out, bool rot,
+                                 cudaStream_t s);
 cudaError_t launch_pad_ref(const float* ref, int N, int pitch, float* pad, cudaStream_t s);
 size_t window_scratch_reals(int N, int W);
 template <typename T>
@@ -158,5 +172,10 @@ size_t ups_scratch_bytes(int N, int kappa, size_t csz);  // per particle
 template <typename T>
 cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
                              void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s);
+
+// half-map sums of the aligned particles per class (k_recon.cu); Rt: workspace real [B][12]
+template <typename T>
+cudaError_t launch_reconstruct(const float* vols, int64_t B, int N, const T* poses, int pstride, int ccol, int ncls,
+                               int64_t first, T* Rt, T* sums, int* counts, cudaStream_t s);
 
 }  // namespace matcha

@@ -522,6 +522,77 @@ template cudaError_t launch_eval_corr<double>(const NewtonArgs<double>&, bool, c
 template cudaError_t launch_newton_refine<float>(const NewtonArgs<float>&, cudaStream_t);
 template cudaError_t launch_newton_refine<double>(const NewtonArgs<double>&, cudaStream_t);
 
+// SURVEY f4 ("evaluate alignment against multiple candidate templates"): the best template per particle
+// reading C29: templates are compared by C_{L_J} / ||H_{<=L_J}||_w (the raw inner product grows with the template's
+// energy; the particle's norm is common to all templates); ties -> lowest template index
+template <typename T>
+__global__ void k_select_template(const T* __restrict__ cand, const double* __restrict__ tnorm, int nt, int64_t B,
+                                  bool keep_shift, T* poses, int pstride, int* __restrict__ tsel) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int k = 0;
+  double bv = (double)cand[b * 8 + 6] / tnorm[0];
+  for (int t = 1; t < nt; ++t) {
+    const double v = (double)cand[((int64_t)t * B + b) * 8 + 6] / tnorm[t];
+    if (v > bv) {
+      bv = v;
+      k = t;
+    }
+  }
+  const T* c = cand + ((int64_t)k * B + b) * 8;
+  T* o = poses + b * pstride;
+  for (int q = 0; q < 8; ++q)
+    if (!(keep_shift && q >= 3 && q <= 5)) o[q] = c[q];
+  if (pstride >= 9) o[8] = (T)k;
+  if (tsel) tsel[b] = k;
+}
+
+template <typename T>
+cudaError_t launch_select_template(const T* cand, const double* tnorm, int nt, int64_t B, bool keep_shift, T* poses,
+                                   int pstride, int* tsel, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  k_select_template<T><<<(unsigned)((B + 127) / 128), 128, 0, s>>>(cand, tnorm, nt, B, keep_shift, poses, pstride,
+                                                                    tsel);
+  return cudaGetLastError();
+}
+template cudaError_t launch_select_template<float>(const float*, const double*, int, int64_t, bool, float*, int, int*,
+                                                   cudaStream_t);
+template cudaError_t launch_select_template<double>(const double*, const double*, int, int64_t, bool, double*, int,
+                                                    int*, cudaStream_t);
+
+// ||H_k||_w over l <= L for templates k < nt (one CTA each, fixed-order FP64 block reduction)
+template <typename T>
+__global__ void __launch_bounds__(256) k_template_norms(const cplx_t<T>* __restrict__ H, int Lmax, int L, int R,
+                                                        double* __restrict__ out) {
+  __shared__ double red[256];
+  const cplx_t<T>* h = H + (int64_t)blockIdx.x * ncoef(Lmax) * R;
+  double e = 0;
+  for (int t = threadIdx.x; t < ncoef(L) * R; t += blockDim.x) {
+    const int lm = t / R, i = t - lm * R;
+    int l = 0;
+    while ((l + 1) * (l + 2) / 2 <= lm) ++l;
+    const int m = lm - l * (l + 1) / 2;
+    const double r = i + 0.5;
+    const cplx_t<T> v = h[t];
+    e += (m ? 2.0 : 1.0) * r * r * ((double)v.x * v.x + (double)v.y * v.y);  // |h_{l,-m}| = |h_{l,m}|
+  }
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if ((int)threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = sqrt(red[0]);
+}
+
+template <typename T>
+cudaError_t launch_template_norms(const cplx_t<T>* H, int nt, int Lmax, int L, int R, double* out, cudaStream_t s) {
+  k_template_norms<T><<<(unsigned)nt, 256, 0, s>>>(H, Lmax, L, R, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_template_norms<float>(const float2*, int, int, int, int, double*, cudaStream_t);
+template cudaError_t launch_template_norms<double>(const double2*, int, int, int, int, double*, cudaStream_t);
+
 // poses[b] = {alpha, beta, gamma, (shift untouched), score, best}
 template <typename T>
 __global__ void k_gather_poses(const T* euler, const T* score, const int32_t* best, int64_t B, int Q, bool zero_shift,

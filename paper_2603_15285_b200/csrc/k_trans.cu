@@ -75,11 +75,13 @@ __device__ __forceinline__ T trilinear_g(const float* __restrict__ v, int N, T p
 // corners are staged as 0, so the arithmetic is exactly trilinear_g's.  N is a multiple of 8 (matcha_create).
 constexpr int kRotTile = 8, kRotBox = 16, kRotCtas = 96;
 template <typename T>
-__global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ ref, int N, const T* __restrict__ euler,
-                                                    int estride, T* __restrict__ rho) {
+__global__ void __launch_bounds__(256) k_rotate_ref(const float* __restrict__ refs, int N, const T* __restrict__ euler,
+                                                    int estride, const int* __restrict__ tsel, T* __restrict__ rho) {
   __shared__ double Rm[9];
   __shared__ float box[kRotBox * kRotBox * kRotBox];
   const int64_t p = blockIdx.y;
+  // multi-template alignment: particle p's translation uses its selected template
+  const float* ref = refs + (tsel ? (int64_t)tsel[p] * N * N * N : 0);
   const int nt = N / kRotTile;
   const T c = T(0.5) * (T)(N - 1);
   if (threadIdx.x == 0) rot_matrix<T>(euler + p * estride, Rm);
@@ -567,7 +569,9 @@ template <int N> constexpr size_t plane_fast_smem() {
 // zero-padded plane stack (row z (N+1) + y; row z (N+1) + N is zero; border = 0), two tld4 gathers per voxel (the
 // 2 x 2 footprints of planes z0 and z0 + 1), with k_rotate_ref's exact trilinear arithmetic; rho never touches HBM.
 template <int N, bool ROT>
-__global__ void __launch_bounds__(kFftThreads, 2) k_plane_fft(const float* __restrict__ vol, cudaTextureObject_t tex,
+__global__ void __launch_bounds__(kFftThreads, 2) k_plane_fft(const float* __restrict__ vol,
+                                                              const cudaTextureObject_t* __restrict__ texs,
+                                                              const int* __restrict__ tsel,
                                                               const float* __restrict__ euler, int estride,
                                                               float2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -582,7 +586,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_plane_fft(const float* __res
   build_roots<float>(tw, N, -1);
   float r0 = 0.f, r1 = 0.f, r2 = 0.f, r3 = 0.f, r4 = 0.f, r5 = 0.f, r6 = 0.f, r7 = 0.f, r8 = 0.f;
   const float c = 0.5f * (float)(N - 1), uz = (float)z - c;
+  cudaTextureObject_t tex = 0;
   if (ROT) {
+    tex = texs[tsel ? tsel[p] : 0];  // the particle's template or the single reference
     if (threadIdx.x == 0) rot_matrix<float>(euler + p * estride, Rm);
     __syncthreads();
     r0 = (float)Rm[0], r1 = (float)Rm[1], r2 = (float)Rm[2], r3 = (float)Rm[3], r4 = (float)Rm[4],
@@ -1017,7 +1023,7 @@ __global__ void k_ups_final(const T* __restrict__ bval, const int* __restrict__ 
 }  // namespace
 
 template <typename T>
-cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estride, int64_t nb, T* rho,
+cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estride, const int* tsel, int64_t nb, T* rho,
                               cudaStream_t s) {
   if (nb == 0) return cudaSuccess;
   const int64_t n3 = (int64_t)N * N * N;
@@ -1025,7 +1031,7 @@ cudaError_t launch_rotate_ref(const float* ref, int N, const T* euler, int estri
   if (N % kRotTile) return cudaErrorInvalidValue;
   const int nt = N / kRotTile;
   k_rotate_ref<T><<<dim3((unsigned)std::min(nt * nt * nt, kRotCtas), (unsigned)nb), 256, 0, s>>>(ref, N, euler,
-                                                                                                  estride, rho);
+                                                                                                  estride, tsel, rho);
   return cudaGetLastError();
 }
 
@@ -1090,25 +1096,27 @@ cudaError_t launch_plane_r2c(const Tin* vol, int N, int64_t nb, cplx_t<T>* out, 
 bool plane_fast_supported(int N) { return N == 32 || N == 64 || N == 96 || N == 128; }
 
 template <int N>
-static cudaError_t launch_plane_fast(const float* vol, cudaTextureObject_t tex, const float* euler, int estride,
-                                     int64_t nb, float2* out, bool rot, cudaStream_t s) {
+static cudaError_t launch_plane_fast(const float* vol, const cudaTextureObject_t* tex, const int* tsel,
+                                     const float* euler, int estride, int64_t nb, float2* out, bool rot,
+                                     cudaStream_t s) {
   constexpr size_t smem = plane_fast_smem<N>();
   static_assert(smem <= 227 * 1024, "plane buffers exceed shared memory");
   auto kern = rot ? k_plane_fft<N, true> : k_plane_fft<N, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3((unsigned)N, (unsigned)nb), kFftThreads, smem, s>>>(vol, tex, euler, estride, out);
+  kern<<<dim3((unsigned)N, (unsigned)nb), kFftThreads, smem, s>>>(vol, tex, tsel, euler, estride, out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_plane_fft_f32(const float* vol, cudaTextureObject_t tex, const float* euler, int estride, int N,
-                                 int64_t nb, float2* out, bool rot, cudaStream_t s) {
+cudaError_t launch_plane_fft_f32(const float* vol, const cudaTextureObject_t* tex, const int* tsel,
+                                 const float* euler, int estride, int N, int64_t nb, float2* out, bool rot,
+                                 cudaStream_t s) {
   if (nb == 0) return cudaSuccess;
   switch (N) {
-    case 32: return launch_plane_fast<32>(vol, tex, euler, estride, nb, out, rot, s);
-    case 64: return launch_plane_fast<64>(vol, tex, euler, estride, nb, out, rot, s);
-    case 96: return launch_plane_fast<96>(vol, tex, euler, estride, nb, out, rot, s);
-    case 128: return launch_plane_fast<128>(vol, tex, euler, estride, nb, out, rot, s);
+    case 32: return launch_plane_fast<32>(vol, tex, tsel, euler, estride, nb, out, rot, s);
+    case 64: return launch_plane_fast<64>(vol, tex, tsel, euler, estride, nb, out, rot, s);
+    case 96: return launch_plane_fast<96>(vol, tex, tsel, euler, estride, nb, out, rot, s);
+    case 128: return launch_plane_fast<128>(vol, tex, tsel, euler, estride, nb, out, rot, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1240,8 +1248,10 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
   return cudaGetLastError();
 }
 
-template cudaError_t launch_rotate_ref<float>(const float*, int, const float*, int, int64_t, float*, cudaStream_t);
-template cudaError_t launch_rotate_ref<double>(const float*, int, const double*, int, int64_t, double*, cudaStream_t);
+template cudaError_t launch_rotate_ref<float>(const float*, int, const float*, int, const int*, int64_t, float*,
+                                              cudaStream_t);
+template cudaError_t launch_rotate_ref<double>(const float*, int, const double*, int, const int*, int64_t, double*,
+                                               cudaStream_t);
 template cudaError_t launch_upsampled<float>(const float2*, float2*, int, int, int64_t, const int*, void*, float*, int,
                                              float*, cudaStream_t);
 template cudaError_t launch_upsampled<double>(const double2*, double2*, int, int, int64_t, const int*, void*, double*,

@@ -69,9 +69,16 @@ struct matcha_ctx {
   void* ws_ups = nullptr;    // [mb] x ups_scratch_bytes(N, kappa): upsampled-DFT scratch
   int ws_ups_kappa = -1;
   bool trans_fast = false;   // FP32 and N in {32, 64, 96, 128}: compile-time FFTs, rotation fused into rho's transform
-  float* ws_refpad = nullptr;  // zero-padded plane stack of the reference (texture source of the fused rotation)
+  float* ws_refpad = nullptr;  // zero-padded plane stacks of the references (texture sources of the fused rotation)
   int refpad_pitch = 0;        // floats per row
-  cudaTextureObject_t tex_ref = 0;
+  cudaTextureObject_t tex_ref[kMaxTemplates] = {};
+  cudaTextureObject_t* d_tex = nullptr;  // device copy of tex_ref
+  // multi-template alignment
+  void* ws_Hs = nullptr;     // complex [kMaxTemplates][ncoef][R] reference coefficients
+  void* ws_cand = nullptr;   // real [kMaxTemplates][mb][8] per-template poses
+  int* ws_tsel = nullptr;    // int [mb] selected template per particle
+  void* ws_Rt = nullptr;     // real [n][12] pose matrices of matcha_reconstruct
+  int64_t ws_Rt_n = 0;
   void* ws_euler1 = nullptr; // real [mb][3]
   // per-stage event tracing
   bool prof = false;
@@ -316,24 +323,30 @@ static matcha_status_t trans_prepare(matcha_handle_t h, int W, int kappa) {
       cudaDeviceGetAttribute(&align, cudaDevAttrTexturePitchAlignment, h->device);
       const int af = std::max(1, align / (int)sizeof(float));
       h->refpad_pitch = (N + af - 1) / af * af;
-      e = cudaMalloc((void**)&h->ws_refpad, sizeof(float) * (size_t)h->refpad_pitch * N * (N + 1));
+      const size_t pad = (size_t)h->refpad_pitch * N * (N + 1);
+      e = cudaMalloc((void**)&h->ws_refpad, sizeof(float) * pad * kMaxTemplates);
+      if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_tex, sizeof(cudaTextureObject_t) * kMaxTemplates);
       if (e != cudaSuccess) return fail(h, MATCHA_ERR_ALLOC, "translation reference texture allocation failed");
-      cudaResourceDesc rd;
-      std::memset(&rd, 0, sizeof(rd));
-      rd.resType = cudaResourceTypePitch2D;
-      rd.res.pitch2D.devPtr = h->ws_refpad;
-      rd.res.pitch2D.desc = cudaCreateChannelDesc<float>();
-      rd.res.pitch2D.width = N;
-      rd.res.pitch2D.height = (size_t)N * (N + 1);
-      rd.res.pitch2D.pitchInBytes = sizeof(float) * (size_t)h->refpad_pitch;
-      cudaTextureDesc td;
-      std::memset(&td, 0, sizeof(td));
-      td.addressMode[0] = td.addressMode[1] = cudaAddressModeBorder;  // border colour 0: zero outside the box
-      td.filterMode = cudaFilterModePoint;
-      td.readMode = cudaReadModeElementType;
-      td.normalizedCoords = 0;
-      e = cudaCreateTextureObject(&h->tex_ref, &rd, &td, nullptr);
-      if (e != cudaSuccess) return cuda_fail(h, e, "translation: reference texture");
+      for (int k = 0; k < kMaxTemplates; ++k) {
+        cudaResourceDesc rd;
+        std::memset(&rd, 0, sizeof(rd));
+        rd.resType = cudaResourceTypePitch2D;
+        rd.res.pitch2D.devPtr = h->ws_refpad + pad * k;
+        rd.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+        rd.res.pitch2D.width = N;
+        rd.res.pitch2D.height = (size_t)N * (N + 1);
+        rd.res.pitch2D.pitchInBytes = sizeof(float) * (size_t)h->refpad_pitch;
+        cudaTextureDesc td;
+        std::memset(&td, 0, sizeof(td));
+        td.addressMode[0] = td.addressMode[1] = cudaAddressModeBorder;  // border colour 0: zero outside the box
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        e = cudaCreateTextureObject(&h->tex_ref[k], &rd, &td, nullptr);
+        if (e != cudaSuccess) return cuda_fail(h, e, "translation: reference texture");
+      }
+      e = cudaMemcpy(h->d_tex, h->tex_ref, sizeof(cudaTextureObject_t) * kMaxTemplates, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail(h, e, "translation: texture table");
     }
   }
   if (h->ws_win_W < W) {
@@ -369,7 +382,8 @@ static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t 
   if (st != MATCHA_OK) return st;
   cudaError_t e = h->fp64 ? launch_plane_r2c<double, float>(vols, h->cfg.N, nb, (double2*)h->ws_Fhat, s)
                   : h->trans_fast
-                      ? launch_plane_fft_f32(vols, 0, nullptr, 0, h->cfg.N, nb, (float2*)h->ws_Fhat, false, s)
+                      ? launch_plane_fft_f32(vols, nullptr, nullptr, nullptr, 0, h->cfg.N, nb, (float2*)h->ws_Fhat,
+                                             false, s)
                       : launch_plane_r2c<float, float>(vols, h->cfg.N, nb, (float2*)h->ws_Fhat, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of the particles");
   h->launches++;
@@ -377,8 +391,10 @@ static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t 
 }
 
 // t = windowed argmax of c(t) = sum_x f(x) rho(x - t) for the rotations `euler` (stride estride)
-static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* ref, const void* euler, int estride,
-                                    int W, int kappa, void* shifts, int sstride, void* peak, cudaStream_t s) {
+// refs: float [nt][N^3]; tsel: the template of every particle (NULL when nt == 1)
+static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* ref, int nt, const int* tsel,
+                                    const void* euler, int estride, int W, int kappa, void* shifts, int sstride,
+                                    void* peak, cudaStream_t s) {
   const int N = h->cfg.N;
   cudaError_t e;
   ProfScope ps(h, 5, s);
@@ -386,13 +402,18 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
   if (st != MATCHA_OK) return st;
   if (h->trans_fast) {
     // rho~ straight from the reference texture: the rotated references never touch HBM
-    e = launch_pad_ref(ref, N, h->refpad_pitch, h->ws_refpad, s);
-    if (e != cudaSuccess) return cuda_fail(h, e, "translation: pad_ref");
-    e = launch_plane_fft_f32(nullptr, h->tex_ref, (const float*)euler, estride, N, nb, (float2*)h->ws_Xhat, true, s);
+    const size_t pad = (size_t)h->refpad_pitch * N * (N + 1);
+    for (int k = 0; k < nt; ++k) {
+      e = launch_pad_ref(ref + (int64_t)k * N * N * N, N, h->refpad_pitch, h->ws_refpad + pad * k, s);
+      if (e != cudaSuccess) return cuda_fail(h, e, "translation: pad_ref");
+    }
+    h->launches += nt - 1;
+    e = launch_plane_fft_f32(nullptr, h->d_tex, tsel, (const float*)euler, estride, N, nb, (float2*)h->ws_Xhat, true,
+                             s);
     if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_fft of rho");
   } else {
-    e = h->fp64 ? launch_rotate_ref<double>(ref, N, (const double*)euler, estride, nb, (double*)h->ws_rho, s)
-                : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, nb, (float*)h->ws_rho, s);
+    e = h->fp64 ? launch_rotate_ref<double>(ref, N, (const double*)euler, estride, tsel, nb, (double*)h->ws_rho, s)
+                : launch_rotate_ref<float>(ref, N, (const float*)euler, estride, tsel, nb, (float*)h->ws_rho, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "translation: rotate_ref");
     e = h->fp64 ? launch_plane_r2c<double, double>((const double*)h->ws_rho, N, nb, (double2*)h->ws_Xhat, s)
                 : launch_plane_r2c<float, float>((const float*)h->ws_rho, N, nb, (float2*)h->ws_Xhat, s);
@@ -416,54 +437,92 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
   return MATCHA_OK;
 }
 
-// App. C alternation around Algorithm 1 for particles [0, B) of `vols`, chunked by max_batch.
-static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_t B, const float* ref,
-                                    const void* ref_coeffs, const matcha_params_t* p, void* poses, cudaStream_t s) {
+// template norms live behind the per-particle template indices in ws_tsel (8-byte aligned: max_batch ints padded)
+static double* tnorm(matcha_handle_t h) {
+  return (double*)((char*)h->ws_tsel + ((sizeof(int) * h->cfg.max_batch + 7) / 8) * 8);
+}
+
+// App. C alternation around Algorithm 1 for particles [0, B) of `vols`, chunked by max_batch, against nt templates
+// (refs float [nt][N^3]; ref_coeffs complex [nt][ncoef][R] or NULL): per alternation stage 1 once, stages 2-4 per
+// template, the best-scoring template per particle (nt = 1: plain Algorithm 1), then the translation
+// update against that template.  poses [B][pstride]: pstride 8, or 9 with the template index in column 8.
+static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_t B, const float* refs, int nt,
+                                    const void* ref_coeffs, const matcha_params_t* p, void* poses, int pstride,
+                                    cudaStream_t s) {
   const int N = h->cfg.N;
-  const int64_t n3 = (int64_t)N * N * N;
+  const int64_t n3 = (int64_t)N * N * N, hstride = (int64_t)h->ncf * h->R * 2 * h->rsz;
   const int LJ = p->bands[p->n_bands - 1], L0 = p->bands[0];
   const void* H = ref_coeffs;
   matcha_status_t st;
   if (!H) {
-    st = matcha_sh_analysis(h, ref, 1, nullptr, h->ws_H, s);
+    if (nt > 1 && !h->ws_Hs && cudaMalloc(&h->ws_Hs, hstride * kMaxTemplates) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "align: template coefficient allocation failed");
+    void* dst = nt == 1 ? h->ws_H : h->ws_Hs;
+    st = matcha_sh_analysis(h, refs, nt, nullptr, dst, s);
     if (st != MATCHA_OK) return st;
-    H = h->ws_H;
+    H = dst;
+  }
+  const bool direct = nt == 1 && pstride == 8;  // gather straight into the caller's poses (bitwise as before)
+  if (!direct) {
+    const size_t cb = (size_t)h->rsz * 8 * h->cfg.max_batch * kMaxTemplates;
+    if (!h->ws_cand && cudaMalloc(&h->ws_cand, cb) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "align: template pose allocation failed");
+    if (!h->ws_tsel && cudaMalloc((void**)&h->ws_tsel, (sizeof(int) * h->cfg.max_batch + 7) / 8 * 8 +
+                                                           sizeof(double) * kMaxTemplates) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "align: template selection allocation failed");
+    cudaError_t e = h->fp64 ? launch_template_norms<double>((const double2*)H, nt, h->L, LJ, h->R, tnorm(h), s)
+                            : launch_template_norms<float>((const float2*)H, nt, h->L, LJ, h->R, tnorm(h), s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "align: template norms");
+    h->launches++;
   }
   const bool translate = p->shift_window > 0;
   const int T = translate ? p->n_alternations : 1;  // without a translation update the T passes are identical
   for (int64_t c0 = 0; c0 < B; c0 += h->cfg.max_batch) {
     const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
-    char* pc = (char*)poses + c0 * 8 * h->rsz;
+    char* pc = (char*)poses + c0 * pstride * h->rsz;
     for (int tau = 0; tau < T; ++tau) {
       const void* sh = (tau > 0 && translate) ? (const void*)(pc + 3 * h->rsz) : nullptr;
       cudaError_t e;
       {
       ProfScope ps(h, 0, s);
       if (h->fp64)
-        e = launch_sh_analysis<double>(vols + c0 * n3, nb, (const double*)sh, 8, sh_tables<double>(h),
+        e = launch_sh_analysis<double>(vols + c0 * n3, nb, (const double*)sh, pstride, sh_tables<double>(h),
                                        (double2*)h->ws_F, (double2*)h->ws_G, h->gws_particles, s);
       else
-        e = launch_sh_analysis<float>(vols + c0 * n3, nb, (const float*)sh, 8, sh_tables<float>(h), (float2*)h->ws_F,
-                                      (float2*)h->ws_G, h->gws_particles, s);
+        e = launch_sh_analysis<float>(vols + c0 * n3, nb, (const float*)sh, pstride, sh_tables<float>(h),
+                                      (float2*)h->ws_F, (float2*)h->ws_G, h->gws_particles, s);
       }
       if (e != cudaSuccess) return cuda_fail(h, e, "align: sh_analysis");
       h->launches++;
-      if ((st = matcha_corr_coeffs(h, h->ws_F, H, nb, LJ, h->ws_M, s)) != MATCHA_OK) return st;
-      if ((st = matcha_so3_search(h, h->ws_M, LJ, nb, L0, p->oversample, p->n_cand, h->ws_euler, h->ws_score,
-                                  h->ws_idx, s)) != MATCHA_OK)
-        return st;
-      if ((st = matcha_newton_refine(h, h->ws_M, LJ, nb, p->n_cand, p, h->ws_euler, h->ws_idx, h->ws_score,
-                                     h->ws_best, s)) != MATCHA_OK)
-        return st;
-      {
-      ProfScope ps(h, 4, s);
-      e = h->fp64 ? launch_gather_poses<double>((const double*)h->ws_euler, (const double*)h->ws_score, h->ws_best,
-                                                nb, p->n_cand, !translate, (double*)pc, s)
-                  : launch_gather_poses<float>((const float*)h->ws_euler, (const float*)h->ws_score, h->ws_best, nb,
-                                               p->n_cand, !translate, (float*)pc, s);
+      for (int k = 0; k < nt; ++k) {
+        const void* Hk = (const char*)H + k * hstride;
+        if ((st = matcha_corr_coeffs(h, h->ws_F, Hk, nb, LJ, h->ws_M, s)) != MATCHA_OK) return st;
+        if ((st = matcha_so3_search(h, h->ws_M, LJ, nb, L0, p->oversample, p->n_cand, h->ws_euler, h->ws_score,
+                                    h->ws_idx, s)) != MATCHA_OK)
+          return st;
+        if ((st = matcha_newton_refine(h, h->ws_M, LJ, nb, p->n_cand, p, h->ws_euler, h->ws_idx, h->ws_score,
+                                       h->ws_best, s)) != MATCHA_OK)
+          return st;
+        void* dst = direct ? (void*)pc : (void*)((char*)h->ws_cand + (size_t)k * nb * 8 * h->rsz);
+        {
+        ProfScope ps(h, 4, s);
+        e = h->fp64 ? launch_gather_poses<double>((const double*)h->ws_euler, (const double*)h->ws_score, h->ws_best,
+                                                  nb, p->n_cand, !translate, (double*)dst, s)
+                    : launch_gather_poses<float>((const float*)h->ws_euler, (const float*)h->ws_score, h->ws_best, nb,
+                                                 p->n_cand, !translate, (float*)dst, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(h, e, "align: gather_poses");
+        h->launches++;
       }
-      if (e != cudaSuccess) return cuda_fail(h, e, "align: gather_poses");
-      h->launches++;
+      if (!direct) {
+        ProfScope ps(h, 4, s);
+        e = h->fp64 ? launch_select_template<double>((const double*)h->ws_cand, tnorm(h), nt, nb, translate,
+                                                     (double*)pc, pstride, h->ws_tsel, s)
+                    : launch_select_template<float>((const float*)h->ws_cand, tnorm(h), nt, nb, translate, (float*)pc,
+                                                    pstride, h->ws_tsel, s);
+        if (e != cudaSuccess) return cuda_fail(h, e, "align: select_template");
+        h->launches++;
+      }
       if (translate) {
         if (tau == 0) {
           ProfScope ps(h, 5, s);
@@ -471,7 +530,8 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
           if (st != MATCHA_OK) return st;
         }
         // t^tau from the rotation just estimated (poses[b][0..2]) -> poses[b][3..5]
-        st = trans_update(h, nb, ref, pc, 8, p->shift_window, p->upsample, pc + 3 * h->rsz, 8, h->ws_peak, s);
+        st = trans_update(h, nb, refs, nt, nt > 1 ? h->ws_tsel : nullptr, pc, pstride, p->shift_window, p->upsample,
+                          pc + 3 * h->rsz, pstride, h->ws_peak, s);
         if (st != MATCHA_OK) return st;
       }
     }
@@ -631,9 +691,11 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
-  if (h->tex_ref) cudaDestroyTextureObject(h->tex_ref);
+  for (int k = 0; k < kMaxTemplates; ++k)
+    if (h->tex_ref[k]) cudaDestroyTextureObject(h->tex_ref[k]);
   for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad,
-                  (void*)h->ws_tint, h->ws_ups, h->ws_grid})
+                  (void*)h->ws_tint, h->ws_ups, h->ws_grid, (void*)h->d_tex, h->ws_Hs, h->ws_cand,
+                  (void*)h->ws_tsel, h->ws_Rt})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -841,7 +903,7 @@ MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const fl
     const int64_t nb = std::min<int64_t>(h->cfg.max_batch, B - c0);
     matcha_status_t st = trans_fhat(h, vols + c0 * n3, nb, window, upsample, s);
     if (st != MATCHA_OK) return st;
-    st = trans_update(h, nb, ref, (const char*)euler + c0 * 3 * h->rsz, 3, window, upsample,
+    st = trans_update(h, nb, ref, 1, nullptr, (const char*)euler + c0 * 3 * h->rsz, 3, window, upsample,
                       (char*)shifts + c0 * 3 * h->rsz, 3, peak ? (char*)peak + c0 * h->rsz : h->ws_peak, s);
     if (st != MATCHA_OK) return st;
   }
@@ -863,7 +925,58 @@ MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vo
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: box too large for the stage-5 kernels");
   if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: upsample factor / box exceed the kernels' limits");
-  return align_device(h, vols, B, ref, ref_coeffs, params, poses, (cudaStream_t)stream);
+  return align_device(h, vols, B, ref, 1, ref_coeffs, params, poses, 8, (cudaStream_t)stream);
+}
+
+MATCHA_API matcha_status_t matcha_align_multi(matcha_handle_t h, const float* vols, int64_t B, const float* refs,
+                                              int32_t n_templates, const void* ref_coeffs,
+                                              const matcha_params_t* params, void* poses, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!vols || !poses))) return fail(h, MATCHA_ERR_INVALID_ARG, "align_multi: bad arguments");
+  if (n_templates < 1 || n_templates > kMaxTemplates)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "align_multi: n_templates must be in [1, 16]");
+  std::string why;
+  if (!valid_params(params, h->L, why)) return fail(h, MATCHA_ERR_CUTOFF, "align_multi: " + why);
+  if (!ref_coeffs && !refs) return fail(h, MATCHA_ERR_INVALID_ARG, "align_multi: need refs or ref_coeffs");
+  if (params->shift_window > 0 && (!refs || params->shift_window > h->cfg.N / 4))
+    return fail(h, MATCHA_ERR_WINDOW, "align_multi: shift window needs refs and W <= N/4");
+  if (params->shift_window > 0 && !trans_supported(h->cfg.N, params->shift_window, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_multi: box too large for the stage-5 kernels");
+  if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
+    return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_multi: upsample factor / box exceed the kernels' limits");
+  return align_device(h, vols, B, refs, n_templates, ref_coeffs, params, poses, 9, (cudaStream_t)stream);
+}
+
+MATCHA_API matcha_status_t matcha_reconstruct(matcha_handle_t h, const float* vols, int64_t B, const void* poses,
+                                              int32_t pose_stride, int32_t class_col, int32_t n_classes,
+                                              int64_t first_index, void* sums, int32_t* counts, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!vols || !poses)) || !sums || !counts)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "reconstruct: bad arguments");
+  if (pose_stride < 6 || n_classes < 1 || n_classes > 32 || class_col >= pose_stride || (class_col < 0 && n_classes != 1) ||
+      (class_col >= 0 && class_col < 6) || first_index < 0)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "reconstruct: bad pose layout / class arguments");
+  if (h->cfg.N % 8) return fail(h, MATCHA_ERR_INVALID_ARG, "reconstruct: N must be a multiple of 8");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t mb = std::max<int64_t>(B, 1);
+  if (h->ws_Rt_n < mb) {
+    if (h->ws_Rt) cudaFree(h->ws_Rt);
+    h->ws_Rt = nullptr;
+    h->ws_Rt_n = 0;
+    if (cudaMalloc(&h->ws_Rt, 12 * h->rsz * mb) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "reconstruct: pose matrix allocation failed");
+    h->ws_Rt_n = mb;
+  }
+  ProfScope ps(h, 6, s);
+  cudaError_t e = h->fp64 ? launch_reconstruct<double>(vols, B, h->cfg.N, (const double*)poses, pose_stride, class_col,
+                                                       n_classes, first_index, (double*)h->ws_Rt, (double*)sums,
+                                                       counts, s)
+                          : launch_reconstruct<float>(vols, B, h->cfg.N, (const float*)poses, pose_stride, class_col,
+                                                      n_classes, first_index, (float*)h->ws_Rt, (float*)sums, counts,
+                                                      s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "reconstruct launch");
+  h->launches += B > 0 ? 3 : 2;
+  return MATCHA_OK;
 }
 
 MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const float* vols_host, int64_t B,
@@ -907,7 +1020,7 @@ MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const floa
                                    cudaMemcpyHostToDevice, h->copy_stream));
     MATCHA_CUDA(h, cudaEventRecord(h->ev_copied[buf], h->copy_stream));
     MATCHA_CUDA(h, cudaStreamWaitEvent(s, h->ev_copied[buf], 0));
-    st = align_device(h, h->ws_vols[buf], nb, h->ws_ref, h->ws_H, params, h->ws_poses, s);
+    st = align_device(h, h->ws_vols[buf], nb, h->ws_ref, 1, h->ws_H, params, h->ws_poses, 8, s);
     if (st != MATCHA_OK) return st;
     MATCHA_CUDA(h, cudaMemcpyAsync((char*)poses_host + c0 * 8 * h->rsz, h->ws_poses, 8 * h->rsz * nb,
                                    cudaMemcpyDeviceToHost, s));

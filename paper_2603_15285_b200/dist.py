@@ -1,9 +1,11 @@
 """Data-parallel driver over particles: one process per GPU, torch.distributed for plumbing.
 
-The path shards naturally -- particles are independent -- so there is no exchange inside it.  The only two
-collectives (NCCL over NVLink on B200; any backend works, the CPU tests use gloo):
+The path shards naturally -- particles are independent -- so there is no exchange inside it.  The collectives
+(NCCL over NVLink on B200; any backend works, the CPU tests use gloo):
   1. broadcast of the reference coefficients H (complex [ncoef][R], 140 KiB at 64^3/L=32) from rank 0;
-  2. all_gather of the poses (8 reals = 32 B per particle in FP32).
+  2. all_gather of the poses (8 reals = 32 B per particle in FP32);
+  3. (the reference update after an alignment pass) all_reduce of the half-map sums (2 N^3 reals per
+     class) and counts -- the only N^3 exchange of the domain.
 Rank r of G owns the contiguous particle range [floor(r P/G), floor((r+1) P/G)).
 """
 from __future__ import annotations
@@ -71,3 +73,17 @@ def align_step(handle, vols_local: torch.Tensor, ref: torch.Tensor, params, H: t
         broadcast_ref_coeffs(ref, src=0, group=group)
     poses = handle.align_batch(vols_local, ref if translate else None, params, ref_coeffs=H)
     return gather_poses(poses, counts=counts, group=group)
+
+
+def reconstruct_step(handle, vols_local: torch.Tensor, poses_local: torch.Tensor, first_index: int,
+                     n_classes: int = 1, class_col: int = -1, group=None):
+    """Reference update of subtomogram averaging (P:1184 half-set split): every rank sums its shard's aligned
+    particles per (class, half set) with the library kernel, the sums and counts are all-reduced, and the half maps
+    are the ratio (classes/halves without particles stay 0).  -> (half maps [n_classes, 2, N, N, N], counts)."""
+    sums, counts = handle.reconstruct(vols_local, poses_local, n_classes=n_classes, class_col=class_col,
+                                      first_index=first_index)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(sums, group=group)
+        dist.all_reduce(counts, group=group)
+    c = counts.to(sums.dtype).clamp(min=1).reshape(n_classes, 2, 1, 1, 1)
+    return sums / c, counts

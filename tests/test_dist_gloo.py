@@ -4,6 +4,7 @@ gathered in global particle order (ragged shards too), and the elapsed time is t
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
@@ -101,3 +102,50 @@ def test_align_step_world2_gloo(P, T, W):
         assert t == 2.0                                             # max over ranks
         # rotation only: no reference volume is passed; translating: rank 0's volume on every rank
         assert refsum == [-1.0 if (not T or W == 0) else 0.5 * 64] * P
+
+
+class FakeReconHandle:
+    """CPU double of Handle.reconstruct: sums = (global index) planted per particle, counts per half."""
+
+    def reconstruct(self, vols, poses, n_classes=1, class_col=-1, first_index=0):
+        n = vols.shape[0]
+        sums = torch.zeros((n_classes, 2, 2, 2, 2), dtype=torch.float64)
+        counts = torch.zeros((n_classes, 2), dtype=torch.int32)
+        for p in range(n):
+            g = first_index + p
+            sums[0, g % 2] += float(g)
+            counts[0, g % 2] += 1
+        return sums, counts
+
+
+def _recon_worker(rank, world, port, P, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = D.shard(P, world, rank)
+        avg, counts = D.reconstruct_step(FakeReconHandle(), torch.zeros((b - a, 2, 2, 2)), torch.zeros((b - a, 8)),
+                                         first_index=a)
+        q.put((rank, avg[0, :, 0, 0, 0].tolist(), counts.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reconstruct_step_world2_gloo():
+    """half-map sums and counts are all-reduced across ranks before the division (global half sets)."""
+    P = 9
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_recon_worker, args=(r, 2, port, P, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    even = [g for g in range(P) if g % 2 == 0]
+    odd = [g for g in range(P) if g % 2 == 1]
+    for rank, avg, counts in res:
+        assert counts == [[len(even), len(odd)]]
+        assert abs(avg[0] - np.mean(even)) < 1e-12 and abs(avg[1] - np.mean(odd)) < 1e-12

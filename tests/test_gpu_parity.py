@@ -519,3 +519,64 @@ def test_paper_operating_point_end_to_end():
             compared += 1
             assert idx[0, k] == all_idx[k], (k, idx[0, k], all_idx[k])
     assert compared >= 3
+
+
+# ------------------------------------------------------------------ multi-template + reference update
+def _two_template_batch(N, B, snr, seed, cls):
+    b = gen.particles(N, B, float("inf"), seed=seed, shift_mode=gen.SHIFT_UNIFORM, shift_max=1.5)
+    blobs1 = gen.reference_blobs(seed=0xBEEF)
+    ref1 = gen.render(blobs1, N)[0]
+    vols = b.vols.copy()
+    for p in np.nonzero(cls == 1)[0]:
+        vols[p] = gen.render(blobs1, N, R=b.truth_R[p], t=b.truth_t[p])[0]
+    if np.isfinite(snr):
+        r = np.random.default_rng(seed)
+        vols += (r.normal(size=vols.shape) * np.sqrt(b.p_ref / snr)).astype(np.float32)
+    return b, vols, np.stack([b.ref, ref1])
+
+
+@pytest.mark.parametrize("T,W", [(1, 0), (3, 4)])
+def test_align_multi_template_parity(T, W, prec):
+    """matcha_align_multi (reading C29) vs the oracle: the same template per particle, rotations within
+    0.05 deg, shifts within 0.1 voxel; the classes match the planted ones."""
+    N, B = 32, 8
+    cls = np.array([0, 1, 1, 0, 1, 0, 0, 1])
+    b, vols, refs = _two_template_batch(N, B, 1.0, 62, cls)
+    h = handle(N, 8, prec, max_batch=5)   # two chunks
+    params = mt.Params(bands=[4, 6, 8], n_cand=4, oversample=2, n_alternations=T, shift_window=W)
+    poses = to_np(h.align_multi(cuda(vols), cuda(refs), params))
+    h.status()
+    po = O.align_batch_multi(vols, refs, dict(L=8, qover=2, L0=4, K=2, ncand=4, bands=[4, 6, 8], iters=1, T=T, W=W))
+    assert poses[:, 8].astype(int).tolist() == po[:, 8].astype(int).tolist() == cls.tolist()
+    for p in range(B):
+        assert rot_err_deg(poses[p, :3], po[p, :3]) < TOL_ROT_DEG, p
+        assert np.abs(poses[p, 3:6] - po[p, 3:6]).max() < 0.1, p
+
+
+def test_align_multi_one_template_equals_align_batch():
+    b = gen.particles(32, 6, 0.5, seed=63)
+    h = handle(32, 8)
+    params = mt.Params(bands=[4, 6, 8], n_cand=4)
+    p1 = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    pm = to_np(h.align_multi(cuda(b.vols), cuda(b.ref[None]), params))
+    assert np.array_equal(p1, pm[:, :8]) and np.all(pm[:, 8] == 0)
+
+
+def test_reconstruct_parity(prec):
+    """matcha_reconstruct (P:1184 half sets; reading C28) vs the oracle's FP64 back-projection, 2 classes,
+    shifted poses, an odd first index: elementwise within the FP32 summation bound (FP64: 1e-12)."""
+    N, B = 32, 20
+    b = gen.particles(N, B, 0.5, seed=64)
+    r = np.random.default_rng(64)
+    poses = np.zeros((B, 9))
+    poses[:, :3] = [O.matrix_to_euler(R) for R in b.truth_R]
+    poses[:, 3:6] = r.uniform(-2, 2, (B, 3))
+    poses[:, 8] = r.integers(0, 2, B)
+    h = handle(N, 8, prec)
+    sums, counts = h.reconstruct(cuda(b.vols), cuda(poses, h.real), n_classes=2, class_col=8, first_index=7)
+    sums, counts = to_np(sums), to_np(counts)
+    poses_used = to_np(cuda(poses, h.real)).astype(np.float64)
+    so, co = O.reconstruct(b.vols, poses_used, n_classes=2, class_col=8, first_index=7)
+    assert np.array_equal(counts, co)
+    bound = np.abs(b.vols).max() * B
+    assert np.abs(sums - so).max() <= (1e-12 if prec == "fp64" else 1e-5) * bound, np.abs(sums - so).max() / bound

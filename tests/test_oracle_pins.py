@@ -628,3 +628,83 @@ def test_alternation_fractional_shift_upsampled_c1():
     for p in range(2):
         assert O.geodesic_deg_matrix(O.euler_to_matrix(po[p, :3]), b.truth_R[p]) <= 0.05
         assert np.abs(po[p, 3:6] - b.truth_t[p]).max() <= 0.01
+
+
+# ------------------------------------------------------------------ reference update and multi-template
+def test_reconstruct_identity_shift_and_quarter_turn_exact():
+    """The back-projection f_p(g_p (y - c) + c + t_p) (reading C28) is exact where trilinear interpolation is: identity
+    pose -> the half sums are the plain sums of the volumes; identity rotation + integer shift t -> the volume rolled
+    by -t with zeros shifted in; r_z(pi/2) -> the exact grid permutation.  Half sets by global-index parity."""
+    N = 16
+    vols = gen.particles(N, 5, 0.3, seed=9).vols.astype(np.float32)
+    poses = np.zeros((5, 8))
+    s, c = O.reconstruct(vols, poses, first_index=3)
+    assert c.tolist() == [[2, 3]]   # global indices 3..7: odd 3, 5, 7; even 4, 6
+    assert np.array_equal(s[0, 0], vols[1].astype(np.float64) + vols[3])
+    assert np.array_equal(s[0, 1], vols[0].astype(np.float64) + vols[2] + vols[4])
+    t = (2, -1, 3)
+    poses = np.zeros((1, 8))
+    poses[0, 3:6] = t
+    s, _ = O.reconstruct(vols[:1], poses)
+    exp = np.zeros((N, N, N))
+    v = vols[0].astype(np.float64)
+    # h(y) = f(y + t): exp[z, y, x] = v[z + tz, y + ty, x + tx] where inside
+    for z in range(N):
+        for y in range(N):
+            for x in range(N):
+                zz, yy, xx = z + t[2], y + t[1], x + t[0]
+                if 0 <= zz < N and 0 <= yy < N and 0 <= xx < N:
+                    exp[z, y, x] = v[zz, yy, xx]
+    assert np.abs(s[0, 0] - exp).max() == 0
+    poses = np.zeros((1, 8))
+    poses[0, 0] = np.pi / 2   # g = r_z(pi/2): h(y) = f(g (y - c) + c): x' = -(y - c) + c, y' = (x - c) + c
+    s, _ = O.reconstruct(vols[:1], poses)
+    exp = np.zeros((N, N, N))
+    for y in range(N):
+        for x in range(N):
+            exp[:, y, x] = v[:, x, N - 1 - y]
+    assert np.abs(s[0, 0] - exp).max() < 1e-9
+
+
+def test_reconstruct_truth_poses_recover_reference():
+    """Noise-free particles f_p = S_t(g_p o h) back-projected with their PLANTED poses average to the reference
+    (interpolation error only: relative L2 < 5 %); the inverse rotations do not (> 30 %): pins the direction of the
+    pose convention (reading C17)."""
+    N = 32
+    b = gen.particles(N, 6, float("inf"), seed=5, shift_mode=gen.SHIFT_FIXED, fixed_shift=(1.0, -2.0, 0.5))
+    poses = np.zeros((6, 8))
+    poses[:, :3] = [O.matrix_to_euler(R) for R in b.truth_R]
+    poses[:, 3:6] = b.truth_t
+    s, c = O.reconstruct(b.vols, poses)
+    avg = s[0] / c[0][:, None, None, None]
+    ref = b.ref.astype(np.float64)
+    for half in range(2):
+        assert np.linalg.norm(avg[half] - ref) < 0.05 * np.linalg.norm(ref)
+    poses[:, :3] = [O.matrix_to_euler(R.T) for R in b.truth_R]
+    s, c = O.reconstruct(b.vols, poses)
+    assert np.linalg.norm(s[0, 0] / c[0, 0] - ref) > 0.3 * np.linalg.norm(ref)
+
+
+def _second_template(N):
+    return gen.render(gen.reference_blobs(seed=0xBEEF), N)[0]
+
+
+def test_align_multi_template_recovers_class_and_pose():
+    """particles of two different templates, noise-free, c1 shape; the multi-template path picks
+    each particle's own template and its planted rotation (<= 0.1 deg)."""
+    N = 32
+    b = gen.particles(N, 4, float("inf"), seed=61)
+    ref1 = _second_template(N)
+    vols = b.vols.copy()
+    cls = np.array([0, 1, 1, 0])
+    for p in np.nonzero(cls == 1)[0]:
+        vols[p] = gen.render(gen.reference_blobs(seed=0xBEEF), N, R=b.truth_R[p])[0]
+    refs = np.stack([b.ref, ref1])
+    P = dict(L=8, qover=2, L0=4, K=2, ncand=4, bands=[4, 6, 8], iters=1, T=1, W=0)
+    po = O.align_batch_multi(vols, refs, P)
+    assert po[:, 8].astype(int).tolist() == cls.tolist()
+    for p in range(4):
+        assert O.geodesic_deg_matrix(O.euler_to_matrix(po[p, :3]), b.truth_R[p]) < 0.1
+    # one template only: identical to align_batch
+    po1 = O.align_batch_multi(vols[:1], refs[:1], P)
+    assert np.allclose(po1[:, :8], O.align_batch(vols[:1], b.ref, P), rtol=0, atol=0)
