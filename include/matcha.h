@@ -89,9 +89,14 @@ typedef struct {
                               kappa >= 1 = upsampled DFT (Guizar-Sicairos, App. C remark iii; reading C27):
                               the correlation's trigonometric interpolant on a 1/kappa grid over +-1.5 voxel around
                               the integer peak (kappa <= 21; 16 in SURVEY f3) */
+  int32_t radial;          /* radial representation of stage 2: 0 = shells (reading C2, default);
+                              1 = the paper's ball harmonics (App. A.1) with the eigenvalue cutoff
+                              ball_lambda: M^l = sum_{k in K_l} f^_kl conj(h^_kl), rank <= |K_l| */
   double tol_grad;         /* early stop: ||grad|| < tol_grad*|C|; 0 = off */
   double tol_step;         /* early stop: ||delta|| < tol_step (rad); 0 = off */
   double tol_obj;          /* early stop: |dC| < tol_obj*|C|; 0 = off */
+  double ball_lambda;      /* Lambda of the ball-harmonic truncation lambda_lk <= Lambda (unit-ball frequency);
+                              <= 0: pi (R - 1/2), the radial Nyquist of the R midpoint shells (reading C30) */
 } matcha_params_t;
 
 /* Create a handle on the CURRENT CUDA device: builds the quadrature, Legendre and Wigner
@@ -170,6 +175,22 @@ MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const fl
 MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vols, int64_t B, const float* ref,
                                               const void* ref_coeffs, const matcha_params_t* params, void* poses,
                                               void* stream);
+
+/* Ball-harmonic radial basis (App. A.1; reading C30).  psi_klm = c_lk j_l(lambda_lk rho)
+   Y_lm on the box's inscribed ball (rho = r / R), lambda_lk the k-th positive root of j_l, c_lk = sqrt(2) /
+   |j_{l+1}(lambda_lk)|, kept while lambda_lk <= lambda (lambda <= 0: pi (R - 1/2)).
+   matcha_ball_kmax: fills K_host[0..L_max] with |K_l| (host array, may be NULL) and returns Kmax = max_l |K_l|
+   (negative on error).
+   matcha_ball_transform: shell coefficients F complex [B][ncoef(L_max)][R] (stage 1) -> ball coefficients
+   Fball complex [B][ncoef(L_max)][Kmax], f^_klm = sum_i (1/R) rho_i^2 c_lk j_l(lambda_lk rho_i) f_lm(r_i) (midpoint
+   rule, rho_i = (i - 1/2)/R), zero for k >= |K_l|.
+   matcha_corr_coeffs_ball: M complex [B][Mh(L)] half plane, M^l_mn = sum_{k < |K_l|} f^_klm conj(h^_kln)
+   (sigma_{l m m'} of P:1311-1314 with K_l; hball complex [ncoef(L_max)][Kmax]). */
+MATCHA_API int32_t matcha_ball_kmax(matcha_handle_t h, double lambda, int32_t* K_host);
+MATCHA_API matcha_status_t matcha_ball_transform(matcha_handle_t h, const void* F, int64_t B, double lambda,
+                                                 void* Fball, void* stream);
+MATCHA_API matcha_status_t matcha_corr_coeffs_ball(matcha_handle_t h, const void* fball, const void* hball, int64_t B,
+                                                   int32_t L, double lambda, void* M, void* stream);
 
 /* Multi-template alignment ("evaluate alignment against multiple candidate templates per
    iteration"): per alternation, stage 1 once per particle, stages 2-4 against every template, the template whose

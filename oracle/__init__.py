@@ -60,6 +60,10 @@ def _lib():
             "orc_align_batch": [_fp, ctypes.c_int64, _fp, _dp, ctypes.c_int, _ip, _dp, _dp, ctypes.c_int],
             "orc_align_batch_multi": [_fp, ctypes.c_int64, _fp, ctypes.c_int, _dp, ctypes.c_int, _ip, _dp, _dp,
                                       ctypes.c_int],
+            "orc_ball_tables": [ctypes.c_int, ctypes.c_int, _d, _ip, _dp],
+            "orc_sph_bessel": [ctypes.c_int, _d],
+            "orc_ball_transform": [_dp, ctypes.c_int, ctypes.c_int, _d, _dp],
+            "orc_corr_ball_full": [_dp, _dp, ctypes.c_int, ctypes.c_int, _d, ctypes.c_int, _dp],
             "orc_reconstruct": [_fp, ctypes.c_int64, ctypes.c_int, _dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int64, _dp, _ip],
         }
@@ -68,6 +72,8 @@ def _lib():
         lib.orc_find_maxima.restype = ctypes.c_int
         lib.orc_energy.restype = ctypes.c_double
         lib.orc_upsampled_corr_at.restype = ctypes.c_double
+        lib.orc_ball_tables.restype = ctypes.c_int
+        lib.orc_sph_bessel.restype = ctypes.c_double
         _LIB = lib
     return _LIB
 
@@ -320,11 +326,7 @@ def align_batch(vols, ref, params, H=None, nthreads=0):
     ref = np.ascontiguousarray(ref, np.float32)
     B, N = vols.shape[0], vols.shape[-1]
     bands = list(params["bands"])
-    ip = np.zeros(26, np.int32)
-    ip[0:6] = [params["L"], params.get("qover", 2), params["L0"], params.get("K", 2), params["ncand"], len(bands)]
-    ip[6:6 + len(bands)] = bands
-    ip[22:26] = [params.get("iters", 1), params.get("T", 1), params.get("W", 0), params.get("ups", 0)]
-    dp = np.array([params.get("tol_grad", 0.0), params.get("tol_step", 0.0), params.get("tol_obj", 0.0)])
+    ip, dp = _param_arrays(params)
     Hc = None if H is None else _c128(H)
     poses = np.zeros((B, 8))
     _lib().orc_align_batch(_p(vols, _fp), B, _p(ref, _fp), None if Hc is None else _p(Hc.view(np.float64)), N,
@@ -334,11 +336,13 @@ def align_batch(vols, ref, params, H=None, nthreads=0):
 
 def _param_arrays(params):
     bands = list(params["bands"])
-    ip = np.zeros(26, np.int32)
+    ip = np.zeros(27, np.int32)
     ip[0:6] = [params["L"], params.get("qover", 2), params["L0"], params.get("K", 2), params["ncand"], len(bands)]
     ip[6:6 + len(bands)] = bands
-    ip[22:26] = [params.get("iters", 1), params.get("T", 1), params.get("W", 0), params.get("ups", 0)]
-    dp = np.array([params.get("tol_grad", 0.0), params.get("tol_step", 0.0), params.get("tol_obj", 0.0)])
+    ip[22:27] = [params.get("iters", 1), params.get("T", 1), params.get("W", 0), params.get("ups", 0),
+                 params.get("radial", 0)]
+    dp = np.array([params.get("tol_grad", 0.0), params.get("tol_step", 0.0), params.get("tol_obj", 0.0),
+                   params.get("lam", 0.0)])
     return ip, dp
 
 
@@ -364,3 +368,35 @@ def reconstruct(vols, poses, n_classes=1, class_col=-1, first_index=0):
     _lib().orc_reconstruct(_p(vols, _fp), B, N, _p(poses), poses.shape[1], class_col, n_classes, first_index,
                            _p(sums), _p(counts, _ip))
     return sums, counts
+
+
+# ---------------------------------------------------------------- ball-harmonic radial basis
+def ball_tables(L, R, lam=0.0):
+    """-> (K [L+1] = |K_l|, Bt [L+1, Kmax, R] radial weights (1/R) rho_i^2 c_lk j_l(lambda_lk rho_i))."""
+    K = np.zeros(L + 1, np.int32)
+    Kmax = _lib().orc_ball_tables(L, R, lam, _p(K, _ip), None)
+    Bt = np.zeros((L + 1, Kmax, R))
+    _lib().orc_ball_tables(L, R, lam, _p(K, _ip), _p(Bt))
+    return K, Bt
+
+
+def sph_bessel(l, x):
+    return _lib().orc_sph_bessel(l, float(x))
+
+
+def ball_transform(F, lam=0.0):
+    F = _c128(F)
+    L = int(round((np.sqrt(8 * F.shape[0] + 1) - 3) / 2))
+    R = F.shape[1]
+    K, _ = ball_tables(L, R, lam)
+    Fb = np.zeros((F.shape[0], int(K.max())), np.complex128)
+    _lib().orc_ball_transform(_p(F.view(np.float64)), L, R, lam, _p(Fb.view(np.float64)))
+    return Fb
+
+
+def corr_ball_full(Fb, Hb, R, Lc, lam=0.0):
+    Fb, Hb = _c128(Fb), _c128(Hb)
+    L = int(round((np.sqrt(8 * Fb.shape[0] + 1) - 3) / 2))
+    M = np.zeros(full_size(Lc), np.complex128)
+    _lib().orc_corr_ball_full(_p(Fb.view(np.float64)), _p(Hb.view(np.float64)), L, R, lam, Lc, _p(M.view(np.float64)))
+    return M

@@ -726,9 +726,104 @@ void translation_upsampled(const float* vol, const float* ref, int N, const doub
   *peak = bv;
 }
 
+/* ---------------- ball-harmonic radial basis (App. A.1; reading C30) ----------------
+   j_l(x) = (1/2) (-i)^l int_{-1}^{1} e^{i x t} P_l(t) dt (the plane-wave integral, by Gauss-Legendre quadrature
+   with n_q >= x/2 + l + 40 nodes: exact to rounding for this entire integrand); lambda_lk the k-th positive root of
+   j_l (sign changes on a 0.05 grid, then bisection); c_lk = sqrt(2)/|j_{l+1}(lambda_lk)|;
+   f^_klm = sum_i (1/R) rho_i^2 c_lk j_l(lambda_lk rho_i) f_lm(r_i), rho_i = (i - 1/2)/R;
+   M^l_mn = sum_{k in K_l} f^_klm conj(h^_kln). */
+struct SphBessel {
+  int L, nq;
+  vector<double> t, w, P;  /* nodes, weights, P[l * nq + q] = P_l(t_q) */
+  SphBessel(int L_, double xmax) : L(L_) {
+    nq = (int)(xmax / 2 + L + 40);
+    gauss_legendre(nq, t, w);
+    P.assign((size_t)(L + 2) * nq, 0.0);
+    for (int q = 0; q < nq; ++q) {
+      double p0 = 1.0, p1 = t[q];
+      P[q] = 1.0;
+      if (L + 1 >= 1) P[nq + q] = p1;
+      for (int l = 2; l <= L + 1; ++l) {
+        const double p2 = ((2.0 * l - 1.0) * t[q] * p1 - (l - 1.0) * p0) / l;
+        P[(size_t)l * nq + q] = p2;
+        p0 = p1;
+        p1 = p2;
+      }
+    }
+  }
+  double operator()(int l, double x) const {
+    cd s(0, 0);
+    for (int q = 0; q < nq; ++q) s += w[q] * P[(size_t)l * nq + q] * std::polar(1.0, x * t[q]);
+    cd f(1, 0);
+    for (int k = 0; k < l % 4; ++k) f *= cd(0, -1);
+    return 0.5 * std::real(f * s);
+  }
+};
+
+void ball_tables(int L, int R, double lam, vector<int>& K, vector<vector<double>>& Bt) {
+  if (lam <= 0) lam = PI * (R - 0.5);
+  SphBessel jl(L, lam + 1.0);
+  K.assign(L + 1, 0);
+  Bt.assign(L + 1, vector<double>());
+  for (int l = 0; l <= L; ++l) {
+    vector<double> roots;
+    double x0 = std::max(0.5, (double)l), f0 = jl(l, x0);
+    for (double x1 = x0 + 0.05; x0 <= lam; x1 += 0.05) {
+      const double f1 = jl(l, x1);
+      if (f0 == 0.0 || f0 * f1 < 0.0) {
+        double a = x0, b = x1, fa = f0;
+        for (int it = 0; it < 200 && b - a > 1e-15 * b; ++it) {
+          const double m = 0.5 * (a + b), fm = jl(l, m);
+          if ((fm < 0) == (fa < 0)) { a = m; fa = fm; } else { b = m; }
+        }
+        if (0.5 * (a + b) <= lam) roots.push_back(0.5 * (a + b));
+      }
+      x0 = x1;
+      f0 = f1;
+    }
+    if ((int)roots.size() > R) roots.resize(R);
+    K[l] = (int)roots.size();
+    Bt[l].assign((size_t)K[l] * R, 0.0);
+    for (int k = 0; k < K[l]; ++k) {
+      const double c = std::sqrt(2.0) / std::fabs(jl(l + 1, roots[k]));
+      for (int i = 0; i < R; ++i) {
+        const double rho = (i + 0.5) / R;
+        Bt[l][(size_t)k * R + i] = rho * rho / R * c * jl(l, roots[k] * rho);
+      }
+    }
+  }
+}
+
+/* F complex [ncoef(L)][R] -> Fb complex [ncoef(L)][Kmax] */
+void ball_transform(const double* F, int L, int R, const vector<int>& K, const vector<vector<double>>& Bt, int Kmax,
+                    double* Fb) {
+  const cd* f = reinterpret_cast<const cd*>(F);
+  cd* o = reinterpret_cast<cd*>(Fb);
+  for (int l = 0; l <= L; ++l)
+    for (int m = 0; m <= l; ++m)
+      for (int k = 0; k < Kmax; ++k) {
+        cd s(0, 0);
+        if (k < K[l])
+          for (int i = 0; i < R; ++i) s += Bt[l][(size_t)k * R + i] * f[(size_t)lm_index(l, m) * R + i];
+        o[(size_t)lm_index(l, m) * Kmax + k] = s;
+      }
+}
+
+/* full-plane M^l_mn = sum_{k < K_l} f^_klm conj(h^_kln), all m, n (reality of f, h: reading C3) */
+void corr_ball_full(const double* Fb, const double* Hb, const vector<int>& K, int Kmax, int Lc, double* Mout) {
+  cd* M = reinterpret_cast<cd*>(Mout);
+  for (int l = 0; l <= Lc; ++l)
+    for (int m = -l; m <= l; ++m)
+      for (int n = -l; n <= l; ++n) {
+        cd s(0, 0);
+        for (int k = 0; k < K[l]; ++k) s += coef(Fb, Kmax, l, m, k) * std::conj(coef(Hb, Kmax, l, n, k));
+        M[full_offset(l) + (m + l) * (2 * l + 1) + (n + l)] = s;
+      }
+}
+
 struct Params {
-  int L, qover, L0, K, ncand, nbands, bands[16], iters, T, W, ups;
-  double tol_grad, tol_step, tol_obj;
+  int L, qover, L0, K, ncand, nbands, bands[16], iters, T, W, ups, radial;
+  double tol_grad, tol_step, tol_obj, lambda;
 };
 
 /* whole path for one particle: App. C alternation around Algorithm 1 (reading C19). */
@@ -747,7 +842,20 @@ void align_one(const float* vol, const float* ref, const double* H, int N, const
   for (int tau = 0; tau < std::max(1, p.T); ++tau) {
     double centre[3] = {c + t[0], c + t[1], c + t[2]};
     sh_analysis(VolSampler{vol, N}, N, p.L, p.qover, centre, F.data());
-    corr_full(F.data(), H, R, p.L, M.data());
+    if (p.radial == 1) {
+      /* M from the ball-harmonic coefficients (tables per call: plain, slow) */
+      vector<int> K;
+      vector<vector<double>> Bt;
+      ball_tables(p.L, R, p.lambda, K, Bt);
+      int Kmax = 0;
+      for (int k : K) Kmax = std::max(Kmax, k);
+      vector<double> Fb((size_t)2 * ncoef(p.L) * Kmax), Hb((size_t)2 * ncoef(p.L) * Kmax);
+      ball_transform(F.data(), p.L, R, K, Bt, Kmax, Fb.data());
+      ball_transform(H, p.L, R, K, Bt, Kmax, Hb.data());
+      corr_ball_full(Fb.data(), Hb.data(), K, Kmax, p.L, M.data());
+    } else {
+      corr_full(F.data(), H, R, p.L, M.data());
+    }
     grid_eval(M.data(), p.L0, p.K, grid.data());
     find_maxima(grid.data(), nb, na, ng, p.ncand, idx.data(), sc.data());
     for (int n = 0; n < p.ncand; ++n) {
@@ -1006,8 +1114,9 @@ double orc_energy(const double* F, const double* H, int Lc, int R) {
       }
   return std::sqrt(ef * eh);
 }
-/* params: ints [L, qover, L0, K, ncand, nbands, bands[16], iters, T, W, ups]; dbl [tol_grad, tol_step, tol_obj]
-   (ups = 0: parabolic subpixel; ups = kappa > 0: the upsampled DFT of translation_upsampled)
+/* params: ints [L, qover, L0, K, ncand, nbands, bands[16], iters, T, W, ups, radial];
+   dbl [tol_grad, tol_step, tol_obj, lambda]  (ups = 0: parabolic subpixel; ups = kappa > 0: the upsampled DFT of
+   translation_upsampled; radial = 1: the ball-harmonic basis with cutoff lambda)
    H: complex [ncoef(L)][R] reference coefficients (NULL -> analysed from ref at t = 0).
    poses [B][8] = {alpha, beta, gamma, tx, ty, tz, score, best}. */
 void orc_align_batch(const float* vols, int64_t B, const float* ref, const double* H, int N, const int* ip,
@@ -1015,8 +1124,8 @@ void orc_align_batch(const float* vols, int64_t B, const float* ref, const doubl
   Params p;
   p.L = ip[0]; p.qover = ip[1]; p.L0 = ip[2]; p.K = ip[3]; p.ncand = ip[4]; p.nbands = ip[5];
   for (int k = 0; k < 16; ++k) p.bands[k] = ip[6 + k];
-  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24]; p.ups = ip[25];
-  p.tol_grad = dp[0]; p.tol_step = dp[1]; p.tol_obj = dp[2];
+  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24]; p.ups = ip[25]; p.radial = ip[26];
+  p.tol_grad = dp[0]; p.tol_step = dp[1]; p.tol_obj = dp[2]; p.lambda = dp[3];
   const int R = N / 2;
   vector<double> Hl;
   if (!H) {
@@ -1038,8 +1147,8 @@ void orc_align_batch_multi(const float* vols, int64_t B, const float* refs, int 
   Params p;
   p.L = ip[0]; p.qover = ip[1]; p.L0 = ip[2]; p.K = ip[3]; p.ncand = ip[4]; p.nbands = ip[5];
   for (int k = 0; k < 16; ++k) p.bands[k] = ip[6 + k];
-  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24]; p.ups = ip[25];
-  p.tol_grad = dp[0]; p.tol_step = dp[1]; p.tol_obj = dp[2];
+  p.iters = ip[22]; p.T = ip[23]; p.W = ip[24]; p.ups = ip[25]; p.radial = 0;
+  p.tol_grad = dp[0]; p.tol_step = dp[1]; p.tol_obj = dp[2]; p.lambda = 0;
   const int R = N / 2;
   const size_t n3 = (size_t)N * N * N, hsz = (size_t)2 * ncoef(p.L) * R;
   vector<double> Hl;
@@ -1057,6 +1166,39 @@ void orc_align_batch_multi(const float* vols, int64_t B, const float* refs, int 
 void orc_reconstruct(const float* vols, int64_t B, int N, const double* poses, int stride, int ccol, int ncls,
                      int64_t first, double* sums, int* counts) {
   reconstruct(vols, B, N, poses, stride, ccol, ncls, first, sums, counts);
+}
+
+/* ball basis: K [L+1] (|K_l|), returns Kmax; Bt [L+1][Kmax][R] if not NULL */
+int orc_ball_tables(int L, int R, double lambda, int* K, double* Bt) {
+  vector<int> Kv;
+  vector<vector<double>> Bv;
+  ball_tables(L, R, lambda, Kv, Bv);
+  int Kmax = 0;
+  for (int k : Kv) Kmax = std::max(Kmax, k);
+  for (int l = 0; l <= L; ++l) {
+    K[l] = Kv[l];
+    if (Bt)
+      for (int k = 0; k < Kmax; ++k)
+        for (int i = 0; i < R; ++i) Bt[((size_t)l * Kmax + k) * R + i] = k < Kv[l] ? Bv[l][(size_t)k * R + i] : 0.0;
+  }
+  return Kmax;
+}
+double orc_sph_bessel(int l, double x) { return SphBessel(l, x + 1.0)(l, x); }
+void orc_ball_transform(const double* F, int L, int R, double lambda, double* Fb) {
+  vector<int> K;
+  vector<vector<double>> Bt;
+  ball_tables(L, R, lambda, K, Bt);
+  int Kmax = 0;
+  for (int k : K) Kmax = std::max(Kmax, k);
+  ball_transform(F, L, R, K, Bt, Kmax, Fb);
+}
+void orc_corr_ball_full(const double* Fb, const double* Hb, int L, int R, double lambda, int Lc, double* M) {
+  vector<int> K;
+  vector<vector<double>> Bt;
+  ball_tables(L, R, lambda, K, Bt);
+  int Kmax = 0;
+  for (int k : K) Kmax = std::max(Kmax, k);
+  corr_ball_full(Fb, Hb, K, Kmax, Lc, M);
 }
 
 }  // extern "C"

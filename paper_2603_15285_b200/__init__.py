@@ -44,8 +44,9 @@ class _Config(ctypes.Structure):
 class _Params(ctypes.Structure):
     _fields_ = [("n_bands", ctypes.c_int32), ("bands", ctypes.c_int32 * 16), ("newton_iters", ctypes.c_int32),
                 ("n_cand", ctypes.c_int32), ("oversample", ctypes.c_int32), ("n_alternations", ctypes.c_int32),
-                ("shift_window", ctypes.c_int32), ("upsample", ctypes.c_int32), ("tol_grad", ctypes.c_double), ("tol_step", ctypes.c_double),
-                ("tol_obj", ctypes.c_double)]
+                ("shift_window", ctypes.c_int32), ("upsample", ctypes.c_int32), ("radial", ctypes.c_int32),
+                ("tol_grad", ctypes.c_double), ("tol_step", ctypes.c_double), ("tol_obj", ctypes.c_double),
+                ("ball_lambda", ctypes.c_double)]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -64,6 +65,9 @@ _SIGS = {
     "matcha_translation_update": ([_H, _vp, _i64, _vp, _vp, _i32, _i32, _vp, _vp, _vp], ctypes.c_int),
     "matcha_align_batch": ([_H, _vp, _i64, _vp, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_align_batch_host": ([_H, _vp, _i64, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
+    "matcha_ball_kmax": ([_H, ctypes.c_double, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int32),
+    "matcha_ball_transform": ([_H, _vp, _i64, ctypes.c_double, _vp, _vp], ctypes.c_int),
+    "matcha_corr_coeffs_ball": ([_H, _vp, _vp, _i64, _i32, ctypes.c_double, _vp, _vp], ctypes.c_int),
     "matcha_align_multi": ([_H, _vp, _i64, _vp, _i32, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_reconstruct": ([_H, _vp, _i64, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _vp], ctypes.c_int),
     "matcha_get_status": ([_H, _vp], ctypes.c_int),
@@ -106,9 +110,11 @@ class Params:
     n_alternations: int = 1
     shift_window: int = 0
     upsample: int = 0          # 0: parabolic subpixel; kappa: upsampled-DFT subpixel
+    radial: int = 0            # 0: shells; 1: ball harmonics with cutoff ball_lambda
     tol_grad: float = 0.0
     tol_step: float = 0.0
     tol_obj: float = 0.0
+    ball_lambda: float = 0.0   # <= 0: pi (R - 1/2)
 
     def c(self) -> _Params:
         p = _Params()
@@ -118,6 +124,7 @@ class Params:
         p.newton_iters, p.n_cand, p.oversample = self.newton_iters, self.n_cand, self.oversample
         p.n_alternations, p.shift_window, p.upsample = self.n_alternations, self.shift_window, self.upsample
         p.tol_grad, p.tol_step, p.tol_obj = self.tol_grad, self.tol_step, self.tol_obj
+        p.radial, p.ball_lambda = self.radial, self.ball_lambda
         return p
 
 
@@ -291,6 +298,40 @@ class Handle:
         p = params.c()
         self._check(_lib.matcha_align_batch(self._h, _ptr(vols), B, _ptr(ref), _ptr(ref_coeffs), ctypes.byref(p),
                                             _ptr(out), _stream()))
+        return out
+
+    # ---------------------------------------------------------------- ball-harmonic radial basis
+    def ball_kmax(self, lam: float = 0.0):
+        """-> (Kmax, [|K_l| for l = 0..L_max]) of the ball basis with cutoff lam (<= 0: pi (R - 1/2))."""
+        K = (ctypes.c_int32 * (self.L_max + 1))()
+        km = int(_lib.matcha_ball_kmax(self._h, lam, K))
+        if km < 0:
+            self._check(-1)
+        return km, list(K)
+
+    def ball_transform(self, F: torch.Tensor, lam: float = 0.0, out=None) -> torch.Tensor:
+        """Shell coefficients [B, ncoef, R] -> ball coefficients [B, ncoef, Kmax] (App. A.1)."""
+        B = F.shape[0]
+        self._arg(F, "F", self.cplx, (B, ncoef(self.L_max), self.R))
+        km, _ = self.ball_kmax(lam)
+        if out is None:
+            out = torch.empty((B, ncoef(self.L_max), km), dtype=self.cplx, device=self.device)
+        self._arg(out, "out", self.cplx, (B, ncoef(self.L_max), km))
+        self._check(_lib.matcha_ball_transform(self._h, _ptr(F), B, lam, _ptr(out), _stream()))
+        return out
+
+    def corr_coeffs_ball(self, fb: torch.Tensor, hb: torch.Tensor, L: Optional[int] = None, lam: float = 0.0,
+                         out=None) -> torch.Tensor:
+        """M^l_mn = sum_{k in K_l} f^_klm conj(h^_kln) -> [B, Mh(L)] half plane (rank <= |K_l|)."""
+        L = self.L_max if L is None else L
+        km, _ = self.ball_kmax(lam)
+        B = fb.shape[0]
+        self._arg(fb, "fb", self.cplx, (B, ncoef(self.L_max), km))
+        self._arg(hb, "hb", self.cplx, (ncoef(self.L_max), km))
+        if out is None:
+            out = torch.empty((B, corr_count(L)), dtype=self.cplx, device=self.device)
+        self._arg(out, "out", self.cplx, (B, corr_count(L)))
+        self._check(_lib.matcha_corr_coeffs_ball(self._h, _ptr(fb), _ptr(hb), B, L, lam, _ptr(out), _stream()))
         return out
 
     def align_multi(self, vols: torch.Tensor, refs: Optional[torch.Tensor], params: Params,

@@ -173,6 +173,15 @@ template <typename T>
 cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
                              void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s);
 
+// ball-harmonic radial transform and the correlation tensor from its rank-|K_l| factors (k_ball.cu);
+// Bt real [Lmax+1][Kmax][R] radial table, Kl int [Lmax+1]; ball coefficients complex [B][ncoef(Lmax)][Kmax]
+template <typename T>
+cudaError_t launch_ball_transform(const cplx_t<T>* F, int64_t B, int Lmax, int R, const T* Bt, const int* Kl, int Kmax,
+                                  cplx_t<T>* out, cudaStream_t s);
+template <typename T>
+cudaError_t launch_corr_ball(const cplx_t<T>* Fb, const cplx_t<T>* Hb, int64_t B, int L, int Lmax, const int* Kl,
+                             int Kmax, cplx_t<T>* M, cudaStream_t s);
+
 // half-map sums of the aligned particles per class (k_recon.cu); Rt: workspace real [B][12]
 template <typename T>
 cudaError_t launch_reconstruct(const float* vols, int64_t B, int N, const T* poses, int pstride, int ccol, int ncls,

@@ -79,6 +79,14 @@ struct matcha_ctx {
   int* ws_tsel = nullptr;    // int [mb] selected template per particle
   void* ws_Rt = nullptr;     // real [n][12] pose matrices of matcha_reconstruct
   int64_t ws_Rt_n = 0;
+  // ball-harmonic radial basis: tables for ball_lambda, workspaces
+  double ball_lambda = -1;
+  int ball_kmax = 0;
+  std::vector<int> ball_K;   // |K_l|, l = 0..L
+  void* d_ballB = nullptr;   // real [L+1][Kmax][R]
+  int* d_ballK = nullptr;    // int [L+1]
+  void* ws_Fb = nullptr;     // complex [mb][ncoef][R] (Kmax <= R) particle ball coefficients
+  void* ws_Hb = nullptr;     // complex [ncoef][R] reference ball coefficients
   void* ws_euler1 = nullptr; // real [mb][3]
   // per-stage event tracing
   bool prof = false;
@@ -166,6 +174,64 @@ void plm_table(int L, double x, std::vector<double>& out) {
   }
 }
 
+// spherical Bessel j_0..j_L at x by Miller's downward recurrence j_{n-1} = (2n+1)/x j_n - j_{n+1}, normalised by
+// j_0(x) = sin x / x (stable for every x > 0; rescaled against overflow)
+void sph_bessel_all(int L, double x, std::vector<double>& j) {
+  j.assign(L + 2, 0.0);
+  if (x == 0.0) {
+    j[0] = 1.0;
+    return;
+  }
+  const int start = (int)std::max<double>(L + 2, x) + 60;
+  std::vector<double> t(start + 2, 0.0);
+  double jp = 0.0, jc = 1e-300;
+  for (int n = start; n >= 1; --n) {
+    const double jm = (2.0 * n + 1.0) / x * jc - jp;
+    jp = jc;
+    jc = jm;
+    if (n - 1 <= L + 1) t[n - 1] = jc;
+    if (std::fabs(jc) > 1e250) {
+      jc *= 1e-250;
+      jp *= 1e-250;
+      for (int q = n - 1; q <= std::min(start, L + 1); ++q) t[q] *= 1e-250;
+    }
+  }
+  const double s = std::sin(x) / x / t[0];
+  for (int n = 0; n <= L + 1; ++n) j[n] = t[n] * s;
+}
+
+double sph_bessel(int l, double x) {
+  std::vector<double> j;
+  sph_bessel_all(l, x, j);
+  return j[l];
+}
+
+// positive roots of j_l below lam: sign changes on a 0.05 grid from x = l (the first root exceeds l), bisection
+std::vector<double> sph_bessel_roots(int l, double lam) {
+  std::vector<double> r;
+  double x0 = std::max(0.5, (double)l), f0 = sph_bessel(l, x0);
+  for (double x1 = x0 + 0.05; x0 <= lam; x1 += 0.05) {
+    const double f1 = sph_bessel(l, x1);
+    if (f0 == 0.0 || f0 * f1 < 0.0) {
+      double a = x0, b = x1, fa = f0;
+      for (int it = 0; it < 100 && b - a > 1e-15 * b; ++it) {
+        const double m = 0.5 * (a + b), fm = sph_bessel(l, m);
+        if ((fm < 0) == (fa < 0)) {
+          a = m;
+          fa = fm;
+        } else {
+          b = m;
+        }
+      }
+      const double root = 0.5 * (a + b);
+      if (root <= lam) r.push_back(root);
+    }
+    x0 = x1;
+    f0 = f1;
+  }
+  return r;
+}
+
 template <typename T> void upload(void** dst, const std::vector<double>& src, cudaError_t& e) {
   std::vector<T> v(src.begin(), src.end());
   if (e == cudaSuccess) e = cudaMalloc(dst, sizeof(T) * std::max<size_t>(1, v.size()));
@@ -209,6 +275,7 @@ bool valid_params(const matcha_params_t* p, int LM, std::string& why) {
   if (p->oversample < 1 || p->oversample > 8) { why = "oversample must be in [1,8]"; return false; }
   if (p->n_alternations < 1 || p->n_alternations > 64) { why = "n_alternations must be in [1,64]"; return false; }
   if (p->upsample < 0) { why = "upsample must be >= 0"; return false; }
+  if (p->radial != 0 && p->radial != 1) { why = "radial must be 0 (shells) or 1 (ball harmonics)"; return false; }
   return true;
 }
 
@@ -437,6 +504,72 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
   return MATCHA_OK;
 }
 
+// ball-harmonic tables for Lambda (reading C30: Lambda <= 0 -> pi (R - 1/2), the radial Nyquist of the R midpoint
+// shells of the unit ball): B_l[k][i] = (1/R) rho_i^2 c_lk j_l(lambda_lk rho_i), c_lk = sqrt(2)/|j_{l+1}(lambda_lk)|
+static matcha_status_t ball_prepare(matcha_handle_t h, double lam) {
+  if (lam <= 0) lam = kPi * (h->R - 0.5);
+  if (lam == h->ball_lambda) return MATCHA_OK;
+  const int L = h->L, R = h->R;
+  std::vector<std::vector<double>> roots(L + 1);
+  int kmax = 0;
+  for (int l = 0; l <= L; ++l) {
+    roots[l] = sph_bessel_roots(l, lam);
+    if ((int)roots[l].size() > R) roots[l].resize(R);
+    kmax = std::max<int>(kmax, (int)roots[l].size());
+  }
+  if (kmax == 0) return fail(h, MATCHA_ERR_INVALID_ARG, "ball basis: Lambda below the first root of j_0");
+  std::vector<double> tab((size_t)(L + 1) * kmax * R, 0.0), jv;
+  std::vector<int> K(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    K[l] = (int)roots[l].size();
+    for (int k = 0; k < K[l]; ++k) {
+      const double lk = roots[l][k];
+      sph_bessel_all(l + 1, lk, jv);
+      const double c = std::sqrt(2.0) / std::fabs(jv[l + 1]);
+      for (int i = 0; i < R; ++i) {
+        const double rho = (i + 0.5) / R;
+        tab[((size_t)l * kmax + k) * R + i] = rho * rho / R * c * sph_bessel(l, lk * rho);
+      }
+    }
+  }
+  if (h->d_ballB) cudaFree(h->d_ballB);
+  if (h->d_ballK) cudaFree(h->d_ballK);
+  h->d_ballB = nullptr;
+  h->d_ballK = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (h->fp64) upload<double>(&h->d_ballB, tab, e);
+  else upload<float>(&h->d_ballB, tab, e);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_ballK, sizeof(int) * (L + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_ballK, K.data(), sizeof(int) * (L + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(h, e, "ball basis tables");
+  h->ball_K = K;
+  h->ball_kmax = kmax;
+  h->ball_lambda = lam;
+  return MATCHA_OK;
+}
+
+static matcha_status_t ball_transform(matcha_handle_t h, const void* F, int64_t B, void* out, cudaStream_t s) {
+  cudaError_t e = h->fp64 ? launch_ball_transform<double>((const double2*)F, B, h->L, h->R, (const double*)h->d_ballB,
+                                                          h->d_ballK, h->ball_kmax, (double2*)out, s)
+                          : launch_ball_transform<float>((const float2*)F, B, h->L, h->R, (const float*)h->d_ballB,
+                                                         h->d_ballK, h->ball_kmax, (float2*)out, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "ball_transform launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
+static matcha_status_t corr_ball(matcha_handle_t h, const void* Fb, const void* Hb, int64_t B, int L, void* M,
+                                 cudaStream_t s) {
+  ProfScope ps(h, 1, s);
+  cudaError_t e = h->fp64 ? launch_corr_ball<double>((const double2*)Fb, (const double2*)Hb, B, L, h->L, h->d_ballK,
+                                                     h->ball_kmax, (double2*)M, s)
+                          : launch_corr_ball<float>((const float2*)Fb, (const float2*)Hb, B, L, h->L, h->d_ballK,
+                                                    h->ball_kmax, (float2*)M, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "corr_ball launch");
+  h->launches += B > 0;
+  return MATCHA_OK;
+}
+
 // template norms live behind the per-particle template indices in ws_tsel (8-byte aligned: max_batch ints padded)
 static double* tnorm(matcha_handle_t h) {
   return (double*)((char*)h->ws_tsel + ((sizeof(int) * h->cfg.max_batch + 7) / 8) * 8);
@@ -462,6 +595,18 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
     if (st != MATCHA_OK) return st;
     H = dst;
   }
+  const bool ball = p->radial == 1;  // the correlation tensor from ball-harmonic coefficients
+  if (ball) {
+    if ((st = ball_prepare(h, p->ball_lambda)) != MATCHA_OK) return st;
+    const size_t fbb = (size_t)h->cfg.max_batch * h->ncf * h->R * 2 * h->rsz;
+    if (!h->ws_Fb && cudaMalloc(&h->ws_Fb, fbb) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "align: ball coefficient allocation failed");
+    if (!h->ws_Hb && cudaMalloc(&h->ws_Hb, hstride * kMaxTemplates) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "align: reference ball coefficient allocation failed");
+    // reference ball coefficients (Kmax <= R: the [nt][ncoef][Kmax] block fits the [nt][ncoef][R] workspace)
+    if ((st = ball_transform(h, H, nt, h->ws_Hb, s)) != MATCHA_OK) return st;
+  }
+  const int64_t hbstride = (int64_t)h->ncf * h->ball_kmax * 2 * h->rsz;
   const bool direct = nt == 1 && pstride == 8;  // gather straight into the caller's poses (bitwise as before)
   if (!direct) {
     const size_t cb = (size_t)h->rsz * 8 * h->cfg.max_batch * kMaxTemplates;
@@ -494,9 +639,12 @@ static matcha_status_t align_device(matcha_handle_t h, const float* vols, int64_
       }
       if (e != cudaSuccess) return cuda_fail(h, e, "align: sh_analysis");
       h->launches++;
+      if (ball && (st = ball_transform(h, h->ws_F, nb, h->ws_Fb, s)) != MATCHA_OK) return st;
       for (int k = 0; k < nt; ++k) {
         const void* Hk = (const char*)H + k * hstride;
-        if ((st = matcha_corr_coeffs(h, h->ws_F, Hk, nb, LJ, h->ws_M, s)) != MATCHA_OK) return st;
+        if (ball) st = corr_ball(h, h->ws_Fb, (const char*)h->ws_Hb + k * hbstride, nb, LJ, h->ws_M, s);
+        else st = matcha_corr_coeffs(h, h->ws_F, Hk, nb, LJ, h->ws_M, s);
+        if (st != MATCHA_OK) return st;
         if ((st = matcha_so3_search(h, h->ws_M, LJ, nb, L0, p->oversample, p->n_cand, h->ws_euler, h->ws_score,
                                     h->ws_idx, s)) != MATCHA_OK)
           return st;
@@ -695,7 +843,7 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
     if (h->tex_ref[k]) cudaDestroyTextureObject(h->tex_ref[k]);
   for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad,
                   (void*)h->ws_tint, h->ws_ups, h->ws_grid, (void*)h->d_tex, h->ws_Hs, h->ws_cand,
-                  (void*)h->ws_tsel, h->ws_Rt})
+                  (void*)h->ws_tsel, h->ws_Rt, h->d_ballB, (void*)h->d_ballK, h->ws_Fb, h->ws_Hb})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -977,6 +1125,34 @@ MATCHA_API matcha_status_t matcha_reconstruct(matcha_handle_t h, const float* vo
   if (e != cudaSuccess) return cuda_fail(h, e, "reconstruct launch");
   h->launches += B > 0 ? 3 : 2;
   return MATCHA_OK;
+}
+
+MATCHA_API int32_t matcha_ball_kmax(matcha_handle_t h, double lambda, int32_t* K_host) {
+  if (!h) return -1;
+  if (ball_prepare(h, lambda) != MATCHA_OK) return -1;
+  if (K_host)
+    for (int l = 0; l <= h->L; ++l) K_host[l] = h->ball_K[l];
+  return h->ball_kmax;
+}
+
+MATCHA_API matcha_status_t matcha_ball_transform(matcha_handle_t h, const void* F, int64_t B, double lambda,
+                                                 void* Fball, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!F || !Fball))) return fail(h, MATCHA_ERR_INVALID_ARG, "ball_transform: bad arguments");
+  matcha_status_t st = ball_prepare(h, lambda);
+  if (st != MATCHA_OK) return st;
+  return ball_transform(h, F, B, Fball, (cudaStream_t)stream);
+}
+
+MATCHA_API matcha_status_t matcha_corr_coeffs_ball(matcha_handle_t h, const void* fball, const void* hball, int64_t B,
+                                                   int32_t L, double lambda, void* M, void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || (B > 0 && (!fball || !hball || !M)))
+    return fail(h, MATCHA_ERR_INVALID_ARG, "corr_coeffs_ball: bad arguments");
+  if (L < 0 || L > h->L) return fail(h, MATCHA_ERR_DEGREE, "corr_coeffs_ball: L > L_max");
+  matcha_status_t st = ball_prepare(h, lambda);
+  if (st != MATCHA_OK) return st;
+  return corr_ball(h, fball, hball, B, L, M, (cudaStream_t)stream);
 }
 
 MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const float* vols_host, int64_t B,

@@ -580,3 +580,48 @@ def test_reconstruct_parity(prec):
     assert np.array_equal(counts, co)
     bound = np.abs(b.vols).max() * B
     assert np.abs(sums - so).max() <= (1e-12 if prec == "fp64" else 1e-5) * bound, np.abs(sums - so).max() / bound
+
+
+# ------------------------------------------------------------------ ball-harmonic radial basis
+@pytest.mark.parametrize("N,L,lam", [(64, 32, 0.0), (32, 8, 20.0)])
+def test_ball_transform_and_corr_parity(N, L, lam, prec):
+    """matcha_ball_kmax / matcha_ball_transform / matcha_corr_coeffs_ball (App. A.1; reading C30) vs the
+    oracle (independent j_l by the plane-wave integral): identical truncation sets K_l, ball coefficients and the
+    rank-|K_l| correlation tensor elementwise."""
+    B = 3
+    b = gen.particles(N, B, 0.2, seed=72)
+    Fo = O.sh_analysis_batch(b.vols, L)
+    Ho = O.sh_analysis(b.ref, L)
+    h = handle(N, L, prec)
+    km, K = h.ball_kmax(lam)
+    Ko, _ = O.ball_tables(L, N // 2, lam)
+    assert K == Ko.tolist() and km == Ko.max()
+    fb = h.ball_transform(cuda(Fo, h.cplx), lam)
+    hb = h.ball_transform(cuda(Ho[None], h.cplx), lam)[0]
+    M = to_np(h.corr_coeffs_ball(fb, hb, L, lam))
+    fb = to_np(fb)
+    tol_b = 1e-12 if prec == "fp64" else 2e-6
+    Hbo = O.ball_transform(Ho.astype(np.complex64).astype(np.complex128) if prec == "fp32" else Ho, lam)
+    for p in range(B):
+        Fin = Fo[p].astype(np.complex64).astype(np.complex128) if prec == "fp32" else Fo[p]
+        Fbo = O.ball_transform(Fin, lam)
+        assert np.abs(fb[p] - Fbo).max() <= tol_b * np.abs(Fbo).max()
+        Mo = O.full_to_half(O.corr_ball_full(Fbo, Hbo, N // 2, L, lam), L)
+        assert np.abs(M[p] - Mo).max() <= (1e-11 if prec == "fp64" else 1e-5) * np.abs(Mo).max()
+
+
+def test_align_ball_basis_c2_shape():
+    """align_batch with radial = 1 (the paper's ball-harmonic representation with the default cutoff): c2 shape,
+    8 particles vs the oracle's ball path, and near the planted rotations."""
+    N, L, B = 64, 32, 8
+    b = gen.particles(N, B, 0.1, seed=73)
+    bands = [8, 12, 16, 24, 32]
+    h = handle(N, L, max_batch=B)
+    params = mt.Params(bands=bands, n_cand=10, oversample=2, radial=1)
+    poses = to_np(h.align_batch(cuda(b.vols), cuda(b.ref), params))
+    h.status()
+    po = O.align_batch(b.vols, b.ref, dict(L=L, qover=2, L0=8, K=2, ncand=10, bands=bands, iters=1, radial=1))
+    for p in range(B):
+        assert rot_err_deg(poses[p, :3], po[p, :3]) < TOL_ROT_DEG or abs(poses[p, 6] - po[p, 6]) <= 1e-4 * abs(po[p, 6])
+    errs = [O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) for p in range(B)]
+    assert np.median(errs) < 1.0

@@ -708,3 +708,74 @@ def test_align_multi_template_recovers_class_and_pose():
     # one template only: identical to align_batch
     po1 = O.align_batch_multi(vols[:1], refs[:1], P)
     assert np.allclose(po1[:, :8], O.align_batch(vols[:1], b.ref, P), rtol=0, atol=0)
+
+
+# ------------------------------------------------------------------ ball-harmonic radial basis
+def test_spherical_bessel_roots_and_normalisation():
+    """App. A.1: the oracle's j_l (plane-wave integral) against scipy, lambda_lk roots of j_l, |K_l|
+    non-increasing in l, and the radial functions c_lk j_l(lambda_lk rho) orthonormal on [0, 1] with weight rho^2."""
+    from scipy.integrate import quad
+    from scipy.special import spherical_jn
+    for l, x in [(0, 0.7), (3, 9.1), (17, 33.3), (30, 80.2)]:
+        assert abs(O.sph_bessel(l, x) - spherical_jn(l, x)) < 1e-13
+    R = 24
+    K, Bt = O.ball_tables(20, R, 0.75 * np.pi * R)
+    assert all(K[l] >= K[l + 1] for l in range(20))
+    rho = (np.arange(R) + 0.5) / R
+    for l in (0, 7, 20):
+        for k in range(min(3, K[l])):
+            # recover c j_l(lambda rho_i) from the table and locate lambda as a root of scipy's j_l
+            f = Bt[l, k] * R / rho ** 2
+            lam_guess = None
+            xs = np.linspace(max(0.5, l), 0.75 * np.pi * R + 1, 20000)
+            v = spherical_jn(l, xs)
+            from scipy.optimize import brentq
+            brk = np.nonzero(np.sign(v[:-1]) != np.sign(v[1:]))[0]
+            lam_guess = brentq(lambda x: spherical_jn(l, x), xs[brk[k]], xs[brk[k] + 1], xtol=1e-14)
+            c = np.sqrt(2) / abs(spherical_jn(l + 1, lam_guess))
+            assert np.abs(f - c * spherical_jn(l, lam_guess * rho)).max() < 1e-3 * c
+            nrm = quad(lambda r: (c * spherical_jn(l, lam_guess * r)) ** 2 * r * r, 0, 1, limit=200)[0]
+            assert abs(nrm - 1) < 2e-3
+
+
+def test_ball_transform_recovers_a_single_radial_mode():
+    """A shell profile f_lm(r_i) = c_lk j_l(lambda_lk rho_i) for one (l, m, k) maps to f^ ~ delta_k (midpoint rule
+    well inside the radial Nyquist: off-diagonal <= 2e-3)."""
+    R, L = 32, 6
+    lam = 0.75 * np.pi * R
+    K, Bt = O.ball_tables(L, R, lam)
+    rho = (np.arange(R) + 0.5) / R
+    for l, m, k in [(0, 0, 0), (3, 2, 4), (6, 5, 1)]:
+        prof = Bt[l, k] * R / rho ** 2  # c_lk j_l(lambda_lk rho_i)
+        F = np.zeros((O.ncoef(L), R), np.complex128)
+        F[l * (l + 1) // 2 + m] = prof * (1 + 0.5j)
+        Fb = O.ball_transform(F, lam)
+        row = Fb[l * (l + 1) // 2 + m, :K[l]] / (1 + 0.5j)
+        e = np.zeros(K[l])
+        e[k] = 1
+        assert np.abs(row - e).max() < 2e-3, np.abs(row - e).max()
+        others = np.delete(np.abs(Fb), l * (l + 1) // 2 + m, axis=0)
+        assert others.max() == 0
+
+
+def test_ball_correlation_rank_bound():
+    """rank(A_l) <= |K_l| for the ball-basis correlation tensor (singular values beyond |K_l| vanish
+    to rounding), and for f = h the blocks are Hermitian positive semidefinite."""
+    b = gen.particles(16, 1, 0.5, seed=71)
+    L = 7
+    F = O.sh_analysis(b.vols[0], L)
+    H = O.sh_analysis(b.ref, L)
+    lam = 2.0 * np.pi  # tight cutoff: |K_l| < 2l + 1 for l >= 2
+    K, _ = O.ball_tables(L, 8, lam)
+    Fb, Hb = O.ball_transform(F, lam), O.ball_transform(H, lam)
+    M = O.corr_ball_full(Fb, Hb, 8, L, lam)
+    Mhh = O.corr_ball_full(Hb, Hb, 8, L, lam)
+    for l in range(L + 1):
+        w = 2 * l + 1
+        blk = M[O.full_offset(l):O.full_offset(l) + w * w].reshape(w, w)
+        sv = np.linalg.svd(blk, compute_uv=False)
+        if K[l] < w:
+            assert sv[K[l]:].max() <= 1e-12 * max(sv[0], 1e-300), (l, K[l], sv)
+        hh = Mhh[O.full_offset(l):O.full_offset(l) + w * w].reshape(w, w)
+        assert np.abs(hh - hh.conj().T).max() <= 1e-12 * np.abs(hh).max()
+        assert np.linalg.eigvalsh(hh).min() >= -1e-12 * np.abs(hh).max()
