@@ -174,8 +174,9 @@ void plm_table(int L, double x, std::vector<double>& out) {
   }
 }
 
-// spherical Bessel j_0..j_L at x by Miller's downward recurrence j_{n-1} = (2n+1)/x j_n - j_{n+1}, normalised by
-// j_0(x) = sin x / x (stable for every x > 0; rescaled against overflow)
+// spherical Bessel j_0..j_L at x by Miller's downward recurrence j_{n-1} = (2n+1)/x j_n - j_{n+1}, normalised by the
+// identity sum_n (2n+1) j_n(x)^2 = 1 (robust near the zeros of j_0), the sign taken from the larger of
+// j_0 = sin x / x and j_1 = sin x / x^2 - cos x / x; rescaled against overflow
 void sph_bessel_all(int L, double x, std::vector<double>& j) {
   j.assign(L + 2, 0.0);
   if (x == 0.0) {
@@ -183,21 +184,25 @@ void sph_bessel_all(int L, double x, std::vector<double>& j) {
     return;
   }
   const int start = (int)std::max<double>(L + 2, x) + 60;
-  std::vector<double> t(start + 2, 0.0);
-  double jp = 0.0, jc = 1e-300;
+  std::vector<double> t(L + 2, 0.0);
+  double jp = 0.0, jc = 1e-30, sum = (2.0 * start + 1.0) * jc * jc;
   for (int n = start; n >= 1; --n) {
     const double jm = (2.0 * n + 1.0) / x * jc - jp;
     jp = jc;
     jc = jm;
+    sum += (2.0 * (n - 1) + 1.0) * jc * jc;
     if (n - 1 <= L + 1) t[n - 1] = jc;
-    if (std::fabs(jc) > 1e250) {
-      jc *= 1e-250;
-      jp *= 1e-250;
-      for (int q = n - 1; q <= std::min(start, L + 1); ++q) t[q] *= 1e-250;
+    if (std::fabs(jc) > 1e150) {
+      jc *= 1e-150;
+      jp *= 1e-150;
+      sum *= 1e-300;
+      for (int q = n - 1; q <= L + 1; ++q) t[q] *= 1e-150;
     }
   }
-  const double s = std::sin(x) / x / t[0];
-  for (int n = 0; n <= L + 1; ++n) j[n] = t[n] * s;
+  double sc = 1.0 / std::sqrt(sum);
+  const double j0 = std::sin(x) / x, j1 = std::sin(x) / (x * x) - std::cos(x) / x;
+  if (std::fabs(j0) >= std::fabs(j1) ? (j0 * t[0] < 0) : (j1 * t[1] < 0)) sc = -sc;
+  for (int n = 0; n <= L + 1; ++n) j[n] = t[n] * sc;
 }
 
 double sph_bessel(int l, double x) {
