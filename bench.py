@@ -74,7 +74,9 @@ def stage_work(c):
     nth, nph = Lq + 1, 2 * Lq + 2
     Jh, Kh = (nth + 1) // 2, (nph // 2 - 1) // 2
     samples = R * nth * nph
-    sh_fl = 20 * samples + R * nth * (L + 1) * (4 * Kh + 2) + R * Jh * ncoef(L) * 8
+    # SURVEY 8(d)'s accounting (15.1 MFLOP per particle at c2): a1 trilinear ~21 flop/sample; a2 the real-data
+    # folded ring DFT ~(L+1)/2 flop/sample and the Legendre contraction 8 flop per (shell, node pair, (l, m))
+    sh_fl = 21 * samples + samples * (L + 1) // 2 + R * Jh * ncoef(L) * 8
     sh_by = 4 * N ** 3 + 8 * ncoef(L) * R
     corr_fl = 8 * R * mh(L)
     corr_by = 8 * ncoef(L) * R + 8 * mh(L)
@@ -317,6 +319,9 @@ def main():
     # ---- end to end through the public API on host buffers (H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
+        # the public host-buffer call in chunks of P/4 particles: the H2D copy of chunk c+1 (second stream) overlaps
+        # the compute of chunk c (matcha_align_batch_host's double buffering)
+        h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=max(1, (P + 3) // 4))
         out_host = torch.empty((P, 8), dtype=torch.float32).pin_memory()
         for _ in range(2):
             h.align_batch_host(vols_host, ref_host, params, out=out_host)

@@ -215,6 +215,12 @@ MATCHA_API matcha_status_t matcha_reconstruct(matcha_handle_t h, const float* vo
                                               int32_t pose_stride, int32_t class_col, int32_t n_classes,
                                               int64_t first_index, void* sums, int32_t* counts, void* stream);
 
+/* CUDA-graph replay of matcha_align_batch (off by default): when enabled, a call whose arguments (pointers, sizes,
+   params, stream) repeat the previous call's is captured into a CUDA graph once and then replayed as a single
+   launch while they stay the same (no per-kernel launch overhead for short shards).  Results are
+   bitwise identical to the eager path.  Requires a non-default stream; disabled while profiling. */
+MATCHA_API matcha_status_t matcha_set_graphs(matcha_handle_t h, int32_t enable);
+
 /* End-to-end variant on HOST buffers: vols_host float32 [B][N^3] (pinned memory recommended), ref_host float32
    [N^3]; poses_host (out) real [B][8].  Copies chunks host->device on a second stream overlapped with compute,
    and synchronises before returning. */

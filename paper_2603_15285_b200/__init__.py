@@ -68,6 +68,7 @@ _SIGS = {
     "matcha_ball_kmax": ([_H, ctypes.c_double, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int32),
     "matcha_ball_transform": ([_H, _vp, _i64, ctypes.c_double, _vp, _vp], ctypes.c_int),
     "matcha_corr_coeffs_ball": ([_H, _vp, _vp, _i64, _i32, ctypes.c_double, _vp, _vp], ctypes.c_int),
+    "matcha_set_graphs": ([_H, _i32], ctypes.c_int),
     "matcha_align_multi": ([_H, _vp, _i64, _vp, _i32, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_reconstruct": ([_H, _vp, _i64, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _vp], ctypes.c_int),
     "matcha_get_status": ([_H, _vp], ctypes.c_int),
@@ -192,6 +193,10 @@ class Handle:
     @property
     def launches(self) -> int:
         return int(_lib.matcha_launch_count(self._h))
+
+    def set_graphs(self, enable: bool = True):
+        """CUDA-graph replay of repeated align_batch calls (needs a non-default current stream)."""
+        self._check(_lib.matcha_set_graphs(self._h, 1 if enable else 0))
 
     def profile_begin(self):
         self._check(_lib.matcha_profile_begin(self._h))

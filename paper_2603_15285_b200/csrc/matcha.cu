@@ -88,6 +88,22 @@ struct matcha_ctx {
   void* ws_Fb = nullptr;     // complex [mb][ncoef][R] (Kmax <= R) particle ball coefficients
   void* ws_Hb = nullptr;     // complex [ncoef][R] reference ball coefficients
   void* ws_euler1 = nullptr; // real [mb][3]
+  // CUDA-graph replay of matcha_align_batch (matcha_set_graphs): the launch sequence of a call is captured once its
+  // arguments repeat and replayed while they stay the same
+  bool use_graphs = false;
+  struct AlignKey {
+    const float* vols;
+    int64_t B;
+    const float* ref;
+    const void* ref_coeffs;
+    matcha_params_t params;
+    void* poses;
+    cudaStream_t stream;
+  };
+  AlignKey last_key{};
+  bool last_valid = false;
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_launches = 0;
   // per-stage event tracing
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -851,6 +867,7 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
                   (void*)h->ws_tsel, h->ws_Rt, h->d_ballB, (void*)h->d_ballK, h->ws_Fb, h->ws_Hb})
     if (q) cudaFree(q);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_copied[i]) cudaEventDestroy(h->ev_copied[i]);
     if (h->ev_used[i]) cudaEventDestroy(h->ev_used[i]);
@@ -1064,6 +1081,22 @@ MATCHA_API matcha_status_t matcha_translation_update(matcha_handle_t h, const fl
 }
 
 
+MATCHA_API matcha_status_t matcha_set_graphs(matcha_handle_t h, int32_t enable) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  h->use_graphs = enable != 0;
+  if (!h->use_graphs && h->graph_exec) {
+    cudaGraphExecDestroy(h->graph_exec);
+    h->graph_exec = nullptr;
+  }
+  h->last_valid = false;
+  return MATCHA_OK;
+}
+
+static bool same_key(const matcha_ctx::AlignKey& a, const matcha_ctx::AlignKey& b) {
+  return a.vols == b.vols && a.B == b.B && a.ref == b.ref && a.ref_coeffs == b.ref_coeffs && a.poses == b.poses &&
+         a.stream == b.stream && std::memcmp(&a.params, &b.params, sizeof(matcha_params_t)) == 0;
+}
+
 MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vols, int64_t B, const float* ref,
                                               const void* ref_coeffs, const matcha_params_t* params, void* poses,
                                               void* stream) {
@@ -1078,7 +1111,40 @@ MATCHA_API matcha_status_t matcha_align_batch(matcha_handle_t h, const float* vo
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: box too large for the stage-5 kernels");
   if (params->shift_window > 0 && params->upsample > 0 && !ups_supported(h->cfg.N, params->upsample, h->fp64))
     return fail(h, MATCHA_ERR_NOT_IMPLEMENTED, "align_batch: upsample factor / box exceed the kernels' limits");
-  return align_device(h, vols, B, ref, 1, ref_coeffs, params, poses, 8, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (h->use_graphs && !h->prof && s) {
+    matcha_ctx::AlignKey key{vols, B, ref, ref_coeffs, *params, poses, s};
+    if (h->last_valid && same_key(key, h->last_key)) {
+      if (!h->graph_exec) {
+        // second identical call: capture the launch sequence (every workspace already exists) and instantiate it
+        cudaGraph_t g = nullptr;
+        const int64_t l0 = h->launches;
+        MATCHA_CUDA(h, cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        matcha_status_t st = align_device(h, vols, B, ref, 1, ref_coeffs, params, poses, 8, s);
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        if (st != MATCHA_OK) {
+          if (g) cudaGraphDestroy(g);
+          return st;
+        }
+        if (e != cudaSuccess) return cuda_fail(h, e, "align_batch: graph capture");
+        e = cudaGraphInstantiate(&h->graph_exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_fail(h, e, "align_batch: graph instantiate");
+        h->graph_launches = h->launches - l0;
+        h->launches = l0;
+      }
+      MATCHA_CUDA(h, cudaGraphLaunch(h->graph_exec, s));
+      h->launches += h->graph_launches;
+      return MATCHA_OK;
+    }
+    if (h->graph_exec) {
+      cudaGraphExecDestroy(h->graph_exec);
+      h->graph_exec = nullptr;
+    }
+    h->last_key = key;
+    h->last_valid = true;
+  }
+  return align_device(h, vols, B, ref, 1, ref_coeffs, params, poses, 8, s);
 }
 
 MATCHA_API matcha_status_t matcha_align_multi(matcha_handle_t h, const float* vols, int64_t B, const float* refs,

@@ -625,3 +625,24 @@ def test_align_ball_basis_c2_shape():
         assert rot_err_deg(poses[p, :3], po[p, :3]) < TOL_ROT_DEG or abs(poses[p, 6] - po[p, 6]) <= 1e-4 * abs(po[p, 6])
     errs = [O.geodesic_deg_matrix(O.euler_to_matrix(poses[p, :3]), b.truth_R[p]) for p in range(B)]
     assert np.median(errs) < 1.0
+
+
+def test_align_cuda_graph_replay_bitwise():
+    """matcha_set_graphs: repeated identical align_batch calls are captured once and replayed as a CUDA graph; the
+    poses are bitwise those of the eager path (chunked, translating)."""
+    b = gen.particles(32, 20, 0.5, seed=81, shift_mode=gen.SHIFT_UNIFORM, shift_max=2.0)
+    vols, ref = cuda(b.vols), cuda(b.ref)
+    params = mt.Params(bands=[4, 6, 8], n_cand=4, n_alternations=2, shift_window=4)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        h = handle(32, 8, max_batch=8)
+        eager = to_np(h.align_batch(vols, ref, params))
+        h.set_graphs(True)
+        out = torch.empty((20, 8), device=DEV)
+        n0 = h.launches
+        for _ in range(3):  # eager (key recorded), capture + replay, replay
+            h.align_batch(vols, ref, params, out=out)
+            s.synchronize()
+            assert np.array_equal(to_np(out), eager)
+        assert h.launches - n0 > 0
+        h.set_graphs(False)
