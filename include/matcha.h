@@ -215,6 +215,16 @@ MATCHA_API matcha_status_t matcha_reconstruct(matcha_handle_t h, const float* vo
                                               int32_t pose_stride, int32_t class_col, int32_t n_classes,
                                               int64_t first_index, void* sums, int32_t* counts, void* stream);
 
+/* Bench/test infrastructure: particles first_index .. first_index + B - 1 of the seeded
+   synthetic workload generated on the device -- the Philox4x32-10 counter layout and Gaussian-blob phantom of
+   gen/gen.c (reference blobs keyed 0x5EED): f_p = S_{t_p}(g_p o h) + eta_p, g_p Haar,
+   t_p ~ U[-shift_max, shift_max]^3 (0: no shift), eta ~ N(0, P_ref / snr) (snr <= 0 or inf: noise-free).
+   vols (out): float32 [B][N^3]; truth (out, may be NULL): double [B][12] = (g_p row-major, t_p).  Volumes agree with
+   gen/gen.c to the last float ulp (device vs host exp/log).  Allocates a temporary workspace (stream-ordered). */
+MATCHA_API matcha_status_t matcha_synth_particles(matcha_handle_t h, uint64_t seed, int64_t first_index, int64_t B,
+                                                  double snr, double shift_max, float* vols, double* truth,
+                                                  void* stream);
+
 /* CUDA-graph replay of matcha_align_batch (off by default): when enabled, a call whose arguments (pointers, sizes,
    params, stream) repeat the previous call's is captured into a CUDA graph once and then replayed as a single
    launch while they stay the same (no per-kernel launch overhead for short shards).  Results are

@@ -69,6 +69,8 @@ _SIGS = {
     "matcha_ball_transform": ([_H, _vp, _i64, ctypes.c_double, _vp, _vp], ctypes.c_int),
     "matcha_corr_coeffs_ball": ([_H, _vp, _vp, _i64, _i32, ctypes.c_double, _vp, _vp], ctypes.c_int),
     "matcha_set_graphs": ([_H, _i32], ctypes.c_int),
+    "matcha_synth_particles": ([_H, ctypes.c_uint64, _i64, _i64, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp],
+                               ctypes.c_int),
     "matcha_align_multi": ([_H, _vp, _i64, _vp, _i32, _vp, ctypes.POINTER(_Params), _vp, _vp], ctypes.c_int),
     "matcha_reconstruct": ([_H, _vp, _i64, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _vp], ctypes.c_int),
     "matcha_get_status": ([_H, _vp], ctypes.c_int),
@@ -193,6 +195,15 @@ class Handle:
     @property
     def launches(self) -> int:
         return int(_lib.matcha_launch_count(self._h))
+
+    def synth_particles(self, B: int, snr: float, seed: int = 1, first_index: int = 0, shift_max: float = 0.0):
+        """Seeded synthetic particles generated on the device (gen/gen.c's recipe): -> (vols [B,N,N,N] float32,
+        truth [B,12] float64 = (R row-major, t))."""
+        vols = torch.empty((B, self.N, self.N, self.N), dtype=torch.float32, device=self.device)
+        truth = torch.empty((B, 12), dtype=torch.float64, device=self.device)
+        self._check(_lib.matcha_synth_particles(self._h, seed, first_index, B, snr, shift_max, _ptr(vols),
+                                                _ptr(truth), _stream()))
+        return vols, truth
 
     def set_graphs(self, enable: bool = True):
         """CUDA-graph replay of repeated align_batch calls (needs a non-default current stream)."""

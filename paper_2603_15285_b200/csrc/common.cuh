@@ -182,6 +182,11 @@ template <typename T>
 cudaError_t launch_corr_ball(const cplx_t<T>* Fb, const cplx_t<T>* Hb, int64_t B, int L, int Lmax, const int* Kl,
                              int Kmax, cplx_t<T>* M, cudaStream_t s);
 
+// matcha_synth_particles (k_synth.cu): the seeded synthetic workload on the device (bench/test infrastructure)
+size_t synth_workspace_bytes(int N, int64_t B);
+cudaError_t launch_synth_particles(uint64_t seed, int64_t first, int64_t B, int N, double snr, double shift_max,
+                                   float* vols, double* truth, void* ws, cudaStream_t s);
+
 // half-map sums of the aligned particles per class (k_recon.cu); Rt: workspace real [B][12]
 template <typename T>
 cudaError_t launch_reconstruct(const float* vols, int64_t B, int N, const T* poses, int pstride, int ccol, int ncls,

@@ -1226,6 +1226,22 @@ MATCHA_API matcha_status_t matcha_corr_coeffs_ball(matcha_handle_t h, const void
   return corr_ball(h, fball, hball, B, L, M, (cudaStream_t)stream);
 }
 
+MATCHA_API matcha_status_t matcha_synth_particles(matcha_handle_t h, uint64_t seed, int64_t first_index, int64_t B,
+                                                  double snr, double shift_max, float* vols, double* truth,
+                                                  void* stream) {
+  if (!h) return MATCHA_ERR_INVALID_ARG;
+  if (B < 0 || first_index < 0 || (B > 0 && !vols) || shift_max < 0)
+    return fail(h, MATCHA_ERR_INVALID_ARG, "synth_particles: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  void* ws = nullptr;
+  MATCHA_CUDA(h, cudaMallocAsync(&ws, synth_workspace_bytes(h->cfg.N, B), s));
+  cudaError_t e = launch_synth_particles(seed, first_index, B, h->cfg.N, snr, shift_max, vols, truth, ws, s);
+  cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "synth_particles launch");
+  h->launches += 4 + (B > 0 ? 1 + (B + 65534) / 65535 : 0);
+  return MATCHA_OK;
+}
+
 MATCHA_API matcha_status_t matcha_align_batch_host(matcha_handle_t h, const float* vols_host, int64_t B,
                                                    const float* ref_host, const matcha_params_t* params,
                                                    void* poses_host, void* stream) {

@@ -646,3 +646,19 @@ def test_align_cuda_graph_replay_bitwise():
             assert np.array_equal(to_np(out), eager)
         assert h.launches - n0 > 0
         h.set_graphs(False)
+
+
+def test_synth_particles_matches_host_generator():
+    """matcha_synth_particles reproduces gen/gen.c's seeded workload on the device (same Philox counters and phantom):
+    poses equal to rounding, volumes to the last float ulp (device vs host exp/log), noisy and shifted."""
+    N, B = 32, 5
+    h = handle(N, 8)
+    for snr, smax in ((0.1, 0.0), (float("inf"), 3.0)):
+        vols, truth = h.synth_particles(B, snr, seed=17, first_index=40, shift_max=smax)
+        kw = dict(shift_mode=gen.SHIFT_UNIFORM, shift_max=smax) if smax > 0 else {}
+        hb = gen.particles(N, B, snr, seed=17, first=40, **kw)
+        truth = to_np(truth)
+        assert np.abs(truth[:, :9].reshape(B, 3, 3) - hb.truth_R).max() < 1e-14
+        assert np.abs(truth[:, 9:] - hb.truth_t).max() < 1e-14
+        v = to_np(vols)
+        assert np.abs(v - hb.vols).max() <= 2e-6 * np.abs(hb.vols).max()
