@@ -42,7 +42,8 @@ namespace {
 constexpr int kThr = 512;
 __device__ unsigned long long g_sh_prof[8];  // MATCHA_SH_DBG & 8: cycles per phase, summed over sampler warps
 constexpr int kWarps = kThr / 32;
-constexpr int kNR = 64;   // rings per tile (UMMA_N)
+// rings per tile (UMMA_N): 64, or 32 for L > 32 (two k rounds per lane, Kh <= 64: the S buffers of the larger K
+// and the bigger planes must fit next to each other)
 constexpr int kTM = 128;  // UMMA_M
 
 __host__ __device__ inline int plane_pitch_tc(int N) { return N + 8; }
@@ -54,13 +55,13 @@ struct TcLayout {
   int Kp, Kc, lbo, P, maxtiles;
 };
 
-__host__ __device__ inline TcLayout tc_layout(int N, int R, int nth, int nph, int P) {
+__host__ __device__ inline TcLayout tc_layout(int N, int R, int nth, int nph, int P, int NR) {
   TcLayout s;
   s.Kp = (nph + 15) / 16 * 16;  // K padded to the fp16 MMA K-step
   s.Kc = s.Kp / 8;              // 16-byte K chunks (8 fp16)
-  s.lbo = kNR * 16 + 16;        // K-chunk stride, padded by 16 B against bank conflicts
+  s.lbo = NR * 16 + 16;         // K-chunk stride, padded by 16 B against bank conflicts
   s.P = P;
-  s.maxtiles = (R * nth + kNR - 1) / kNR + N + 4;
+  s.maxtiles = (R * nth + NR - 1) / NR + N + 4;
   size_t o = 0;
   auto take = [&](size_t b, size_t al) {
     o = (o + al - 1) / al * al;
@@ -73,7 +74,7 @@ __host__ __device__ inline TcLayout tc_layout(int N, int R, int nth, int nph, in
   s.node = take(sizeof(float2) * nth, 16);
   s.planes = take(sizeof(float) * (size_t)P * N * plane_pitch_tc(N), 16);
   s.list = take(sizeof(int) * (size_t)R * nth, 16);
-  s.slots = take(sizeof(int) * 3 * kSlotFields * kNR, 16);
+  s.slots = take(sizeof(int) * 3 * kSlotFields * NR, 16);
   s.tiles = take(sizeof(int) * ((size_t)3 * s.maxtiles + 1 + (N + 4) + (N + 2)), 16);
   s.misc = take(64 + sizeof(int) * (4 + kWarps), 16);
   s.total = o;
@@ -262,7 +263,8 @@ __device__ __forceinline__ uint32_t pack_h2(float lo16, float hi16) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-template <int NT>
+// NR rings per tile, KR rounds of 32 k per lane (Kh <= 32 KR)
+template <int NT, int NR, int KR>
 __global__ void __launch_bounds__(kThr + 32, 1)
     k_sh_rings_tc(const float* __restrict__ vols, int64_t B, const float* __restrict__ shifts, int shift_stride,
                   ShTables<float> tab, int P, float2* __restrict__ G, int* __restrict__ flags, int dbg) {
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
   const int R = tab.R, L = tab.L, nth = tab.nth, nph = tab.nph;
   const int Mp = nph / 2, Kh = (Mp - 1) / 2;
   const bool mid = (Mp % 2) == 0;
-  const TcLayout lay = tc_layout(N, R, nth, nph, P);
+  const TcLayout lay = tc_layout(N, R, nth, nph, P, NR);
   const int Kp = lay.Kp, Kc = lay.Kc, LBO = lay.lbo;
   const int PW = plane_pitch_tc(N), PS = N * PW;
   unsigned char* Bs = smem + lay.B;  // buffer b: hi at Bs + (2b) Kc LBO, lo at + (2b+1) Kc LBO
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
   float* planes = (float*)(smem + lay.planes);
   int* list = (int*)(smem + lay.list);
   int* cnt = (int*)(smem + lay.planes);  // counting-sort table [N+3][nth], aliases the planes between particles
-  int* slots = (int*)(smem + lay.slots);  // [3 tiles][kSlotFields][kNR]
+  int* slots = (int*)(smem + lay.slots);  // [3 tiles][kSlotFields][NR]
   int* tstart = (int*)(smem + lay.tiles);  // [max tiles + 1] first ring of each tile
   int* tlo = tstart + lay.maxtiles + 1;     // [max tiles] lowest plane
   int* thi = tlo + lay.maxtiles;            // [max tiles] highest plane
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
   if (warp == kWarps) {
     if (lane == 0 && !(dbg & 1)) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const uint32_t idesc = idesc_f16(kTM, kNR);
+      const uint32_t idesc = idesc_f16(kTM, NR);
       const uint64_t step = (uint64_t)((2 * LBO) >> 4);  // one K-step (16 fp16) = two 16-byte core-matrix columns
       uint32_t fph = 0u;
       for (uint32_t it = 0;; ++it) {
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         const unsigned char* Shi = Bs + (size_t)(2 * buf) * Kc * LBO;
         const uint64_t dhi = desc_nosw(su32(Shi), LBO, 128), dlo = desc_nosw(su32(Shi + (size_t)Kc * LBO), LBO, 128);
-        const uint32_t dcol = tmem + colD + (uint32_t)(kNR * buf);
+        const uint32_t dcol = tmem + colD + (uint32_t)(NR * buf);
         for (int pass = 0; pass < 3; ++pass) {
           uint32_t acol = tmem + (pass == 2 ? colA_lo : colA_hi);
           uint64_t bd = (pass == 1) ? dlo : dhi;
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
         asm volatile("cp.async.commit_group;\n" ::);
       };
       request(min(zfirst + P - 1, N));
-      // ---- 2. tiles: <= kNR consecutive rings whose planes fit the P-slot window (cut at z-bucket boundaries)
+      // ---- 2. tiles: <= NR consecutive rings whose planes fit the P-slot window (cut at z-bucket boundaries)
       if (tid == 0) {
         auto zlo_of = [&](int b) { return min(max(b - 2, -1), N - 1); };
         int nt = 0, s0 = 0;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           const int zl = zlo_of(b0);
           int bx = b0;  // first bucket whose plane is beyond the window
           while (bx < nbk && zlo_of(bx) <= zl + P - 2) ++bx;
-          const int e = min(s0 + kNR, boff[bx]);
+          const int e = min(s0 + NR, boff[bx]);
           const int rl = list[e - 1];
           tstart[nt] = s0;
           tlo[nt] = zl;
@@ -529,8 +531,8 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           // w, w + 16, ...; lanes walk k along the ring (4 mirrored phi indices per lane, one 8-byte store each)
           unsigned char* Shi = Bs + (size_t)(2 * buf) * Kc * LBO;
           unsigned char* Slo = Shi + (size_t)Kc * LBO;
-          int* sl = slots + (t % 3) * kSlotFields * kNR;
-          constexpr int RPW = kNR / kWarps;  // rings per warp
+          int* sl = slots + (t % 3) * kSlotFields * NR;
+          constexpr int RPW = NR / kWarps;  // rings per warp
           const int nx = mid ? 4 : 2;
           // ring geometry: lane rr < RPW computes ring slot warp + rr * kWarps, then broadcasts
           float g_rs = 0.f, g_fz = 0.f;
@@ -557,13 +559,14 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             }
             sl[r] = goff;
           }
-          float sv[RPW][4], ex = 0.f;
-          const int k = lane + 1;  // Kh <= 32 (host-checked)
-          float2 ph[4];
-          {
+          float sv[KR][RPW][4], ex = 0.f;
+          float2 ph[KR][4];
+#pragma unroll
+          for (int kr = 0; kr < KR; ++kr) {
+            const int k = 32 * kr + lane + 1;  // Kh <= 32 KR (host-checked)
             const int kk[4] = {k, k + Mp, Mp - k, 2 * Mp - k};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ph[q] = tw[k <= Kh ? kk[q] : 0];
+            for (int q = 0; q < 4; ++q) ph[kr][q] = tw[k <= Kh ? kk[q] : 0];
           }
           const int xr = lane / nx, xe = lane % nx;  // extra sample xe of the warp's ring xr
           const int xcol = xe == 0 ? 0 : xe == 1 ? Mp : xe == 2 ? Mp / 2 : 3 * Mp / 2;
@@ -573,16 +576,17 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             const int b0 = __shfl_sync(0xffffffffu, g_b0, rr), dz = __shfl_sync(0xffffffffu, g_dz, rr);
             const int in = __shfl_sync(0xffffffffu, g_in, rr);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) sv[rr][q] = 0.f;
-            if (in) {
-              if (k <= Kh) {
+            for (int kr = 0; kr < KR; ++kr) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) sv[kr][rr][q] = 0.f;
+              if (in && 32 * kr + lane + 1 <= Kh) {
                 float px[4], py[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  px[q] = fmaf(rs, ph[q].x, cx);
-                  py[q] = fmaf(rs, ph[q].y, cy);
+                  px[q] = fmaf(rs, ph[kr][q].x, cx);
+                  py[q] = fmaf(rs, ph[kr][q].y, cy);
                 }
-                tri4_xy<NT>(planes + b0, dz, N, px, py, fz, sv[rr]);
+                tri4_xy<NT>(planes + b0, dz, N, px, py, fz, sv[kr][rr]);
               }
             }
           }
@@ -604,7 +608,11 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           float mxv[RPW];
 #pragma unroll
           for (int rr = 0; rr < RPW; ++rr) {
-            mxv[rr] = fmaxf(fmaxf(fabsf(sv[rr][0]), fabsf(sv[rr][1])), fmaxf(fabsf(sv[rr][2]), fabsf(sv[rr][3])));
+            mxv[rr] = 0.f;
+#pragma unroll
+            for (int kr = 0; kr < KR; ++kr)
+              mxv[rr] = fmaxf(mxv[rr], fmaxf(fmaxf(fabsf(sv[kr][rr][0]), fabsf(sv[kr][rr][1])),
+                                             fmaxf(fabsf(sv[kr][rr][2]), fabsf(sv[kr][rr][3]))));
             if (xr == rr) mxv[rr] = fmaxf(mxv[rr], fabsf(ex));
           }
           // |x| as an unsigned bit pattern orders like the value: one warp-reduce instruction (REDUX) per ring
@@ -619,23 +627,27 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             const int es = min(max(14 - e, -100), 100);  // sc = 2^es, 1 / (1024 sc) = 2^-(es + 10)
             const float sc = __uint_as_float((uint32_t)(127 + es) << 23);
             const uint32_t rowoff = (uint32_t)((r >> 3) * 128 + (r & 7) * 16);
-            if (k <= Kh) {
-              const float2 sc2 = make_float2(sc, sc);
-              const float2 x01 = __fmul2_rn(make_float2(sv[rr][0], sv[rr][1]), sc2);
-              const float2 x23 = __fmul2_rn(make_float2(sv[rr][2], sv[rr][3]), sc2);
-              const __half2 h01 = __float22half2_rn(x01), h23 = __float22half2_rn(x23);
-              const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-              const __half2 l01 = __float22half2_rn(__fadd2_rn(x01, make_float2(-f01.x, -f01.y)));
-              const __half2 l23 = __float22half2_rn(__fadd2_rn(x23, make_float2(-f23.x, -f23.y)));
-              const int c = 4 * (k - 1);  // K position of the lane's first sample (8-byte aligned)
-              const uint32_t off = (uint32_t)(c >> 3) * LBO + rowoff + (uint32_t)(c & 7) * 2;
-              uint2 hv, lv;
-              hv.x = *reinterpret_cast<const uint32_t*>(&h01);
-              hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-              lv.x = *reinterpret_cast<const uint32_t*>(&l01);
-              lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-              *(uint2*)(Shi + off) = hv;
-              *(uint2*)(Slo + off) = lv;
+#pragma unroll
+            for (int kr = 0; kr < KR; ++kr) {
+              const int k = 32 * kr + lane + 1;
+              if (k <= Kh) {
+                const float2 sc2 = make_float2(sc, sc);
+                const float2 x01 = __fmul2_rn(make_float2(sv[kr][rr][0], sv[kr][rr][1]), sc2);
+                const float2 x23 = __fmul2_rn(make_float2(sv[kr][rr][2], sv[kr][rr][3]), sc2);
+                const __half2 h01 = __float22half2_rn(x01), h23 = __float22half2_rn(x23);
+                const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+                const __half2 l01 = __float22half2_rn(__fadd2_rn(x01, make_float2(-f01.x, -f01.y)));
+                const __half2 l23 = __float22half2_rn(__fadd2_rn(x23, make_float2(-f23.x, -f23.y)));
+                const int c = 4 * (k - 1);  // K position of the lane's first sample (8-byte aligned)
+                const uint32_t off = (uint32_t)(c >> 3) * LBO + rowoff + (uint32_t)(c & 7) * 2;
+                uint2 hv, lv;
+                hv.x = *reinterpret_cast<const uint32_t*>(&h01);
+                hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+                lv.x = *reinterpret_cast<const uint32_t*>(&l01);
+                lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+                *(uint2*)(Shi + off) = hv;
+                *(uint2*)(Slo + off) = lv;
+              }
             }
             if (xr == rr) {
               const int c = 4 * Kh + xe;
@@ -645,7 +657,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
               *(__half*)(Shi + off) = h;
               *(__half*)(Slo + off) = __float2half_rn(x - __half2float(h));
             }
-            if (lane == 0) sl[kNR + r] = (int)((uint32_t)(127 - es - 10) << 23);
+            if (lane == 0) sl[NR + r] = (int)((uint32_t)(127 - es - 10) << 23);
           }
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[3], (unsigned long long)(clock64() - tq2));
           // S[buf] -> async proxy; hand the tile to the MMA warp
@@ -661,9 +673,9 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           const int q = warp & 3, g = warp >> 2;
           mbar_wait(su32(&done[pb]), (dph >> pb) & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-          if (32 * q < nrow) {
+          if (32 * q < nrow && 16 * g < NR) {
             uint32_t v[16];
-            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + colD + (uint32_t)(kNR * pb + 16 * g);
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + colD + (uint32_t)(NR * pb + 16 * g);
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
                          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
                            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
@@ -671,12 +683,12 @@ __global__ void __launch_bounds__(kThr + 32, 1)
                          : "r"(ta));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
             const int o = 32 * q + lane;
-            const int* slp = slots + (tp % 3) * kSlotFields * kNR + 16 * g;
+            const int* slp = slots + (tp % 3) * kSlotFields * NR + 16 * g;
             if (o < nrow) {
 #pragma unroll
               for (int u = 0; u < 16; ++u) {
                 const int goff = slp[u];
-                if (goff >= 0) Gp[goff + o] = __uint_as_float(v[u]) * __int_as_float(slp[kNR + u]);
+                if (goff >= 0) Gp[goff + o] = __uint_as_float(v[u]) * __int_as_float(slp[NR + u]);
               }
             }
           }
@@ -699,18 +711,21 @@ __global__ void __launch_bounds__(kThr + 32, 1)
 
 // plane slots for the TC ring kernel (0 = not supported for this handle: use the SIMT kernel).  Tiles are cut at
 // z-bucket boundaries so that they never need more than P planes; larger P prefetches further ahead.
+// rings per tile of the handle: 64 with one k round (Kh <= 32), 32 with two (Kh <= 64)
+static int tc_nr(const ShTables<float>& tab) { return (tab.nph / 2 - 1) / 2 <= 32 ? 64 : 32; }
+
 int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode) {
   (void)xnode;
   if (2 * (tab.L + 1) > kTM) return 0;
-  const int Mp = tab.nph / 2, Kh = (Mp - 1) / 2;
-  if (Kh > 32 || Kh < 1) return 0;  // one k per lane
+  const int Mp = tab.nph / 2, Kh = (Mp - 1) / 2, NR = tc_nr(tab);
+  if (Kh > 64 || Kh < 1) return 0;  // at most two rounds of 32 k per lane
   const int Kp = (tab.nph + 15) / 16 * 16;
-  if ((Kp + 31) / 32 * 32 + 2 * kNR > 512) return 0;
+  if ((Kp + 31) / 32 * 32 + 2 * NR > 512) return 0;
   if (tab.N % 4 || tab.R * tab.nth >= (1 << 22) || tab.nth > 0xffff) return 0;
   const size_t budget = 225 * 1024;
   int P = 3;
-  if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P).total > budget) return 0;
-  while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1).total <= budget) ++P;
+  if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total > budget) return 0;
+  while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1, NR).total <= budget) ++P;
   // the counting-sort table aliases the planes
   if ((size_t)2 * (tab.N + 3) * tab.nth * sizeof(int) > (size_t)P * tab.N * plane_pitch_tc(tab.N) * sizeof(float)) return 0;
   return P;
@@ -720,28 +735,25 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
                                const ShTables<float>& tab, int P, float2* G, int* flags, int num_sms,
                                cudaStream_t st) {
   if (nb == 0) return cudaSuccess;
-  const size_t bytes = tc_layout(tab.N, tab.R, tab.nth, tab.nph, P).total;
+  const int NR = tc_nr(tab);
+  const size_t bytes = tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total;
   const int grid = (int)std::min<int64_t>(nb, num_sms);
   const char* dv = getenv("MATCHA_SH_DBG");  // profiling knob: 1 = no MMA/drain, 2 = no gathers
   const int dbg = dv ? atoi(dv) : 0;
   cudaError_t e;
-  switch (tab.N) {
-    case 32:
-      e = cudaFuncSetAttribute(k_sh_rings_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (e != cudaSuccess) return e;
-      k_sh_rings_tc<32><<<grid, kThr + 32, bytes, st>>>(vols, nb, shifts, shift_stride, tab, P, G, flags, dbg);
-      break;
-    case 64:
-      e = cudaFuncSetAttribute(k_sh_rings_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (e != cudaSuccess) return e;
-      k_sh_rings_tc<64><<<grid, kThr + 32, bytes, st>>>(vols, nb, shifts, shift_stride, tab, P, G, flags, dbg);
-      break;
-    default:
-      e = cudaFuncSetAttribute(k_sh_rings_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (e != cudaSuccess) return e;
-      k_sh_rings_tc<0><<<grid, kThr + 32, bytes, st>>>(vols, nb, shifts, shift_stride, tab, P, G, flags, dbg);
-      break;
+  auto go = [&](auto kern) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) kern<<<grid, kThr + 32, bytes, st>>>(vols, nb, shifts, shift_stride, tab, P, G, flags, dbg);
+  };
+  if (NR == 64) {
+    if (tab.N == 32) go(k_sh_rings_tc<32, 64, 1>);
+    else if (tab.N == 64) go(k_sh_rings_tc<64, 64, 1>);
+    else go(k_sh_rings_tc<0, 64, 1>);
+  } else {
+    if (tab.N == 96) go(k_sh_rings_tc<96, 32, 2>);
+    else go(k_sh_rings_tc<0, 32, 2>);
   }
+  if (e != cudaSuccess) return e;
   if (dbg & 8) {
     cudaStreamSynchronize(st);
     unsigned long long h[8];
