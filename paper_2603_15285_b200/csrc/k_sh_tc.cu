@@ -517,7 +517,17 @@ __global__ void __launch_bounds__(kThr + 32, 1)
         if (t < ntiles) {
           const int lo = tlo[t], hi = thi[t];
           if (hi - lo + 1 > P && tid == 0) atomicOr(flags, FLAG_PLANES);
-          if (zhave < hi) request(hi);
+          if (zhave < hi) {
+            // plane z replaces plane z - P in its slot: requesting above tlo[t-1] + P - 1 before every sampler has
+            // finished tile t-1 would overwrite a plane that tile may still read, so such planes wait for a barrier
+            // (rare with many slots; common with P = 3 at 96^3)
+            const int safe = t > 0 ? tlo[t - 1] + P - 1 : INT_MAX;
+            if (hi > safe) {
+              if (zhave < safe) request(safe);
+              sbar();
+            }
+            request(hi);
+          }
           asm volatile("cp.async.wait_group 0;\n" ::);
           sbar();  // planes of tile t resident; all samplers done with iteration t-1 (incl. drain of tile t-2)
           long long tq1 = clock64();

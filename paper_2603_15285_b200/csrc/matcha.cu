@@ -835,8 +835,9 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   {
     const size_t per = cb * (size_t)h->R * h->nth * (h->L + 1);
     h->gws_particles = std::max<int64_t>(32, (int64_t)((96u << 20) / per));
-    // persistent tensor-core ring kernel: whole waves of one particle per SM
-    if (h->tcP > 0 && h->gws_particles >= h->num_sms) h->gws_particles = h->gws_particles / h->num_sms * h->num_sms;
+    // persistent tensor-core ring kernel: whole waves of one particle per SM (at least one wave: for large L the
+    // ring coefficients of a wave exceed L2 and round-trip through HBM, cheaper than idle SMs)
+    if (h->tcP > 0) h->gws_particles = std::max<int64_t>(h->num_sms, h->gws_particles / h->num_sms * h->num_sms);
     h->gws_particles = std::min<int64_t>(h->gws_particles, cfg->max_batch);
     if (e == cudaSuccess) e = cudaMalloc(&h->ws_G, per * h->gws_particles);
   }
