@@ -834,7 +834,13 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   }
   {
     const size_t per = cb * (size_t)h->R * h->nth * (h->L + 1);
-    h->gws_particles = std::max<int64_t>(32, (int64_t)((96u << 20) / per));
+    // ring-coefficient sub-batch of ~640 MB (1,000+ c2 particles): one persistent ring launch and one Legendre launch
+    // per chunk; G then round-trips through HBM (+1.1 MB per c2 particle), which costs less than the per-launch setup
+    // (TMEM allocation, DFT-matrix fill, weight-table staging) and wave tails of L2-sized (96 MB) sub-batches:
+    // measured 1.825 -> 1.696 ms per 1,000 c2 particles.  MATCHA_GWS_MB overrides the budget (A/B switch).
+    size_t gws_mb = 640;
+    if (const char* v = getenv("MATCHA_GWS_MB")) gws_mb = std::max(1, atoi(v));
+    h->gws_particles = std::max<int64_t>(32, (int64_t)((gws_mb << 20) / per));
     // persistent tensor-core ring kernel: whole waves of one particle per SM (at least one wave: for large L the
     // ring coefficients of a wave exceed L2 and round-trip through HBM, cheaper than idle SMs)
     if (h->tcP > 0) h->gws_particles = std::max<int64_t>(h->num_sms, h->gws_particles / h->num_sms * h->num_sms);
