@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(256) k_window_peak(const T* __restrict__ cw_al
 // into the transform of rho (texture gathers), register-blocked z correlation ====================================
 __host__ __device__ constexpr int ct_nst(int n) {
   int s = 0;
+  while (n % 8 == 0) { n /= 8; ++s; }
   while (n % 4 == 0) { n /= 4; ++s; }
   while (n % 2 == 0) { n /= 2; ++s; }
   while (n % 3 == 0) { n /= 3; ++s; }
@@ -486,6 +487,7 @@ __host__ __device__ constexpr int ct_nst(int n) {
 // k-th radix (same order as fft_radix) and the product of the radices before it
 __host__ __device__ constexpr int ct_rad(int n, int k) {
   int s = 0;
+  while (n % 8 == 0) { if (s++ == k) return 8; n /= 8; }
   while (n % 4 == 0) { if (s++ == k) return 4; n /= 4; }
   while (n % 2 == 0) { if (s++ == k) return 2; n /= 2; }
   while (n % 3 == 0) { if (s++ == k) return 3; n /= 3; }
@@ -515,7 +517,34 @@ __device__ __forceinline__ void ct_stage(const float2* __restrict__ a, float2* _
     if (TOT % kFftThreads != 0 && t >= TOT) break;
     const int l = t / NB, j = t - l * NB, k = j % Ns;
     const int ib = l * LS + j, ob = l * LS + (j - k) * R + k;
-    if constexpr (R == 4) {
+    if constexpr (R == 8) {
+      // radix 8 in registers (one smem pass instead of two radix-4/2 passes): a = v_r + v_{r+4}, b = v_r - v_{r+4},
+      // X[2q] = DFT4(a)[q], X[2q+1] = DFT4(b_r W8^r)[q], W8 = e^{-i pi/4}
+      float2 v[8];
+      v[0] = a[fpad(ib)];
+#pragma unroll
+      for (int r = 1; r < 8; ++r) v[r] = cmul<float>(a[fpad(ib + r * NB)], tw[r * k * TS]);
+      const float h = 0.70710678118654752440f;
+      float2 A4[4], B4[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        A4[r] = cadd<float>(v[r], v[r + 4]);
+        B4[r] = csub<float>(v[r], v[r + 4]);
+      }
+      B4[1] = make_float2((B4[1].x + B4[1].y) * h, (B4[1].y - B4[1].x) * h);
+      B4[2] = cmi<float>(B4[2]);
+      B4[3] = make_float2((B4[3].y - B4[3].x) * h, (-B4[3].x - B4[3].y) * h);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const float2* u = half ? B4 : A4;
+        const float2 s02 = cadd<float>(u[0], u[2]), d02 = csub<float>(u[0], u[2]), s13 = cadd<float>(u[1], u[3]),
+                     d13 = cmi<float>(csub<float>(u[1], u[3]));
+        b[fpad(ob + (0 + half) * Ns)] = cadd<float>(s02, s13);
+        b[fpad(ob + (2 + half) * Ns)] = cadd<float>(d02, d13);
+        b[fpad(ob + (4 + half) * Ns)] = csub<float>(s02, s13);
+        b[fpad(ob + (6 + half) * Ns)] = csub<float>(d02, d13);
+      }
+    } else if constexpr (R == 4) {
       const float2 v0 = a[fpad(ib)], v1 = cmul<float>(a[fpad(ib + NB)], tw[k * TS]),
                    v2 = cmul<float>(a[fpad(ib + 2 * NB)], tw[2 * k * TS]),
                    v3 = cmul<float>(a[fpad(ib + 3 * NB)], tw[3 * k * TS]);
@@ -530,7 +559,7 @@ __device__ __forceinline__ void ct_stage(const float2* __restrict__ a, float2* _
       b[fpad(ob)] = cadd<float>(v0, v1);
       b[fpad(ob + Ns)] = csub<float>(v0, v1);
     } else {
-      static_assert(R == 3, "fast path: radices 4, 2, 3");
+      static_assert(R == 3, "fast path: radices 8, 4, 2, 3");
       const float2 v0 = a[fpad(ib)], v1 = cmul<float>(a[fpad(ib + NB)], tw[k * TS]),
                    v2 = cmul<float>(a[fpad(ib + 2 * NB)], tw[2 * k * TS]);
       const float h = 0.86602540378443864676f;
