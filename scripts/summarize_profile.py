@@ -94,22 +94,22 @@ for rep in reps:
             vals.append(r[hdr.index(w)] if w in hdr else "n/a")
         out.append(f"| `{name}` | " + " | ".join(vals) + " |")
         try:
-            rd = float(r[hdr.index("dram__bytes_read.sum")])
-            wr = float(r[hdr.index("dram__bytes_write.sum")])
-            unit = rows[1][hdr.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rd = float(r[hdr.index("dram__bytes_read.sum")]) * sc.get(rows[1][hdr.index("dram__bytes_read.sum")], 1)
+            wr = float(r[hdr.index("dram__bytes_write.sum")]) * sc.get(rows[1][hdr.index("dram__bytes_write.sum")], 1)
+            scale = 1.0
             key = "sh_analysis" if "k_sh" in name else "newton_refine" if "newton" in name else \
                 "so3_search" if ("search" in name or "so3" in name) else "corr_coeffs" if "corr" in name else name
-            # particles in the captured launch: the stage-1 kernels run on sub-batches of 148 (one per SM), the
-            # others on the whole 1,000-particle batch
-            per = 148 if "k_sh" in name else 1000
+            # particles in the captured launch: every captured launch (round 2: stage 1 too, one ring sub-batch per
+            # c2 chunk) covers the whole 1,000-particle batch
+            per = int(os.environ.get("PARTICLES_PER_LAUNCH", "1000"))
             traffic.setdefault(key, 0.0)
             traffic[key] += (rd + wr) * scale / per
         except (ValueError, IndexError):
             pass
     shutil.copy(rep, os.path.join(P, os.path.basename(rep)))
 if header_done:
-    out.append("\n(dram units as printed by ncu; stage-1 launches = sub-batches of 148 particles, the others = 1,000)\n")
+    out.append("\n(dram units as printed by ncu; every captured launch covers the 1,000-particle batch)\n")
     out.append("DRAM traffic per particle (bytes, from the captures above): " +
                ", ".join(f"{k} {v:.0f}" for k, v in traffic.items()) + "\n")
     json.dump({"c2": {k: {"bytes_per_particle": v, "source": f"profiles/{tag}_full_*.ncu-rep dram__bytes_read+write"}
@@ -127,7 +127,7 @@ for f in sorted(glob.glob(os.path.join(G, f"{tag}_warm_*.csv"))):
         shutil.copy(f, os.path.join(P, os.path.basename(f)))
         key = "sh_analysis" if "k_sh" in kname else "newton_refine" if "newton" in kname else \
             "so3_search" if "so3" in kname else "corr_coeffs" if "corr" in kname else kname
-        per = 148 if "k_sh" in kname else 1000
+        per = int(os.environ.get("PARTICLES_PER_LAUNCH", "1000"))
         warm.setdefault(key, 0.0)
         warm[key] += (vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) / per
 if warm:
