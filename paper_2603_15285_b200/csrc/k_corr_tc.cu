@@ -183,8 +183,6 @@ __global__ void __launch_bounds__(kTCThreads + 32, 1)
       row0 = t * kTM;
     }
     int prev_l = -1, prev_n = 0;
-    float4 vpre[kStageUnroll];
-    bool pre_ok = false;
     for (int64_t t = t_begin; t <= t_end; ++t) {
       const int buf = (int)((t - t_begin) & 1);
       const bool have = t < t_end;
@@ -241,26 +239,20 @@ __global__ void __launch_bounds__(kTCThreads + 32, 1)
         }
         wbar();
         // A operand: 128 rows (p, m) of F, interleaved complex along k, split into tf32 hi + lo; all of a thread's
-        // 16-byte loads are issued before any is consumed.  The first kStageUnroll loads of every tile after the
-        // first were issued one iteration early (vpre, before the drain of tile t - 2), so their latency overlaps it.
+        // 16-byte loads are issued before any is consumed
         float* Ahi = Abuf + (2 * buf) * kTM * K;
         float* Alo = Ahi + kTM * K;
         const int k4n = K / 4, nel = kTM * k4n;
         for (int e0 = 0; e0 < nel; e0 += kStageUnroll * kTCThreads) {
           float4 v[kStageUnroll];
-          if (e0 == 0 && pre_ok) {
 #pragma unroll
-            for (int u = 0; u < kStageUnroll; ++u) v[u] = vpre[u];
-          } else {
-#pragma unroll
-            for (int u = 0; u < kStageUnroll; ++u) {
-              const int e = e0 + u * kTCThreads + tid;
-              v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (e < nel) {
-                const int i = e / k4n, k4 = e - i * k4n;
-                const int64_t fo = rowF[buf * kTM + i];
-                if (fo >= 0 && !(dbg & 2)) v[u] = __ldg(reinterpret_cast<const float4*>(F + fo) + k4);
-              }
+          for (int u = 0; u < kStageUnroll; ++u) {
+            const int e = e0 + u * kTCThreads + tid;
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < nel) {
+              const int i = e / k4n, k4 = e - i * k4n;
+              const int64_t fo = rowF[buf * kTM + i];
+              if (fo >= 0 && !(dbg & 2)) v[u] = __ldg(reinterpret_cast<const float4*>(F + fo) + k4);
             }
           }
 #pragma unroll
@@ -286,33 +278,6 @@ __global__ void __launch_bounds__(kTCThreads + 32, 1)
         if (tid == 0) cmd[buf] = N;
         asm volatile("fence.proxy.async.shared::cta;\n" ::);
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&full[buf])) : "memory");
-      }
-      // prefetch the first kStageUnroll A loads of tile t + 1 (its rows computed here, not from the row tables)
-      pre_ok = false;
-      if (have && t + 1 < t_end && !(dbg & 2)) {
-        int ln = l;
-        int64_t rn = row0 + kTM;
-        if (rn >= B * (ln + 1)) {
-          ++ln;
-          rn = 0;
-        }
-        const int Kn = K;  // 2R: the same for every degree
-        const int k4n = Kn / 4, nel = kTM * k4n;
-#pragma unroll
-        for (int u = 0; u < kStageUnroll; ++u) {
-          const int e = u * kTCThreads + tid;
-          vpre[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (e < nel) {
-            const int i = e / k4n, k4 = e - i * k4n;
-            const int64_t row = rn + i;
-            if (row < B * (ln + 1)) {
-              const int64_t pp = row / (ln + 1);
-              const int m = (int)(row - pp * (ln + 1));
-              vpre[u] = __ldg(reinterpret_cast<const float4*>(F + (pp * ncf + lm_index(ln, m)) * R) + k4);
-            }
-          }
-        }
-        pre_ok = true;
       }
       // drain tile t - 1 (overlaps the MMAs of tile t): warp w reads TMEM lane quarter w % 4 (= tile rows) and a
       // contiguous range of 8-column chunks; all tcgen05.ld of the range are issued before one wait
