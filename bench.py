@@ -45,6 +45,10 @@ CONFIGS = {
     # the paper's operating point: N = 200, coarse grid at L0 = 30 with K = 2
     # (953k nodes), N_C = 10, one Newton step per band at {30, 40, 60, L_max}, L_max = 100; 0 dB (SNR 1.0)
     "paper": dict(N=200, L=100, bands=[30, 40, 60, 100], ncand=10, K=2, snr=1.0, particles=500, iters=1),
+    # c2 with the paper's ball-harmonic radial basis (eigenvalue cutoff pi (R - 1/2))
+    "c2b": dict(N=64, L=32, bands=[8, 12, 16, 24, 32], ncand=10, K=2, snr=0.1, particles=1000, iters=1, radial=1),
+    # one multi-template STA iteration at c2 shape: alignment against 2 templates + the half-map update
+    "c2m": dict(N=64, L=32, bands=[8, 12, 16, 24, 32], ncand=10, K=2, snr=0.1, particles=1000, iters=1, templates=2),
     # configs[0] (c1) rotation part, small
     "c1": dict(N=32, L=8, bands=[4, 6, 8], ncand=4, K=2, snr=float("inf"), particles=64, iters=1),
 }
@@ -171,7 +175,7 @@ def make_batch(c, rank, world, P):
 
 def oracle_params(c):
     return dict(L=c["L"], qover=2, L0=c["bands"][0], K=c["K"], ncand=c["ncand"], bands=c["bands"],
-                iters=c["iters"], T=c.get("T", 1), W=c.get("W", 0), ups=c.get("ups", 0))
+                iters=c["iters"], T=c.get("T", 1), W=c.get("W", 0), ups=c.get("ups", 0), radial=c.get("radial", 0))
 
 
 def time_oracle(vols, ref, c, n, nthreads):
@@ -232,6 +236,11 @@ def metric_of(name, c):
     if name in ("c2", "c4"):
         return METRIC
     alt = f", T={c['T']} alternations" if c.get("T", 1) > 1 else ""
+    if c.get("radial"):
+        alt += ", ball-harmonic radial basis"
+    if c.get("templates", 1) > 1:
+        return (f"particles refined/s (box {c['N']}³, L0={c['bands'][0]}→L={c['L']}, {c['templates']} templates + "
+                "half-map update, device-timed)")
     if c.get("ups"):
         alt += f", upsampled subpixel kappa={c['ups']}"
     return f"particles aligned/s (box {c['N']}³, L0={c['bands'][0]}→L={c['L']}{alt}, device-timed)"
@@ -275,12 +284,25 @@ def main():
     ref = ref_host.to(dev)
     h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=P)
     params = mt.Params(bands=c["bands"], n_cand=c["ncand"], oversample=c["K"], newton_iters=c["iters"],
-                       n_alternations=c.get("T", 1), shift_window=c.get("W", 0), upsample=c.get("ups", 0))
+                       n_alternations=c.get("T", 1), shift_window=c.get("W", 0), upsample=c.get("ups", 0),
+                       radial=c.get("radial", 0))
     from paper_2603_15285_b200 import dist as D
     H = torch.empty((ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
     counts = [P] * world
 
+    nt = c.get("templates", 1)
+    if nt > 1:
+        # f4: the templates are the reference and further phantoms of the same recipe (other Philox keys)
+        import gen as G
+        refs = torch.stack([ref] + [torch.from_numpy(G.render(G.reference_blobs(seed=0xBEEF + k), c["N"])[0]).to(dev)
+                                    for k in range(nt - 1)])
+        Hs = torch.empty((nt, ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
+
     def step():
+        if nt > 1:
+            # f4: multi-template alignment + the half-map reference update (NCCL all-reduce of 2 T N^3 sums)
+            D.sta_step(h, vols, refs, params, Hs, rank, first_index=rank * P, counts=counts)
+            return
         # rank 0: reference coefficients (stage a3) -> NCCL broadcast (140 KiB at c2) -> every rank aligns its
         # shard -> NCCL all_gather of the poses (32 B per particle)
         D.align_step(h, vols, ref, params, H, rank, counts=counts)
@@ -318,7 +340,7 @@ def main():
 
     # ---- end to end through the public API on host buffers (H2D + D2H inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and nt == 1:
         # the public host-buffer call in chunks of P/4 particles: the H2D copy of chunk c+1 (second stream) overlaps
         # the compute of chunk c (matcha_align_batch_host's double buffering)
         h = mt.Handle(N=c["N"], L_max=c["L"], quad_oversample=2, max_batch=max(1, (P + 3) // 4))
@@ -386,7 +408,7 @@ def main():
                  "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()}})
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and nt == 1:
         cpu = cpu_baseline(batch, c)
 
     out = {"metric": metric_of(args.config, c), "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
@@ -398,7 +420,10 @@ def main():
                                   + (f"T={c['T']} alternations with the FFT translation update (W={c['W']}, "
                                      + (f"upsampled-DFT subpixel kappa={c['ups']}" if c.get("ups") else
                                         "parabolic subpixel") + f"), shifts U[-{c['shift_max']:g},{c['shift_max']:g}]^3"
-                                     if c.get("T", 1) > 1 else "rotation only"),
+                                     if c.get("T", 1) > 1 else "rotation only")
+                                  + (", ball-harmonic radial basis (radial=1)" if c.get("radial") else "")
+                                  + (f", {c['templates']} templates + half-map reference update per step"
+                                     if c.get("templates", 1) > 1 else ""),
                       "particles_per_rank": P, "parallelism": f"dp{world}",
                       "l2": f"inputs larger than L2 ({P * c['N'] ** 3 * 4 / 2**30:.2f} GiB per rank resident)"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch, "clocks": clocks}

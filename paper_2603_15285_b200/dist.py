@@ -87,3 +87,21 @@ def reconstruct_step(handle, vols_local: torch.Tensor, poses_local: torch.Tensor
         dist.all_reduce(counts, group=group)
     c = counts.to(sums.dtype).clamp(min=1).reshape(n_classes, 2, 1, 1, 1)
     return sums / c, counts
+
+
+def sta_step(handle, vols_local: torch.Tensor, refs: torch.Tensor, params, Hs: torch.Tensor, rank: int,
+             first_index: int, group=None, counts=None):
+    """One iteration of multi-template subtomogram averaging: rank 0 analyses the T
+    templates, the coefficients (and, when translating, the template volumes) are broadcast, every rank aligns its
+    shard against all templates (matcha_align_multi), the half maps of every class are summed per rank and
+    all-reduced (reconstruct_step), the poses gathered.  -> (poses [P, 9], half maps [T, 2, N, N, N], counts)."""
+    nt = refs.shape[0]
+    if rank == 0:
+        handle.sh_analysis(refs, out=Hs)
+    broadcast_ref_coeffs(Hs, src=0, group=group)
+    translate = getattr(params, "shift_window", 0) > 0
+    if translate:
+        broadcast_ref_coeffs(refs, src=0, group=group)
+    poses = handle.align_multi(vols_local, refs if translate else None, params, ref_coeffs=Hs)
+    maps, cnt = reconstruct_step(handle, vols_local, poses, first_index, n_classes=nt, class_col=8, group=group)
+    return gather_poses(poses, counts=counts, group=group), maps, cnt
