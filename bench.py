@@ -91,9 +91,17 @@ def stage_work(c):
     nw_fl = sum(c["iters"] * mh(Lj) * nc * 28 for Lj in c["bands"]) + mh(c["bands"][-1]) * nc * 8
     nw_by = sum(c["iters"] * 8 * mh(Lj) for Lj in c["bands"]) + 8 * mh(c["bands"][-1])
     T = c.get("T", 1)
+    nt = c.get("templates", 1)
+    if nt > 1:
+        corr_fl, corr_by = nt * corr_fl, nt * corr_by  # M per template
     work = {"sh_analysis": (T * sh_fl, T * sh_by), "corr_coeffs": (T * corr_fl, T * corr_by),
             "so3_search": (T * srch_fl, T * srch_by), "newton_refine": (T * nw_fl, T * nw_by),
-            "gather_poses": (0, 48)}
+            "gather_poses": (0, 48),
+            # f4 half-map update: ~30 flop per (voxel, particle) (rotation + trilinear), the particle read once
+            "reconstruct": (30 * N ** 3, 4 * N ** 3)}
+    if nt > 1:
+        for k in ("so3_search", "newton_refine"):
+            work[k] = (nt * work[k][0], nt * work[k][1])
     if c.get("W", 0) > 0:
         # a11-a13 per alternation (k_trans.cu, no FFT library): rho~ = 2-D R2C of every z-plane of the rotated
         # reference (rotation fused: ~30 flop/voxel, 2.5 N^2 log2 N^2 flop per plane), the z correlation of the plane
