@@ -191,5 +191,6 @@ cudaError_t launch_synth_particles(uint64_t seed, int64_t first, int64_t B, int 
 template <typename T>
 cudaError_t launch_reconstruct(const float* vols, int64_t B, int N, const T* poses, int pstride, int ccol, int ncls,
                                int64_t first, T* Rt, T* sums, int* counts, cudaStream_t s);
+size_t reconstruct_workspace_bytes(int64_t B, int ncls, size_t rsz);  // Rt + per-(class, half) particle lists
 
 }  // namespace matcha

@@ -77,8 +77,8 @@ struct matcha_ctx {
   void* ws_Hs = nullptr;     // complex [kMaxTemplates][ncoef][R] reference coefficients
   void* ws_cand = nullptr;   // real [kMaxTemplates][mb][8] per-template poses
   int* ws_tsel = nullptr;    // int [mb] selected template per particle
-  void* ws_Rt = nullptr;     // real [n][12] pose matrices of matcha_reconstruct
-  int64_t ws_Rt_n = 0;
+  void* ws_Rt = nullptr;     // matcha_reconstruct workspace: pose matrices + per-(class, half) particle lists
+  int64_t ws_Rt_n = 0;       // bytes
   // ball-harmonic radial basis: tables for ball_lambda, workspaces
   double ball_lambda = -1;
   int ball_kmax = 0;
@@ -1184,14 +1184,14 @@ MATCHA_API matcha_status_t matcha_reconstruct(matcha_handle_t h, const float* vo
     return fail(h, MATCHA_ERR_INVALID_ARG, "reconstruct: bad pose layout / class arguments");
   if (h->cfg.N % 8) return fail(h, MATCHA_ERR_INVALID_ARG, "reconstruct: N must be a multiple of 8");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t mb = std::max<int64_t>(B, 1);
-  if (h->ws_Rt_n < mb) {
+  const int64_t need = (int64_t)reconstruct_workspace_bytes(B, n_classes, h->rsz);
+  if (h->ws_Rt_n < need) {
     if (h->ws_Rt) cudaFree(h->ws_Rt);
     h->ws_Rt = nullptr;
     h->ws_Rt_n = 0;
-    if (cudaMalloc(&h->ws_Rt, 12 * h->rsz * mb) != cudaSuccess)
-      return fail(h, MATCHA_ERR_ALLOC, "reconstruct: pose matrix allocation failed");
-    h->ws_Rt_n = mb;
+    if (cudaMalloc(&h->ws_Rt, need) != cudaSuccess)
+      return fail(h, MATCHA_ERR_ALLOC, "reconstruct: workspace allocation failed");
+    h->ws_Rt_n = need;
   }
   ProfScope ps(h, 6, s);
   cudaError_t e = h->fp64 ? launch_reconstruct<double>(vols, B, h->cfg.N, (const double*)poses, pose_stride, class_col,
