@@ -98,7 +98,9 @@ def stage_work(c):
             "so3_search": (T * srch_fl, T * srch_by), "newton_refine": (T * nw_fl, T * nw_by),
             "gather_poses": (0, 48),
             # f4 half-map update: ~30 flop per (voxel, particle) (rotation + trilinear), the particle read once
-            "reconstruct": (30 * N ** 3, 4 * N ** 3)}
+            "reconstruct": (30 * N ** 3, 4 * N ** 3),
+            # f2 radial transform: 8 flop per (shell, (l, m), k); F read, f^ written
+            "ball_transform": (8 * R * ncoef(L) * R, 16 * ncoef(L) * R)}
     if nt > 1:
         for k in ("so3_search", "newton_refine"):
             work[k] = (nt * work[k][0], nt * work[k][1])

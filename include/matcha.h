@@ -246,7 +246,7 @@ MATCHA_API int64_t matcha_launch_count(matcha_handle_t h);
 
 /* Per-stage tracing with CUDA events recorded on the launching stream around every stage launch.
    Stage ids: 0 sh_analysis, 1 corr_coeffs, 2 so3_search, 3 newton_refine/eval_corr, 4 pose gather / template
-   selection, 5 translation_update, 6 reconstruct.  matcha_profile_end synchronises on the last event and returns, per stage,
+   selection, 5 translation_update, 6 reconstruct, 7 ball_transform.  matcha_profile_end synchronises on the last event and returns, per stage,
    the summed device milliseconds and the number of launches since matcha_profile_begin
    (stage_ms, stage_launches: host arrays of MATCHA_NUM_STAGES entries; either may be NULL). */
 #define MATCHA_NUM_STAGES 8

@@ -81,7 +81,7 @@ _SIGS = {
 }
 NUM_STAGES = 8
 STAGES = ("sh_analysis", "corr_coeffs", "so3_search", "newton_refine", "gather_poses", "translation_update",
-          "reconstruct")
+          "reconstruct", "ball_transform")
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
     _f.argtypes = _args

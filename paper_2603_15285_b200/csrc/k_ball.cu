@@ -17,71 +17,79 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// one CTA per (l, particle): out[p][lm][k] = sum_i Bt[l][k][i] F[p][lm][i] for 0 <= m <= l, k < K_l (zero padding
-// up to Kmax); the CTA stages F's l rows and the l table in shared memory
+constexpr int kPG = 16;  // particles per CTA: the per-degree table (or reference block) is staged once for all
+
+// one CTA per (l, group of kPG particles): out[p][lm][k] = sum_i Bt[l][k][i] F[p][lm][i] for 0 <= m <= l, k < K_l
+// (zero padding up to Kmax); the l table is staged once, F's l rows particle by particle
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_ball_transform(const cplx_t<T>* __restrict__ F, int Lmax, int R,
-                                                             const T* __restrict__ Bt, const int* __restrict__ Kl,
-                                                             int Kmax, cplx_t<T>* __restrict__ out) {
+__global__ void __launch_bounds__(kThreads) k_ball_transform(const cplx_t<T>* __restrict__ F, int64_t B, int Lmax,
+                                                             int R, const T* __restrict__ Bt,
+                                                             const int* __restrict__ Kl, int Kmax,
+                                                             cplx_t<T>* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int l = blockIdx.x, K = Kl[l];
-  const int64_t p = blockIdx.y;
   const int ncf = ncoef(Lmax);
   cplx_t<T>* Fs = reinterpret_cast<cplx_t<T>*>(smem);  // [l+1][R]
   T* Bs = reinterpret_cast<T*>(Fs + (l + 1) * R);      // [K][R]
-  const cplx_t<T>* Fp = F + (p * ncf + lm_index(l, 0)) * (int64_t)R;
-  for (int t = threadIdx.x; t < (l + 1) * R; t += kThreads) Fs[t] = Fp[t];
   const T* Bl = Bt + (int64_t)l * Kmax * R;
   for (int t = threadIdx.x; t < K * R; t += kThreads) Bs[t] = Bl[t];
-  __syncthreads();
-  cplx_t<T>* o = out + (p * ncf + lm_index(l, 0)) * (int64_t)Kmax;
-  for (int t = threadIdx.x; t < (l + 1) * Kmax; t += kThreads) {
-    const int m = t / Kmax, k = t - m * Kmax;
-    T ar = T(0), ai = T(0);
-    if (k < K) {
-      const cplx_t<T>* fr = Fs + m * R;
-      const T* br = Bs + k * R;
-      for (int i = 0; i < R; ++i) {
-        ar = fma(br[i], fr[i].x, ar);
-        ai = fma(br[i], fr[i].y, ai);
+  for (int64_t p = (int64_t)blockIdx.y * kPG; p < min(B, (int64_t)(blockIdx.y + 1) * kPG); ++p) {
+    const cplx_t<T>* Fp = F + (p * ncf + lm_index(l, 0)) * (int64_t)R;
+    __syncthreads();  // the previous particle's rows are consumed
+    for (int t = threadIdx.x; t < (l + 1) * R; t += kThreads) Fs[t] = Fp[t];
+    __syncthreads();
+    cplx_t<T>* o = out + (p * ncf + lm_index(l, 0)) * (int64_t)Kmax;
+    for (int t = threadIdx.x; t < (l + 1) * Kmax; t += kThreads) {
+      const int m = t / Kmax, k = t - m * Kmax;
+      T ar = T(0), ai = T(0);
+      if (k < K) {
+        const cplx_t<T>* fr = Fs + m * R;
+        const T* br = Bs + k * R;
+        for (int i = 0; i < R; ++i) {
+          ar = fma(br[i], fr[i].x, ar);
+          ai = fma(br[i], fr[i].y, ai);
+        }
       }
+      o[t] = mk<T>(ar, ai);
     }
-    o[t] = mk<T>(ar, ai);
   }
 }
 
-// one CTA per (l, particle): M^l_mn = sum_{k < K_l} f^_klm conj(h^_kln), conj(h^_{k,l,n}) = (-1)^n h^_{k,l,|n|} for
-// n < 0 (reality of h, reading C3; the radial transform is real)
+// one CTA per (l, group of kPG particles): M^l_mn = sum_{k < K_l} f^_klm conj(h^_kln), conj(h^_{k,l,n}) =
+// (-1)^n h^_{k,l,|n|} for n < 0 (reality of h, reading C3; the radial transform is real); the conjugated reference
+// block is staged once per CTA
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_corr_ball(const cplx_t<T>* __restrict__ Fb,
-                                                        const cplx_t<T>* __restrict__ Hb, int L, int Lmax,
+                                                        const cplx_t<T>* __restrict__ Hb, int64_t B, int L, int Lmax,
                                                         const int* __restrict__ Kl, int Kmax,
                                                         cplx_t<T>* __restrict__ M) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int l = L - (int)blockIdx.x, K = Kl[l], w = 2 * l + 1;
-  const int64_t p = blockIdx.y;
   const int ncf = ncoef(Lmax);
-  cplx_t<T>* Fs = reinterpret_cast<cplx_t<T>*>(smem);  // [l+1][K]
+  cplx_t<T>* Fs = reinterpret_cast<cplx_t<T>*>(smem);  // [l+1][Kmax]
   cplx_t<T>* Hs = Fs + (l + 1) * Kmax;                  // [K][w]  conj(h^_kln)
-  const cplx_t<T>* Fp = Fb + (p * ncf + lm_index(l, 0)) * (int64_t)Kmax;
   const cplx_t<T>* Hp = Hb + (int64_t)lm_index(l, 0) * Kmax;
-  for (int t = threadIdx.x; t < (l + 1) * Kmax; t += kThreads) Fs[t] = Fp[t];
   for (int t = threadIdx.x; t < K * w; t += kThreads) {
     const int n = t / K - l, k = t - (t / K) * K;
     const cplx_t<T> h = Hp[(int64_t)abs(n) * Kmax + k];
     Hs[k * w + n + l] = (n >= 0) ? mk<T>(h.x, -h.y) : ((n & 1) ? mk<T>(-h.x, -h.y) : h);
   }
-  __syncthreads();
-  cplx_t<T>* Mo = M + p * half_size(L) + half_offset(l);
-  for (int o = threadIdx.x; o < (l + 1) * w; o += kThreads) {
-    const int m = o / w, nn = o - m * w;
-    T ar = T(0), ai = T(0);
-    for (int k = 0; k < K; ++k) {
-      const cplx_t<T> f = Fs[m * Kmax + k], h = Hs[k * w + nn];
-      ar = fma(f.x, h.x, fma(-f.y, h.y, ar));
-      ai = fma(f.x, h.y, fma(f.y, h.x, ai));
+  for (int64_t p = (int64_t)blockIdx.y * kPG; p < min(B, (int64_t)(blockIdx.y + 1) * kPG); ++p) {
+    const cplx_t<T>* Fp = Fb + (p * ncf + lm_index(l, 0)) * (int64_t)Kmax;
+    __syncthreads();
+    for (int t = threadIdx.x; t < (l + 1) * Kmax; t += kThreads) Fs[t] = Fp[t];
+    __syncthreads();
+    cplx_t<T>* Mo = M + p * half_size(L) + half_offset(l);
+    for (int o = threadIdx.x; o < (l + 1) * w; o += kThreads) {
+      const int m = o / w, nn = o - m * w;
+      T ar = T(0), ai = T(0);
+      for (int k = 0; k < K; ++k) {
+        const cplx_t<T> f = Fs[m * Kmax + k], h = Hs[k * w + nn];
+        ar = fma(f.x, h.x, fma(-f.y, h.y, ar));
+        ai = fma(f.x, h.y, fma(f.y, h.x, ai));
+      }
+      Mo[o] = mk<T>(ar, ai);
     }
-    Mo[o] = mk<T>(ar, ai);
   }
 }
 
@@ -95,10 +103,12 @@ cudaError_t launch_ball_transform(const cplx_t<T>* F, int64_t B, int Lmax, int R
   if (bytes > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_ball_transform<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
-  for (int64_t b0 = 0; b0 < B; b0 += 65535) {
-    const int64_t nb = B - b0 < 65535 ? B - b0 : 65535;
-    k_ball_transform<T><<<dim3((unsigned)(Lmax + 1), (unsigned)nb), kThreads, bytes, s>>>(
-        F + b0 * (int64_t)ncoef(Lmax) * R, Lmax, R, Bt, Kl, Kmax, out + b0 * (int64_t)ncoef(Lmax) * Kmax);
+  const int64_t ng = (B + kPG - 1) / kPG;
+  for (int64_t g0 = 0; g0 < ng; g0 += 65535) {
+    const int64_t n = ng - g0 < 65535 ? ng - g0 : 65535;
+    const int64_t b0 = g0 * kPG;
+    k_ball_transform<T><<<dim3((unsigned)(Lmax + 1), (unsigned)n), kThreads, bytes, s>>>(
+        F + b0 * (int64_t)ncoef(Lmax) * R, B - b0, Lmax, R, Bt, Kl, Kmax, out + b0 * (int64_t)ncoef(Lmax) * Kmax);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -112,10 +122,12 @@ cudaError_t launch_corr_ball(const cplx_t<T>* Fb, const cplx_t<T>* Hb, int64_t B
   if (bytes > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_corr_ball<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
-  for (int64_t b0 = 0; b0 < B; b0 += 65535) {
-    const int64_t nb = B - b0 < 65535 ? B - b0 : 65535;
-    k_corr_ball<T><<<dim3((unsigned)(L + 1), (unsigned)nb), kThreads, bytes, s>>>(
-        Fb + b0 * (int64_t)ncoef(Lmax) * Kmax, Hb, L, Lmax, Kl, Kmax, M + b0 * half_size(L));
+  const int64_t ng = (B + kPG - 1) / kPG;
+  for (int64_t g0 = 0; g0 < ng; g0 += 65535) {
+    const int64_t n = ng - g0 < 65535 ? ng - g0 : 65535;
+    const int64_t b0 = g0 * kPG;
+    k_corr_ball<T><<<dim3((unsigned)(L + 1), (unsigned)n), kThreads, bytes, s>>>(
+        Fb + b0 * (int64_t)ncoef(Lmax) * Kmax, Hb, B - b0, L, Lmax, Kl, Kmax, M + b0 * half_size(L));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;

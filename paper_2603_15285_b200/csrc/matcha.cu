@@ -570,6 +570,7 @@ static matcha_status_t ball_prepare(matcha_handle_t h, double lam) {
 }
 
 static matcha_status_t ball_transform(matcha_handle_t h, const void* F, int64_t B, void* out, cudaStream_t s) {
+  ProfScope ps(h, 7, s);
   cudaError_t e = h->fp64 ? launch_ball_transform<double>((const double2*)F, B, h->L, h->R, (const double*)h->d_ballB,
                                                           h->d_ballK, h->ball_kmax, (double2*)out, s)
                           : launch_ball_transform<float>((const float2*)F, B, h->L, h->R, (const float*)h->d_ballB,
