@@ -30,9 +30,12 @@ __global__ void __launch_bounds__(kThreads) k_ball_transform(const cplx_t<T>* __
   const int l = blockIdx.x, K = Kl[l];
   const int ncf = ncoef(Lmax);
   cplx_t<T>* Fs = reinterpret_cast<cplx_t<T>*>(smem);  // [l+1][R]
-  T* Bs = reinterpret_cast<T*>(Fs + (l + 1) * R);      // [K][R]
+  T* Bs = reinterpret_cast<T*>(Fs + (l + 1) * R);      // [R][Kmax] (transposed: lanes take consecutive k)
   const T* Bl = Bt + (int64_t)l * Kmax * R;
-  for (int t = threadIdx.x; t < K * R; t += kThreads) Bs[t] = Bl[t];
+  for (int t = threadIdx.x; t < K * R; t += kThreads) {
+    const int k = t / R, i = t - k * R;
+    Bs[i * Kmax + k] = Bl[t];
+  }
   for (int64_t p = (int64_t)blockIdx.y * kPG; p < min(B, (int64_t)(blockIdx.y + 1) * kPG); ++p) {
     const cplx_t<T>* Fp = F + (p * ncf + lm_index(l, 0)) * (int64_t)R;
     __syncthreads();  // the previous particle's rows are consumed
@@ -44,10 +47,11 @@ __global__ void __launch_bounds__(kThreads) k_ball_transform(const cplx_t<T>* __
       T ar = T(0), ai = T(0);
       if (k < K) {
         const cplx_t<T>* fr = Fs + m * R;
-        const T* br = Bs + k * R;
+        const T* br = Bs + k;
         for (int i = 0; i < R; ++i) {
-          ar = fma(br[i], fr[i].x, ar);
-          ai = fma(br[i], fr[i].y, ai);
+          const T b = br[i * Kmax];
+          ar = fma(b, fr[i].x, ar);
+          ai = fma(b, fr[i].y, ai);
         }
       }
       o[t] = mk<T>(ar, ai);
