@@ -231,14 +231,28 @@ def run_reference(args, c, rank, world):
            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"{args.config}: {c['N']}^3, L0={c['bands'][0]}->L={c['L']}, "
-                                  f"bands {c['bands']}, N_C={c['ncand']}, K={c['K']}, SNR {c['snr']}",
-                      "particles_per_step": S},
+           "config": {"workload": workload_of(args.config, c, c["particles"]),
+                      "particles_per_rank": c["particles"], "parallelism": "dp1",
+                      "oracle_particles_per_step": S},
            "cpu_baseline": {"value": value, "unit": "particles/s", "cores": cores, "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": value, "unit": "particles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
+
+
+def workload_of(name, c, P):
+    """The workload string both arms print (the matcha arm's config.workload; the reference arm times the oracle on
+    a bounded sample of the same workload)."""
+    return (f"{name}: {P} particles/rank of {c['N']}^3, SNR {c['snr']}, "
+            f"L0={c['bands'][0]}->L={c['L']} bands {c['bands']}, N_C={c['ncand']}, "
+            f"K={c['K']}, 1 Newton step/band, "
+            + (f"T={c['T']} alternations with the FFT translation update (W={c['W']}, "
+               + (f"upsampled-DFT subpixel kappa={c['ups']}" if c.get("ups") else "parabolic subpixel")
+               + f"), shifts U[-{c['shift_max']:g},{c['shift_max']:g}]^3" if c.get("T", 1) > 1 else "rotation only")
+            + (", ball-harmonic radial basis (radial=1)" if c.get("radial") else "")
+            + (f", {c['templates']} templates + half-map reference update per step"
+               if c.get("templates", 1) > 1 else ""))
 
 
 def metric_of(name, c):
@@ -424,16 +438,7 @@ def main():
     out = {"metric": metric_of(args.config, c), "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": f"{args.config}: {P} particles/rank of {c['N']}^3, SNR {c['snr']}, "
-                                  f"L0={c['bands'][0]}->L={c['L']} bands {c['bands']}, N_C={c['ncand']}, "
-                                  f"K={c['K']}, 1 Newton step/band, "
-                                  + (f"T={c['T']} alternations with the FFT translation update (W={c['W']}, "
-                                     + (f"upsampled-DFT subpixel kappa={c['ups']}" if c.get("ups") else
-                                        "parabolic subpixel") + f"), shifts U[-{c['shift_max']:g},{c['shift_max']:g}]^3"
-                                     if c.get("T", 1) > 1 else "rotation only")
-                                  + (", ball-harmonic radial basis (radial=1)" if c.get("radial") else "")
-                                  + (f", {c['templates']} templates + half-map reference update per step"
-                                     if c.get("templates", 1) > 1 else ""),
+           "config": {"workload": workload_of(args.config, c, P),
                       "particles_per_rank": P, "parallelism": f"dp{world}",
                       "l2": f"inputs larger than L2 ({P * c['N'] ** 3 * 4 / 2**30:.2f} GiB per rank resident)"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": n_launch, "clocks": clocks}
