@@ -188,10 +188,21 @@ def oracle_params(c):
                 iters=c["iters"], T=c.get("T", 1), W=c.get("W", 0), ups=c.get("ups", 0), radial=c.get("radial", 0))
 
 
+def template_refs(c, ref):
+    """f4 workloads: the reference plus further phantoms of the same recipe (Philox keys 0xBEEF + k)."""
+    import gen as G
+    return np.stack([ref] + [G.render(G.reference_blobs(seed=0xBEEF + k), c["N"])[0]
+                             for k in range(c.get("templates", 1) - 1)])
+
+
 def time_oracle(vols, ref, c, n, nthreads):
     import oracle as O
     t = time.perf_counter()
-    O.align_batch(vols[:n], ref, oracle_params(c), nthreads=nthreads)
+    if c.get("templates", 1) > 1:
+        poses = O.align_batch_multi(vols[:n], template_refs(c, ref), oracle_params(c), nthreads=nthreads)
+        O.reconstruct(vols[:n], poses, n_classes=c["templates"], class_col=8)
+    else:
+        O.align_batch(vols[:n], ref, oracle_params(c), nthreads=nthreads)
     return time.perf_counter() - t
 
 
@@ -317,9 +328,7 @@ def main():
     nt = c.get("templates", 1)
     if nt > 1:
         # f4: the templates are the reference and further phantoms of the same recipe (other Philox keys)
-        import gen as G
-        refs = torch.stack([ref] + [torch.from_numpy(G.render(G.reference_blobs(seed=0xBEEF + k), c["N"])[0]).to(dev)
-                                    for k in range(nt - 1)])
+        refs = torch.from_numpy(template_refs(c, batch.ref)).to(dev)
         Hs = torch.empty((nt, ncoef(c["L"]), c["N"] // 2), dtype=torch.complex64, device=dev)
 
     def step():
@@ -432,7 +441,7 @@ def main():
                  "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()}})
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline and nt == 1:
+    if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(batch, c)
 
     out = {"metric": metric_of(args.config, c), "value": value, "unit": "particles/s", "n_gpus": world, "steps": args.steps,
