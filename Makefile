@@ -7,7 +7,7 @@ CC        ?= gcc
 CUDA_HOME ?= /usr/local/cuda
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
-             --expt-relaxed-constexpr -Iinclude -Xptxas -v
+             --expt-relaxed-constexpr -Iinclude -Xptxas -v $(EXTRA)
 PKG       := paper_2603_15285_b200
 CU_SRCS   := $(wildcard $(PKG)/csrc/*.cu)
 CU_HDRS   := $(wildcard $(PKG)/csrc/*.cuh) include/matcha.h

@@ -48,6 +48,18 @@ struct PairDesc {
   int32_t off0;  // half-plane offset of M^{l0}_mn, l0 = max(m, |n|): half_offset(l0) + m (2 l0 + 1) + n + l0
 };
 
+// Stage-4 recurrence run: the l-run of pair A = (l0, nA) (mA = l0) and, when mB >= 0, of its symmetry partner B whose
+// Wigner d equals A's up to a sign at every l and beta (d^l_{nm} = (-1)^{m-n} d^l_{mn}, d^l_{-n,-m} = d^l_{mn}):
+//   nA in [0, l0):   B = (nA, l0),   d_B = (-1)^{l0-nA} d_A
+//   nA in (-l0, 0):  B = (-nA, -l0), d_B = d_A
+// (l0, +-l0) and (0, -l0) run alone (mB = -1).  Grouped by shell l0 ascending, so the runs of degree <= L are the
+// first run_count(L).
+struct RunDesc {
+  int16_t mA, nA, mB, nB;
+  int32_t offA, offB;  // half-plane offsets of M^{l0}_{mA nA}, M^{l0}_{mB nB} (offB = offA when alone)
+};
+__host__ __device__ __forceinline__ int run_count(int L) { return L * L + 3 * L + 1; }
+
 // ------------------------------------------------------------------ kernel argument packs
 template <typename T> struct ShTables {
   const cplx_t<T>* node;  // [n_theta] (cos th_j, sin th_j), x_j ascending
@@ -85,8 +97,8 @@ template <typename T> struct NewtonArgs {
   double tol_grad, tol_step, tol_obj;
   T* score;
   int32_t* best;
-  const PairDesc* pairs;
-  const T* pair_lnc;
+  const RunDesc* runs;
+  const T* run_lnc;      // 1/2 ln C(2 l0, |mA+nA|) per run
   int* flags;
 };
 

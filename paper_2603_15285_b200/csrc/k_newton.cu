@@ -8,13 +8,15 @@
 //   q_mn = (m^2 + n^2 - 2mn cos b)/sin^2 b;  z_k = T_k e^{-i(ma+ng)}, w = 1 (m=0) or 2:
 //   C = sum w Re z0, dC/da = sum w m Im z0, dC/db = sum w Re z1, dC/dg = sum w n Im z0,
 //   H_aa = -sum w m^2 Re z0, H_gg = -sum w n^2 Re z0, H_ag = -sum w mn Re z0,
-//   H_ab = sum w m Im z1, H_bg = sum w n Im z1, H_bb = sum w Re z2.
+//   H_ab = sum w m Im z1, H_bg = sum w n Im z1, H_bb = sum w Re z2 = sum w Re((q_mn T0 - U) e) - cot(b) dC/db.
 //
-// B200 mapping: one CTA per particle; every (m,n) pair's l-run is walked by one thread which keeps
-// CG candidates' recurrence state in registers, so each M^l_mn load (8 B) and each recurrence
-// coefficient (one rsqrt) is shared by CG candidates.  Pairs are grouped by l0 (long runs first) and
-// dealt to threads in a boustrophedon order for balance.  Block reductions are warp-shuffle butterflies
-// plus a fixed-order shared-memory pass (deterministic: no atomics).  The 3x3 Newton solve runs in FP64.
+// B200 mapping: one CTA per particle.  Work item = one recurrence run (RunDesc, common.cuh): the l-run of the pair
+// (l0, n) also yields the Wigner d of its symmetry partner ((n, l0) or (-n, -l0)) up to a sign, so one recurrence
+// feeds two pairs' sums -- half the recurrence work of a per-pair walk.  A thread keeps CG candidates' recurrence
+// state in registers (each M^l load and recurrence coefficient shared by CG candidates); the candidate groups run
+// concurrently on slices of the CTA; M^l streams through a per-thread cp.async ring in shared memory.  Runs are
+// grouped by l0 (long runs first) and dealt boustrophedon.  Block reductions are fixed-order (deterministic: no
+// atomics), FP64 from the lane partials on.  The 3x3 Newton solve runs in FP64.
 #include <float.h>
 
 #include <cstdlib>
@@ -29,6 +31,14 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCG = 10;  // candidates per register group
+constexpr int kRing = 4;    // M^l is requested kRing degrees ahead of its use (per-thread cp.async ring in smem)
+
+template <int BYTES> __device__ __forceinline__ void cp_async_ca(void* sdst, const void* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(sa), "l"(gsrc), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <typename T> struct CandShared {
   T cb, sb, cot, invs2;
@@ -37,7 +47,7 @@ template <typename T> struct CandShared {
 
 struct SmemLayout {
   // offsets in bytes
-  size_t theta, cand, ea, eg, red, sums, prevc, invl, invll, flags, total;
+  size_t theta, cand, ea, eg, red, ring, sums, prevc, invl, invll, flags, total;
 };
 
 template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, int L, int cg) {
@@ -53,6 +63,7 @@ template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, i
   s.ea = take(sizeof(cplx_t<T>) * Q * (L + 1));
   s.eg = take(sizeof(cplx_t<T>) * Q * (2 * L + 1));
   s.red = take(sizeof(T) * 10 * cg * kThreads);  // per-thread partial sums [value][thread]
+  s.ring = take(sizeof(cplx_t<T>) * kRing * 2 * kThreads);  // per-thread cp.async ring of M^l (pairs A, B)
   s.sums = take(sizeof(double) * 10 * Q);
   s.prevc = take(sizeof(double) * Q);
   s.invl = take(sizeof(T) * (kMaxL + 2));
@@ -165,46 +176,70 @@ __device__ void prepare_candidates(const double* theta, int Q, int L, CandShared
     double ph;
     if (r < na) ph = -(double)r * theta[3 * c + 0];
     else ph = -(double)(r - na - L) * theta[3 * c + 2];
-    ph = fmod(ph, 2.0 * kPi);
-    double s, co;
-    sincos(ph, &s, &co);
-    if (r < na) ea[c * na + r] = mk<T>((T)co, (T)s);
-    else eg[c * ng + (r - na)] = mk<T>((T)co, (T)s);
+    ph -= 2.0 * kPi * rint(ph * (0.5 / kPi));  // FP64 reduction to [-pi, pi] (|ph| <= 2 pi kMaxL)
+    T s, co;
+    if (sizeof(T) == 4) {
+      float sf, cf;
+      sincosf((float)ph, &sf, &cf);  // reduced argument: the accurate fast path of sincosf
+      s = (T)sf;
+      co = (T)cf;
+    } else {
+      double sd, cd;
+      sincos(ph, &sd, &cd);
+      s = (T)sd;
+      co = (T)cd;
+    }
+    if (r < na) ea[c * na + r] = mk<T>(co, s);
+    else eg[c * ng + (r - na)] = mk<T>(co, s);
   }
 }
 
 // Evaluate C_L (and, if DERIV, grad and Hess) at rotations [0,Q) -> sums[c][10] (FP64 in smem).
+// Work item = one RunDesc: the recurrence of pair A = (l0, nA) also yields its partner B's d (up to the sign sB), so
+// one set of recurrence registers feeds two pairs' sums (T0, T1, U for A and for B).  The G = ceil(Q/CG) candidate
+// groups run concurrently on G slices of the CTA (Tg = kThreads/G threads each, every slice walks all runs), so the
+// few long runs of a small band are not walked G times in sequence.
 template <typename T, int CG, bool DERIV>
-__device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const PairDesc* __restrict__ pairs,
-                           const T* __restrict__ pair_lnc, const CandShared<T>* cs, const cplx_t<T>* ea,
-                           const cplx_t<T>* eg, const T* inv_l, const T* inv_ll, T* red, double* sums) {
+__device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const RunDesc* __restrict__ runs,
+                           const T* __restrict__ run_lnc, const CandShared<T>* cs, const cplx_t<T>* ea,
+                           const cplx_t<T>* eg, const T* inv_l, const T* inv_ll, T* red, cplx_t<T>* ring,
+                           double* sums) {
   constexpr int NV = DERIV ? 10 : 1;
-  const int npairs = pair_count(L);
+  const int nruns = run_count(L);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int na = L + 1, ng = 2 * L + 1;
   constexpr int NVAL = NV * CG;
+  const int G = (Q + CG - 1) / CG, Tg = kThreads / G;
+  const int g = tid / Tg, lt = tid - g * Tg;
   T* acc = red + tid;  // this thread's partial sums: value (v, k) at acc[(v * CG + k) * kThreads]
-  for (int c0 = 0; c0 < Q; c0 += CG) {
 #pragma unroll
-    for (int i = 0; i < NVAL; ++i) acc[i * kThreads] = T(0);
+  for (int i = 0; i < NVAL; ++i) acc[i * kThreads] = T(0);
+  if (g < G) {
+    const int c0 = g * CG;
     // candidate indices of this group (clamped: duplicates of the last are computed, then ignored)
     int cid[CG];
 #pragma unroll
     for (int k = 0; k < CG; ++k) cid[k] = min(c0 + k, Q - 1);
 
     for (int r = 0;; ++r) {
-      const int base = r * kThreads;
-      if (base >= npairs) break;
-      const int pi = base + ((r & 1) ? (kThreads - 1 - tid) : tid);
-      if (pi >= npairs) continue;
-      const PairDesc pd = pairs[pi];
-      const int m = pd.m, n = pd.n;
-      const int l0 = max(m, abs(n));
-      const T lnC = pair_lnc[pi];
+      const int base = r * Tg;
+      if (base >= nruns) break;
+      const int ri = base + ((r & 1) ? (Tg - 1 - lt) : lt);
+      if (ri >= nruns) continue;
+      const RunDesc rd = runs[ri];
+      const int m = rd.mA, n = rd.nA;
+      const int l0 = m > abs(n) ? m : abs(n);
+      const bool pairB = rd.mB >= 0;
+      const int mB = pairB ? rd.mB : m, nB = pairB ? rd.nB : n;
+      // weight of B's terms: (1 or 2) x the symmetry sign, 0 when A runs alone
+      const T sB = (nB == m && ((m - n) & 1)) ? T(-1) : T(1);
+      const T wB = pairB ? sB * ((mB == 0) ? T(1) : T(2)) : T(0);
+      const T lnC = run_lnc[ri];
       const int mn = m * n, m2 = m * m, n2 = n * n;
       // recurrence state
       T d[CG], dprev[CG], dp[CG], dpprev[CG];
-      T t0r[CG], t0i[CG], t1r[CG], t1i[CG], ur[CG], ui[CG];
+      T a0r[CG], a0i[CG], a1r[CG], a1i[CG], aur[CG], aui[CG];  // pair A: T0, T1, U
+      T b0r[CG], b0i[CG], b1r[CG], b1i[CG], bur[CG], bui[CG];  // pair B
 #pragma unroll
       for (int k = 0; k < CG; ++k) {
         T dd, ddp = T(0);
@@ -213,7 +248,8 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
         dp[k] = ddp;
         dprev[k] = T(0);
         dpprev[k] = T(0);
-        t0r[k] = t0i[k] = t1r[k] = t1i[k] = ur[k] = ui[k] = T(0);
+        a0r[k] = a0i[k] = a1r[k] = a1i[k] = aur[k] = aui[k] = T(0);
+        b0r[k] = b0i[k] = b1r[k] = b1i[k] = bur[k] = bui[k] = T(0);
       }
       T cbk[CG], sbk[CG];
 #pragma unroll
@@ -222,40 +258,57 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
         sbk[k] = cs[cid[k]].sb;
       }
       (void)sbk;
-      // M^l_mn for l = l0.. lives at half_offset(l) + m(2l+1) + n + l (consecutive l differ by (l+1)(2l+1)+2m+1).
-      // The l-loop is unrolled by two so that d^{l-1} is overwritten in place by d^{l+1} (no register rotation);
-      // M is loaded two degrees ahead of its use.
-      const cplx_t<T>* pM = M + pd.off0;
-      int inc = (l0 + 1) * (2 * l0 + 1) + 2 * m + 1;  // pointer step l0 -> l0 + 1; grows by 4l + 5
-      auto next_ptr = [&](int l) {                   // advance pM from degree l to l + 1
-        pM += inc;
-        inc += 4 * l + 5;
+      // M^l_mn for l = l0.. lives at half_offset(l) + m(2l+1) + n + l: consecutive degrees differ by
+      // (l+1)(2l+1) + 2m + 1 (B's step is A's + 2(mB - m)).  Each thread streams its run's M^l (A and B) through
+      // its own kRing-deep cp.async ring in shared memory, kRing degrees ahead of use (no registers held by the
+      // loads in flight); the l-loop is unrolled by two so that d^{l-1} is overwritten in place by d^{l+1}.
+      const cplx_t<T>* pA = M + rd.offA;
+      const cplx_t<T>* pB = M + rd.offB;
+      int inc = (l0 + 1) * (2 * l0 + 1) + 2 * m + 1;  // pointer step li -> li + 1; grows by 4 li + 5
+      const int dB = 2 * (mB - m);
+      int li = l0;                                     // next degree to request
+      cplx_t<T>* rg = ring + tid;                      // slot (j, pair) at rg[(2 j + pair) * kThreads]
+      auto request = [&](int slot) {
+        if (li <= L) {
+          cp_async_ca<sizeof(cplx_t<T>)>(rg + (2 * slot) * kThreads, pA);
+          cp_async_ca<sizeof(cplx_t<T>)>(rg + (2 * slot + 1) * kThreads, pB);
+        }
+        cp_async_commit();
+        pA += inc;
+        pB += inc + dB;
+        inc += 4 * li + 5;
+        ++li;
       };
-      const cplx_t<T> zero = mk<T>(T(0), T(0));
-      cplx_t<T> M0 = __ldg(pM), M1 = zero;
-      if (l0 < L) {
-        next_ptr(l0);
-        M1 = __ldg(pM);
-      }
+#pragma unroll
+      for (int j = 0; j < kRing; ++j) request(j);
       T sq = T(0);
-      auto accumulate = [&](int l, cplx_t<T> Ml, const T* dd, const T* ddp) {
-        const T mr = Ml.x, mi = Ml.y;  // conj(M) = (mr, -mi)
+      auto accumulate = [&](int l, int slot, const T* dd, const T* ddp) {
+        cp_async_wait<kRing - 1>();  // degree l has landed
+        const cplx_t<T> Ma = rg[(2 * slot) * kThreads], Mb = rg[(2 * slot + 1) * kThreads];
+        // conj(M) = (mr, -mi)
 #pragma unroll
         for (int k = 0; k < CG; ++k) {
-          t0r[k] = fma(mr, dd[k], t0r[k]);
-          t0i[k] = fma(-mi, dd[k], t0i[k]);
+          a0r[k] = fma(Ma.x, dd[k], a0r[k]);
+          a0i[k] = fma(-Ma.y, dd[k], a0i[k]);
+          b0r[k] = fma(Mb.x, dd[k], b0r[k]);
+          b0i[k] = fma(-Mb.y, dd[k], b0i[k]);
         }
         if (DERIV) {
           const T ll = (T)(l * (l + 1));
-          const T umr = ll * mr, umi = ll * mi;
+          const T uar = ll * Ma.x, uai = ll * Ma.y, ubr = ll * Mb.x, ubi = ll * Mb.y;
 #pragma unroll
           for (int k = 0; k < CG; ++k) {
-            t1r[k] = fma(mr, ddp[k], t1r[k]);
-            t1i[k] = fma(-mi, ddp[k], t1i[k]);
-            ur[k] = fma(umr, dd[k], ur[k]);
-            ui[k] = fma(-umi, dd[k], ui[k]);
+            a1r[k] = fma(Ma.x, ddp[k], a1r[k]);
+            a1i[k] = fma(-Ma.y, ddp[k], a1i[k]);
+            aur[k] = fma(uar, dd[k], aur[k]);
+            aui[k] = fma(-uai, dd[k], aui[k]);
+            b1r[k] = fma(Mb.x, ddp[k], b1r[k]);
+            b1i[k] = fma(-Mb.y, ddp[k], b1i[k]);
+            bur[k] = fma(ubr, dd[k], bur[k]);
+            bui[k] = fma(-ubi, dd[k], bui[k]);
           }
         }
+        request(slot);  // the slot is consumed (its values are in registers): degree l + kRing
       };
       // (cur, old) = (d^l, d^{l-1}) -> old := d^{l+1}:  d^{l+1} = (A cos b - B) d^l - C d^{l-1},
       //                                                 d'^{l+1} = (A cos b - B) d'^l - A sin b d^l - C d'^{l-1}
@@ -269,67 +322,68 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
           old[k] = fma(coef, cur[k], -Cc * old[k]);
         }
       };
-      for (int l = l0;; l += 2) {
-        cplx_t<T> N0 = zero, N1 = zero;
-        if (l + 2 <= L) {
-          next_ptr(l + 1);
-          N0 = __ldg(pM);
-          if (l + 3 <= L) {
-            next_ptr(l + 2);
-            N1 = __ldg(pM);
-          }
-        }
-        accumulate(l, M0, d, dp);
+      for (int l = l0, slot = 0;; l += 2, slot = (slot + 2) & (kRing - 1)) {
+        accumulate(l, slot, d, dp);
         if (l == L) break;
         advance(l, d, dprev, dp, dpprev);  // dprev := d^{l+1}
-        accumulate(l + 1, M1, dprev, dpprev);
+        accumulate(l + 1, slot + 1, dprev, dpprev);
         if (l + 1 == L) break;
         advance(l + 1, dprev, d, dpprev, dp);  // d := d^{l+2}
-        M0 = N0;
-        M1 = N1;
       }
-      // assembly with the phase e^{-i(m a + n g)}
-      const T w = (m == 0) ? T(1) : T(2);
-      const T fm = (T)m, fn = (T)n;
-      const T wm = w * fm, wn = w * fn, wmm = -fm * fm, wnn = -fn * fn, wmn = -fm * fn;
+      // assembly with the phase e^{-i(m a + n g)} of each pair; both pairs' terms are summed in registers before
+      // the one read-modify-write of this thread's partial sums.  H_bb's -cot(b) T1 part is factored out of the sum
+      // (cot is per rotation): value 5 collects w Re((q_mn T0 - U) e) and -cot dC/db is added after the reduction.
+      const T wA = (m == 0) ? T(1) : T(2);
 #pragma unroll
       for (int k = 0; k < CG; ++k) {
-        const cplx_t<T> pa = ea[cid[k] * na + m], pg = eg[cid[k] * ng + (n + L)];
-        const T er = pa.x * pg.x - pa.y * pg.y, ei = pa.x * pg.y + pa.y * pg.x;
-        const T z0r = t0r[k] * er - t0i[k] * ei, z0i = t0r[k] * ei + t0i[k] * er;
-        acc[(0 * CG + k) * kThreads] += w * z0r;
-        if (DERIV) {
-          const CandShared<T>& c = cs[cid[k]];
-          const T z1r = t1r[k] * er - t1i[k] * ei, z1i = t1r[k] * ei + t1i[k] * er;
-          const T qmn = ((T)(m2 + n2) - T(2) * (T)mn * c.cb) * c.invs2;
-          const T t2r = -c.cot * t1r[k] + qmn * t0r[k] - ur[k];
-          const T t2i = -c.cot * t1i[k] + qmn * t0i[k] - ui[k];
-          const T z2r = t2r * er - t2i * ei;
-          const T wz0 = w * z0r;
-          acc[(1 * CG + k) * kThreads] += wm * z0i;
-          acc[(2 * CG + k) * kThreads] += w * z1r;
-          acc[(3 * CG + k) * kThreads] += wn * z0i;
-          acc[(4 * CG + k) * kThreads] += wmm * wz0;
-          acc[(5 * CG + k) * kThreads] += w * z2r;
-          acc[(6 * CG + k) * kThreads] += wnn * wz0;
-          acc[(7 * CG + k) * kThreads] += wm * z1i;
-          acc[(8 * CG + k) * kThreads] += wmn * wz0;
-          acc[(9 * CG + k) * kThreads] += wn * z1i;
-        }
+        T v[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = T(0);
+        auto contrib = [&](int pm, int pn, T w, T t0r, T t0i, T t1r, T t1i, T ur, T ui) {
+          const cplx_t<T> pa = ea[cid[k] * na + pm], pg = eg[cid[k] * ng + (pn + L)];
+          const T er = pa.x * pg.x - pa.y * pg.y, ei = pa.x * pg.y + pa.y * pg.x;
+          const T z0r = t0r * er - t0i * ei, z0i = t0r * ei + t0i * er;
+          v[0] = fma(w, z0r, v[0]);
+          if (DERIV) {
+            const CandShared<T>& c = cs[cid[k]];
+            const T fm = (T)pm, fn = (T)pn;
+            const T z1r = t1r * er - t1i * ei, z1i = t1r * ei + t1i * er;
+            const T qmn = ((T)(pm * pm + pn * pn) - T(2) * (T)(pm * pn) * c.cb) * c.invs2;
+            const T uR = ur * er - ui * ei;
+            const T wz0 = w * z0r, wz0i = w * z0i, wz1i = w * z1i;
+            v[1] = fma(fm, wz0i, v[1]);
+            v[2] = fma(w, z1r, v[2]);
+            v[3] = fma(fn, wz0i, v[3]);
+            v[4] = fma(-fm * fm, wz0, v[4]);
+            v[5] = fma(w, fma(qmn, z0r, -uR), v[5]);
+            v[6] = fma(-fn * fn, wz0, v[6]);
+            v[7] = fma(fm, wz1i, v[7]);
+            v[8] = fma(-fm * fn, wz0, v[8]);
+            v[9] = fma(fn, wz1i, v[9]);
+          }
+        };
+        contrib(m, n, wA, a0r[k], a0i[k], a1r[k], a1i[k], aur[k], aui[k]);
+        contrib(mB, nB, wB, b0r[k], b0i[k], b1r[k], b1i[k], bur[k], bui[k]);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[(i * CG + k) * kThreads] += v[i];
       }
     }
-    // deterministic block reduction: warp w sums values w, w + kWarps, ... over the 256 threads in a fixed order
-    // (FP64 lane partials, then a butterfly)
-    __syncthreads();
-    for (int i = warp; i < NVAL; i += kWarps) {
-      const T* row = red + i * kThreads;
-      double sacc = 0.0;
-#pragma unroll
-      for (int u = 0; u < kThreads / 32; ++u) sacc += (double)row[lane + 32 * u];
-      sacc = warp_sum(sacc);
-      const int v = i / CG, k = i % CG;
-      if (lane == 0 && c0 + k < Q) sums[(c0 + k) * 10 + v] = sacc;
-    }
+  }
+  // deterministic block reduction: warp w sums rows (group, value) w, w + kWarps, ... over the group's Tg threads in
+  // a fixed order (FP64 lane partials, then a butterfly)
+  __syncthreads();
+  for (int i = warp; i < G * NVAL; i += kWarps) {
+    const int gg = i / NVAL, vk = i - gg * NVAL;
+    const T* row = red + vk * kThreads + gg * Tg;
+    double sacc = 0.0;
+    for (int t = lane; t < Tg; t += 32) sacc += (double)row[t];
+    sacc = warp_sum(sacc);
+    const int v = vk / CG, k = vk % CG, c = gg * CG + k;
+    if (lane == 0 && c < Q) sums[c * 10 + v] = sacc;
+  }
+  __syncthreads();
+  if (DERIV) {
+    for (int c = tid; c < Q; c += kThreads) sums[c * 10 + 5] -= (double)cs[c].cot * sums[c * 10 + 2];
     __syncthreads();
   }
 }
@@ -353,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
   cplx_t<T>* eg = (cplx_t<T>*)(smem + lay.eg);
   T* red = (T*)(smem + lay.red);
+  cplx_t<T>* ring = (cplx_t<T>*)(smem + lay.ring);
   double* sums = (double*)(smem + lay.sums);
   T* inv_l = (T*)(smem + lay.invl);
   T* inv_ll = (T*)(smem + lay.invll);
@@ -363,8 +418,8 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   __syncthreads();
   prepare_candidates<T>(theta, Q, L, cs, ea, eg);
   __syncthreads();
-  if (derivs) eval_block<T, CG, true>(M, L, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
-  else eval_block<T, CG, false>(M, L, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+  if (derivs) eval_block<T, CG, true>(M, L, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
+  else eval_block<T, CG, false>(M, L, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
   for (int c = threadIdx.x; c < Q; c += blockDim.x) {
     const double* s = sums + c * 10;
     a.value[p * Q + c] = (T)s[0];
@@ -392,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   cplx_t<T>* ea = (cplx_t<T>*)(smem + lay.ea);
   cplx_t<T>* eg = (cplx_t<T>*)(smem + lay.eg);
   T* red = (T*)(smem + lay.red);
+  cplx_t<T>* ring = (cplx_t<T>*)(smem + lay.ring);
   double* sums = (double*)(smem + lay.sums);
   T* inv_l = (T*)(smem + lay.invl);
   T* inv_ll = (T*)(smem + lay.invll);
@@ -418,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
       if (!*any) break;
       prepare_candidates<T>(theta, Q, L, cs, ea, eg);
       __syncthreads();
-      eval_block<T, CG, true>(M, L, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+      eval_block<T, CG, true>(M, L, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
       for (int c = threadIdx.x; c < Q; c += blockDim.x) {
         if (!run[c]) continue;
         const double* sm = sums + c * 10;
@@ -450,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   // final C_{L_J} of every candidate and the argmax
   prepare_candidates<T>(theta, Q, Lmax_b, cs, ea, eg);
   __syncthreads();
-  eval_block<T, CG, false>(M, Lmax_b, Q, a.pairs, a.pair_lnc, cs, ea, eg, inv_l, inv_ll, red, sums);
+  eval_block<T, CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
   for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) a.euler[cb0 * 3 + t] = (T)theta[t];
   for (int c = threadIdx.x; c < Q; c += blockDim.x) {
     const double v = act[c] ? sums[c * 10] : -INFINITY;

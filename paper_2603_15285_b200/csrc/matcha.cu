@@ -36,6 +36,8 @@ struct matcha_ctx {
   int tcP = 0;              // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel)
   PairDesc* d_pairs = nullptr;
   void* d_pair_lnc = nullptr;
+  RunDesc* d_runs = nullptr;
+  void* d_run_lnc = nullptr;
   int* d_flags = nullptr;
   // align workspace (sized by max_batch)
   void* ws_F = nullptr;
@@ -303,8 +305,8 @@ bool valid_params(const matcha_params_t* p, int LM, std::string& why) {
 template <typename T> NewtonArgs<T> newton_args(matcha_handle_t h) {
   NewtonArgs<T> a;
   std::memset(&a, 0, sizeof(a));
-  a.pairs = h->d_pairs;
-  a.pair_lnc = (const T*)h->d_pair_lnc;
+  a.runs = h->d_runs;
+  a.run_lnc = (const T*)h->d_run_lnc;
   a.flags = h->d_flags;
   return a;
 }
@@ -799,6 +801,24 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     for (int n = -k; n <= k; ++n) add(k, n);
     for (int m = 0; m < k; ++m) { add(m, -k); add(m, k); }
   }
+  // stage-4 runs (RunDesc): each shell's pairs folded by the d symmetries, singles (k,+-k), (0,-k) alone
+  std::vector<RunDesc> runs;
+  std::vector<double> rlnc;
+  auto hoff = [](int l, int m, int n) { return (int32_t)(half_offset(l) + (int64_t)m * (2 * l + 1) + (n + l)); };
+  for (int k = 0; k <= h->L; ++k) {
+    auto addr = [&](int mA, int nA, int mB, int nB) {
+      const int32_t oA = hoff(k, mA, nA);
+      runs.push_back(RunDesc{(int16_t)mA, (int16_t)nA, (int16_t)mB, (int16_t)nB, oA, mB >= 0 ? hoff(k, mB, nB) : oA});
+      const int p = std::abs(mA + nA);
+      rlnc.push_back(0.5 * (std::lgamma(2.0 * k + 1.0) - std::lgamma(p + 1.0) - std::lgamma(2.0 * k - p + 1.0)));
+    };
+    if (k == 0) { addr(0, 0, -1, 0); continue; }
+    for (int n = -k + 1; n < 0; ++n) addr(k, n, -n, -k);
+    for (int n = 0; n < k; ++n) addr(k, n, n, k);
+    addr(k, k, -1, 0);
+    addr(k, -k, -1, 0);
+    addr(0, -k, -1, 0);
+  }
   cudaError_t e = cudaSuccess;
   if (h->fp64) {
     upload<double>(&h->d_node, node, e);
@@ -807,6 +827,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     upload<double>(&h->d_pwp, pwp, e);
     upload<double>(&h->d_dft, dft, e);
     upload<double>(&h->d_pair_lnc, plnc, e);
+    upload<double>(&h->d_run_lnc, rlnc, e);
   } else {
     upload<float>(&h->d_node, node, e);
     upload<float>(&h->d_tw, tw, e);
@@ -814,6 +835,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
     upload<float>(&h->d_pwp, pwp, e);
     upload<float>(&h->d_dft, dft, e);
     upload<float>(&h->d_pair_lnc, plnc, e);
+    upload<float>(&h->d_run_lnc, rlnc, e);
   }
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pwp_off, sizeof(int) * poff.size());
   if (e == cudaSuccess) e = cudaMemcpy(h->d_pwp_off, poff.data(), sizeof(int) * poff.size(), cudaMemcpyHostToDevice);
@@ -821,6 +843,8 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   if (e == cudaSuccess) e = cudaMemcpy(h->d_pw_moff, moff.data(), sizeof(int) * moff.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_pairs, sizeof(PairDesc) * pairs.size());
   if (e == cudaSuccess) e = cudaMemcpy(h->d_pairs, pairs.data(), sizeof(PairDesc) * pairs.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_runs, sizeof(RunDesc) * runs.size());
+  if (e == cudaSuccess) e = cudaMemcpy(h->d_runs, runs.data(), sizeof(RunDesc) * runs.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc((void**)&h->d_flags, sizeof(int) * 4);
   if (e == cudaSuccess) e = cudaMemset(h->d_flags, 0, sizeof(int) * 4);
   // align workspace
@@ -862,7 +886,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
 
 MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (!h) return MATCHA_ERR_INVALID_ARG;
-  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
+  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_runs, h->d_run_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
                   h->ws_euler, h->ws_score, h->ws_idx, h->ws_best, h->ws_vols[0], h->ws_vols[1], h->ws_poses,
                   h->ws_ref};
   for (void* p : ptrs)

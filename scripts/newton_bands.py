@@ -1,5 +1,6 @@
 """Time the evaluation kernel per band (derivs / value-only) on c2-shaped M: where stage 4's time goes."""
 import numpy as np, torch, time
+import sys, os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_15285_b200 as mt
 torch.manual_seed(0)
 B, L = 1000, 32

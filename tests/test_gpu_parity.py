@@ -128,6 +128,32 @@ def test_eval_corr_parity(N, L, Leval, prec):
             assert np.abs(hess[p, q] - H).max() <= h_tol(H, E, Leval, fp64), (p, q, hess[p, q], H)
 
 
+@pytest.mark.parametrize("Q", [1, 2, 3, 4, 5, 9, 10])
+@pytest.mark.parametrize("derivs", [True, False], ids=["derivs", "value"])
+def test_eval_corr_candidate_groups(Q, derivs, prec):
+    """Every register-group size the kernel picks for Q candidates (pick_cg: 1, 2, 4, 5 in FP32; 1, 2 in FP64),
+    with and without derivatives (the value-only path is the final C_{L_J} of newton_refine)."""
+    N, L = 64, 32
+    b = gen.particles(N, 1, 0.1, seed=29)
+    Fo = O.sh_analysis_batch(b.vols, L)
+    Ho = O.sh_analysis(b.ref, L)
+    r = np.random.default_rng(Q)
+    eul = np.stack([r.uniform(0, 2 * np.pi, (1, Q)), r.uniform(0, np.pi, (1, Q)), r.uniform(0, 2 * np.pi, (1, Q))], -1)
+    h = handle(N, L, prec)
+    Mf = O.corr_full(Fo[0], Ho, L)
+    val, grad, hess = h.eval_corr(cuda(O.full_to_half(Mf, L)[None], h.cplx), L, L, cuda(eul, h.real), derivs)
+    eul_used = to_np(cuda(eul, h.real)).astype(np.float64)
+    E = O.energy(Fo[0], Ho, L)
+    fp64 = prec == "fp64"
+    val = to_np(val)
+    for q in range(Q):
+        C, g, H = O.eval_corr(Mf, L, eul_used[0, q])
+        assert abs(val[0, q] - C) <= c_tol(C, E, fp64), (q, val[0, q], C)
+        if derivs:
+            assert np.abs(to_np(grad)[0, q] - g).max() <= g_tol(g, E, L, fp64), q
+            assert np.abs(to_np(hess)[0, q] - H).max() <= h_tol(H, E, L, fp64), q
+
+
 # ------------------------------------------------------------------ stage 3
 @pytest.mark.parametrize("N,L,L0,K,nc", [(64, 32, 8, 2, 10), (32, 8, 4, 2, 4), (128, 64, 12, 2, 16),
                                          (32, 8, 8, 1, 32), (64, 32, 30, 2, 10)])
@@ -214,11 +240,14 @@ def test_newton_refine_parity(N, L, bands, nc, iters, prec):
                 nbad += 1
             else:
                 assert abs(sg[p, c] - so[c]) <= c_tol(so[c], E, prec == "fp64")
-        # the selected pose: same candidate, or a tie within the C tolerance (reading C23)
+        # the selected pose: same candidate, or (reading C23, several correct results) another pose that the oracle
+        # itself scores at least as high as its own choice -- e.g. a chaotic candidate whose FP32 path climbed to a
+        # better maximum than its FP64 path; the GPU's reported score must be the oracle's score at that pose
         assert stable[bo]
-        if bg[p] != bo:
-            assert abs(so[bg[p]] - so[bo]) <= c_tol(so[bo], E)
-        assert rot_err_deg(eg[p, bg[p]], eo[bo]) <= TOL_ROT_DEG or abs(so[bg[p]] - so[bo]) <= c_tol(so[bo], E)
+        if bg[p] != bo and rot_err_deg(eg[p, bg[p]], eo[bo]) > TOL_ROT_DEG:
+            Cg = O.eval_corr(Mf, bands[-1], eg[p, bg[p]].astype(np.float64))[0]
+            assert abs(sg[p, bg[p]] - Cg) <= c_tol(Cg, E, prec == "fp64"), (p, sg[p, bg[p]], Cg)
+            assert Cg >= so[bo] - c_tol(so[bo], E), (p, bg[p], bo, Cg, so[bo])
     assert ntot >= B and nbad <= 0.001 * ntot, (nbad, ntot)
 
 

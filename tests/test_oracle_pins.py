@@ -99,6 +99,21 @@ def test_wigner_d_vs_explicit_sum(l):
                 assert abs(d[m + l, n + l] - _d_explicit(l, m, n, b)) < 1e-13
 
 
+@pytest.mark.parametrize("l", [1, 4, 9])
+def test_wigner_d_pair_symmetries(l):
+    """The identities stage 4 folds its (m, n) runs by (common.cuh RunDesc): d^l_{nm} = (-1)^{m-n} d^l_{mn} and
+    d^l_{-n,-m} = d^l_{mn}, checked on Wigner's explicit sum and on the oracle's d."""
+    for b in (0.37, 1.9, 2.8):
+        d = O.wigner_d(l, b)
+        for m in range(-l, l + 1):
+            for n in range(-l, l + 1):
+                ref = _d_explicit(l, m, n, b)
+                assert abs(_d_explicit(l, n, m, b) - (-1) ** (m - n) * ref) < 1e-13
+                assert abs(_d_explicit(l, -n, -m, b) - ref) < 1e-13
+                assert abs(d[n + l, m + l] - (-1) ** (m - n) * d[m + l, n + l]) < 1e-13
+                assert abs(d[-n + l, -m + l] - d[m + l, n + l]) < 1e-13
+
+
 def test_wigner_d1_golden():
     for line in open(os.path.join(GOLD, "wigner_d1.txt")):
         if line.startswith("#") or not line.strip():
