@@ -6,10 +6,12 @@
 // with conj(h_{l,n}) = (-1)^n h_{l,|n|} for n < 0 (reality of h, reading C3).
 // Per degree l this is the complex GEMM [(l+1) x R] . [R x (2l+1)], batched over particles.
 //
-// This is the SIMT version (FP64 handles, and degrees / shell counts the tensor-core kernel does not take): one CTA per
-// (m block, l, particle) stages its rows of F^l [mb x R] and the weighted, conjugated, TRANSPOSED reference block
-// Ht^l [R x (2l+1)] in shared memory (consecutive n on consecutive banks; F rows broadcast), in chunks of rc shells
-// when a whole block does not fit (large R, FP64); each thread owns up to 4 outputs M^l_mn accumulated over the chunks.
+// This is the SIMT version (FP64 handles, and degrees / shell counts the tensor-core kernel does not take).  Per degree l
+// the product is one real-shaped GEMM over all particles, rows (p, m), columns n, K = R shells, with the (weighted,
+// conjugated) reference block Ht^l [R x (2l+1)] shared by every row.  One CTA computes a 64 x 64 complex tile of it:
+// 16-shell chunks of the F rows and of Ht^l (built from H on the way in) are double-buffered in shared memory, k-major,
+// and each thread accumulates a 4 x 4 register tile (6 shared loads per 64 FMAs).  Tiles of all degrees form one grid,
+// large l first.
 #include <algorithm>
 
 #include "common.cuh"
@@ -18,112 +20,120 @@ namespace matcha {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kOut = 4;  // outputs per thread
+constexpr int kBM = 64, kBN = 64, kBK = 16;  // tile rows (p, m), tile columns n, shells per chunk
+constexpr int kThreads = 256;                 // 16 x 16 threads, 4 x 4 outputs each
+
+struct CorrTiles {
+  int L;
+  int64_t start[kMaxL + 2];  // start[i]: first tile of degree L - i; start[L + 1] = number of tiles
+};
+
+__host__ __device__ inline int col_tiles(int l) { return (2 * l + 1 + kBN - 1) / kBN; }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_corr_coeffs(const cplx_t<T>* __restrict__ F,
-                                                          const cplx_t<T>* __restrict__ H, int L, int Lmax, int R,
-                                                          int mb, int rc, cplx_t<T>* __restrict__ M) {
+__global__ void __launch_bounds__(kThreads) k_corr_tiled(const cplx_t<T>* __restrict__ F, const cplx_t<T>* __restrict__ H,
+                                                         int64_t B, int Lmax, int R, const __grid_constant__ CorrTiles tl,
+                                                         cplx_t<T>* __restrict__ M) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int l = L - (int)blockIdx.y;  // big blocks first
-  const int m0 = blockIdx.x * mb;
-  if (m0 > l) return;
-  const int nm = min(mb, l + 1 - m0);
-  const int64_t p = blockIdx.z;
-  const int w = 2 * l + 1;
+  cplx_t<T>* As = (cplx_t<T>*)smem;      // [2][kBK][kBM]
+  cplx_t<T>* Bs = As + 2 * kBK * kBM;    // [2][kBK][kBN]
+  const int L = tl.L;
+  const int64_t t = blockIdx.x;
+  int i = 0;
+  while (t >= tl.start[i + 1]) ++i;      // uniform walk over <= L + 1 entries (constant bank)
+  const int l = L - i, w = 2 * l + 1, ct = col_tiles(l);
+  const int64_t local = t - tl.start[i];
+  const int64_t rt = local / ct;
+  const int c0 = (int)(local - rt * ct) * kBN;
+  const int64_t rho0 = rt * kBM, nrows = B * (l + 1);
   const int ncf = ncoef(Lmax);
-  cplx_t<T>* Fl = (cplx_t<T>*)smem;   // [nm][rc]
-  cplx_t<T>* Ht = Fl + mb * rc;       // [rc][w]
-  const cplx_t<T>* Fp = F + p * (int64_t)ncf * R + (int64_t)lm_index(l, m0) * R;
-  const cplx_t<T>* Hl = H + (int64_t)lm_index(l, 0) * R;
-  T ar[kOut], ai[kOut];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  // staging assignments: A row ar, shells ak..ak+3; B column bc, shells bk..bk+3
+  const int ar = tid >> 2, ak = (tid & 3) * 4, bc = tid & 63, bk = (tid >> 6) * 4;
+  const int64_t rho = rho0 + ar;
+  const cplx_t<T>* Frow = nullptr;
+  if (rho < nrows) {
+    const int64_t p = rho / (l + 1);
+    const int m = (int)(rho - p * (l + 1));
+    Frow = F + p * (int64_t)ncf * R + (int64_t)(lm_index(l, 0) + m) * R;
+  }
+  const int n = c0 + bc - l;
+  const cplx_t<T>* Hrow = (c0 + bc < w) ? H + (int64_t)lm_index(l, abs(n)) * R : nullptr;
+  const cplx_t<T> zero = mk<T>(T(0), T(0));
+  cplx_t<T> ra[4], rb[4];
+  auto fetch = [&](int r0) {
 #pragma unroll
-  for (int q = 0; q < kOut; ++q) ar[q] = ai[q] = T(0);
-  for (int r0 = 0; r0 < R; r0 += rc) {
-    const int nr = min(rc, R - r0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < nm * nr; t += kThreads) {
-      const int m = t / nr, i = t - m * nr;
-      Fl[m * rc + i] = Fp[(int64_t)m * R + r0 + i];
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + ak + j;
+      ra[j] = (Frow && r < R) ? Frow[r] : zero;
     }
-    for (int t = threadIdx.x; t < nr * w; t += kThreads) {
-      const int n = t / nr - l, i = t % nr;  // read H coalesced along r
-      const T r = (T)(r0 + i) + T(0.5), wr = r * r;
-      const cplx_t<T> h = Hl[(size_t)abs(n) * R + r0 + i];
-      cplx_t<T> v;
-      if (n >= 0) v = mk<T>(wr * h.x, -wr * h.y);                  // w conj(h_{l,n})
-      else v = (n & 1) ? mk<T>(-wr * h.x, -wr * h.y) : mk<T>(wr * h.x, wr * h.y);  // w (-1)^n h_{l,|n|}
-      Ht[i * w + (n + l)] = v;
-    }
-    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < kOut; ++q) {
-      const int o = threadIdx.x + q * kThreads;
-      if (o < nm * w) {
-        const int m = o / w, nn = o - m * w;
-        const cplx_t<T>* fr = Fl + m * rc;
-        T xr = ar[q], xi = ai[q];
-#pragma unroll 4
-        for (int i = 0; i < nr; ++i) {
-          const cplx_t<T> f = fr[i], h = Ht[i * w + nn];
-          xr = fma(f.x, h.x, xr);
-          xr = fma(-f.y, h.y, xr);
-          xi = fma(f.x, h.y, xi);
-          xi = fma(f.y, h.x, xi);
-        }
-        ar[q] = xr;
-        ai[q] = xi;
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + bk + j;
+      cplx_t<T> v = zero;
+      if (Hrow && r < R) {
+        const T rr = (T)r + T(0.5), wr = rr * rr;
+        const cplx_t<T> h = Hrow[r];
+        if (n >= 0) v = mk<T>(wr * h.x, -wr * h.y);                                  // w conj(h_{l,n})
+        else v = (n & 1) ? mk<T>(-wr * h.x, -wr * h.y) : mk<T>(wr * h.x, wr * h.y);  // w (-1)^n h_{l,|n|}
       }
+      rb[j] = v;
     }
-  }
-  cplx_t<T>* Mo = M + p * half_size(L) + half_offset(l) + (int64_t)m0 * w;
+  };
+  auto stash = [&](int buf) {
+    cplx_t<T>* a = As + buf * kBK * kBM;
+    cplx_t<T>* b = Bs + buf * kBK * kBN;
 #pragma unroll
-  for (int q = 0; q < kOut; ++q) {
-    const int o = threadIdx.x + q * kThreads;
-    if (o < nm * w) Mo[o] = mk<T>(ar[q], ai[q]);
-  }
-}
-
-// one CTA per (particle, l) when the whole block fits shared memory (all of c3 / c5): F^l and Ht^l staged once
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_corr_coeffs_whole(const cplx_t<T>* __restrict__ F,
-                                                          const cplx_t<T>* __restrict__ H, int L, int Lmax, int R,
-                                                          cplx_t<T>* __restrict__ M) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int l = L - (int)(blockIdx.x % (L + 1));  // big blocks first
-  const int64_t p = blockIdx.x / (L + 1);
-  const int w = 2 * l + 1;
-  const int ncf = ncoef(Lmax);
-  cplx_t<T>* Fl = (cplx_t<T>*)smem;   // [(l+1)][R]
-  cplx_t<T>* Ht = Fl + (l + 1) * R;   // [R][w]
-  const cplx_t<T>* Fp = F + p * (int64_t)ncf * R + (int64_t)lm_index(l, 0) * R;
-  const cplx_t<T>* Hl = H + (int64_t)lm_index(l, 0) * R;
-  for (int t = threadIdx.x; t < (l + 1) * R; t += kThreads) Fl[t] = Fp[t];
-  for (int t = threadIdx.x; t < R * w; t += kThreads) {
-    const int n = t / R - l, i = t % R;  // read H coalesced along r
-    const T r = (T)i + T(0.5), wr = r * r;
-    const cplx_t<T> h = Hl[(size_t)abs(n) * R + i];
-    cplx_t<T> v;
-    if (n >= 0) v = mk<T>(wr * h.x, -wr * h.y);                  // w conj(h_{l,n})
-    else v = (n & 1) ? mk<T>(-wr * h.x, -wr * h.y) : mk<T>(wr * h.x, wr * h.y);  // w (-1)^n h_{l,|n|}
-    Ht[i * w + (n + l)] = v;
-  }
-  __syncthreads();
-  cplx_t<T>* Mo = M + p * half_size(L) + half_offset(l);
-  for (int o = threadIdx.x; o < (l + 1) * w; o += kThreads) {
-    const int m = o / w, nn = o - m * w;
-    const cplx_t<T>* fr = Fl + m * R;
-    T ar = T(0), ai = T(0);
-#pragma unroll 4
-    for (int i = 0; i < R; ++i) {
-      const cplx_t<T> f = fr[i], h = Ht[i * w + nn];
-      ar = fma(f.x, h.x, ar);
-      ar = fma(-f.y, h.y, ar);
-      ai = fma(f.x, h.y, ai);
-      ai = fma(f.y, h.x, ai);
+    for (int j = 0; j < 4; ++j) {
+      a[(ak + j) * kBM + ar] = ra[j];
+      b[(bk + j) * kBN + bc] = rb[j];
     }
-    Mo[o] = mk<T>(ar, ai);
+  };
+  T accr[4][4], acci[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) accr[u][v] = acci[u][v] = T(0);
+  const int nch = (R + kBK - 1) / kBK;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) fetch((c + 1) * kBK);  // global loads of chunk c + 1 in flight during the FMAs of chunk c
+    const cplx_t<T>* a = As + buf * kBK * kBM + ty * 4;
+    const cplx_t<T>* b = Bs + buf * kBK * kBN + tx;
+#pragma unroll
+    for (int k = 0; k < kBK; ++k) {
+      cplx_t<T> av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = a[k * kBM + u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = b[k * kBN + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          accr[u][v] = fma(av[u].x, bv[v].x, fma(-av[u].y, bv[v].y, accr[u][v]));
+          acci[u][v] = fma(av[u].x, bv[v].y, fma(av[u].y, bv[v].x, acci[u][v]));
+        }
+    }
+    if (c + 1 < nch) stash(buf ^ 1);
+    __syncthreads();
+  }
+  const int64_t hs = half_size(L), ho = half_offset(l);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t r = rho0 + ty * 4 + u;
+    if (r >= nrows) continue;
+    const int64_t p = r / (l + 1);
+    const int m = (int)(r - p * (l + 1));
+    cplx_t<T>* Mo = M + p * hs + ho + (int64_t)m * w;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int col = c0 + tx + 16 * v;
+      if (col < w) Mo[col] = mk<T>(accr[u][v], acci[u][v]);
+    }
   }
 }
 
@@ -133,30 +143,19 @@ template <typename T>
 cudaError_t launch_corr_coeffs(const cplx_t<T>* F, const cplx_t<T>* H, int64_t B, int L, int Lmax, int R,
                                cplx_t<T>* M, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
-  const size_t whole = sizeof(cplx_t<T>) * (size_t)R * ((L + 1) + (2 * L + 1));
-  if (whole <= 200 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_corr_coeffs_whole<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)whole);
-    if (e != cudaSuccess) return e;
-    k_corr_coeffs_whole<T><<<(unsigned)(B * (L + 1)), kThreads, whole, s>>>(F, H, L, Lmax, R, M);
-    return cudaGetLastError();
+  if (L > kMaxL) return cudaErrorInvalidValue;
+  CorrTiles tl;
+  tl.L = L;
+  tl.start[0] = 0;
+  for (int i = 0; i <= L; ++i) {
+    const int l = L - i;
+    tl.start[i + 1] = tl.start[i] + (B * (l + 1) + kBM - 1) / kBM * col_tiles(l);
   }
-  const int w = 2 * L + 1;
-  const int mb = std::max(1, std::min(L + 1, kOut * kThreads / w));  // rows of the widest block per CTA
-  const size_t cs = sizeof(cplx_t<T>), budget = 200 * 1024;
-  int rc = R;
-  while (rc > 1 && cs * (size_t)rc * (mb + w) > budget) rc = (rc + 1) / 2;
-  const size_t bytes = cs * (size_t)rc * (mb + w);
-  cudaError_t e = cudaFuncSetAttribute(k_corr_coeffs<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const size_t bytes = sizeof(cplx_t<T>) * 2 * kBK * (kBM + kBN);
+  cudaError_t e = cudaFuncSetAttribute(k_corr_tiled<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
-  for (int64_t b0 = 0; b0 < B; b0 += 65535) {  // gridDim.z <= 65535
-    const int64_t nb = std::min<int64_t>(65535, B - b0);
-    const dim3 grid((unsigned)((L + 1 + mb - 1) / mb), (unsigned)(L + 1), (unsigned)nb);
-    k_corr_coeffs<T><<<grid, kThreads, bytes, s>>>(F + b0 * (int64_t)ncoef(Lmax) * R, H, L, Lmax, R, mb, rc,
-                                                   M + b0 * half_size(L));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  k_corr_tiled<T><<<(unsigned)tl.start[L + 1], kThreads, bytes, s>>>(F, H, B, Lmax, R, tl, M);
+  return cudaGetLastError();
 }
 
 template cudaError_t launch_corr_coeffs<float>(const float2*, const float2*, int64_t, int, int, int, float2*,

@@ -99,6 +99,29 @@ def test_corr_coeffs_parity(N, L, Lc, prec):
         assert np.abs(M[p] - Mo).max() <= (1e-12 if prec == "fp64" else 1e-5) * scale
 
 
+@pytest.mark.parametrize("L,R,B,Lc", [(48, 48, 70, 48), (64, 64, 9, 61), (100, 100, 3, 100), (20, 20, 37, 20),
+                                      (7, 4, 300, 7)])
+def test_corr_coeffs_tiled_parity(L, R, B, Lc, prec):
+    """Stage 2 on the tiled SIMT kernel (every degree / shell count the tensor-core kernel does not take, and FP64):
+    row tiles spanning particles with ragged tails, column tiles of 2l+1 > 64, shell chunks with R % 16 != 0 (R = N/2, N a multiple of 8).
+    F and H are seeded complex Gaussians shaped like shell coefficients (inputs, not method output)."""
+    r = np.random.default_rng(L * 1000 + R)
+    nc = mt.ncoef(L)
+    scale = (1.0 / (1.0 + np.arange(nc)))[:, None] * np.ones((1, R))
+    F = (r.normal(size=(B, nc, R)) + 1j * r.normal(size=(B, nc, R))) * scale
+    H = (r.normal(size=(nc, R)) + 1j * r.normal(size=(nc, R))) * scale
+    for l in range(L + 1):  # m = 0 entries real (reading C3)
+        F[:, l * (l + 1) // 2, :] = F[:, l * (l + 1) // 2, :].real
+        H[l * (l + 1) // 2, :] = H[l * (l + 1) // 2, :].real
+    h = handle(2 * R, L, prec)
+    M = to_np(h.corr_coeffs(cuda(F, h.cplx), cuda(H, h.cplx), Lc))
+    Fq = to_np(cuda(F, h.cplx)).astype(np.complex128)
+    Hq = to_np(cuda(H, h.cplx)).astype(np.complex128)
+    for p in sorted({0, B // 2, B - 1}):
+        Mo = O.full_to_half(O.corr_full(Fq[p], Hq, Lc), Lc)
+        assert np.abs(M[p] - Mo).max() <= (1e-12 if prec == "fp64" else 1e-5) * np.abs(Mo).max(), p
+
+
 # ------------------------------------------------------------------ C_L, grad, Hess (the evaluation kernel)
 @pytest.mark.parametrize("N,L,Leval", [(64, 32, 32), (64, 32, 24), (64, 32, 8), (32, 8, 8), (128, 64, 64),
                                        (64, 100, 100), (64, 100, 60)])
