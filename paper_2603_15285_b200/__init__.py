@@ -159,7 +159,7 @@ class Handle:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # _lib is None during interpreter shutdown
             _lib.matcha_destroy(h)
             self._h = None
 

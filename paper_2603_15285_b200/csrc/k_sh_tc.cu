@@ -399,6 +399,14 @@ __global__ void __launch_bounds__(kThr + 32, 1)
   } else {
     // ================================================================ sampler warps (512 threads)
     auto sbar = []() { asm volatile("bar.sync 1, %0;\n" ::"r"(kThr)); };
+    auto sbar_or = [](bool v) {  // sampler barrier that also ORs a predicate over the 512 sampler threads
+      int r;
+      asm volatile(
+          "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 q, %1, 0;\n\tbar.red.or.pred p, 1, %2, q;\n\tselp.s32 %0, 1, 0, p;\n\t}\n"
+          : "=r"(r)
+          : "r"((int)v), "n"(kThr));
+      return r != 0;
+    };
     uint32_t dph = 0u;       // bit b: parity of the next completion of done[b]
     uint64_t l2_stream;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(l2_stream));
@@ -481,29 +489,49 @@ __global__ void __launch_bounds__(kThr + 32, 1)
         asm volatile("cp.async.commit_group;\n" ::);
       };
       request(min(zfirst + P - 1, N));
-      // ---- 2. tiles: <= NR consecutive rings whose planes fit the P-slot window (cut at z-bucket boundaries)
-      if (tid == 0) {
-        auto zlo_of = [&](int b) { return min(max(b - 2, -1), N - 1); };
-        int nt = 0, s0 = 0;
-        while (s0 < nrings) {
-          int b0 = 0;
-          {
-            const int r = list[s0];
-            b0 = bucket(zfloor(r >> 16, r & 0xffff));
-          }
-          const int zl = zlo_of(b0);
-          int bx = b0;  // first bucket whose plane is beyond the window
-          while (bx < nbk && zlo_of(bx) <= zl + P - 2) ++bx;
-          const int e = min(s0 + NR, boff[bx]);
-          const int rl = list[e - 1];
-          tstart[nt] = s0;
-          tlo[nt] = zl;
-          thi[nt] = zlo_of(bucket(zfloor(rl >> 16, rl & 0xffff))) + 1;
-          ++nt;
-          s0 = e;
+      // ---- 2. tiles: <= NR consecutive rings whose planes fit the P-slot window.  Fixed chunks of NR rings when every
+      //      chunk needs <= P planes (the common case: one thread per chunk); otherwise a greedy cut at z-bucket
+      //      boundaries by one thread.  The tiling does not change any result (rings are independent MMA columns).
+      auto zlo_of = [&](int b) { return min(max(b - 2, -1), N - 1); };
+      {
+        const int nchunk = (nrings + NR - 1) / NR;
+        bool bad = false;
+        for (int c = tid; c < nchunk; c += kThr) {
+          const int s0 = c * NR, e = min(s0 + NR, nrings);
+          const int r0 = list[s0], r1 = list[e - 1];
+          const int lo = zlo_of(bucket(zfloor(r0 >> 16, r0 & 0xffff)));
+          const int hi = zlo_of(bucket(zfloor(r1 >> 16, r1 & 0xffff))) + 1;
+          tstart[c] = s0;
+          tlo[c] = lo;
+          thi[c] = hi;
+          bad = bad || (hi - lo + 1 > P);
         }
-        tstart[nt] = nrings;
-        *s_nt = nt;
+        if (tid == 0) {
+          tstart[nchunk] = nrings;
+          *s_nt = nchunk;
+        }
+        if (sbar_or(bad) && tid == 0) {
+          int nt = 0, s0 = 0;
+          while (s0 < nrings) {
+            int b0 = 0;
+            {
+              const int r = list[s0];
+              b0 = bucket(zfloor(r >> 16, r & 0xffff));
+            }
+            const int zl = zlo_of(b0);
+            int bx = b0;  // first bucket whose plane is beyond the window
+            while (bx < nbk && zlo_of(bx) <= zl + P - 2) ++bx;
+            const int e = min(s0 + NR, boff[bx]);
+            const int rl = list[e - 1];
+            tstart[nt] = s0;
+            tlo[nt] = zl;
+            thi[nt] = zlo_of(bucket(zfloor(rl >> 16, rl & 0xffff))) + 1;
+            ++nt;
+            s0 = e;
+          }
+          tstart[nt] = nrings;
+          *s_nt = nt;
+        }
       }
       sbar();
       const int ntiles = *s_nt;
@@ -610,6 +638,42 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             if (xr < RPW && in) {
               const float2 phx = tw[xcol];
               ex = tri_xy<NT>(planes + b0, dz, N, fmaf(rs, phx.x, cx), fmaf(rs, phx.y, cy), fz);
+            }
+          }
+          // m = L when 2(L+1) = 130 > 128 MMA rows (L = 64): its two DFT rows from the FP32 samples, in the sampler.
+          // The lane's mirrored phi indices k, k+Mp, Mp-k, 2Mp-k (n_phi = 2Mp) carry e^{-iL phi} = e, s e, s conj(e),
+          // conj(e) with e = e^{-iL phi_k}, s = (-1)^L.
+          if (nrow > kTM) {
+            const float sgn = (L & 1) ? -1.f : 1.f;
+            __syncwarp();  // sl[] written by lane rr above
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+              float re = 0.f, im = 0.f;
+#pragma unroll
+              for (int kr = 0; kr < KR; ++kr) {
+                const int k = 32 * kr + lane + 1;
+                if (k <= Kh) {
+                  const float2 e = tw[(L * k) % nph];
+                  const float* x = sv[kr][rr];
+                  re = fmaf(e.x, (x[0] + x[3]) + sgn * (x[1] + x[2]), re);
+                  im = fmaf(e.y, (sgn * x[2] + x[3]) - (x[0] + sgn * x[1]), im);
+                }
+              }
+              if (xr == rr) {
+                const float2 e = tw[(L * xcol) % nph];
+                re = fmaf(ex, e.x, re);
+                im = fmaf(-ex, e.y, im);
+              }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                re += __shfl_xor_sync(0xffffffffu, re, o);
+                im += __shfl_xor_sync(0xffffffffu, im, o);
+              }
+              const int goff = sl[warp + rr * kWarps];
+              if (lane == 0 && goff >= 0) {
+                Gp[goff + 2 * L] = re * dscale;
+                Gp[goff + 2 * L + 1] = im * dscale;
+              }
             }
           }
           long long tq2 = clock64();
@@ -721,31 +785,42 @@ __global__ void __launch_bounds__(kThr + 32, 1)
 
 // plane slots for the TC ring kernel (0 = not supported for this handle: use the SIMT kernel).  Tiles are cut at
 // z-bucket boundaries so that they never need more than P planes; larger P prefetches further ahead.
-// rings per tile of the handle: 64 with one k round (Kh <= 32), 32 with two (Kh <= 64)
-static int tc_nr(const ShTables<float>& tab) { return (tab.nph / 2 - 1) / 2 <= 32 ? 64 : 32; }
-
-int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode) {
+// Plane slots P and rings per tile NR for a handle (0 = not supported: use the SIMT kernel).  Preferred: 64 rings per
+// tile with one k round (Kh <= 32), 32 with two (Kh <= 64), at least 3 plane slots (one tile of prefetch); large
+// boxes (128^3: a 128 x 136 plane is 70 KB) fall back to 16-ring tiles and/or 2 plane slots (tiles then stay inside
+// one z bucket and each bucket's new plane is loaded between tiles).
+int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode, int* nr_out) {
   (void)xnode;
-  if (2 * (tab.L + 1) > kTM) return 0;
-  const int Mp = tab.nph / 2, Kh = (Mp - 1) / 2, NR = tc_nr(tab);
+  if (2 * (tab.L + 1) > kTM + 2) return 0;  // the MMA's 128 rows hold m < 64; m = L = 64 is computed by the samplers
+  const int Mp = tab.nph / 2, Kh = (Mp - 1) / 2;
   if (Kh > 64 || Kh < 1) return 0;  // at most two rounds of 32 k per lane
+  if (2 * (tab.L + 1) > kTM && Kh <= 32) return 0;
   const int Kp = (tab.nph + 15) / 16 * 16;
-  if ((Kp + 31) / 32 * 32 + 2 * NR > 512) return 0;
   if (tab.N % 4 || tab.R * tab.nth >= (1 << 22) || tab.nth > 0xffff) return 0;
   const size_t budget = 225 * 1024;
-  int P = 3;
-  if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total > budget) return 0;
-  while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1, NR).total <= budget) ++P;
-  // the counting-sort table aliases the planes
-  if ((size_t)2 * (tab.N + 3) * tab.nth * sizeof(int) > (size_t)P * tab.N * plane_pitch_tc(tab.N) * sizeof(float)) return 0;
-  return P;
+  const int pref = Kh <= 32 ? 64 : 32;
+  const int opts[4][2] = {{pref, 3}, {16, 3}, {pref, 2}, {16, 2}};
+  for (const auto& o : opts) {
+    const int NR = o[0];
+    if (NR == 16 && Kh <= 32) continue;  // 16-ring tiles exist in the two-round variant only
+    if ((Kp + 31) / 32 * 32 + 2 * NR > 512) continue;
+    int P = o[1];
+    if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total > budget) continue;
+    while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1, NR).total <= budget) ++P;
+    // the counting-sort table aliases the planes
+    if ((size_t)2 * (tab.N + 3) * tab.nth * sizeof(int) > (size_t)P * tab.N * plane_pitch_tc(tab.N) * sizeof(float))
+      continue;
+    *nr_out = NR;
+    return P;
+  }
+  return 0;
 }
 
 cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shifts, int shift_stride,
                                const ShTables<float>& tab, int P, float2* G, int* flags, int num_sms,
                                cudaStream_t st) {
   if (nb == 0) return cudaSuccess;
-  const int NR = tc_nr(tab);
+  const int NR = tab.tcNR;
   const size_t bytes = tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total;
   const int grid = (int)std::min<int64_t>(nb, num_sms);
   const char* dv = getenv("MATCHA_SH_DBG");  // profiling knob: 1 = no MMA/drain, 2 = no gathers
@@ -759,9 +834,12 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
     if (tab.N == 32) go(k_sh_rings_tc<32, 64, 1>);
     else if (tab.N == 64) go(k_sh_rings_tc<64, 64, 1>);
     else go(k_sh_rings_tc<0, 64, 1>);
-  } else {
+  } else if (NR == 32) {
     if (tab.N == 96) go(k_sh_rings_tc<96, 32, 2>);
     else go(k_sh_rings_tc<0, 32, 2>);
+  } else {
+    if (tab.N == 128) go(k_sh_rings_tc<128, 16, 2>);
+    else go(k_sh_rings_tc<0, 16, 2>);
   }
   if (e != cudaSuccess) return e;
   if (dbg & 8) {

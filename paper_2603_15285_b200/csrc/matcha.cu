@@ -34,6 +34,7 @@ struct matcha_ctx {
   void* d_dft = nullptr;    // parity-split cos/sin table of the folded ring DFT
   int Kh = 0, MP = 0, pw_stride = 0;
   int tcP = 0;              // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel)
+  int tcNR = 64;            // its rings per tile
   PairDesc* d_pairs = nullptr;
   void* d_pair_lnc = nullptr;
   RunDesc* d_runs = nullptr;
@@ -281,6 +282,7 @@ template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
   t.nph = h->nph;
   t.Jh = h->Jh;
   t.tcP = sizeof(T) == 4 ? h->tcP : 0;
+  t.tcNR = h->tcNR;
   t.num_sms = h->num_sms;
   t.flags = h->d_flags;
   return t;
@@ -855,7 +857,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   if (!h->fp64 && !(getenv("MATCHA_SH_SIMT") && getenv("MATCHA_SH_SIMT")[0] == '1')) {
     std::vector<float> xn(h->nth);
     for (int j = 0; j < h->nth; ++j) xn[j] = (float)x[j];
-    h->tcP = sh_tc_plane_slots(sh_tables<float>(h), xn);
+    h->tcP = sh_tc_plane_slots(sh_tables<float>(h), xn, &h->tcNR);
   }
   {
     const size_t per = cb * (size_t)h->R * h->nth * (h->L + 1);

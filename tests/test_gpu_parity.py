@@ -57,13 +57,14 @@ def test_sh_analysis_parity(N, L, B, prec):
 
 
 @pytest.mark.parametrize("N,L,B", [(64, 32, 150), (32, 8, 160), (16, 5, 48), (48, 20, 40), (96, 48, 40),
-                                   (64, 60, 40)])
+                                   (64, 60, 40), (128, 64, 40)])
 def test_sh_analysis_tensor_core_path_parity(N, L, B):
     """Batches of at least a quarter of the SMs take the persistent tensor-core ring kernel (fp16 hi/lo split DFT,
     z-sorted rings, plane ring buffer) -- compared with the oracle on sampled particles, unshifted and shifted
     (including shifts that push samples out of the box and planes outside the volume), at the bench's launch
     configuration (sub-batches of whole waves of particles).  L = 48 and 60 take the two-k-round variant (32 rings
-    per tile, Kh <= 64: c3's stage 1 on tensor cores)."""
+    per tile, Kh <= 64: c3's stage 1 on tensor cores); 128^3 / L = 64 (c5) the 16-ring, 2-plane-slot
+    variant whose m = 64 rows come from the samplers (2(L+1) = 130 > 128 MMA rows)."""
     b = gen.particles(N, B, 0.1, seed=26)
     h = handle(N, L, "fp32", max_batch=B)
     vols = cuda(b.vols)
