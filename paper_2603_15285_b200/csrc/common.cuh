@@ -74,6 +74,7 @@ template <typename T> struct ShTables {
   int N, R, L, nth, nph, Jh, Kh, MP, pw_stride;
   int tcP;                // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel), FP32 only
   int tcNR;               // rings per tile of the tensor-core ring kernel (64, 32 or 16)
+  int* tc_list;           // its per-CTA ring-list workspace [num_sms][R * nth] when the list leaves shared memory
   int num_sms;
   int* flags;
 };
@@ -146,7 +147,7 @@ size_t search_smem_bytes(int L0, int K, bool fp64);
 bool so3_large_needed(int L0, int K, bool fp64);
 size_t so3_large_workspace_bytes(int L0, int K, int ncand, bool fp64);
 template <typename T> cudaError_t launch_so3_search_large(const SearchArgs<T>& a, void* ws, cudaStream_t s);
-int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode, int* nr);
+int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode, int* nr, int* glist);
 cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shifts, int shift_stride,
                                const ShTables<float>& tab, int P, float2* G, int* flags, int num_sms,
                                cudaStream_t st);

@@ -55,7 +55,8 @@ struct TcLayout {
   int Kp, Kc, lbo, P, maxtiles;
 };
 
-__host__ __device__ inline TcLayout tc_layout(int N, int R, int nth, int nph, int P, int NR) {
+// glist: the z-sorted ring list lives in a global workspace instead of shared memory (large boxes)
+__host__ __device__ inline TcLayout tc_layout(int N, int R, int nth, int nph, int P, int NR, bool glist = false) {
   TcLayout s;
   s.Kp = (nph + 15) / 16 * 16;  // K padded to the fp16 MMA K-step
   s.Kc = s.Kp / 8;              // 16-byte K chunks (8 fp16)
@@ -73,7 +74,7 @@ __host__ __device__ inline TcLayout tc_layout(int N, int R, int nth, int nph, in
   s.tw = take(sizeof(float2) * nph, 16);
   s.node = take(sizeof(float2) * nth, 16);
   s.planes = take(sizeof(float) * (size_t)P * N * plane_pitch_tc(N), 16);
-  s.list = take(sizeof(int) * (size_t)R * nth, 16);
+  s.list = take(glist ? 0 : sizeof(int) * (size_t)R * nth, 16);
   s.slots = take(sizeof(int) * 3 * kSlotFields * NR, 16);
   s.tiles = take(sizeof(int) * ((size_t)3 * s.maxtiles + 1 + (N + 4) + (N + 2)), 16);
   s.misc = take(64 + sizeof(int) * (4 + kWarps), 16);
@@ -273,14 +274,14 @@ __global__ void __launch_bounds__(kThr + 32, 1)
   const int R = tab.R, L = tab.L, nth = tab.nth, nph = tab.nph;
   const int Mp = nph / 2, Kh = (Mp - 1) / 2;
   const bool mid = (Mp % 2) == 0;
-  const TcLayout lay = tc_layout(N, R, nth, nph, P, NR);
+  const TcLayout lay = tc_layout(N, R, nth, nph, P, NR, tab.tc_list != nullptr);
   const int Kp = lay.Kp, Kc = lay.Kc, LBO = lay.lbo;
   const int PW = plane_pitch_tc(N), PS = N * PW;
   unsigned char* Bs = smem + lay.B;  // buffer b: hi at Bs + (2b) Kc LBO, lo at + (2b+1) Kc LBO
   float2* tw = (float2*)(smem + lay.tw);
   float2* node = (float2*)(smem + lay.node);
   float* planes = (float*)(smem + lay.planes);
-  int* list = (int*)(smem + lay.list);
+  int* list = tab.tc_list ? tab.tc_list + (size_t)blockIdx.x * R * nth : (int*)(smem + lay.list);
   int* cnt = (int*)(smem + lay.planes);  // counting-sort table [N+3][nth], aliases the planes between particles
   int* slots = (int*)(smem + lay.slots);  // [3 tiles][kSlotFields][NR]
   int* tstart = (int*)(smem + lay.tiles);  // [max tiles + 1] first ring of each tile
@@ -789,7 +790,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
 // tile with one k round (Kh <= 32), 32 with two (Kh <= 64), at least 3 plane slots (one tile of prefetch); large
 // boxes (128^3: a 128 x 136 plane is 70 KB) fall back to 16-ring tiles and/or 2 plane slots (tiles then stay inside
 // one z bucket and each bucket's new plane is loaded between tiles).
-int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode, int* nr_out) {
+int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnode, int* nr_out, int* glist_out) {
   (void)xnode;
   if (2 * (tab.L + 1) > kTM + 2) return 0;  // the MMA's 128 rows hold m < 64; m = L = 64 is computed by the samplers
   const int Mp = tab.nph / 2, Kh = (Mp - 1) / 2;
@@ -799,18 +800,21 @@ int sh_tc_plane_slots(const ShTables<float>& tab, const std::vector<float>& xnod
   if (tab.N % 4 || tab.R * tab.nth >= (1 << 22) || tab.nth > 0xffff) return 0;
   const size_t budget = 225 * 1024;
   const int pref = Kh <= 32 ? 64 : 32;
-  const int opts[4][2] = {{pref, 3}, {16, 3}, {pref, 2}, {16, 2}};
+  // {rings per tile, minimum plane slots, ring list in global memory}, in order of preference (measured)
+  const int opts[6][3] = {{pref, 3, 0}, {pref, 3, 1}, {16, 3, 0}, {pref, 2, 1}, {16, 2, 0}, {16, 2, 1}};
   for (const auto& o : opts) {
     const int NR = o[0];
+    const bool gl = o[2] != 0;
     if (NR == 16 && Kh <= 32) continue;  // 16-ring tiles exist in the two-round variant only
     if ((Kp + 31) / 32 * 32 + 2 * NR > 512) continue;
     int P = o[1];
-    if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total > budget) continue;
-    while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1, NR).total <= budget) ++P;
+    if (tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR, gl).total > budget) continue;
+    while (P < tab.N + 2 && tc_layout(tab.N, tab.R, tab.nth, tab.nph, P + 1, NR, gl).total <= budget) ++P;
     // the counting-sort table aliases the planes
     if ((size_t)2 * (tab.N + 3) * tab.nth * sizeof(int) > (size_t)P * tab.N * plane_pitch_tc(tab.N) * sizeof(float))
       continue;
     *nr_out = NR;
+    *glist_out = gl ? 1 : 0;
     return P;
   }
   return 0;
@@ -821,7 +825,7 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
                                cudaStream_t st) {
   if (nb == 0) return cudaSuccess;
   const int NR = tab.tcNR;
-  const size_t bytes = tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR).total;
+  const size_t bytes = tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR, tab.tc_list != nullptr).total;
   const int grid = (int)std::min<int64_t>(nb, num_sms);
   const char* dv = getenv("MATCHA_SH_DBG");  // profiling knob: 1 = no MMA/drain, 2 = no gathers
   const int dbg = dv ? atoi(dv) : 0;
@@ -836,6 +840,7 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
     else go(k_sh_rings_tc<0, 64, 1>);
   } else if (NR == 32) {
     if (tab.N == 96) go(k_sh_rings_tc<96, 32, 2>);
+    else if (tab.N == 128) go(k_sh_rings_tc<128, 32, 2>);
     else go(k_sh_rings_tc<0, 32, 2>);
   } else {
     if (tab.N == 128) go(k_sh_rings_tc<128, 16, 2>);

@@ -35,6 +35,7 @@ struct matcha_ctx {
   int Kh = 0, MP = 0, pw_stride = 0;
   int tcP = 0;              // plane slots of the tensor-core ring kernel (0 = SIMT ring kernel)
   int tcNR = 64;            // its rings per tile
+  int* ws_tclist = nullptr; // its ring-list workspace when the list does not fit shared memory
   PairDesc* d_pairs = nullptr;
   void* d_pair_lnc = nullptr;
   RunDesc* d_runs = nullptr;
@@ -283,6 +284,7 @@ template <typename T> ShTables<T> sh_tables(matcha_handle_t h) {
   t.Jh = h->Jh;
   t.tcP = sizeof(T) == 4 ? h->tcP : 0;
   t.tcNR = h->tcNR;
+  t.tc_list = h->ws_tclist;
   t.num_sms = h->num_sms;
   t.flags = h->d_flags;
   return t;
@@ -857,7 +859,9 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
   if (!h->fp64 && !(getenv("MATCHA_SH_SIMT") && getenv("MATCHA_SH_SIMT")[0] == '1')) {
     std::vector<float> xn(h->nth);
     for (int j = 0; j < h->nth; ++j) xn[j] = (float)x[j];
-    h->tcP = sh_tc_plane_slots(sh_tables<float>(h), xn, &h->tcNR);
+    int gl = 0;
+    h->tcP = sh_tc_plane_slots(sh_tables<float>(h), xn, &h->tcNR, &gl);
+    if (h->tcP > 0 && gl && e == cudaSuccess) e = cudaMalloc((void**)&h->ws_tclist, sizeof(int) * (size_t)h->num_sms * h->R * h->nth);
   }
   {
     const size_t per = cb * (size_t)h->R * h->nth * (h->L + 1);
@@ -888,7 +892,7 @@ MATCHA_API matcha_status_t matcha_create(const matcha_config_t* cfg, matcha_hand
 
 MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (!h) return MATCHA_ERR_INVALID_ARG;
-  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_runs, h->d_run_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G,
+  void* ptrs[] = {h->d_node, h->d_tw, h->d_pw, h->d_pw_moff, h->d_pwp, h->d_pwp_off, h->d_dft, h->d_pairs, h->d_pair_lnc, h->d_runs, h->d_run_lnc, h->d_flags, h->ws_F, h->ws_M, h->ws_H, h->ws_G, h->ws_tclist,
                   h->ws_euler, h->ws_score, h->ws_idx, h->ws_best, h->ws_vols[0], h->ws_vols[1], h->ws_poses,
                   h->ws_ref};
   for (void* p : ptrs)
