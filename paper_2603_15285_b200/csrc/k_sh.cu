@@ -805,6 +805,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   asm volatile("cp.async.wait_group 1;\n" ::);  // this thread's part of the weight table
   const int ntiles = leg_tiles_par(L);
   __shared__ int tmap[kLegLaneThreads];            // thread tile -> (m, parity, l-block)
+  __shared__ int toff[kLegLaneThreads];            // thread tile -> offset of its first weight in a W row
   for (int t = tid; t < ntiles; t += 2 * LT) {
     int m = 0, par = 0, lb = t;
     for (; m <= L; ++m) {
@@ -816,6 +817,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
       lb -= to;
     }
     tmap[t] = (lb << 17) | (par << 16) | m;
+    toff[t] = tab.pwp_off[2 * m + par] + 4 * lb;
   }
   __syncthreads();                                // the whole weight table and the tile map
   const int half = nth / 2;
@@ -853,7 +855,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
     for (int tile = ltid; tile < ntiles; tile += LT) {
       const int m = tmap[tile] & 0xffff, par = (tmap[tile] >> 16) & 1, lb = tmap[tile] >> 17;
       const int l0t = m + par + 8 * lb;  // degrees l0t, l0t + 2, l0t + 4, l0t + 6 (same parity of l - m)
-      const T* wrow = W + __ldg(&tab.pwp_off[2 * m + par]) + 4 * lb;
+      const T* wrow = W + toff[tile];
       T ar[4][SG], ai[4][SG];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
