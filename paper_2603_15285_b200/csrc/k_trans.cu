@@ -783,19 +783,24 @@ __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft,
 // Around the integer window peak t0 the correlation's real trigonometric interpolant (reading C27)
 //   c~(t) = (1/N^3) sum_{k in [0,N)^3} F^(k) conj(rho^(k)) D(kx,tx) D(ky,ty) D(kz,tz)   (see ups_phase)
 // is evaluated on t = t0 + (u - h) / kappa, u in [0, U)^3, U = 2h + 1, h = ceil(1.5 kappa), by three matrix-multiply
-// DFTs; the result is the grid argmax (ties -> lowest index, z-major).
+// DFTs; the result is the grid argmax (ties -> lowest index, z-major).  D(k, t0 + s) = e^{2 pi i k t0 / N} D(k, s) for
+// the integer t0 (at the Nyquist index too: cos(pi (t0 + s)) = (-1)^t0 cos(pi s)), so the per-particle part is one
+// phase e^{2 pi i (kx tx0 + ky ty0 + kz tz0) / N} folded into X, and the three DFT matrices D(k, s_u) are constants:
 //   k_zfft_cross  3-D spectra from the plane spectra: the z FFT of f~ and rho~ pencils (Stockham in shared memory),
-//                 X = F^ conj(rho^) written over rho~ (never needed again this alternation);
-//   k_ups_xy      per (kz plane, particle): Z2[kz][uy][ux] = sum_ky Ey[ky][uy] sum_kx wx Ex[kx][ux] X[kz][ky][kx]
-//                 (half spectrum in kx: w = 1 at kx = 0 and N/2, else w = 2; Re taken at the end makes the half sum
-//                 exact for the Hermitian X);
-//   k_ups_z       per (block of (uy, ux), particle): c~ = Re sum_kz Ez[kz][uz] Z2[kz][uy][ux] for all uz, block argmax;
-//   k_ups_final   per particle: argmax over the blocks, t = t0 + (u - h)/kappa, peak = c~ / ... (already 1/N^3).
+//                 X' = F^ conj(rho^) e^{2 pi i k.t0 / N} written over rho~ (never needed again this alternation);
+//   k_ups_left    mode products with the constant D [U][N] (register-tiled GEMMs, 64-column tiles):
+//                 Z1[uz][ky][kx] = sum_kz D[uz][kz] X'[kz][ky][kx]   (one [U x N] x [N x N H] GEMM per particle)
+//                 Z2[uz][uy][kx] = sum_ky D[uy][ky] Z1[uz][ky][kx]   (one [U x N] x [N x H] GEMM per (particle, uz));
+//   k_ups_xmax    c~ = Re sum_kx w D[kx][ux] Z2[uz][uy][kx] (half spectrum in kx: w = 1 at kx = 0 and N/2, else 2;
+//                 Re at the end makes the half sum exact for the Hermitian X) per 64-row block, block argmax;
+//   k_ups_final   per particle: argmax over the blocks, t = t0 + (u - h)/kappa, peak = c~ / N^3.
+// Contracting z, y, x in that order costs U N^2 H + U^2 N H + U^3 H complex MACs (39 M at 96^3, kappa = 16).
 
 // z FFT of the plane spectra of one (ky row, kx chunk) -> X over rt
 template <typename T>
 __global__ void __launch_bounds__(256) k_zfft_cross(const cplx_t<T>* __restrict__ ft, cplx_t<T>* __restrict__ rt,
-                                                    const __grid_constant__ FftRadix fr, int hc) {
+                                                    const __grid_constant__ FftRadix fr, int hc,
+                                                    const int* __restrict__ tint) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = fr.n, H = N / 2 + 1, nkc = (H + hc - 1) / hc;
   cplx_t<T>* tw = reinterpret_cast<cplx_t<T>*>(smem_raw);
@@ -815,17 +820,23 @@ __global__ void __launch_bounds__(256) k_zfft_cross(const cplx_t<T>* __restrict_
   __syncthreads();
   const cplx_t<T>* Fz = stockham<T>(f0, f1, nk, fr, tw);
   const cplx_t<T>* Rz = stockham<T>(r0, r1, nk, fr, tw);
+  const int tx0 = tint[p * 3], ty0 = tint[p * 3 + 1], tz0 = tint[p * 3 + 2];
   for (int i = threadIdx.x; i < N * nk; i += blockDim.x) {
     const int kz = i / nk, kl = i - kz * nk;
     const cplx_t<T> f = Fz[kl * N + kz], r = Rz[kl * N + kz];
-    rt[((p * N + kz) * N + ky) * (int64_t)H + kx0 + kl] = mk<T>(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
+    const cplx_t<T> x = mk<T>(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
+    // e^{+2 pi i m / N} = conj(tw[m]),  m = k . t0 mod N
+    const int m = (int)((((int64_t)(kx0 + kl) * tx0 + (int64_t)ky * ty0 + (int64_t)kz * tz0) % N + N) % N);
+    const cplx_t<T> e = tw[m];
+    rt[((p * N + kz) * N + ky) * (int64_t)H + kx0 + kl] = mk<T>(x.x * e.x + x.y * e.y, x.y * e.x - x.x * e.y);
   }
 }
 
 // FP32, compile-time N: the same z FFTs with ct_fft, cp.async-staged lines, one CTA per (ky row, particle)
 template <int N>
 __global__ void __launch_bounds__(kFftThreads, 1) k_zfft_cross_fast(const float2* __restrict__ ft,
-                                                                    float2* __restrict__ rt) {
+                                                                    float2* __restrict__ rt,
+                                                                    const int* __restrict__ tint) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int H = N / 2 + 1, LB = fpad(H * N);
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -851,10 +862,16 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_zfft_cross_fast(const float2
   float2* rtmp = (Fz == f0) ? t1 : f0;        // the buffer not holding F^
   // r0 -> rtmp -> r0 ...: ct_fft alternates the two buffers it is given
   const float2* Rz = ct_fft<N, H, N>(rin, rtmp, tw);
+  const int tx0 = tint[p * 3], ty0 = tint[p * 3 + 1], tz0 = tint[p * 3 + 2];
+  const int myz = ((ky * ty0) % N + N) % N;
   for (int i = threadIdx.x; i < N * H; i += kFftThreads) {
     const int kz = i / H, kx = i - kz * H;
     const float2 f = Fz[fpad(kx * N + kz)], r = Rz[fpad(kx * N + kz)];
-    rt[row0 + (int64_t)kz * N * H + kx] = make_float2(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
+    const float2 x = make_float2(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
+    // the per-particle phase of the upsampled DFT: e^{+2 pi i m / N} = conj(tw[m]),  m = k . t0 mod N
+    const int m = ((kx * tx0 + kz * tz0) % N + N + myz) % N;
+    const float2 e = tw[m];
+    rt[row0 + (int64_t)kz * N * H + kx] = make_float2(x.x * e.x + x.y * e.y, x.y * e.x - x.x * e.y);
   }
 }
 
@@ -873,155 +890,168 @@ template <typename T> __device__ __forceinline__ cplx_t<T> ups_phase(int k, int 
   return mk<T>(cs, sn);
 }
 
-// register-tiled complex GEMM in shared memory: C[m][n] (+)= sum_k A[m*lda + k] B[k*ldb + n] for m < M, n < NP
-// (NP a multiple of 4; columns beyond the valid range are computed on zero-padded B and discarded by the caller).
-// Each thread owns 4 x 4 outputs: per k, 8 shared-memory loads for 16 complex MACs.
+__host__ __device__ inline int ups_pad4(int U) { return (U + 3) / 4 * 4; }
+
+constexpr int kUpsMaxU = 65;       // kappa <= 21
+constexpr int kUpsThreads = 224;   // 208 active: 13 x 16 (left) or 16 x 13 (xmax) thread tiles of 4 x 4
+constexpr int kUpsCols = 64;       // columns per CTA tile
+
+// the constant DFT matrices: D [U][N] = D(k, s_u) (reading C27 with t0 = 0), Dx [H][UP] = w(kx) D(kx, s_ux)
 template <typename T>
-__device__ __forceinline__ void cgemm_4x4(const cplx_t<T>* __restrict__ A, int lda, const cplx_t<T>* __restrict__ B,
-                                          int ldb, int M, int K, int NP, cplx_t<T>* __restrict__ C, int ldc) {
-  const int tn = NP / 4, ntile = ((M + 3) / 4) * tn;
-  for (int t = threadIdx.x; t < ntile; t += blockDim.x) {
-    const int m0 = (t / tn) * 4, n0 = (t - (t / tn) * tn) * 4;
-    T ar[4][4], ai[4][4];
+__global__ void k_ups_tables(int N, int kappa, cplx_t<T>* __restrict__ D, cplx_t<T>* __restrict__ Dx) {
+  const int H = N / 2 + 1, h = (int)ceil(1.5 * kappa), U = 2 * h + 1, UP = ups_pad4(U);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < U * N + H * UP; i += gridDim.x * blockDim.x) {
+    if (i < U * N) {
+      const int u = i / N, k = i - u * N;
+      D[i] = ups_phase<T>(k, N, 0, u, h, kappa);
+    } else {
+      const int j = i - U * N, kx = j / UP, u = j - kx * UP;
+      const T w = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
+      const cplx_t<T> e = u < U ? ups_phase<T>(kx, N, 0, u, h, kappa) : mk<T>(T(0), T(0));
+      Dx[j] = mk<T>(w * e.x, w * e.y);
+    }
+  }
+}
+
+template <typename T> __host__ __device__ inline size_t ups_left_smem(int N, int U) {
+  return sizeof(cplx_t<T>) * (size_t)N * (ups_pad4(U) + kUpsCols);
+}
+
+// out[s][u][c] = sum_{k < K} D[u][k] in[s][k][c]  (c < C; slice s = blockIdx.y, 64-column tile blockIdx.x): D staged
+// k-major, the input tile [K][64] staged, 4 (u) x 4 (c) complex outputs per thread (8 shared loads per 16 MACs)
+template <typename T>
+__global__ void __launch_bounds__(kUpsThreads) k_ups_left(const cplx_t<T>* __restrict__ D, int U, int K,
+                                                          const cplx_t<T>* __restrict__ in, int64_t in_ss, int C,
+                                                          cplx_t<T>* __restrict__ out, int64_t out_ss) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int UP = ups_pad4(U);
+  cplx_t<T>* Ds = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [K][UP]
+  cplx_t<T>* Is = Ds + K * UP;                                // [K][64]
+  const int64_t sl = blockIdx.y;
+  const int c0 = blockIdx.x * kUpsCols;
+  const cplx_t<T> zero = mk<T>(T(0), T(0));
+  for (int i = threadIdx.x; i < K * UP; i += blockDim.x) {
+    const int k = i / UP, u = i - k * UP;
+    Ds[i] = u < U ? D[u * K + k] : zero;
+  }
+  const cplx_t<T>* src = in + sl * in_ss + c0;
+  for (int i = threadIdx.x; i < K * kUpsCols; i += blockDim.x) {
+    const int k = i / kUpsCols, c = i - k * kUpsCols;
+    Is[i] = c0 + c < C ? src[(int64_t)k * C + c] : zero;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= 13 * 16) return;
+  const int tu = t >> 4, tc = t & 15;
+  T ar[4][4], ai[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ar[i][j] = ai[i][j] = T(0);
+  const cplx_t<T>* dp = Ds + 4 * tu;
+  const cplx_t<T>* ip = Is + tc;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    cplx_t<T> a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = dp[k * UP + i];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = ip[k * kUpsCols + 16 * j];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) ar[i][j] = ai[i][j] = T(0);
-    for (int k = 0; k < K; ++k) {
-      cplx_t<T> a[4], b[4];
+      for (int j = 0; j < 4; ++j) {
+        ar[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, ar[i][j]));
+        ai[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, ai[i][j]));
+      }
+  }
+  cplx_t<T>* dst = out + sl * out_ss + c0 + tc;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = (m0 + i < M) ? A[(m0 + i) * lda + k] : mk<T>(T(0), T(0));
+  for (int i = 0; i < 4; ++i) {
+    const int u = 4 * tu + i;
+    if (u >= U) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = B[k * ldb + n0 + j];
+    for (int j = 0; j < 4; ++j)
+      if (c0 + tc + 16 * j < C) dst[(int64_t)u * C + 16 * j] = mk<T>(ar[i][j], ai[i][j]);
+  }
+}
+
+template <typename T> __host__ __device__ inline size_t ups_xmax_smem(int N, int U) {
+  const int H = N / 2 + 1;
+  return sizeof(cplx_t<T>) * ((size_t)H * ups_pad4(U) + (size_t)kUpsCols * H);
+}
+
+// c~[r][ux] = Re sum_kx Z2[r][kx] Dx[kx][ux] for a block of 64 rows r = (uz, uy) of one particle (blockIdx.y), then
+// the block's argmax (z-major index r U + ux, ties -> lowest) -> bval / bidx [particle][block]
+template <typename T>
+__global__ void __launch_bounds__(kUpsThreads) k_ups_xmax(const cplx_t<T>* __restrict__ Z2, const cplx_t<T>* __restrict__ Dx,
+                                                          int N, int U, T* __restrict__ bval, int* __restrict__ bidx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ T sv[kUpsThreads / 32];
+  __shared__ int si[kUpsThreads / 32];
+  const int H = N / 2 + 1, UP = ups_pad4(U), nrow = U * U;
+  cplx_t<T>* Ds = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [H][UP]
+  cplx_t<T>* Zs = Ds + H * UP;                               // [64][H]
+  const int64_t p = blockIdx.y;
+  const int r0 = blockIdx.x * kUpsCols;
+  for (int i = threadIdx.x; i < H * UP; i += blockDim.x) Ds[i] = Dx[i];
+  const cplx_t<T>* src = Z2 + p * (int64_t)nrow * H;
+  for (int i = threadIdx.x; i < kUpsCols * H; i += blockDim.x) {
+    const int r = i / H;
+    Zs[i] = r0 + r < nrow ? src[(int64_t)r0 * H + i] : mk<T>(T(0), T(0));
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  T bv = -INFINITY;
+  int bi = 0x7fffffff;
+  if (t < 16 * 13) {
+    const int tr = t / 13, tcol = t - tr * 13;
+    T acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
+    const cplx_t<T>* zp = Zs + 4 * tr * H;
+    const cplx_t<T>* dp = Ds + 4 * tcol;
+#pragma unroll 4
+    for (int k = 0; k < H; ++k) {
+      cplx_t<T> z[4], d[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) z[i] = zp[i * H + k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = dp[k * UP + j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          ar[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, ar[i][j]));
-          ai[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, ai[i][j]));
-        }
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(z[i].x, d[j].x, fma(-z[i].y, d[j].y, acc[i][j]));
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (m0 + i < M)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) C[(m0 + i) * ldc + n0 + j] = mk<T>(ar[i][j], ai[i][j]);
-  }
-}
-
-__host__ __device__ inline int ups_pad4(int U) { return (U + 3) / 4 * 4; }
-
-constexpr int kUpsPlanes = 4;  // kz planes per CTA (the per-particle phase tables are built once per CTA)
-
-template <typename T> __host__ __device__ inline size_t ups_xy_smem(int N, int U) {
-  const int H = N / 2 + 1, UP = ups_pad4(U);
-  // X plane [N][H] | Ex [H][UP] | Ey^T [UP][N] | Z1 [N][UP] | Z2 [UP][UP]
-  return sizeof(cplx_t<T>) * ((size_t)N * H + (size_t)H * UP + (size_t)UP * N + (size_t)N * UP + (size_t)UP * UP);
-}
-
-// per (kUpsPlanes kz planes, particle): Z1 = X Ex  ([N][H] x [H][U]),  Z2 = Ey^T Z1  ([U][N] x [N][U]), two
-// register-tiled GEMMs per plane; the phase tables Ex, Ey depend only on the particle and are built once per CTA
-template <typename T>
-__global__ void __launch_bounds__(256) k_ups_xy(const cplx_t<T>* __restrict__ X, int N, int kappa,
-                                                const int* __restrict__ tint, cplx_t<T>* __restrict__ Z2) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int H = N / 2 + 1, h = (int)ceil(1.5 * kappa), U = 2 * h + 1, UP = ups_pad4(U);
-  cplx_t<T>* Xs = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N][H]
-  cplx_t<T>* Ex = Xs + N * H;                               // [H][UP] (weights folded in, zero padded)
-  cplx_t<T>* EyT = Ex + H * UP;                             // [UP][N] (zero padded rows)
-  cplx_t<T>* Z1 = EyT + UP * N;                             // [N][UP]
-  cplx_t<T>* Zs = Z1 + N * UP;                              // [UP][UP]
-  const int64_t p = blockIdx.y;
-  const int tx0 = tint[p * 3 + 0], ty0 = tint[p * 3 + 1];
-  for (int i = threadIdx.x; i < H * UP; i += blockDim.x) {
-    const int kx = i / UP, u = i - kx * UP;
-    // Hermitian half spectrum: 1 <= kx < N/2 stand for +-kx (weight 2, Re at the end); kx = 0 and the Nyquist
-    // column (real kernel cos(pi t)) count once -- exact because D(-k, t) = conj D(k, t) for every index
-    const T w = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
-    const cplx_t<T> e = u < U ? ups_phase<T>(kx, N, tx0, u, h, kappa) : mk<T>(T(0), T(0));
-    Ex[i] = mk<T>(w * e.x, w * e.y);
-  }
-  for (int i = threadIdx.x; i < UP * N; i += blockDim.x) {
-    const int u = i / N, ky = i - u * N;
-    EyT[i] = u < U ? ups_phase<T>(ky, N, ty0, u, h, kappa) : mk<T>(T(0), T(0));
-  }
-  for (int kz = blockIdx.x * kUpsPlanes; kz < min(N, (int)(blockIdx.x + 1) * kUpsPlanes); ++kz) {
-    const cplx_t<T>* xp = X + (p * N + kz) * (int64_t)N * H;
-    for (int i = threadIdx.x; i < N * H; i += blockDim.x) Xs[i] = xp[i];
-    __syncthreads();
-    cgemm_4x4<T>(Xs, H, Ex, UP, N, H, UP, Z1, UP);
-    __syncthreads();
-    cgemm_4x4<T>(EyT, N, Z1, UP, UP, N, UP, Zs, UP);
-    __syncthreads();
-    cplx_t<T>* zo = Z2 + (p * N + kz) * (int64_t)U * U;
-    for (int i = threadIdx.x; i < U * U; i += blockDim.x) {
-      const int uy = i / U, ux = i - uy * U;
-      zo[i] = Zs[uy * UP + ux];
-    }
-  }
-}
-
-constexpr int kUpsZThreads = 128;
-constexpr int kUpsMaxU = 65;  // kappa <= 21
-
-// grid (ceil(U^2 / 128), nb): thread (uy, ux), all U values of uz in registers
-template <typename T>
-__global__ void __launch_bounds__(kUpsZThreads) k_ups_z(const cplx_t<T>* __restrict__ Z2, int N, int kappa,
-                                                        const int* __restrict__ tint, T* __restrict__ bval,
-                                                        int* __restrict__ bidx) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int h = (int)ceil(1.5 * kappa), U = 2 * h + 1;
-  cplx_t<T>* Ez = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [N][U]
-  __shared__ T sv[kUpsZThreads / 32];
-  __shared__ int si[kUpsZThreads / 32];
-  const int64_t p = blockIdx.y;
-  const int tz0 = tint[p * 3 + 2];
-  for (int i = threadIdx.x; i < N * U; i += blockDim.x) {
-    const int kz = i / U, u = i - kz * U;
-    Ez[i] = ups_phase<T>(kz, N, tz0, u, h, kappa);
-  }
-  __syncthreads();
-  const int o = blockIdx.x * kUpsZThreads + threadIdx.x;  // (uy, ux)
-  T bv = -INFINITY;
-  int bi = 0x7fffffff;
-  if (o < U * U) {
-    T acc[kUpsMaxU];
-#pragma unroll
-    for (int w = 0; w < kUpsMaxU; ++w) acc[w] = T(0);
-    const cplx_t<T>* zp = Z2 + p * (int64_t)N * U * U + o;
-    for (int kz = 0; kz < N; ++kz) {
-      const cplx_t<T> z = zp[(int64_t)kz * U * U];
-      const cplx_t<T>* er = Ez + kz * U;
-#pragma unroll
-      for (int w = 0; w < kUpsMaxU; ++w)
-        if (w < U) acc[w] = fma(z.x, er[w].x, fma(-z.y, er[w].y, acc[w]));  // Re(z e)
-    }
-#pragma unroll
-    for (int w = 0; w < kUpsMaxU; ++w)
-      if (w < U) {
-        const int idx = w * U * U + o;  // z-major grid index
-        if (better(acc[w], idx, bv, bi)) {
-          bv = acc[w];
-          bi = idx;
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + 4 * tr + i, ux = 4 * tcol + j;
+        if (r < nrow && ux < U && better(acc[i][j], r * U + ux, bv, bi)) {
+          bv = acc[i][j];
+          bi = r * U + ux;
         }
       }
   }
 #pragma unroll
-  for (int s = 16; s > 0; s >>= 1) {
-    const T v2 = __shfl_xor_sync(0xffffffffu, bv, s);
-    const int i2 = __shfl_xor_sync(0xffffffffu, bi, s);
+  for (int o = 16; o > 0; o >>= 1) {
+    const T v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
     if (better(v2, i2, bv, bi)) {
       bv = v2;
       bi = i2;
     }
   }
-  if ((threadIdx.x & 31) == 0) {
-    sv[threadIdx.x >> 5] = bv;
-    si[threadIdx.x >> 5] = bi;
+  if ((t & 31) == 0) {
+    sv[t >> 5] = bv;
+    si[t >> 5] = bi;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < kUpsZThreads / 32; ++k)
+  if (t == 0) {
+    for (int k = 1; k < kUpsThreads / 32; ++k)
       if (better(sv[k], si[k], bv, bi)) {
         bv = sv[k];
         bi = si[k];
@@ -1205,9 +1235,10 @@ cudaError_t launch_window_zcorr(const cplx_t<T>* ft, const cplx_t<T>* rt, int N,
 int ups_points(int kappa) { return 2 * (int)std::ceil(1.5 * kappa) + 1; }
 
 size_t ups_scratch_bytes(int N, int kappa, size_t csz) {
-  const size_t U = (size_t)ups_points(kappa);
-  const size_t nblk = (U * U + kUpsZThreads - 1) / kUpsZThreads;
-  return csz * (size_t)N * U * U + nblk * (csz / 2 + sizeof(int)) + 3 * sizeof(int) + 256;
+  // per particle: Z1 [U][N][H] and the block bests; the constant tables D, Dx ride along (at most once per chunk)
+  const size_t U = (size_t)ups_points(kappa), H = (size_t)N / 2 + 1;
+  const size_t nblk = (U * U + kUpsCols - 1) / kUpsCols;
+  return csz * (U * N * H) + nblk * (csz / 2 + sizeof(int)) + csz * (U * N + H * ups_pad4((int)U)) + 256;
 }
 
 static int zfft_chunk(int N, size_t csz) {
@@ -1219,15 +1250,15 @@ static int zfft_chunk(int N, size_t csz) {
 
 bool ups_supported(int N, int kappa, bool fp64) {
   const size_t csz = fp64 ? 16 : 8;
-  const int U = ups_points(kappa), H = N / 2 + 1, UP = ups_pad4(U);
-  const size_t xy = fp64 ? ups_xy_smem<double>(N, U) : ups_xy_smem<float>(N, U);
-  (void)H;
-  (void)UP;
-  return kappa >= 1 && U <= kUpsMaxU && xy <= 227 * 1024 && csz * (size_t)N * U <= 200 * 1024 &&
+  const int U = ups_points(kappa);
+  const size_t lsm = fp64 ? ups_left_smem<double>(N, U) : ups_left_smem<float>(N, U);
+  const size_t xsm = fp64 ? ups_xmax_smem<double>(N, U) : ups_xmax_smem<float>(N, U);
+  return kappa >= 1 && U <= kUpsMaxU && lsm <= 200 * 1024 && xsm <= 200 * 1024 &&
          csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
 }
 
-// per-particle scratch: Z2 [N][U][U] complex, then the block bests; tint [nb][3] from k_window_peak
+// scratch: the tables D, Dx, then Z1 [nb][U][N][H], then the block bests; Z2 [nb][U][U][H] over X (rt);
+// tint [nb][3] from k_window_peak
 template <typename T>
 cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
                              void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s) {
@@ -1243,7 +1274,7 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
     auto go = [&](auto kern, int NN) {
       const size_t sm = sizeof(float2) * ((size_t)NN + 3 * (size_t)fpad((NN / 2 + 1) * NN));
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e == cudaSuccess) kern<<<dim3((unsigned)NN, (unsigned)nb), kFftThreads, sm, s>>>(ft, rt);
+      if (e == cudaSuccess) kern<<<dim3((unsigned)NN, (unsigned)nb), kFftThreads, sm, s>>>(ft, rt, tint);
       fast = true;
     };
     if (N == 32) go(k_zfft_cross_fast<32>, 32);
@@ -1254,23 +1285,37 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
   if (!fast) {
     e = cudaFuncSetAttribute(k_zfft_cross<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
     if (e != cudaSuccess) return e;
-    k_zfft_cross<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, fft_radix(N), hc);
+    k_zfft_cross<T><<<dim3((unsigned)(N * nkc), (unsigned)nb), 256, zsm, s>>>(ft, rt, fft_radix(N), hc, tint);
   }
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
-  cplx_t<T>* Z2 = reinterpret_cast<cplx_t<T>*>(scratch);
-  const int nblk = (U * U + kUpsZThreads - 1) / kUpsZThreads;
-  T* bval = reinterpret_cast<T*>(Z2 + nb * (int64_t)N * U * U);
+  const int UP = ups_pad4(U);
+  cplx_t<T>* D = reinterpret_cast<cplx_t<T>*>(scratch);
+  cplx_t<T>* Dx = D + (size_t)U * N;
+  cplx_t<T>* Z1 = Dx + (size_t)H * UP;
+  const int nblk = (U * U + kUpsCols - 1) / kUpsCols;
+  T* bval = reinterpret_cast<T*>(Z1 + nb * (int64_t)U * N * H);
   int* bidx = reinterpret_cast<int*>(bval + nb * nblk);
-  const size_t xsm = ups_xy_smem<T>(N, U);
-  e = cudaFuncSetAttribute(k_ups_xy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
-  if (e != cudaSuccess) return e;
-  k_ups_xy<T><<<dim3((unsigned)((N + kUpsPlanes - 1) / kUpsPlanes), (unsigned)nb), 256, xsm, s>>>(rt, N, kappa, tint,
-                                                                                                 Z2);
+  cplx_t<T>* Z2 = rt;  // X' is consumed by the z contraction
+  k_ups_tables<T><<<(unsigned)((U * N + H * UP + 255) / 256), 256, 0, s>>>(N, kappa, D, Dx);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const size_t esm = csz * (size_t)N * U;
-  e = cudaFuncSetAttribute(k_ups_z<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+  const size_t lsm = ups_left_smem<T>(N, U);
+  e = cudaFuncSetAttribute(k_ups_left<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
   if (e != cudaSuccess) return e;
-  k_ups_z<T><<<dim3((unsigned)nblk, (unsigned)nb), kUpsZThreads, esm, s>>>(Z2, N, kappa, tint, bval, bidx);
+  const int cz = N * H;  // z contraction: per particle [U x N] x [N x N H]
+  k_ups_left<T><<<dim3((unsigned)((cz + kUpsCols - 1) / kUpsCols), (unsigned)nb), kUpsThreads, lsm, s>>>(
+      D, U, N, rt, (int64_t)N * N * H, cz, Z1, (int64_t)U * N * H);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // y contraction: per (particle, uz) [U x N] x [N x H]  (gridDim.y <= 65535: nb U stays below it for nb <= 1337)
+  for (int64_t s0 = 0; s0 < nb * U; s0 += 65535) {
+    const int64_t ns = std::min<int64_t>(65535, nb * U - s0);
+    k_ups_left<T><<<dim3((unsigned)((H + kUpsCols - 1) / kUpsCols), (unsigned)ns), kUpsThreads, lsm, s>>>(
+        D, U, N, Z1 + s0 * N * H, (int64_t)N * H, H, Z2 + s0 * U * H, (int64_t)U * H);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  const size_t xsm = ups_xmax_smem<T>(N, U);
+  e = cudaFuncSetAttribute(k_ups_xmax<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
+  if (e != cudaSuccess) return e;
+  k_ups_xmax<T><<<dim3((unsigned)nblk, (unsigned)nb), kUpsThreads, xsm, s>>>(Z2, Dx, N, U, bval, bidx);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_ups_final<T><<<(unsigned)((nb + 127) / 128), 128, 0, s>>>(bval, bidx, nblk, N, kappa, tint, nb, shifts, sstride,
                                                                peak);
