@@ -788,10 +788,11 @@ __global__ void __launch_bounds__(512) k_zcorr_rb(const float2* __restrict__ ft,
 // phase e^{2 pi i (kx tx0 + ky ty0 + kz tz0) / N} folded into X, and the three DFT matrices D(k, s_u) are constants:
 //   k_zfft_cross  3-D spectra from the plane spectra: the z FFT of f~ and rho~ pencils (Stockham in shared memory),
 //                 X' = F^ conj(rho^) e^{2 pi i k.t0 / N} written over rho~ (never needed again this alternation);
-//   k_ups_left    mode products with the constant D [U][N] (register-tiled GEMMs, 64-column tiles):
-//                 Z1[uz][ky][kx] = sum_kz D[uz][kz] X'[kz][ky][kx]   (one [U x N] x [N x N H] GEMM per particle)
-//                 Z2[uz][uy][kx] = sum_ky D[uy][ky] Z1[uz][ky][kx]   (one [U x N] x [N x H] GEMM per (particle, uz));
-//   k_ups_xmax    c~ = Re sum_kx w D[kx][ux] Z2[uz][uy][kx] (half spectrum in kx: w = 1 at kx = 0 and N/2, else 2;
+//   k_ups_left    mode products with the constant D [U][N] (register-tiled GEMMs, 64-column tiles), each written with
+//                 the next contracted axis outermost so that every product is one GEMM per particle:
+//                 Z1[ky][uz][kx] = sum_kz D[uz][kz] X'[kz][ky][kx]   ([U x N] x [N x N H])
+//                 Z2[uy][uz][kx] = sum_ky D[uy][ky] Z1[ky][uz][kx]   ([U x N] x [N x U H]);
+//   k_ups_xmax    c~ = Re sum_kx w D[kx][ux] Z2[uy][uz][kx] (half spectrum in kx: w = 1 at kx = 0 and N/2, else 2;
 //                 Re at the end makes the half sum exact for the Hermitian X) per 64-row block, block argmax;
 //   k_ups_final   per particle: argmax over the blocks, t = t0 + (u - h)/kappa, peak = c~ / N^3.
 // Contracting z, y, x in that order costs U N^2 H + U^2 N H + U^3 H complex MACs (39 M at 96^3, kappa = 16).
@@ -896,16 +897,17 @@ constexpr int kUpsMaxU = 65;       // kappa <= 21
 constexpr int kUpsThreads = 224;   // 208 active: 13 x 16 (left) or 16 x 13 (xmax) thread tiles of 4 x 4
 constexpr int kUpsCols = 64;       // columns per CTA tile
 
-// the constant DFT matrices: D [U][N] = D(k, s_u) (reading C27 with t0 = 0), Dx [H][UP] = w(kx) D(kx, s_ux)
+// the constant DFT matrices, k-major: Dt [N][UP] = D(k, s_u) (reading C27 with t0 = 0; zero for u >= U),
+// Dx [H][UP] = w(kx) D(kx, s_ux)
 template <typename T>
-__global__ void k_ups_tables(int N, int kappa, cplx_t<T>* __restrict__ D, cplx_t<T>* __restrict__ Dx) {
+__global__ void k_ups_tables(int N, int kappa, cplx_t<T>* __restrict__ Dt, cplx_t<T>* __restrict__ Dx) {
   const int H = N / 2 + 1, h = (int)ceil(1.5 * kappa), U = 2 * h + 1, UP = ups_pad4(U);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < U * N + H * UP; i += gridDim.x * blockDim.x) {
-    if (i < U * N) {
-      const int u = i / N, k = i - u * N;
-      D[i] = ups_phase<T>(k, N, 0, u, h, kappa);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N * UP + H * UP; i += gridDim.x * blockDim.x) {
+    if (i < N * UP) {
+      const int k = i / UP, u = i - k * UP;
+      Dt[i] = u < U ? ups_phase<T>(k, N, 0, u, h, kappa) : mk<T>(T(0), T(0));
     } else {
-      const int j = i - U * N, kx = j / UP, u = j - kx * UP;
+      const int j = i - N * UP, kx = j / UP, u = j - kx * UP;
       const T w = (kx == 0 || 2 * kx == N) ? T(1) : T(2);
       const cplx_t<T> e = u < U ? ups_phase<T>(kx, N, 0, u, h, kappa) : mk<T>(T(0), T(0));
       Dx[j] = mk<T>(w * e.x, w * e.y);
@@ -917,27 +919,38 @@ template <typename T> __host__ __device__ inline size_t ups_left_smem(int N, int
   return sizeof(cplx_t<T>) * (size_t)N * (ups_pad4(U) + kUpsCols);
 }
 
-// out[s][u][c] = sum_{k < K} D[u][k] in[s][k][c]  (c < C; slice s = blockIdx.y, 64-column tile blockIdx.x): D staged
-// k-major, the input tile [K][64] staged, 4 (u) x 4 (c) complex outputs per thread (8 shared loads per 16 MACs)
+// out[s][u][c] = sum_{k < K} D[u][k] in[s][k][c]  (c < C; slice s = blockIdx.y, 64-column tile blockIdx.x): Dt
+// [K][UP] and the input tile [K][64] staged by cp.async (zero fill past C), 4 (u) x 4 (c) complex outputs per thread
+// (8 shared loads per 16 MACs)
 template <typename T>
-__global__ void __launch_bounds__(kUpsThreads) k_ups_left(const cplx_t<T>* __restrict__ D, int U, int K,
+__global__ void __launch_bounds__(kUpsThreads) k_ups_left(const cplx_t<T>* __restrict__ Dt, int U, int K,
                                                           const cplx_t<T>* __restrict__ in, int64_t in_ss, int C,
-                                                          cplx_t<T>* __restrict__ out, int64_t out_ss) {
+                                                          cplx_t<T>* __restrict__ out, int64_t out_ss, int hs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int CS = (int)sizeof(cplx_t<T>);
   const int UP = ups_pad4(U);
   cplx_t<T>* Ds = reinterpret_cast<cplx_t<T>*>(smem_raw);  // [K][UP]
   cplx_t<T>* Is = Ds + K * UP;                                // [K][64]
   const int64_t sl = blockIdx.y;
   const int c0 = blockIdx.x * kUpsCols;
-  const cplx_t<T> zero = mk<T>(T(0), T(0));
-  for (int i = threadIdx.x; i < K * UP; i += blockDim.x) {
-    const int k = i / UP, u = i - k * UP;
-    Ds[i] = u < U ? D[u * K + k] : zero;
-  }
-  const cplx_t<T>* src = in + sl * in_ss + c0;
-  for (int i = threadIdx.x; i < K * kUpsCols; i += blockDim.x) {
-    const int k = i / kUpsCols, c = i - k * kUpsCols;
-    Is[i] = c0 + c < C ? src[(int64_t)k * C + c] : zero;
+  {
+    const unsigned char* dsrc = reinterpret_cast<const unsigned char*>(Dt);
+    for (int e = threadIdx.x; e < K * UP * CS / 16; e += blockDim.x) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(reinterpret_cast<unsigned char*>(Ds) + 16 * e);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(dsrc + 16 * e));
+    }
+    const cplx_t<T>* src = in + sl * in_ss + c0;
+    for (int i = threadIdx.x; i < K * kUpsCols; i += blockDim.x) {
+      const int k = i / kUpsCols, c = i - k * kUpsCols;
+      const bool ok = c0 + c < C;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Is + i);
+      const cplx_t<T>* g = ok ? src + (int64_t)k * C + c : src;
+      if constexpr (CS == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0));
+      else
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
   }
   __syncthreads();
   const int t = threadIdx.x;
@@ -965,14 +978,19 @@ __global__ void __launch_bounds__(kUpsThreads) k_ups_left(const cplx_t<T>* __res
         ai[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, ai[i][j]));
       }
   }
-  cplx_t<T>* dst = out + sl * out_ss + c0 + tc;
+  // output layout: [u][c], or (hs > 0) [c / hs][u][c % hs] -- the next contraction's axis outermost
+  cplx_t<T>* dst = out + sl * out_ss;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int u = 4 * tu + i;
-    if (u >= U) continue;
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + tc + 16 * j;
+    if (c >= C) continue;
+    const int64_t base = hs ? (int64_t)(c / hs) * U * hs + c % hs : c;
+    const int64_t ustep = hs ? hs : C;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (c0 + tc + 16 * j < C) dst[(int64_t)u * C + 16 * j] = mk<T>(ar[i][j], ai[i][j]);
+    for (int i = 0; i < 4; ++i) {
+      const int u = 4 * tu + i;
+      if (u < U) dst[base + u * ustep] = mk<T>(ar[i][j], ai[i][j]);
+    }
   }
 }
 
@@ -1029,10 +1047,11 @@ __global__ void __launch_bounds__(kUpsThreads) k_ups_xmax(const cplx_t<T>* __res
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int r = r0 + 4 * tr + i, ux = 4 * tcol + j;
-        if (r < nrow && ux < U && better(acc[i][j], r * U + ux, bv, bi)) {
+        const int r = r0 + 4 * tr + i, ux = 4 * tcol + j;  // r = uy U + uz
+        const int idx = ((r % U) * U + r / U) * U + ux;    // z-major grid index uz U^2 + uy U + ux
+        if (r < nrow && ux < U && better(acc[i][j], idx, bv, bi)) {
           bv = acc[i][j];
-          bi = r * U + ux;
+          bi = idx;
         }
       }
   }
@@ -1238,7 +1257,7 @@ size_t ups_scratch_bytes(int N, int kappa, size_t csz) {
   // per particle: Z1 [U][N][H] and the block bests; the constant tables D, Dx ride along (at most once per chunk)
   const size_t U = (size_t)ups_points(kappa), H = (size_t)N / 2 + 1;
   const size_t nblk = (U * U + kUpsCols - 1) / kUpsCols;
-  return csz * (U * N * H) + nblk * (csz / 2 + sizeof(int)) + csz * (U * N + H * ups_pad4((int)U)) + 256;
+  return csz * (U * N * H) + nblk * (csz / 2 + sizeof(int)) + csz * ((size_t)N + H) * ups_pad4((int)U) + 256;
 }
 
 static int zfft_chunk(int N, size_t csz) {
@@ -1257,7 +1276,7 @@ bool ups_supported(int N, int kappa, bool fp64) {
          csz * ((size_t)N + 4 * (size_t)N) <= 200 * 1024;
 }
 
-// scratch: the tables D, Dx, then Z1 [nb][U][N][H], then the block bests; Z2 [nb][U][U][H] over X (rt);
+// scratch: the tables Dt, Dx, then Z1 [nb][N][U][H], then the block bests; Z2 [nb][U][U][H] over X (rt);
 // tint [nb][3] from k_window_peak
 template <typename T>
 cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
@@ -1289,29 +1308,28 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
   }
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) return e;
   const int UP = ups_pad4(U);
-  cplx_t<T>* D = reinterpret_cast<cplx_t<T>*>(scratch);
-  cplx_t<T>* Dx = D + (size_t)U * N;
+  cplx_t<T>* D = reinterpret_cast<cplx_t<T>*>(scratch);  // Dt [N][UP]
+  cplx_t<T>* Dx = D + (size_t)N * UP;
   cplx_t<T>* Z1 = Dx + (size_t)H * UP;
   const int nblk = (U * U + kUpsCols - 1) / kUpsCols;
   T* bval = reinterpret_cast<T*>(Z1 + nb * (int64_t)U * N * H);
   int* bidx = reinterpret_cast<int*>(bval + nb * nblk);
   cplx_t<T>* Z2 = rt;  // X' is consumed by the z contraction
-  k_ups_tables<T><<<(unsigned)((U * N + H * UP + 255) / 256), 256, 0, s>>>(N, kappa, D, Dx);
+  k_ups_tables<T><<<(unsigned)((N * UP + H * UP + 255) / 256), 256, 0, s>>>(N, kappa, D, Dx);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t lsm = ups_left_smem<T>(N, U);
   e = cudaFuncSetAttribute(k_ups_left<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
   if (e != cudaSuccess) return e;
-  const int cz = N * H;  // z contraction: per particle [U x N] x [N x N H]
+  // z contraction: per particle [U x N] x [N x N H] -> Z1 [ky][uz][kx]
+  const int cz = N * H;
   k_ups_left<T><<<dim3((unsigned)((cz + kUpsCols - 1) / kUpsCols), (unsigned)nb), kUpsThreads, lsm, s>>>(
-      D, U, N, rt, (int64_t)N * N * H, cz, Z1, (int64_t)U * N * H);
+      D, U, N, rt, (int64_t)N * N * H, cz, Z1, (int64_t)U * N * H, H);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  // y contraction: per (particle, uz) [U x N] x [N x H]  (gridDim.y <= 65535: nb U stays below it for nb <= 1337)
-  for (int64_t s0 = 0; s0 < nb * U; s0 += 65535) {
-    const int64_t ns = std::min<int64_t>(65535, nb * U - s0);
-    k_ups_left<T><<<dim3((unsigned)((H + kUpsCols - 1) / kUpsCols), (unsigned)ns), kUpsThreads, lsm, s>>>(
-        D, U, N, Z1 + s0 * N * H, (int64_t)N * H, H, Z2 + s0 * U * H, (int64_t)U * H);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
+  // y contraction: per particle [U x N] x [N x U H] -> Z2 [uy][uz][kx]
+  const int cy = U * H;
+  k_ups_left<T><<<dim3((unsigned)((cy + kUpsCols - 1) / kUpsCols), (unsigned)nb), kUpsThreads, lsm, s>>>(
+      D, U, N, Z1, (int64_t)N * U * H, cy, Z2, (int64_t)U * U * H, 0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t xsm = ups_xmax_smem<T>(N, U);
   e = cudaFuncSetAttribute(k_ups_xmax<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsm);
   if (e != cudaSuccess) return e;
