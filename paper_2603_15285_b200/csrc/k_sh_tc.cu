@@ -412,6 +412,22 @@ __global__ void __launch_bounds__(kThr + 32, 1)
     uint64_t l2_stream;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(l2_stream));
     uint32_t gtile = 0;      // global tile counter (buffer = gtile & 1)
+    // this lane's ring positions (the same for every ring): phi indices k, k + Mp, Mp - k, 2Mp - k per k round, and
+    // the extra sample xe (phi index 0, Mp, Mp/2, 3Mp/2) of the warp's ring xr
+    const int nx = mid ? 4 : 2;
+    float2 ph[KR][4];
+    auto load_ph = [&]() {
+#pragma unroll
+      for (int kr = 0; kr < KR; ++kr) {
+        const int k = 32 * kr + lane + 1;  // Kh <= 32 KR (host-checked)
+        const int kk[4] = {k, k + Mp, Mp - k, 2 * Mp - k};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ph[kr][q] = tw[k <= Kh ? kk[q] : 0];
+      }
+    };
+    load_ph();
+    const int xr = lane / nx, xe = lane % nx;
+    const int xcol = xe == 0 ? 0 : xe == 1 ? Mp : xe == 2 ? Mp / 2 : 3 * Mp / 2;
     for (int64_t p = blockIdx.x; p < B; p += gridDim.x) {
       const float* vol = vols + p * (int64_t)N * N * N;
       const float cc = 0.5f * (float)(N - 1);
@@ -481,10 +497,11 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           float* dst = planes + zslot[z + 1] * PS;
           const bool valid = z >= 0 && z < N;
           const float* src = vol + (size_t)(valid ? z : 0) * N * N;
-          for (int t = tid; t < N * n4; t += kThr) {
-            const int y = t / n4, x4 = t - y * n4;
-            cp_async16_stream(dst + y * PW + 4 * x4, src + y * N + 4 * x4, valid, l2_stream);
-          }
+          if (!(dbg & 16))
+            for (int t = tid; t < N * n4; t += kThr) {
+              const int y = t / n4, x4 = t - y * n4;
+              cp_async16_stream(dst + y * PW + 4 * x4, src + y * N + 4 * x4, valid, l2_stream);
+            }
         }
         zhave = max(zhave, zto);
         asm volatile("cp.async.commit_group;\n" ::);
@@ -544,6 +561,55 @@ __global__ void __launch_bounds__(kThr + 32, 1)
         const int buf = (int)(gcur & 1);
         long long tq0 = clock64();
         if (t < ntiles) {
+          // ring geometry of tile t (static per particle: independent of the planes): lane rr < RPW computes ring slot
+          // warp + rr * kWarps, then broadcasts.  With one k round it is done before the plane wait, so that its
+          // dependent chain overlaps the barrier and the plane wait (measured: -2 % at c2; with two k rounds it stays
+          // after the wait: +4 % at 96^3 otherwise, and a runtime choice costs registers everywhere)
+          int* sl = slots + (t % 3) * kSlotFields * NR;
+          constexpr int RPW = NR / kWarps;  // rings per warp
+          float a_rs[RPW], a_fz[RPW], x_rs = 0.f, x_fz = 0.f;
+          int a_b0[RPW], a_dz[RPW], a_in[RPW], x_b0 = 0, x_dz = 0, x_in = 0;
+          auto geometry = [&]() {
+            float g_rs = 0.f, g_fz = 0.f;
+            int g_b0 = 0, g_dz = 0, g_in = 0;
+            if (lane < RPW) {
+              const int r = warp + lane * kWarps, g = tstart[t] + r;
+              int goff = -1;
+              if (g < tstart[t + 1]) {
+                const int ring = list[g];
+                const int i = ring >> 16, j = ring & 0xffff;
+                const float rad = (float)i + 0.5f;
+                const float2 nd = node[j];
+                g_rs = rad * nd.y;
+                const float z = fmaf(rad, nd.x, cz);
+                const float fz0 = floorf(z);
+                const int zb = (int)fz0;
+                g_fz = z - fz0;
+                g_in = (zb >= -1 && zb <= N - 1) && !(dbg & 2);
+                if (g_in) {
+                  g_b0 = zslot[zb + 1] * PS;
+                  g_dz = zslot[zb + 2] * PS - g_b0;
+                }
+                goff = (i * nth + j) * (L + 1) * 2;
+              }
+              sl[r] = goff;
+            }
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+              a_rs[rr] = __shfl_sync(0xffffffffu, g_rs, rr);
+              a_fz[rr] = __shfl_sync(0xffffffffu, g_fz, rr);
+              a_b0[rr] = __shfl_sync(0xffffffffu, g_b0, rr);
+              a_dz[rr] = __shfl_sync(0xffffffffu, g_dz, rr);
+              a_in[rr] = __shfl_sync(0xffffffffu, g_in, rr);
+            }
+            const int xsrc = min(xr, RPW - 1);
+            x_rs = __shfl_sync(0xffffffffu, g_rs, xsrc);
+            x_fz = __shfl_sync(0xffffffffu, g_fz, xsrc);
+            x_b0 = __shfl_sync(0xffffffffu, g_b0, xsrc);
+            x_dz = __shfl_sync(0xffffffffu, g_dz, xsrc);
+            x_in = __shfl_sync(0xffffffffu, g_in, xsrc);
+          };
+          if constexpr (KR == 1) geometry();
           const int lo = tlo[t], hi = thi[t];
           if (hi - lo + 1 > P && tid == 0) atomicOr(flags, FLAG_PLANES);
           if (zhave < hi) {
@@ -566,54 +632,16 @@ __global__ void __launch_bounds__(kThr + 32, 1)
             if (want > zhave) request(want);
           }
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[5], (unsigned long long)(clock64() - tq1));
+          if constexpr (KR > 1) geometry();
           // sample tile t into S[buf] (fp16 hi/lo of the per-ring scaled samples): warp w takes ring slots
           // w, w + 16, ...; lanes walk k along the ring (4 mirrored phi indices per lane, one 8-byte store each)
           unsigned char* Shi = Bs + (size_t)(2 * buf) * Kc * LBO;
           unsigned char* Slo = Shi + (size_t)Kc * LBO;
-          int* sl = slots + (t % 3) * kSlotFields * NR;
-          constexpr int RPW = NR / kWarps;  // rings per warp
-          const int nx = mid ? 4 : 2;
-          // ring geometry: lane rr < RPW computes ring slot warp + rr * kWarps, then broadcasts
-          float g_rs = 0.f, g_fz = 0.f;
-          int g_b0 = 0, g_dz = 0, g_in = 0;
-          if (lane < RPW) {
-            const int r = warp + lane * kWarps, g = tstart[t] + r;
-            int goff = -1;
-            if (g < tstart[t + 1]) {
-              const int ring = list[g];
-              const int i = ring >> 16, j = ring & 0xffff;
-              const float rad = (float)i + 0.5f;
-              const float2 nd = node[j];
-              g_rs = rad * nd.y;
-              const float z = fmaf(rad, nd.x, cz);
-              const float fz0 = floorf(z);
-              const int zb = (int)fz0;
-              g_fz = z - fz0;
-              g_in = (zb >= -1 && zb <= N - 1) && !(dbg & 2);
-              if (g_in) {
-                g_b0 = zslot[zb + 1] * PS;
-                g_dz = zslot[zb + 2] * PS - g_b0;
-              }
-              goff = (i * nth + j) * (L + 1) * 2;
-            }
-            sl[r] = goff;
-          }
           float sv[KR][RPW][4], ex = 0.f;
-          float2 ph[KR][4];
-#pragma unroll
-          for (int kr = 0; kr < KR; ++kr) {
-            const int k = 32 * kr + lane + 1;  // Kh <= 32 KR (host-checked)
-            const int kk[4] = {k, k + Mp, Mp - k, 2 * Mp - k};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) ph[kr][q] = tw[k <= Kh ? kk[q] : 0];
-          }
-          const int xr = lane / nx, xe = lane % nx;  // extra sample xe of the warp's ring xr
-          const int xcol = xe == 0 ? 0 : xe == 1 ? Mp : xe == 2 ? Mp / 2 : 3 * Mp / 2;
 #pragma unroll
           for (int rr = 0; rr < RPW; ++rr) {
-            const float rs = __shfl_sync(0xffffffffu, g_rs, rr), fz = __shfl_sync(0xffffffffu, g_fz, rr);
-            const int b0 = __shfl_sync(0xffffffffu, g_b0, rr), dz = __shfl_sync(0xffffffffu, g_dz, rr);
-            const int in = __shfl_sync(0xffffffffu, g_in, rr);
+            const float rs = a_rs[rr], fz = a_fz[rr];
+            const int b0 = a_b0[rr], dz = a_dz[rr], in = a_in[rr];
 #pragma unroll
             for (int kr = 0; kr < KR; ++kr) {
 #pragma unroll
@@ -631,15 +659,9 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           }
           // phi indices 0 and Mp (and Mp/2, 3Mp/2 when Mp is even) of the warp's rings: one sample per lane, all
           // rings in one pass
-          {
-            const int src = min(xr, RPW - 1);
-            const float rs = __shfl_sync(0xffffffffu, g_rs, src), fz = __shfl_sync(0xffffffffu, g_fz, src);
-            const int b0 = __shfl_sync(0xffffffffu, g_b0, src), dz = __shfl_sync(0xffffffffu, g_dz, src);
-            const int in = __shfl_sync(0xffffffffu, g_in, src);
-            if (xr < RPW && in) {
-              const float2 phx = tw[xcol];
-              ex = tri_xy<NT>(planes + b0, dz, N, fmaf(rs, phx.x, cx), fmaf(rs, phx.y, cy), fz);
-            }
+          if (xr < RPW && x_in) {
+            const float2 phx = tw[xcol];
+            ex = tri_xy<NT>(planes + x_b0, x_dz, N, fmaf(x_rs, phx.x, cx), fmaf(x_rs, phx.y, cy), x_fz);
           }
           // m = L when 2(L+1) = 130 > 128 MMA rows (L = 64): its two DFT rows from the FP32 samples, in the sampler.
           // The lane's mirrored phi indices k, k+Mp, Mp-k, 2Mp-k (n_phi = 2Mp) carry e^{-iL phi} = e, s e, s conj(e),
@@ -680,6 +702,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           long long tq2 = clock64();
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[2], (unsigned long long)(tq2 - tq1));
           // per-ring power-of-two scale (max |sample| -> [2^14, 2^15)), fp16 hi/lo split, 8-byte stores
+          if (!(dbg & 32)) {
           float mxv[RPW];
 #pragma unroll
           for (int rr = 0; rr < RPW; ++rr) {
@@ -733,6 +756,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
               *(__half*)(Slo + off) = __float2half_rn(x - __half2float(h));
             }
             if (lane == 0) sl[NR + r] = (int)((uint32_t)(127 - es - 10) << 23);
+          }
           }
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[3], (unsigned long long)(clock64() - tq2));
           // S[buf] -> async proxy; hand the tile to the MMA warp
@@ -827,7 +851,7 @@ cudaError_t launch_sh_rings_tc(const float* vols, int64_t nb, const float* shift
   const int NR = tab.tcNR;
   const size_t bytes = tc_layout(tab.N, tab.R, tab.nth, tab.nph, P, NR, tab.tc_list != nullptr).total;
   const int grid = (int)std::min<int64_t>(nb, num_sms);
-  const char* dv = getenv("MATCHA_SH_DBG");  // profiling knob: 1 = no MMA/drain, 2 = no gathers
+  const char* dv = getenv("MATCHA_SH_DBG");  // profiling knob: 1 = no MMA/drain, 2 = no gathers, 16 = no plane loads, 32 = no split/store
   const int dbg = dv ? atoi(dv) : 0;
   cudaError_t e;
   auto go = [&](auto kern) {
