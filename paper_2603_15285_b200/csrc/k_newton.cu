@@ -16,7 +16,7 @@
 // state in registers (each M^l load and recurrence coefficient shared by CG candidates); the candidate groups run
 // concurrently on slices of the CTA; M^l streams through a per-thread cp.async ring in shared memory.  Runs are
 // grouped by l0 (long runs first) and dealt boustrophedon.  Block reductions are fixed-order (deterministic: no
-// atomics), FP64 from the lane partials on.  The 3x3 Newton solve runs in FP64.
+// atomics), one FP64 row sum per thread.  The 3x3 Newton solve runs in FP64.
 #include <float.h>
 
 #include <cstdlib>
@@ -31,6 +31,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCG = 10;  // candidates per register group
+constexpr int kRedStride = kThreads + 1;  // row pitch of the partial sums: a lane per row reads conflict-free
 constexpr int kRing = 4;    // M^l is requested kRing degrees ahead of its use (per-thread cp.async ring in smem)
 
 template <int BYTES> __device__ __forceinline__ void cp_async_ca(void* sdst, const void* gsrc) {
@@ -62,7 +63,7 @@ template <typename T> __host__ __device__ inline SmemLayout smem_layout(int Q, i
   s.cand = take(sizeof(CandShared<T>) * Q);
   s.ea = take(sizeof(cplx_t<T>) * Q * (L + 1));
   s.eg = take(sizeof(cplx_t<T>) * Q * (2 * L + 1));
-  s.red = take(sizeof(T) * 10 * cg * kThreads);  // per-thread partial sums [value][thread]
+  s.red = take(sizeof(T) * 10 * cg * kRedStride);  // per-thread partial sums [value][thread] (padded rows)
   s.ring = take(sizeof(cplx_t<T>) * kRing * 2 * kThreads);  // per-thread cp.async ring of M^l (pairs A, B)
   s.sums = take(sizeof(double) * 10 * Q);
   s.prevc = take(sizeof(double) * Q);
@@ -211,9 +212,9 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
   constexpr int NVAL = NV * CG;
   const int G = (Q + CG - 1) / CG, Tg = kThreads / G;
   const int g = tid / Tg, lt = tid - g * Tg;
-  T* acc = red + tid;  // this thread's partial sums: value (v, k) at acc[(v * CG + k) * kThreads]
+  T* acc = red + tid;  // this thread's partial sums: value (v, k) at acc[(v * CG + k) * kRedStride]
 #pragma unroll
-  for (int i = 0; i < NVAL; ++i) acc[i * kThreads] = T(0);
+  for (int i = 0; i < NVAL; ++i) acc[i * kRedStride] = T(0);
   if (g < G) {
     const int c0 = g * CG;
     // candidate indices of this group (clamped: duplicates of the last are computed, then ignored)
@@ -365,21 +366,25 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
         contrib(m, n, wA, a0r[k], a0i[k], a1r[k], a1i[k], aur[k], aui[k]);
         contrib(mB, nB, wB, b0r[k], b0i[k], b1r[k], b1i[k], bur[k], bui[k]);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) acc[(i * CG + k) * kThreads] += v[i];
+        for (int i = 0; i < NV; ++i) acc[(i * CG + k) * kRedStride] += v[i];
       }
     }
   }
-  // deterministic block reduction: warp w sums rows (group, value) w, w + kWarps, ... over the group's Tg threads in
-  // a fixed order (FP64 lane partials, then a butterfly)
+  // deterministic block reduction: one thread per row (group, value) sums the group's Tg partials in a fixed order in
+  // FP64 (four interleaved chains, combined in a fixed order)
   __syncthreads();
-  for (int i = warp; i < G * NVAL; i += kWarps) {
+  for (int i = tid; i < G * NVAL; i += kThreads) {
     const int gg = i / NVAL, vk = i - gg * NVAL;
-    const T* row = red + vk * kThreads + gg * Tg;
-    double sacc = 0.0;
-    for (int t = lane; t < Tg; t += 32) sacc += (double)row[t];
-    sacc = warp_sum(sacc);
+    const T* row = red + vk * kRedStride + gg * Tg;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    int t = 0;
+    for (; t + 4 <= Tg; t += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s4[q] += (double)row[t + q];
+    }
+    for (; t < Tg; ++t) s4[0] += (double)row[t];
     const int v = vk / CG, k = vk % CG, c = gg * CG + k;
-    if (lane == 0 && c < Q) sums[c * 10 + v] = sacc;
+    if (c < Q) sums[c * 10 + v] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
   }
   __syncthreads();
   if (DERIV) {
@@ -506,7 +511,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   // final C_{L_J} of every candidate and the argmax
   prepare_candidates<T>(theta, Q, Lmax_b, cs, ea, eg);
   __syncthreads();
-  eval_block<T, CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
+  // value only: twice the candidates per thread (no derivative state), one walk of the runs instead of two
+  if (sizeof(T) == 4 && CG == 5 && Q > CG && Q <= 2 * CG)
+    eval_block<T, 2 * CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
+  else
+    eval_block<T, CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
   for (int t = threadIdx.x; t < 3 * Q; t += blockDim.x) a.euler[cb0 * 3 + t] = (T)theta[t];
   for (int c = threadIdx.x; c < Q; c += blockDim.x) {
     const double v = act[c] ? sums[c * 10] : -INFINITY;
