@@ -778,10 +778,35 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   const int ngroups = R / SG;
   // this CTA's contiguous item range; lane l takes items l, l + 2, ...
   const int64_t i_begin = nitems * blockIdx.x / gridDim.x, i_end = nitems * (blockIdx.x + 1) / gridDim.x;
-  auto copy_item = [&](int64_t it, cplx_t<T>* dst) {
+  // items are contiguous in G: one TMA bulk copy per item (issued by the lane's first thread, completion on a per-
+  // (lane, buffer) mbarrier) when 16-byte aligned, else per-thread cp.async
+  __shared__ __align__(8) uint64_t gmb[4];
+  const bool bulk = ((gbytes & 15) == 0) && ((reinterpret_cast<uintptr_t>(G) & 15) == 0);
+  if (tid == 0) {
+    for (int b = 0; b < 4; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&gmb[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+  auto copy_item = [&](int64_t it, int b) {
+    cplx_t<T>* dst = gbuf(b);
     const int64_t p = it / ngroups;
     const int i0 = (int)(it % ngroups) * SG;
     const unsigned char* src = (const unsigned char*)(G + ((p * R + i0) * (int64_t)nth) * L1);
+    if (bulk) {
+      if (ltid == 0) {
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&gmb[2 * lane_id + b]);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::);  // the fold's writes to this buffer come first
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"((unsigned)gbytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         sa),
+                     "l"(src), "r"((unsigned)gbytes), "r"(bar)
+                     : "memory");
+      }
+      return;
+    }
     const bool al16 = ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)gbytes) & 15) == 0;
     if (al16) {
       for (int e = ltid; e < (int)(gbytes / 16); e += LT) {
@@ -800,7 +825,7 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"((const unsigned char*)tab.pwp + 16 * e));
   }
   asm volatile("cp.async.commit_group;\n" ::);
-  if (i_begin + lane_id < i_end) copy_item(i_begin + lane_id, gbuf(0));
+  if (i_begin + lane_id < i_end) copy_item(i_begin + lane_id, 0);
   asm volatile("cp.async.commit_group;\n" ::);
   asm volatile("cp.async.wait_group 1;\n" ::);  // this thread's part of the weight table
   const int ntiles = leg_tiles_par(L);
@@ -826,9 +851,20 @@ __global__ void __launch_bounds__(2 * kLegLaneThreads, 1)
   int k = 0;
   for (int64_t it = i_begin + lane_id; it < i_end; it += 2, ++k) {
     cplx_t<T>* Gs = gbuf(k & 1);
-    if (it + 2 < i_end) copy_item(it + 2, gbuf((k + 1) & 1));
+    if (it + 2 < i_end) copy_item(it + 2, (k + 1) & 1);
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 1;\n" ::);
+    if (bulk) {  // the k/2-th fill of buffer k & 1 has landed
+      const unsigned bar = (unsigned)__cvta_generic_to_shared(&gmb[2 * lane_id + (k & 1)]);
+      const unsigned ph = (unsigned)((k >> 1) & 1);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}\n"
+                     : "=r"(done)
+                     : "r"(bar), "r"(ph)
+                     : "memory");
+    }
     lbar();
     // node-pair fold in place: (G_j, G_{n-1-j}) -> (G_j + G_{n-1-j}, G_j - G_{n-1-j})
     for (int e = ltid; e < SG * half * L1; e += LT) {
