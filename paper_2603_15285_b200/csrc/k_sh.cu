@@ -1059,9 +1059,16 @@ cudaError_t launch_sh_analysis(const float* vols, int64_t B, const T* shifts, in
       // the slab-parallel SIMT kernel instead, which spreads one particle over N/S CTAs
       if (tab.tcP > 0 && nb * 4 >= tab.num_sms)
         e = launch_sh_rings_tc(v, nb, sh, shift_stride, tab, tab.tcP, Gws, tab.flags, tab.num_sms, st);
-      else
-        e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
-                          : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
+      else {
+        // small batches (e.g. the reference): thinner slabs, so that one particle still spreads over many SMs
+        ShPlan<T> pl = plan;
+        if (!pl.gd && nb * pl.nslab < tab.num_sms) {
+          pl.S = std::max<int>(1, (int)((int64_t)pl.S * nb * pl.nslab / tab.num_sms));
+          pl.nslab = (N + pl.S - 1) / pl.S;
+        }
+        e = pl.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, pl, Gws, st)
+                        : launch_rings<T, false>(v, nb, sh, shift_stride, tab, pl, Gws, st);
+      }
     } else {
       e = plan.dft_smem ? launch_rings<T, true>(v, nb, sh, shift_stride, tab, plan, Gws, st)
                         : launch_rings<T, false>(v, nb, sh, shift_stride, tab, plan, Gws, st);
