@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       auto zfloor = [&](int i, int j) -> int { return (int)floorf(fmaf((float)i + 0.5f, node[j].x, cz)); };
       auto bucket = [&](int zb) { return min(max(zb, -2), N) + 2; };
 
-      long long tp0 = clock64();
+      long long tp0 = (dbg & 8) ? clock64() : 0;
       // ---- 1. counting sort of the rings by z bucket, then (j, i), one item per ring.  For fixed j the bucket is
       //      monotone in i, so the rings of cell (bucket, j) are a contiguous i-range whose first i gives each ring
       //      its rank: deterministic without ordered atomics.
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
       for (int t = 0; t <= ntiles; ++t) {
         const uint32_t gcur = gtile;  // global index of tile t (tiles handed to the MMA warp so far)
         const int buf = (int)(gcur & 1);
-        long long tq0 = clock64();
+        long long tq0 = (dbg & 8) ? clock64() : 0;
         if (t < ntiles) {
           // ring geometry of tile t (static per particle: independent of the planes): lane rr < RPW computes ring slot
           // warp + rr * kWarps, then broadcasts.  With one k round it is done before the plane wait, so that its
@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           }
           asm volatile("cp.async.wait_group 0;\n" ::);
           sbar();  // planes of tile t resident; all samplers done with iteration t-1 (incl. drain of tile t-2)
-          long long tq1 = clock64();
+          long long tq1 = (dbg & 8) ? clock64() : 0;
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[1], (unsigned long long)(tq1 - tq0));
           if (t + 1 < ntiles) {
             const int want = min(thi[t + 1], lo + P - 1);
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
               }
             }
           }
-          long long tq2 = clock64();
+          long long tq2 = (dbg & 8) ? clock64() : 0;
           if ((dbg & 8) && lane == 0) atomicAdd(&g_sh_prof[2], (unsigned long long)(tq2 - tq1));
           // per-ring power-of-two scale (max |sample| -> [2^14, 2^15)), fp16 hi/lo split, 8-byte stores
           if (!(dbg & 32)) {
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(kThr + 32, 1)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&full[buf])) : "memory");
           gtile = gcur + 1;
         }
-        long long tq3 = clock64();
+        long long tq3 = (dbg & 8) ? clock64() : 0;
         // drain tile t - 1 (overlaps the MMAs of tile t): TMEM lane o = output row, 16 ring columns per warp
         if (t > 0 && !(dbg & 1)) {
           const int pb = (int)((gcur - 1) & 1), tp = t - 1;
