@@ -427,6 +427,18 @@ def main():
         achieved = by * units / t_stage / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic}
+    # every stage against its own bound on the same model (the north_star evaluation kernel is newton_refine)
+    per_stage = {}
+    for k, (ms_k, n_k) in stages.items():
+        if k not in work or ms_k <= 0:
+            continue
+        u_k = args.steps * (P + (1 if k == "sh_analysis" else 0))
+        fl_k, by_k = work[k]
+        if fl_k / (alu_peak * 1e12) >= by_k / (hbm_peak * 1e9):
+            per_stage[k] = {"bound": "alu", "frac": fl_k * u_k / (ms_k / 1e3) / 1e12 / alu_peak}
+        else:
+            per_stage[k] = {"bound": "hbm", "frac": by_k * u_k / (ms_k / 1e3) / 1e9 / hbm_peak}
+    roof["stages"] = per_stage
     roof.update({"kernel": dom, "share_of_step": dms / tot_ms if tot_ms else None,
                  "peak_source": (f"{nsm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (guide unit counts)"
                                  if roof["bound"] == "alu" else f"MEASURED_PEAKS.json hbm_gbs ({src})"),
