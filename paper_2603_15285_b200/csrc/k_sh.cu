@@ -962,27 +962,28 @@ template <typename T> ShPlan<T> sh_plan(const ShTables<T>& tab) {
         }
       }
     }
-  // no slab fits: gathers straight from global memory (slabs of 8 planes only group the rings)
+  // no slab fits: gathers straight from global memory; slabs of 2 planes only group the rings, so that a CTA's
+  // gathers stay within ~3 planes (L1 reuse: 200^3, L = 100: 19.8 vs 23.6 ms per 100 particles with 8-plane slabs)
   for (int warps = kRingWarps; warps >= 2; warps /= 2)
     for (int pass = 0; pass < 2; ++pass) {
       const bool ds = (pass == 0);
-      const size_t tot = ring_layout<T>(tab.N, 8, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, ds, warps, false).total;
+      const size_t tot = ring_layout<T>(tab.N, 2, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, ds, warps, false).total;
       if (tot <= budget) {
-        pl.S = 8;
+        pl.S = 2;
         pl.dft_smem = ds;
         pl.gd = true;
-        pl.nslab = (tab.N + 7) / 8;
+        pl.nslab = (tab.N + 1) / 2;
         pl.rbytes = tot;
         pl.threads = 32 * warps;
         return pl;
       }
     }
-  pl.S = 8;
+  pl.S = 2;
   pl.dft_smem = false;
   pl.gd = true;
-  pl.nslab = (tab.N + 7) / 8;
+  pl.nslab = (tab.N + 1) / 2;
   pl.threads = 64;
-  pl.rbytes = ring_layout<T>(tab.N, 8, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false, 2, false).total;
+  pl.rbytes = ring_layout<T>(tab.N, 2, tab.nth, tab.nph, tab.R, tab.Kh, tab.MP, false, 2, false).total;
   return pl;
 }
 
