@@ -8,7 +8,8 @@
 // The ring DFT is a dense real contraction  D[o][ring] = sum_k A[o][k] S[ring][k]  with o = 2m + (0: Re, 1: Im),
 // A[2m][k] = (2 pi / n_phi) cos(m phi_k), A[2m+1][k] = -(2 pi / n_phi) sin(m phi_k), S = the ring samples (folded
 // over the real-data symmetry to Kh + 1 k-columns per parity class).  It runs as tcgen05.mma with M = 128 DFT rows
-// (2(L+1) <= 128 used), N = 64 rings per tile, K-steps of 16 fp16:
+// (2(L+1) <= 128 used; at L = 64 the 130th/131st rows, m = 64, are summed by the samplers from the FP32 samples),
+// N = 64 rings per tile (one k round per lane, Kh <= 32), 32 or 16 (two rounds, Kh <= 64), K-steps of 16 fp16:
 //   A_hi, A_lo  the DFT matrix x 2^10 split into fp16 hi + lo, in TMEM (written once per CTA; constant),
 //   S_hi, S_lo  each ring's samples scaled by a power of two and split into fp16 hi + lo, in shared memory
 //               (K-major, SWIZZLE_NONE; the K-chunk stride is padded by 16 B so that a warp's consecutive-k stores
@@ -21,7 +22,8 @@
 //
 // Persistent CTAs (one per SM) take whole particles.  Per particle the rings are sorted by the plane index of their
 // z (deterministic counting sort), so consecutive tiles of 64 rings need a small window of z-planes: the planes live
-// in a P-slot ring buffer in shared memory, prefetched one tile ahead with cp.async (the particle crosses HBM once).
+// in a P-slot ring buffer in shared memory, prefetched one tile ahead with cp.async (the particle crosses HBM once);
+// 128^3 boxes run with 2 slots (tiles then stay within one z bucket) and the sorted ring list in a global workspace.
 // Per tile: sample (trilinear from shared memory) -> S[buf]; the MMA warp issues 3 x K/16 MMAs into D[buf];
 // meanwhile the CTA drains D[buf^1] of the previous tile and samples the next one.
 // Deterministic: fixed summation orders, no atomics on data.
