@@ -511,8 +511,10 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && CG <= 5) ? 2 : 1)
   // final C_{L_J} of every candidate and the argmax
   prepare_candidates<T>(theta, Q, Lmax_b, cs, ea, eg);
   __syncthreads();
-  // value only: twice the candidates per thread (no derivative state), one walk of the runs instead of two
+  // value only: twice the candidates per thread (no derivative state): half the walks of the runs
   if (sizeof(T) == 4 && CG == 5 && Q > CG && Q <= 2 * CG)
+    eval_block<T, 2 * CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
+  else if (sizeof(T) == 4 && CG == 4 && Q > CG)
     eval_block<T, 2 * CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
   else
     eval_block<T, CG, false>(M, Lmax_b, Q, a.runs, a.run_lnc, cs, ea, eg, inv_l, inv_ll, red, ring, sums);
