@@ -185,7 +185,10 @@ bool ups_supported(int N, int kappa, bool fp64);
 size_t ups_scratch_bytes(int N, int kappa, size_t csz);  // per particle
 template <typename T>
 cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
-                             void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s);
+                             void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s,
+                             cplx_t<T>* fz = nullptr, int fz_mode = 0);
+// fz: optional cache [nb][N][N][N/2+1] of F^ = the z FFT of f~ (FP32 compile-time-N path): fz_mode 1 computes and
+// stores it with X, 2 reads it instead of transforming f~ again (the particles do not change across alternations)
 
 // ball-harmonic radial transform and the correlation tensor from its rank-|K_l| factors (k_ball.cu);
 // Bt real [Lmax+1][Kmax][R] radial table, Kl int [Lmax+1]; ball coefficients complex [B][ncoef(Lmax)][Kmax]

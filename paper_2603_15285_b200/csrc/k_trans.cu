@@ -834,10 +834,11 @@ __global__ void __launch_bounds__(256) k_zfft_cross(const cplx_t<T>* __restrict_
 }
 
 // FP32, compile-time N: the same z FFTs with ct_fft, cp.async-staged lines, one CTA per (ky row, particle)
-template <int N>
+template <int N, int MODE>  // MODE 0: F^ from f~; 1: also store F^ into fz; 2: F^ read from fz
 __global__ void __launch_bounds__(kFftThreads, 1) k_zfft_cross_fast(const float2* __restrict__ ft,
                                                                     float2* __restrict__ rt,
-                                                                    const int* __restrict__ tint) {
+                                                                    const int* __restrict__ tint,
+                                                                    float2* __restrict__ fz) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int H = N / 2 + 1, LB = fpad(H * N);
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -853,12 +854,13 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_zfft_cross_fast(const float2
     const int64_t g = row0 + (int64_t)zz * N * H + kx;
     const unsigned df = (unsigned)__cvta_generic_to_shared(f0 + fpad(kx * N + zz));
     const unsigned dr = (unsigned)__cvta_generic_to_shared(r0 + fpad(kx * N + zz));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(df), "l"(ft + g));
+    // MODE 2: the cached F^ (kz in place of z), already transformed
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(df), "l"((MODE == 2 ? fz : ft) + g));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dr), "l"(rt + g));
   }
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  float2* Fz = ct_fft<N, H, N>(f0, t1, tw);  // result in f0 or t1
+  float2* Fz = MODE == 2 ? f0 : ct_fft<N, H, N>(f0, t1, tw);  // result in f0 or t1
   float2* rin = r0;
   float2* rtmp = (Fz == f0) ? t1 : f0;        // the buffer not holding F^
   // r0 -> rtmp -> r0 ...: ct_fft alternates the two buffers it is given
@@ -868,6 +870,7 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_zfft_cross_fast(const float2
   for (int i = threadIdx.x; i < N * H; i += kFftThreads) {
     const int kz = i / H, kx = i - kz * H;
     const float2 f = Fz[fpad(kx * N + kz)], r = Rz[fpad(kx * N + kz)];
+    if (MODE == 1) fz[row0 + (int64_t)kz * N * H + kx] = f;
     const float2 x = make_float2(f.x * r.x + f.y * r.y, f.y * r.x - f.x * r.y);
     // the per-particle phase of the upsampled DFT: e^{+2 pi i m / N} = conj(tw[m]),  m = k . t0 mod N
     const int m = ((kx * tx0 + kz * tz0) % N + N + myz) % N;
@@ -1280,7 +1283,8 @@ bool ups_supported(int N, int kappa, bool fp64) {
 // tint [nb][3] from k_window_peak
 template <typename T>
 cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kappa, int64_t nb, const int* tint,
-                             void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s) {
+                             void* scratch, T* shifts, int sstride, T* peak, cudaStream_t s, cplx_t<T>* fz,
+                             int fz_mode) {
   if (nb == 0) return cudaSuccess;
   const size_t csz = sizeof(cplx_t<T>);
   if (!ups_supported(N, kappa, sizeof(T) == 8)) return cudaErrorInvalidValue;
@@ -1293,13 +1297,16 @@ cudaError_t launch_upsampled(const cplx_t<T>* ft, cplx_t<T>* rt, int N, int kapp
     auto go = [&](auto kern, int NN) {
       const size_t sm = sizeof(float2) * ((size_t)NN + 3 * (size_t)fpad((NN / 2 + 1) * NN));
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e == cudaSuccess) kern<<<dim3((unsigned)NN, (unsigned)nb), kFftThreads, sm, s>>>(ft, rt, tint);
+      if (e == cudaSuccess)
+        kern<<<dim3((unsigned)NN, (unsigned)nb), kFftThreads, sm, s>>>(ft, rt, tint, (float2*)fz);
       fast = true;
     };
-    if (N == 32) go(k_zfft_cross_fast<32>, 32);
-    else if (N == 64) go(k_zfft_cross_fast<64>, 64);
-    else if (N == 96) go(k_zfft_cross_fast<96>, 96);
-    else if (N == 128) go(k_zfft_cross_fast<128>, 128);
+    const int md = fz ? fz_mode : 0;
+    auto go3 = [&](auto k0, auto k1, auto k2, int NN) { md == 2 ? go(k2, NN) : md == 1 ? go(k1, NN) : go(k0, NN); };
+    if (N == 32) go3(k_zfft_cross_fast<32, 0>, k_zfft_cross_fast<32, 1>, k_zfft_cross_fast<32, 2>, 32);
+    else if (N == 64) go3(k_zfft_cross_fast<64, 0>, k_zfft_cross_fast<64, 1>, k_zfft_cross_fast<64, 2>, 64);
+    else if (N == 96) go3(k_zfft_cross_fast<96, 0>, k_zfft_cross_fast<96, 1>, k_zfft_cross_fast<96, 2>, 96);
+    else if (N == 128) go3(k_zfft_cross_fast<128, 0>, k_zfft_cross_fast<128, 1>, k_zfft_cross_fast<128, 2>, 128);
   }
   if (!fast) {
     e = cudaFuncSetAttribute(k_zfft_cross<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);
@@ -1345,9 +1352,9 @@ template cudaError_t launch_rotate_ref<float>(const float*, int, const float*, i
 template cudaError_t launch_rotate_ref<double>(const float*, int, const double*, int, const int*, int64_t, double*,
                                                cudaStream_t);
 template cudaError_t launch_upsampled<float>(const float2*, float2*, int, int, int64_t, const int*, void*, float*, int,
-                                             float*, cudaStream_t);
+                                             float*, cudaStream_t, float2*, int);
 template cudaError_t launch_upsampled<double>(const double2*, double2*, int, int, int64_t, const int*, void*, double*,
-                                              int, double*, cudaStream_t);
+                                              int, double*, cudaStream_t, double2*, int);
 template cudaError_t launch_plane_r2c<float, float>(const float*, int, int64_t, float2*, cudaStream_t);
 template cudaError_t launch_plane_r2c<double, float>(const float*, int, int64_t, double2*, cudaStream_t);
 template cudaError_t launch_plane_r2c<double, double>(const double*, int, int64_t, double2*, cudaStream_t);

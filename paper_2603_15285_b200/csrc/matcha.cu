@@ -62,6 +62,8 @@ struct matcha_ctx {
   std::string err;
   // stage 5 (translation): workspaces, allocated on first use
   void* ws_Fhat = nullptr;   // complex [mb][N][N][N/2+1]  f~: 2-D spectra of the particles' z-planes
+  void* ws_FhatZ = nullptr;  // complex [mb][N][N][N/2+1]  F^ = z FFT of f~ (f3, FP32 fast path: once per chunk)
+  bool fz_ready = false;     // ws_FhatZ holds the current chunk's F^
   void* ws_Xhat = nullptr;   // complex [mb][N][N][N/2+1]  rho~: 2-D spectra of the rotated references' planes
   void* ws_rho = nullptr;    // real [mb][N^3]             rotated references
   void* ws_peak = nullptr;   // real [mb]
@@ -443,6 +445,13 @@ static matcha_status_t trans_prepare(matcha_handle_t h, int W, int kappa) {
       if (e != cudaSuccess) return cuda_fail(h, e, "translation: texture table");
     }
   }
+  if (kappa > 0 && h->trans_fast && !h->ws_FhatZ) {  // optional F^ cache of the upsampled path
+    if (cudaMalloc(&h->ws_FhatZ, 2 * h->rsz * nc * mb) != cudaSuccess) {
+      h->ws_FhatZ = nullptr;
+      cudaGetLastError();
+    }
+    h->fz_ready = false;
+  }
   if (h->ws_win_W < W) {
     if (h->ws_win) cudaFree(h->ws_win);
     h->ws_win = nullptr;
@@ -481,6 +490,7 @@ static matcha_status_t trans_fhat(matcha_handle_t h, const float* vols, int64_t 
                       : launch_plane_r2c<float, float>(vols, h->cfg.N, nb, (float2*)h->ws_Fhat, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "translation: plane_r2c of the particles");
   h->launches++;
+  h->fz_ready = false;  // a new chunk: its F^ is computed by the first upsampled update
   return MATCHA_OK;
 }
 
@@ -524,8 +534,10 @@ static matcha_status_t trans_update(matcha_handle_t h, int64_t nb, const float* 
     e = h->fp64 ? launch_upsampled<double>((const double2*)h->ws_Fhat, (double2*)h->ws_Xhat, N, kappa, nb, tint,
                                            h->ws_ups, (double*)shifts, sstride, (double*)peak, s)
                 : launch_upsampled<float>((const float2*)h->ws_Fhat, (float2*)h->ws_Xhat, N, kappa, nb, tint,
-                                          h->ws_ups, (float*)shifts, sstride, (float*)peak, s);
+                                          h->ws_ups, (float*)shifts, sstride, (float*)peak, s,
+                                          (float2*)h->ws_FhatZ, h->fz_ready ? 2 : 1);
     if (e != cudaSuccess) return cuda_fail(h, e, "translation: upsampled DFT");
+    h->fz_ready = h->ws_FhatZ != nullptr;
     h->launches += 4;
   }
   return MATCHA_OK;
@@ -900,7 +912,7 @@ MATCHA_API matcha_status_t matcha_destroy(matcha_handle_t h) {
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (int k = 0; k < kMaxTemplates; ++k)
     if (h->tex_ref[k]) cudaDestroyTextureObject(h->tex_ref[k]);
-  for (void* q : {h->ws_Fhat, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad,
+  for (void* q : {h->ws_Fhat, h->ws_FhatZ, h->ws_Xhat, h->ws_rho, h->ws_peak, h->ws_euler1, h->ws_win, (void*)h->ws_refpad,
                   (void*)h->ws_tint, h->ws_ups, h->ws_grid, (void*)h->d_tex, h->ws_Hs, h->ws_cand,
                   (void*)h->ws_tsel, h->ws_Rt, h->d_ballB, (void*)h->d_ballK, h->ws_Fb, h->ws_Hb})
     if (q) cudaFree(q);
