@@ -29,7 +29,6 @@ namespace matcha {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCG = 10;  // candidates per register group
 constexpr int kRedStride = kThreads + 1;  // row pitch of the partial sums: a lane per row reads conflict-free
 constexpr int kRing = 4;    // M^l is requested kRing degrees ahead of its use (per-thread cp.async ring in smem)
@@ -131,29 +130,6 @@ __device__ void newton_delta(const double* g, const double* h, double* dl) {
   dl[2] = -(c02 * g[0] + c12 * g[1] + c22 * g[2]) * inv;
 }
 
-// Warp reduce-scatter of N (multiple of 32) per-lane values: 5 halving levels with N/2 + N/4 + ... shuffles
-// (instead of 5N); afterwards lane l holds the warp totals of indices l*(N/32) + i, i < N/32.
-template <typename T, int N, int O>
-__device__ __forceinline__ void rs_levels(T* v, int lane) {
-  if constexpr (O >= 1) {
-    constexpr int H = N / 2;
-    const bool upper = (lane & O) != 0;
-#pragma unroll
-    for (int i = 0; i < H; ++i) {
-      const T send = upper ? v[i] : v[i + H];
-      const T keep = upper ? v[i + H] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
-    }
-    rs_levels<T, H, O / 2>(v, lane);
-  }
-}
-
-template <typename T> __device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 // Prepare per-rotation shared data for candidates [0, Q): trig of beta and phase tables.
 template <typename T>
 __device__ void prepare_candidates(const double* theta, int Q, int L, CandShared<T>* cs, cplx_t<T>* ea,
@@ -207,7 +183,7 @@ __device__ void eval_block(const cplx_t<T>* __restrict__ M, int L, int Q, const 
                            double* sums) {
   constexpr int NV = DERIV ? 10 : 1;
   const int nruns = run_count(L);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int na = L + 1, ng = 2 * L + 1;
   constexpr int NVAL = NV * CG;
   const int G = (Q + CG - 1) / CG, Tg = kThreads / G;
